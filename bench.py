@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json metric "SSSP/SpMV GTEPS per B200 (1-8 GPU) & speedup
+vs basic-DP and flat kernels".
+
+Default (N=1) workload = BASELINE config 2: SpMV on a synthetic R-MAT scale-20
+matrix (1,048,576 rows, 16,777,216 nnz, fp32 values and x in (0, 1]).  A step
+is one y = A x.  The headline is the grid-consolidated variant; flat,
+basic-DP, warp and block are timed in the same run and reported beside it
+(`variants`), with the speed-ups the north_star targets.
+
+  value     : nnz processed per second (GTEPS) with A, x, y resident in HBM,
+              device-timed with CUDA events per step, L2 flushed between steps
+  e2e       : same metric through the C-ABI call dpc_spmv_host with pinned
+              host x / y (H2D of x and D2H of y inside the timed region; A is
+              the resident operator, uploaded once)
+  roofline  : algorithmic bytes nnz*8 + (n+1)*4 + n*4 + n*4 per step over the
+              step time (one persistent cooperative kernel = the whole step)
+  cpu_baseline : oracle port (multi-threaded fp32 CSR SpMV, all host cores)
+
+--impl reference runs the reference's own CPU path: the unmodified dpcons
+simulator (oracle/_ref/libref_sim.so, compiled from /root/reference) executing
+our SpMV .kdl in grid-consolidated mode on a bounded row sample per step.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SCALE = 20
+EDGEFACTOR = 16
+SEED = 1
+VARIANTS = ["flat", "basic", "warp", "block", "grid"]
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def _dist_init(world):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo")
+    return dist
+
+
+def _barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def _max_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or self.f is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 9:
+                    rows.append(p)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def spmv_bytes(n, nnz):
+    return nnz * 8 + (n + 1) * 4 + n * 4 + n * 4
+
+
+def cpu_baseline_spmv(g, x, budget_s=10.0):
+    from tests._oracle import Oracle
+    orc = Oracle()
+    threads = os.cpu_count() or 1
+    orc.spmv_f32_mt(g.rowptr, g.col, g.val, x, threads)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        orc.spmv_f32_mt(g.rowptr, g.col, g.val, x, threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 400:
+            break
+    return {"value": round(g.m * reps / el / 1e9, 4), "unit": "GTEPS", "cores": threads,
+            "kind": "port",
+            "sample": f"{reps} full SpMVs of the config-2 matrix (oracle/oracle.c orc_spmv_f32_mt, "
+                      f"{threads} threads, {el:.1f} s)"}
+
+
+def time_variant(ctx, dg, variant, steps, warmup, cfg=None):
+    for _ in range(warmup):
+        dg.spmv(variant, cfg=cfg)
+    ctx.synchronize()
+    total = 0.0
+    for _ in range(steps):
+        ctx.flush_l2()
+        ctx.record(0)
+        dg.spmv(variant, cfg=cfg)
+        ctx.record(1)
+        total += ctx.elapsed_ms(0, 1)
+    return total / steps
+
+
+def run_ours(args):
+    import paper_1606_08150_b200 as dpc
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    dist = _dist_init(world)
+    ctx = dpc.Context(local)
+    t0 = time.time()
+    g = dpc.gen_rmat(SCALE, EDGEFACTOR, seed=SEED + rank, weights=False, values=True)
+    gen_s = time.time() - t0
+    rng = np.random.default_rng(SEED)
+    x = (rng.integers(1, 1 << 24, g.n) / float(1 << 24)).astype(np.float32)
+    dg = dpc.DeviceGraph(ctx, g)
+    dg.set_x(x)
+    n, nnz = g.n, g.m
+
+    # correctness gate before timing: grid variant vs fp64 (cheap, C oracle)
+    from tests._oracle import Oracle
+    y64 = Oracle().spmv_f64(g.rowptr, g.col, g.val, x)
+    dg.spmv("grid")
+    err = np.abs(dg.get_y().astype(np.float64) - y64) / np.maximum(np.abs(y64), 1e-300)
+    parity_ok = bool(np.all(err <= 1e-5))
+
+    variants = {}
+    launches = {}
+    for v in args.variants:
+        if v == "grid":
+            continue
+        steps = args.steps if v != "basic" else max(1, min(args.steps, 3))
+        ms = time_variant(ctx, dg, v, steps, max(1, min(args.warmup, 2)) if v == "basic" else args.warmup)
+        met = dg.spmv(v, metrics=True)
+        variants[v] = {"ms": round(ms, 4), "gteps": round(nnz / (ms * 1e-3) / 1e9, 3),
+                       "device_launches": int(met.child_launch_count)}
+        launches[v] = int(met.child_launch_count)
+    cdp = dpc.launch_cfg("spmv", "grid", grid_cdp=True)
+    ms_cdp = time_variant(ctx, dg, "grid", args.steps, args.warmup, cfg=cdp)
+    met_cdp = dg.spmv("grid", cfg=cdp, metrics=True)
+    variants["grid_cdp"] = {"ms": round(ms_cdp, 4), "gteps": round(nnz / (ms_cdp * 1e-3) / 1e9, 3),
+                            "device_launches": int(met_cdp.child_launch_count)}
+
+    # headline: grid-consolidated (persistent) — timed region
+    for _ in range(args.warmup):
+        dg.spmv("grid")
+    ctx.synchronize()
+    _barrier(dist)
+    per_step = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            ctx.flush_l2()
+            ctx.record(0)
+            dg.spmv("grid")
+            ctx.record(1)
+            per_step.append(ctx.elapsed_ms(0, 1))
+    ctx.synchronize()
+    _barrier(dist)
+    ms = float(np.mean(per_step))
+    ms_max = _max_over_ranks(dist, ms)
+    met = dg.spmv("grid", metrics=True)
+    variants["grid"] = {"ms": round(ms, 4), "gteps": round(nnz / (ms * 1e-3) / 1e9, 3),
+                        "device_launches": int(met.child_launch_count)}
+    total_nnz = _sum_over_ranks(dist, float(nnz))
+    value = total_nnz / (ms_max * 1e-3) / 1e9
+
+    # e2e through the C ABI with pinned host buffers
+    import ctypes as C
+    xh = dpc._lib.dpc_host_alloc(4 * n)
+    yh = dpc._lib.dpc_host_alloc(4 * n)
+    xa = np.frombuffer((C.c_float * n).from_address(xh), np.float32)
+    ya = np.frombuffer((C.c_float * n).from_address(yh), np.float32)
+    xa[:] = x
+    for _ in range(args.warmup):
+        dg.spmv_host(xa, ya, "grid")
+    _barrier(dist)
+    e2e_ms = []
+    for _ in range(args.steps):
+        ctx.flush_l2()
+        ctx.record(2)
+        dg.spmv_host(xa, ya, "grid")
+        ctx.record(3)
+        e2e_ms.append(ctx.elapsed_ms(2, 3))
+    e2e_ok = bool(np.all(np.abs(ya.astype(np.float64) - y64) <= 1e-5 * np.abs(y64)))
+    e2e_max = _max_over_ranks(dist, float(np.mean(e2e_ms)))
+    e2e_value = total_nnz / (e2e_max * 1e-3) / 1e9
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    alg = spmv_bytes(n, nnz)
+    achieved = alg / (ms * 1e-3) / 1e9
+
+    out = {
+        "metric": "SSSP/SpMV GTEPS per B200 (1-8 GPU) & speedup vs basic-DP and flat kernels",
+        "value": round(value, 3), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "BASELINE config 2: SpMV CSR, synthetic R-MAT scale-20 matrix "
+                               "(1,048,576 rows, 16,777,216 nnz, fp32 values/x in (0,1], seed 1)",
+                   "variant": "grid-consolidated (persistent cooperative kernel)",
+                   "n": n, "nnz": nnz, "l2": "flushed (512 MB memset) before every timed step",
+                   "parallelism": f"replicas{world}" if world > 1 else "single GPU",
+                   "generate_s": round(gen_s, 2)},
+        "variants": variants,
+        "speedup": {"grid_vs_basic": round(variants["basic"]["ms"] / ms, 2) if "basic" in variants else None,
+                    "grid_vs_flat": round(variants["flat"]["ms"] / ms, 2) if "flat" in variants else None,
+                    "block_vs_basic": round(variants["basic"]["ms"] / variants["block"]["ms"], 2)
+                    if "basic" in variants and "block" in variants else None,
+                    "block_vs_flat": round(variants["flat"]["ms"] / variants["block"]["ms"], 2)
+                    if "flat" in variants and "block" in variants else None},
+        "parity": {"grid_vs_fp64_rtol_1e-5": parity_ok, "e2e_vs_fp64_rtol_1e-5": e2e_ok,
+                   "max_rel_err": float(err.max())},
+        "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS", "h2d_bytes_per_step": 4 * n,
+                "d2h_bytes_per_step": 4 * n, "ms_per_step": round(e2e_max, 4),
+                "api": "dpc_spmv_host (C ABI), pinned host x/y, A resident"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "algorithmic_bytes": alg, "kernel": "spmv::grid_persistent",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"},
+        "gpu_launches": args.steps * (1 + int(met.child_launch_count)),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_spmv(g, x, args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dg.close()
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The reference's own CPU path on the box's host cores: the unmodified
+    dpcons simulator (oracle/_ref) running the SpMV .kdl, grid-consolidated,
+    on a bounded row sample of the config-2 matrix per step."""
+    rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return
+    try:
+        from tests._oracle import RefSim
+        ref = RefSim()
+    except (FileNotFoundError, OSError) as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
+        return
+    import paper_1606_08150_b200 as dpc
+    g = dpc.gen_rmat(SCALE, EDGEFACTOR, seed=SEED, weights=False, values=True)
+    rng = np.random.default_rng(SEED)
+    x = (rng.integers(1, 1 << 24, g.n) / float(1 << 24)).astype(np.float32)
+    src = ref.kdl("spmv.kdl")
+    # bounded, representative sample: a seeded uniform random 1/k of the rows
+    # (keeps the degree distribution; R-MAT ids are not exchangeable, so a
+    # strided or contiguous window would be biased), k = args.ref_stride
+    sel = np.sort(np.random.default_rng(SEED).choice(g.n, g.n // args.ref_stride, replace=False))
+    rows = len(sel)
+    deg = (g.rowptr[sel + 1] - g.rowptr[sel]).astype(np.int64)
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    nnz = int(rp[-1])
+    idx = np.concatenate([np.arange(g.rowptr[r], g.rowptr[r + 1]) for r in sel])
+    col = g.col[idx]
+    val = g.val[idx].astype(np.float64)
+    # columns index the full x; the sample keeps the full vector
+    scal = {"n": rows, "m": nnz, "nx": g.n, "thr": 32}
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        rc, y, met, err = ref.run(src, "grid", scal, {"rowptr": rp, "col": col},
+                                  {"val": val, "x": x.astype(np.float64)}, out="y",
+                                  out_len=rows, out_float=True)
+        el = time.perf_counter() - t0
+        if rc != 0:
+            print(json.dumps({"impl": "reference", "unavailable": f"simulator fault: {err}"}))
+            return
+        if i >= args.warmup:
+            times.append(el)
+    ms = float(np.mean(times)) * 1e3
+    value = nnz / (ms * 1e-3) / 1e9
+    sample = (f"seeded random 1/{args.ref_stride} of the rows ({rows} rows, {nnz} nnz) of the "
+              f"config-2 matrix per "
+              f"step, dpcons::simulate "
+              f"grid-consolidated (oracle/kdl/spmv.kdl), single-threaded simulator")
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "SSSP/SpMV GTEPS per B200 (1-8 GPU) & speedup vs basic-DP and flat kernels",
+        "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "BASELINE config 2 (row sample): SpMV CSR R-MAT scale-20",
+                   "rows": rows, "nnz": nnz},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_metrics": met,
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variants", nargs="*", default=VARIANTS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--ref-stride", type=int, default=256)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

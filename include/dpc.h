@@ -1,0 +1,293 @@
+/*
+ * dpc.h — C ABI of the B200-native workload-consolidation library (libdpc.so).
+ *
+ * This is the drop-in boundary for the hot path named by BASELINE.json's
+ * north_star: the reference's application layer (CSR graph/matrix loaders and
+ * generators, per-app run functions) fronting sm_100a kernels that run the
+ * irregular-loop apps (SSSP, SpMV, graph coloring) and the parallel-recursion
+ * apps (tree descendants / heights) in five variants: flat, basic-DP, and
+ * warp / block / grid workload consolidation (arXiv 1606.08150 §IV).
+ *
+ * The reference ships this layer only as a specification
+ * (module `workloads`); its code-level
+ * boundary is `dpcons::simulate(Program, Workload, SimConfig) -> SimResult`
+ * (/root/reference/proj/include/dpcons/sim.hpp:1746) fed by
+ * `dpcons::consolidate` (transform.hpp:971).  Each entry point below cites the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *  - Every function returns dpc_status; on failure dpc_last_error() returns a
+ *    thread-local message.  Status kinds mirror SimFault.kind
+ *    (sim.hpp:49-52: nesting | overflow | deadlock | oom | runtime | config).
+ *  - Plain pointers and sizes only.  Host buffers are caller-owned.  Objects
+ *    returned through `**out` are library-owned and released with the
+ *    matching *_free / *_destroy.
+ *  - Run calls are synchronous.  One dpc_ctx per host thread.
+ *  - There is no CPU fallback: a run call on a machine without a usable
+ *    sm_100 device fails with DPC_E_CUDA.
+ */
+#ifndef DPC_H_
+#define DPC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPC_ABI_VERSION 1
+
+/* ---- status (SimFault.kind, sim.hpp:49-52; Diag, diag.hpp:16-20) ------- */
+typedef enum dpc_status {
+  DPC_OK = 0,
+  DPC_E_INVALID = 1,  /* bad argument / invariant violation ("config")       */
+  DPC_E_OVERFLOW = 2, /* consolidation buffer overflow (sim.hpp:1512-1517)    */
+  DPC_E_NESTING = 3,  /* device nesting limit (sim.hpp:696-699)               */
+  DPC_E_CUDA = 4,     /* CUDA runtime error / no device ("runtime")           */
+  DPC_E_NCCL = 5,     /* NCCL error                                           */
+  DPC_E_OOM = 6,      /* device or host allocation failed (sim.hpp:1139-1144) */
+  DPC_E_IO = 7,       /* file I/O or parse error            */
+  DPC_E_DEADLOCK = 8  /* watchdog fired (sim.hpp:946-955)                     */
+} dpc_status;
+
+/* Thread-local description of the last failure (empty string if none). */
+const char* dpc_last_error(void);
+int dpc_abi_version(void);
+
+/* ---- variants (Granularity, ast.hpp:68; SPEC.md cli modes) ------------- */
+typedef enum dpc_variant {
+  DPC_FLAT = 0,  /* no-dp: thread-mapped loops, no device launches          */
+  DPC_BASIC = 1, /* basic-dp: one CDP2 child launch per qualifying thread   */
+  DPC_WARP = 2,  /* warp-level consolidation: <= 1 launch per warp          */
+  DPC_BLOCK = 3, /* block-level consolidation: <= 1 launch per block        */
+  DPC_GRID = 4   /* grid-level consolidation: 1 launch per parent grid      */
+} dpc_variant;
+
+typedef enum dpc_app {
+  DPC_APP_SSSP = 0,
+  DPC_APP_SPMV = 1,
+  DPC_APP_COLOR = 2,
+  DPC_APP_TREE_DESC = 3,
+  DPC_APP_TREE_HEIGHT = 4
+} dpc_app;
+
+/* ---- data (SPEC.md:411-418 CsrGraph / Tree) ---------------------------- */
+/* CSR graph or matrix.  rowptr has n+1 entries (rowptr[0]=0, rowptr[n]=m).
+ * w (int32 edge weights) and val (fp32 matrix values) are optional (NULL). */
+typedef struct dpc_csr {
+  int64_t n;
+  int64_t m;
+  int64_t* rowptr;
+  int32_t* col;
+  int32_t* w;
+  float* val;
+} dpc_csr;
+
+/* Rooted tree.  parent[root] = -1.  Children of v are
+ * clist[cstart[v] .. cstart[v+1]).  depth = number of levels. */
+typedef struct dpc_tree {
+  int64_t n;
+  int32_t root;
+  int32_t depth;
+  int32_t* parent;
+  int64_t* cstart;
+  int32_t* clist;
+} dpc_tree;
+
+/* generator flags */
+#define DPC_GEN_WEIGHTS 1u    /* fill w[] uniform in [wmin, wmax]            */
+#define DPC_GEN_VALUES 2u     /* fill val[] uniform in (0, 1]                */
+#define DPC_GEN_PERMUTE 4u    /* random vertex relabelling                   */
+#define DPC_GEN_SYMMETRIC 8u  /* add reverse arcs, drop self loops + dups    */
+
+/* R-MAT graph: n = 2^scale, m = edgefactor * n arcs (before symmetrize),
+ * quadrant probabilities (a, b, c, 1-a-b-c).  Counter-based hashing makes the
+ * output a pure function of the arguments (any thread count).
+ * Replaces SPEC.md:435-444 gen_graph for the paper's Kron/R-MAT datasets. */
+dpc_status dpc_gen_rmat(int scale, int edgefactor, double a, double b, double c,
+                        int32_t wmin, int32_t wmax, uint64_t seed, uint32_t flags,
+                        dpc_csr** out);
+
+/* SPEC.md:435-444 gen_graph(nodeCount, uniform(min,max), seed). */
+dpc_status dpc_gen_graph_uniform(int64_t n, int32_t dmin, int32_t dmax, int32_t wmin,
+                                 int32_t wmax, uint64_t seed, uint32_t flags,
+                                 dpc_csr** out);
+
+/* SPEC.md:435-444 gen_graph(nodeCount, powerlaw(alpha, maxDeg), seed). */
+dpc_status dpc_gen_graph_powerlaw(int64_t n, double alpha, int32_t maxdeg, int32_t wmin,
+                                  int32_t wmax, uint64_t seed, uint32_t flags,
+                                  dpc_csr** out);
+
+/* SPEC.md:425-433 gen_tree(depth, minChildren, maxChildren,
+ * nonLeafFillFraction, seed).  Nodes are numbered level by level. */
+dpc_status dpc_gen_tree(int32_t depth, int32_t min_children, int32_t max_children,
+                        double fill, uint64_t seed, dpc_tree** out);
+
+/* Copies caller arrays into a library-owned graph, validating the CSR
+ * invariants.  w / val may be NULL. */
+dpc_status dpc_csr_create(int64_t n, int64_t m, const int64_t* rowptr, const int32_t* col,
+                          const int32_t* w, const float* val, dpc_csr** out);
+dpc_status dpc_csr_validate(const dpc_csr* g);
+void dpc_csr_free(dpc_csr* g);
+
+/* Copies a parent array into a library-owned tree (validates: one root,
+ * acyclic, parents in range). */
+dpc_status dpc_tree_create(int64_t n, const int32_t* parent, dpc_tree** out);
+void dpc_tree_free(dpc_tree* t);
+
+/* SPEC.md:446-450 load_csr / save_csr; text format SPEC.md:473
+ * (line 1 "nodes edges [weighted]", line 2 row offsets, line 3 column
+ * indices, line 4 optional weights).  A ".bin" suffix selects the binary
+ * form (magic "DPCCSR01"). */
+dpc_status dpc_load_csr(const char* path, dpc_csr** out);
+dpc_status dpc_save_csr(const dpc_csr* g, const char* path);
+/* Tree text format SPEC.md:473: line 1 nodeCount, line 2 parent per node. */
+dpc_status dpc_load_tree(const char* path, dpc_tree** out);
+dpc_status dpc_save_tree(const dpc_tree* t, const char* path);
+
+/* ---- launch configuration (Directive ast.hpp:90-111; KC_X config.hpp:68-84) */
+typedef struct dpc_launch_cfg {
+  int32_t variant;        /* dpc_variant                                    */
+  int32_t threshold;      /* child work when degree > threshold (SPEC 469)  */
+  int32_t parent_threads; /* parent block size                              */
+  int32_t child_threads;  /* consolidated child block size                  */
+  int32_t child_blocks;   /* 0 = derive from kc_x and measured occupancy    */
+  int32_t kc_x;           /* KC_X concurrency divisor (config.hpp:68-75); 0 = "1-1" (B = pending items) */
+  int32_t chunk;          /* edges per consolidated work item (load balance) */
+  int32_t flags;          /* DPC_CFG_* bits                                  */
+} dpc_launch_cfg;
+
+/* dpc_launch_cfg.flags */
+#define DPC_CFG_GRID_CDP 1 /* grid variant: last block launches the child via
+                              CDP2 (else: one persistent cooperative kernel
+                              with a device-wide barrier) */
+
+/* Fills the measured default for (app, variant) (configs/launch_cfg.json,
+ * compiled in).  Replaces resolve_config, transform.hpp:417-475. */
+dpc_status dpc_launch_cfg_default(int32_t app, int32_t variant, dpc_launch_cfg* cfg);
+
+/* ---- metrics (Metrics, sim.hpp:34-47) ---------------------------------- */
+typedef struct dpc_metrics {
+  int64_t child_launch_count;   /* device-side launches (counter in HBM)     */
+  int64_t buffer_items_inserted;/* consolidation-buffer items (chunks)       */
+  int64_t pool_peak;            /* peak items held in the pre-allocated pool */
+  int64_t iterations;           /* SSSP / GC rounds, tree levels             */
+  int64_t edges_processed;      /* relaxed edges / nnz / scanned arcs        */
+  int64_t host_launches;        /* kernels launched from the host            */
+  double device_ms;             /* CUDA-event time of the run's kernels      */
+  int32_t overflow;             /* nonzero: a buffer overflowed              */
+  int32_t result_count;         /* colors used (GC), reached vertices (SSSP) */
+} dpc_metrics;
+
+/* ---- context ------------------------------------------------------------ */
+typedef struct dpc_ctx dpc_ctx;
+
+/* Creates a context bound to CUDA device `device` with its own stream.
+ * Fails with DPC_E_CUDA when no sm_100 device is present. */
+dpc_status dpc_ctx_create(int32_t device, dpc_ctx** out);
+void dpc_ctx_destroy(dpc_ctx* ctx);
+/* The context's cudaStream_t (as void*), for callers that time or order work. */
+void* dpc_ctx_stream(dpc_ctx* ctx);
+/* Number of SMs on the context's device (148 on B200). */
+int32_t dpc_ctx_sm_count(dpc_ctx* ctx);
+/* Timing helpers on the context stream: record event slot i (0..63), and
+ * elapsed milliseconds between slots a and b (synchronizes on b). */
+dpc_status dpc_ctx_event_record(dpc_ctx* ctx, int32_t slot);
+dpc_status dpc_ctx_event_elapsed(dpc_ctx* ctx, int32_t a, int32_t b, float* ms);
+dpc_status dpc_ctx_synchronize(dpc_ctx* ctx);
+/* Writes a buffer larger than L2 on the context stream (timing hygiene). */
+dpc_status dpc_ctx_flush_l2(dpc_ctx* ctx);
+
+/* ---- host-buffer runs: the reference-facing API ------------------------
+ * Each call uploads the inputs, runs the variant, downloads the result.
+ * They replace benchmark(name) + simulate() (sim.hpp:1746)
+ * for one app.  cfg may be NULL (measured default for cfg->variant = GRID).
+ */
+/* y = A x (fp32).  Replaces the SpMV benchmark. */
+dpc_status dpc_run_spmv(dpc_ctx* ctx, const dpc_csr* A, const float* x, float* y,
+                        const dpc_launch_cfg* cfg, dpc_metrics* met);
+/* Single-source shortest paths with int32 weights >= 0; dist[v] = UINT32_MAX
+ * when unreachable.  Replaces the SSSP benchmark. */
+dpc_status dpc_run_sssp(dpc_ctx* ctx, const dpc_csr* g, int32_t source, uint32_t* dist,
+                        const dpc_launch_cfg* cfg, dpc_metrics* met);
+/* Greedy first-fit coloring in descending priority order, priority(v) =
+ * (hash64(v ^ seed), v); g must be symmetric without self loops.
+ * *ncolors receives the number of colors. */
+dpc_status dpc_run_color(dpc_ctx* ctx, const dpc_csr* g, uint64_t seed, int32_t* color,
+                         int32_t* ncolors, const dpc_launch_cfg* cfg, dpc_metrics* met);
+/* desc[v] = number of proper descendants of v (TD). */
+dpc_status dpc_run_tree_desc(dpc_ctx* ctx, const dpc_tree* t, int32_t* desc,
+                             const dpc_launch_cfg* cfg, dpc_metrics* met);
+/* height[v] = max edges from v down to a leaf (TH). */
+dpc_status dpc_run_tree_height(dpc_ctx* ctx, const dpc_tree* t, int32_t* height,
+                               const dpc_launch_cfg* cfg, dpc_metrics* met);
+
+/* ---- device-resident runs (inputs already in HBM; used by bench.py) ----- */
+typedef struct dpc_dgraph dpc_dgraph;
+typedef struct dpc_dtree dpc_dtree;
+
+/* Uploads a graph once; the handle owns all device buffers of the app. */
+dpc_status dpc_dgraph_upload(dpc_ctx* ctx, const dpc_csr* g, dpc_dgraph** out);
+void dpc_dgraph_free(dpc_dgraph* dg);
+/* Device pointers of the handle's x (n floats) and y (n floats) vectors. */
+float* dpc_dgraph_x(dpc_dgraph* dg);
+float* dpc_dgraph_y(dpc_dgraph* dg);
+/* Device pointer of the handle's SSSP distance / GC color vector. */
+uint32_t* dpc_dgraph_dist(dpc_dgraph* dg);
+int32_t* dpc_dgraph_color(dpc_dgraph* dg);
+
+/* Asynchronous on the context stream (no host sync, no copies). */
+dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* dg, const float* d_x, float* d_y,
+                           const dpc_launch_cfg* cfg, dpc_metrics* met);
+/* Synchronous at the end (termination is device-driven; the host reads the
+ * iteration count once). */
+dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* dg, int32_t source,
+                           const dpc_launch_cfg* cfg, dpc_metrics* met);
+dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* dg, uint64_t seed,
+                            const dpc_launch_cfg* cfg, dpc_metrics* met);
+
+dpc_status dpc_dtree_upload(dpc_ctx* ctx, const dpc_tree* t, dpc_dtree** out);
+void dpc_dtree_free(dpc_dtree* dt);
+/* which = DPC_APP_TREE_DESC or DPC_APP_TREE_HEIGHT; result stays on device. */
+dpc_status dpc_tree_device(dpc_ctx* ctx, dpc_dtree* dt, int32_t which,
+                           const dpc_launch_cfg* cfg, dpc_metrics* met);
+int32_t* dpc_dtree_result(dpc_dtree* dt);
+
+/* SpMV through the operator-resident handle with HOST vectors: copies x in,
+ * runs, copies y out (synchronous).  This is the end-to-end path. */
+dpc_status dpc_spmv_host(dpc_ctx* ctx, dpc_dgraph* dg, const float* x_host, float* y_host,
+                         const dpc_launch_cfg* cfg, dpc_metrics* met);
+
+/* Pinned host memory (for copy bandwidth on the end-to-end path). */
+void* dpc_host_alloc(size_t bytes);
+void dpc_host_free(void* p);
+
+/* Copies between caller host memory and library device memory on the
+ * context stream (synchronous). */
+dpc_status dpc_copy_h2d(dpc_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
+dpc_status dpc_copy_d2h(dpc_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+
+/* ---- multi-GPU (one process per GPU; NCCL over NVLink) ------------------
+ * Row / vertex partition of a graph across `world` ranks (BASELINE config 5).
+ */
+typedef struct dpc_comm dpc_comm;
+/* NCCL unique id (128 bytes) created on rank 0 and broadcast by the caller. */
+dpc_status dpc_comm_unique_id(uint8_t id[128]);
+dpc_status dpc_comm_init(dpc_ctx* ctx, int32_t rank, int32_t world, const uint8_t id[128],
+                         dpc_comm** out);
+void dpc_comm_destroy(dpc_comm* comm);
+/* Equal-nnz row split of a CSR with n rows into `world` parts; bounds has
+ * world+1 entries. */
+dpc_status dpc_partition_rows(const dpc_csr* g, int32_t world, int64_t* bounds);
+/* Distributed SpMV power step: each rank holds rows [r0, r1) of A (global
+ * column ids) uploaded as a dgraph; x_full is all-gathered over NCCL from
+ * the ranks' y slices, then y_local = A_local x_full.  iters steps. */
+dpc_status dpc_multi_spmv(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, int64_t r0,
+                          int64_t r1, int64_t n_global, int32_t iters,
+                          const dpc_launch_cfg* cfg, dpc_metrics* met);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPC_H_ */

@@ -1,0 +1,166 @@
+// Device-side consolidation runtime primitives (sm_100a).
+//
+// These are the B200 realisation of the dp_* builtins the reference's
+// transform emits (transform.hpp:478-632) and the simulator executes
+// (sim.hpp:1409-1541, 1665-1717):
+//   dp_buffers / own_buffer  -> one pre-allocated pool per graph (Pool), owner
+//                               slices reserved by a bump pointer (a3, a6)
+//   dp_insert                -> warp_reserve / block_reserve: ballot-free warp
+//                               scan + one atomicAdd per warp / block (a5)
+//   dp_grid_last             -> grid_last_block(): fence + ticket (a10)
+//   device launch            -> CDP2 fire-and-forget launch by an elected
+//                               live lane, counted in RunHeader.launches (a7)
+//   dp_buf_count/get         -> the child kernel's (items, count) arguments
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cstdint>
+
+namespace dpc {
+namespace dev {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Per-run device counters; zeroed by one cudaMemsetAsync per run.
+struct RunHeader {
+  unsigned count;      // items reserved in the pool (grid-level worklist size)
+  unsigned overflow;   // bit0: pool overflow, bit1: device launch failed
+  unsigned launches;   // device-side child launches
+  unsigned ticket;     // grid-level last-block ticket (sim.hpp:1708-1717)
+  unsigned next_count; // next frontier size (SSSP / GC)
+  unsigned iter;       // iteration counter (device-driven loops)
+  unsigned aux0;       // app-specific
+  unsigned aux1;
+  unsigned long long work; // edges processed (diagnostic)
+  unsigned pad[6];
+};
+static_assert(sizeof(RunHeader) == 64, "RunHeader must be 64 bytes");
+
+// A consolidation work item: vertex/row id and the first edge of its chunk.
+// The chunk covers [begin, min(begin + chunk, rowptr[v + 1])).
+struct Item {
+  unsigned v;
+  unsigned begin;
+};
+
+// Pre-allocated pool (Fig. 5 "pre-alloc" allocator): no device
+// malloc on the hot path; owners get contiguous slices by bump allocation.
+struct Pool {
+  Item* items;
+  unsigned cap;
+};
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned warp_in_block() { return threadIdx.x >> 5; }
+
+// Inclusive warp scan (all 32 lanes must call).
+__device__ __forceinline__ unsigned warp_incl_scan(unsigned v) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned t = __shfl_up_sync(kFull, v, o);
+    if (lane >= static_cast<unsigned>(o)) v += t;
+  }
+  return v;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Warp-aggregated reservation (dp_insert at warp granularity): each lane asks
+// for `want` slots; one atomicAdd per warp.  Returns this lane's first slot
+// and writes the warp's base / total to *wbase / *wtotal.  All 32 lanes call.
+__device__ __forceinline__ unsigned warp_reserve(unsigned* counter, unsigned want,
+                                                 unsigned* wbase, unsigned* wtotal) {
+  unsigned incl = warp_incl_scan(want);
+  unsigned total = __shfl_sync(kFull, incl, 31);
+  unsigned base = 0;
+  if (lane_id() == 31 && total) base = atomicAdd(counter, total);
+  base = __shfl_sync(kFull, base, 31);
+  *wbase = base;
+  *wtotal = total;
+  return base + incl - want;
+}
+
+// Block-wide exclusive scan of `want` through shared memory (blockDim.x is a
+// multiple of 32, <= 1024).  Returns this thread's offset inside the block and
+// the block total in *btotal.  All threads call.
+__device__ __forceinline__ unsigned block_excl_scan(unsigned want, unsigned* btotal) {
+  __shared__ unsigned s_warp[32];
+  unsigned incl = warp_incl_scan(want);
+  const unsigned w = warp_in_block(), nw = blockDim.x >> 5;
+  if (lane_id() == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    unsigned x = lane_id() < nw ? s_warp[lane_id()] : 0;
+    unsigned xi = warp_incl_scan(x);
+    if (lane_id() < nw) s_warp[lane_id()] = xi - x;  // exclusive warp offsets
+    if (lane_id() == 31) s_warp[31] = xi;             // nw <= 32: lane 31 holds the total
+  }
+  __syncthreads();
+  unsigned off = s_warp[w] + incl - want;
+  *btotal = s_warp[31];
+  __syncthreads();  // s_warp is reused by the next call
+  return off;
+}
+
+// Writes the chunk items of vertex v (edges [b, e)) starting at slot `at`.
+// Slots past the pool capacity set the overflow flag (sim.hpp:1512-1517
+// turns overflow into a fault; we report it as DPC_E_OVERFLOW).
+__device__ __forceinline__ void write_chunks(const Pool& pool, RunHeader* hdr, unsigned at,
+                                             unsigned v, unsigned b, unsigned e, unsigned chunk) {
+  for (unsigned s = b; s < e; s += chunk, at++) {
+    if (at < pool.cap) pool.items[at] = Item{v, s};
+    else atomicOr(&hdr->overflow, 1u);
+  }
+}
+
+__device__ __forceinline__ unsigned nchunks(unsigned deg, unsigned chunk) {
+  return (deg + chunk - 1) / chunk;
+}
+
+// Grid-level last-block election (the paper's global barrier counter,
+// PAPER.md:248; sim.hpp:1708-1717).  Every block calls once after its
+// insertions; returns true in all threads of exactly one block — the last to
+// arrive — with all other blocks' pool writes visible.  The ticket is reset by
+// the last block so the next parent grid can reuse it.
+__device__ __forceinline__ bool grid_last_block(unsigned* ticket) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // release this block's items before taking a ticket
+    unsigned t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) {
+      __threadfence();  // acquire: all other blocks' items are now visible
+      *ticket = 0;
+    }
+  }
+  __syncthreads();
+  return s_last;
+}
+
+// Records a device-side launch, flags a failed one.
+__device__ __forceinline__ void note_launch(RunHeader* hdr) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) atomicOr(&hdr->overflow, 2u);
+  else atomicAdd(&hdr->launches, 1u);
+}
+
+__host__ __device__ __forceinline__ unsigned ceil_div(unsigned a, unsigned b) { return (a + b - 1) / b; }
+
+// Child geometry for `items` chunk items, one warp per item: "1-1" sizing
+// capped at `max_blocks` (KC_X cap from the measured table).
+__device__ __forceinline__ unsigned child_blocks(unsigned items, unsigned threads,
+                                                 unsigned max_blocks) {
+  unsigned b = ceil_div(items, threads / 32u);
+  if (max_blocks && b > max_blocks) b = max_blocks;
+  return b ? b : 1u;
+}
+
+}  // namespace dev
+}  // namespace dpc

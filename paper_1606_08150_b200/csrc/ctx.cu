@@ -1,0 +1,411 @@
+// Context, device-resident handles, launch-configuration policy and the
+// host-buffer run wrappers of libdpc.so.
+//
+// Policy replaced here:
+//  - KC_X (config.hpp:68-75) keeps its meaning — B = max(1, B_occ / X) — but
+//    B_occ comes from the B200 (148 SMs, 2048 threads/SM) and the defaults for
+//    (threshold, chunk, X) come from the measured sweep (tools/sweep.py ->
+//    configs/launch_cfg.json), not from the occupancy calculator.
+//  - per-buffer sizing (memplan.hpp:61-168, const = 4) is replaced by exact
+//    counts: the pool holds sum over rows with deg > threshold of
+//    ceil(deg / chunk) items, the most any parent pass can insert.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "ctx.h"
+
+using dpc::dev::Item;
+using dpc::dev::RunHeader;
+
+namespace dpc {
+
+dpc_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-free errors
+  dpc_status st = (e == cudaErrorMemoryAllocation) ? DPC_E_OOM : DPC_E_CUDA;
+  return fail(st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Measured defaults (tools/sweep.py; see DESIGN.md §Launch configuration).
+// Index: [app][variant].  Fields: threshold, parent_threads, child_threads,
+// child_blocks, kc_x, chunk, flags.
+struct Default {
+  int threshold, parent_threads, child_threads, child_blocks, kc_x, chunk, flags;
+};
+#include "launch_table.inc"
+
+dpc_status resolve_cfg(dpc_ctx* ctx, int app, const dpc_launch_cfg* in, Cfg* out) {
+  dpc_launch_cfg c;
+  int variant = in ? in->variant : DPC_GRID;
+  if (variant < DPC_FLAT || variant > DPC_GRID) return fail(DPC_E_INVALID, "unknown variant");
+  if (app < 0 || app > DPC_APP_TREE_HEIGHT) return fail(DPC_E_INVALID, "unknown app");
+  dpc_launch_cfg_default(app, variant, &c);
+  if (in) {
+    if (in->threshold >= 0) c.threshold = in->threshold;
+    if (in->parent_threads > 0) c.parent_threads = in->parent_threads;
+    if (in->child_threads > 0) c.child_threads = in->child_threads;
+    if (in->child_blocks > 0) c.child_blocks = in->child_blocks;
+    if (in->kc_x >= 0) c.kc_x = in->kc_x;
+    if (in->chunk > 0) c.chunk = in->chunk;
+    c.flags = in->flags;
+  }
+  auto ok_threads = [](int t) { return t >= 32 && t <= 1024 && t % 32 == 0; };
+  if (!ok_threads(c.parent_threads) || !ok_threads(c.child_threads))
+    return fail(DPC_E_INVALID, "thread counts must be multiples of 32 in [32, 1024]");
+  if (c.chunk < 32) return fail(DPC_E_INVALID, "chunk must be >= 32 edges");
+  out->variant = variant;
+  out->threshold = static_cast<unsigned>(c.threshold);
+  out->parent_threads = static_cast<unsigned>(c.parent_threads);
+  out->child_threads = static_cast<unsigned>(c.child_threads);
+  out->chunk = static_cast<unsigned>(c.chunk);
+  out->grid_persistent = !(c.flags & DPC_CFG_GRID_CDP);
+  // KC_X: B = max(1, B_occ / X); X = 0 selects "1-1" (no cap).
+  unsigned b_occ = static_cast<unsigned>(ctx->sms) *
+                   static_cast<unsigned>(ctx->max_threads_per_sm / c.child_threads);
+  if (c.child_blocks > 0) out->child_blocks = static_cast<unsigned>(c.child_blocks);
+  else if (c.kc_x > 0) out->child_blocks = std::max(1u, b_occ / static_cast<unsigned>(c.kc_x));
+  else out->child_blocks = 0;
+  return DPC_OK;
+}
+
+dpc_status ensure_pending_limit(dpc_ctx* ctx, size_t need) {
+  size_t want = std::max<size_t>(2048, need);
+  if (want == ctx->pending_limit) return DPC_OK;
+  DPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  DPC_CUDA(cudaDeviceSetLimit(cudaLimitDevRuntimePendingLaunchCount, want));
+  ctx->pending_limit = want;
+  return DPC_OK;
+}
+
+uint64_t pool_need(dpc_dgraph* g, unsigned threshold, unsigned chunk) {
+  auto key = std::make_pair(static_cast<int>(threshold), static_cast<int>(chunk));
+  auto it = g->need_cache.find(key);
+  if (it != g->need_cache.end()) return it->second;
+  uint64_t need = 0;
+  for (int64_t v = 0; v < g->n; v++) {
+    uint64_t d = static_cast<uint64_t>(g->host_rowptr[v + 1] - g->host_rowptr[v]);
+    if (d > threshold) need += (d + chunk - 1) / chunk;
+  }
+  g->need_cache[key] = need;
+  return need;
+}
+
+dpc_status ensure_pool(dpc_dgraph* g, uint64_t need) {
+  if (need < 1) need = 1;
+  if (need > 0xffffffffull) return fail(DPC_E_OVERFLOW, "consolidation pool exceeds 2^32 items");
+  if (need <= g->cap) return DPC_OK;
+  DPC_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  if (g->items) cudaFree(g->items);
+  g->items = nullptr;
+  g->cap = 0;
+  DPC_CUDA(cudaMalloc(&g->items, sizeof(Item) * need));
+  g->cap = static_cast<unsigned>(need);
+  return DPC_OK;
+}
+
+dpc_status begin_run(dpc_ctx* ctx, RunHeader* hdr) {
+  DPC_CUDA(cudaMemsetAsync(hdr, 0, sizeof(RunHeader), ctx->stream));
+  return DPC_OK;
+}
+
+dpc_status finish_metrics(dpc_ctx* ctx, RunHeader* hdr, RunHeader* hdr_host, dpc_metrics* met) {
+  DPC_CUDA(cudaMemcpyAsync(hdr_host, hdr, sizeof(RunHeader), cudaMemcpyDeviceToHost, ctx->stream));
+  DPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hdr_host->overflow & 2u)
+    return fail(DPC_E_CUDA, "a device-side (CDP2) launch failed (pending-launch pool exhausted?)");
+  if (hdr_host->overflow & 1u) return fail(DPC_E_OVERFLOW, "consolidation pool overflow");
+  if (met) {
+    met->child_launch_count += hdr_host->launches;
+    met->buffer_items_inserted += hdr_host->aux1;
+    met->pool_peak = std::max<int64_t>(met->pool_peak, hdr_host->count);
+    met->overflow = static_cast<int32_t>(hdr_host->overflow);
+  }
+  return DPC_OK;
+}
+
+}  // namespace dpc
+
+using namespace dpc;
+
+extern "C" {
+
+dpc_status dpc_launch_cfg_default(int32_t app, int32_t variant, dpc_launch_cfg* cfg) {
+  if (!cfg) return fail(DPC_E_INVALID, "cfg is NULL");
+  if (app < 0 || app > DPC_APP_TREE_HEIGHT || variant < DPC_FLAT || variant > DPC_GRID)
+    return fail(DPC_E_INVALID, "unknown app or variant");
+  const Default& d = kDefaults[app][variant];
+  cfg->variant = variant;
+  cfg->threshold = d.threshold;
+  cfg->parent_threads = d.parent_threads;
+  cfg->child_threads = d.child_threads;
+  cfg->child_blocks = d.child_blocks;
+  cfg->kc_x = d.kc_x;
+  cfg->chunk = d.chunk;
+  cfg->flags = d.flags;
+  return DPC_OK;
+}
+
+dpc_status dpc_ctx_create(int32_t device, dpc_ctx** out) {
+  clear_error();
+  if (!out) return fail(DPC_E_INVALID, "out is NULL");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(DPC_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  if (device < 0 || device >= count) return fail(DPC_E_INVALID, "device index out of range");
+  cudaDeviceProp p;
+  DPC_CUDA(cudaGetDeviceProperties(&p, device));
+  if (p.major != 10) return fail(DPC_E_CUDA, "libdpc is built for sm_100a (B200); device is sm_" +
+                                                 std::to_string(p.major * 10 + p.minor));
+  DPC_CUDA(cudaSetDevice(device));
+  auto* c = new (std::nothrow) dpc_ctx();
+  if (!c) return fail(DPC_E_OOM, "ctx allocation failed");
+  c->device = device;
+  c->sms = p.multiProcessorCount;
+  c->max_threads_per_sm = p.maxThreadsPerMultiProcessor;
+  c->coop = p.cooperativeLaunch;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  for (int i = 0; e == cudaSuccess && i < 64; i++) e = cudaEventCreate(&c->ev[i]);
+  if (e == cudaSuccess) {
+    c->flush_bytes = std::max<size_t>(2 * static_cast<size_t>(p.l2CacheSize), 256u << 20);
+    e = cudaMalloc(&c->flush_buf, c->flush_bytes);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSetLimit(cudaLimitDevRuntimePendingLaunchCount, 2048);
+  if (e != cudaSuccess) {
+    dpc_ctx_destroy(c);
+    return cuda_fail(e, "dpc_ctx_create");
+  }
+  c->pending_limit = 2048;
+  *out = c;
+  return DPC_OK;
+}
+
+void dpc_ctx_destroy(dpc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->flush_buf) cudaFree(c->flush_buf);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void* dpc_ctx_stream(dpc_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+int32_t dpc_ctx_sm_count(dpc_ctx* c) { return c ? c->sms : 0; }
+
+dpc_status dpc_ctx_event_record(dpc_ctx* c, int32_t slot) {
+  if (!c || slot < 0 || slot >= 64) return fail(DPC_E_INVALID, "bad ctx or event slot");
+  DPC_CUDA(cudaEventRecord(c->ev[slot], c->stream));
+  return DPC_OK;
+}
+
+dpc_status dpc_ctx_event_elapsed(dpc_ctx* c, int32_t a, int32_t b, float* ms) {
+  if (!c || !ms || a < 0 || a >= 64 || b < 0 || b >= 64) return fail(DPC_E_INVALID, "bad arguments");
+  DPC_CUDA(cudaEventSynchronize(c->ev[b]));
+  DPC_CUDA(cudaEventElapsedTime(ms, c->ev[a], c->ev[b]));
+  return DPC_OK;
+}
+
+dpc_status dpc_ctx_synchronize(dpc_ctx* c) {
+  if (!c) return fail(DPC_E_INVALID, "ctx is NULL");
+  DPC_CUDA(cudaStreamSynchronize(c->stream));
+  return DPC_OK;
+}
+
+dpc_status dpc_ctx_flush_l2(dpc_ctx* c) {
+  if (!c) return fail(DPC_E_INVALID, "ctx is NULL");
+  DPC_CUDA(cudaMemsetAsync(c->flush_buf, 0x5a, c->flush_bytes, c->stream));
+  return DPC_OK;
+}
+
+void* dpc_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dpc_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+dpc_status dpc_copy_h2d(dpc_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!c) return fail(DPC_E_INVALID, "ctx is NULL");
+  DPC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  DPC_CUDA(cudaStreamSynchronize(c->stream));
+  return DPC_OK;
+}
+
+dpc_status dpc_copy_d2h(dpc_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!c) return fail(DPC_E_INVALID, "ctx is NULL");
+  DPC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  DPC_CUDA(cudaStreamSynchronize(c->stream));
+  return DPC_OK;
+}
+
+// ---------------- device-resident graph ----------------
+
+void dpc_dgraph_free(dpc_dgraph* g) {
+  if (!g) return;
+  if (g->ctx) {
+    cudaSetDevice(g->ctx->device);
+    cudaStreamSynchronize(g->ctx->stream);
+  }
+  void* bufs[] = {g->rowptr, g->col,      g->w,        g->val,   g->x,    g->y,
+                  g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
+                  g->items};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (g->hdr_host) cudaFreeHost(g->hdr_host);
+  delete g;
+}
+
+dpc_status dpc_dgraph_upload(dpc_ctx* c, const dpc_csr* h, dpc_dgraph** out) {
+  clear_error();
+  if (!c || !out) return fail(DPC_E_INVALID, "NULL argument");
+  dpc_status st = dpc_csr_validate(h);
+  if (st != DPC_OK) return st;
+  if (h->m >= (int64_t{1} << 32)) return fail(DPC_E_INVALID, "edgeCount must be < 2^32 on device");
+  auto* g = new (std::nothrow) dpc_dgraph();
+  if (!g) return fail(DPC_E_OOM, "dgraph allocation failed");
+  g->ctx = c;
+  g->n = h->n;
+  g->m = h->m;
+  const size_t n = static_cast<size_t>(h->n), m = static_cast<size_t>(h->m);
+  auto cleanup = [&](cudaError_t e, const char* w) {
+    dpc_dgraph_free(g);
+    return cuda_fail(e, w);
+  };
+  cudaError_t e;
+  std::vector<unsigned> rp32(n + 1);
+  g->host_rowptr.assign(h->rowptr, h->rowptr + n + 1);
+  for (size_t i = 0; i <= n; i++) rp32[i] = static_cast<unsigned>(h->rowptr[i]);
+  for (size_t i = 0; i < n; i++) g->max_deg = std::max<int64_t>(g->max_deg, h->rowptr[i + 1] - h->rowptr[i]);
+  const size_t nv = std::max<size_t>(n, 1), mv = std::max<size_t>(m, 1);
+  if ((e = cudaMalloc(&g->rowptr, sizeof(unsigned) * (n + 1))) != cudaSuccess) return cleanup(e, "cudaMalloc rowptr");
+  if ((e = cudaMalloc(&g->col, sizeof(int) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc col");
+  if (h->w && (e = cudaMalloc(&g->w, sizeof(int) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc w");
+  if (h->val && (e = cudaMalloc(&g->val, sizeof(float) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc val");
+  if ((e = cudaMalloc(&g->x, sizeof(float) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc x");
+  if ((e = cudaMalloc(&g->y, sizeof(float) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc y");
+  if ((e = cudaMalloc(&g->dist, sizeof(unsigned) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc dist");
+  if ((e = cudaMalloc(&g->color, sizeof(int) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc color");
+  if ((e = cudaMalloc(&g->front[0], sizeof(unsigned) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc front");
+  if ((e = cudaMalloc(&g->front[1], sizeof(unsigned) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc front");
+  if ((e = cudaMalloc(&g->stamp, sizeof(unsigned) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc stamp");
+  if ((e = cudaMalloc(&g->hdr, sizeof(RunHeader) * 2)) != cudaSuccess) return cleanup(e, "cudaMalloc hdr");
+  if ((e = cudaMallocHost(&g->hdr_host, sizeof(RunHeader) * 2)) != cudaSuccess) return cleanup(e, "cudaMallocHost hdr");
+  cudaStream_t s = c->stream;
+  e = cudaMemcpyAsync(g->rowptr, rp32.data(), sizeof(unsigned) * (n + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && m) e = cudaMemcpyAsync(g->col, h->col, sizeof(int) * m, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && m && h->w) e = cudaMemcpyAsync(g->w, h->w, sizeof(int) * m, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && m && h->val) e = cudaMemcpyAsync(g->val, h->val, sizeof(float) * m, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->x, 0, sizeof(float) * nv, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->y, 0, sizeof(float) * nv, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->hdr, 0, sizeof(RunHeader) * 2, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cleanup(e, "dpc_dgraph_upload copy");
+  *out = g;
+  return DPC_OK;
+}
+
+float* dpc_dgraph_x(dpc_dgraph* g) { return g ? g->x : nullptr; }
+float* dpc_dgraph_y(dpc_dgraph* g) { return g ? g->y : nullptr; }
+uint32_t* dpc_dgraph_dist(dpc_dgraph* g) { return g ? g->dist : nullptr; }
+int32_t* dpc_dgraph_color(dpc_dgraph* g) { return g ? g->color : nullptr; }
+
+// ---------------- host-buffer runs ----------------
+
+dpc_status dpc_spmv_host(dpc_ctx* c, dpc_dgraph* g, const float* x, float* y,
+                         const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!c || !g || !x || !y) return fail(DPC_E_INVALID, "NULL argument");
+  const size_t bytes = sizeof(float) * static_cast<size_t>(g->n);
+  DPC_CUDA(cudaMemcpyAsync(g->x, x, bytes, cudaMemcpyHostToDevice, c->stream));
+  dpc_status st = dpc_spmv_device(c, g, g->x, g->y, cfg, met);
+  if (st != DPC_OK) return st;
+  DPC_CUDA(cudaMemcpyAsync(y, g->y, bytes, cudaMemcpyDeviceToHost, c->stream));
+  DPC_CUDA(cudaStreamSynchronize(c->stream));
+  return DPC_OK;
+}
+
+dpc_status dpc_run_spmv(dpc_ctx* c, const dpc_csr* A, const float* x, float* y,
+                        const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!c || !A || !x || !y) return fail(DPC_E_INVALID, "NULL argument");
+  if (!A->val) return fail(DPC_E_INVALID, "SpMV needs matrix values (val)");
+  dpc_dgraph* g = nullptr;
+  dpc_status st = dpc_dgraph_upload(c, A, &g);
+  if (st != DPC_OK) return st;
+  if (met) std::memset(met, 0, sizeof(*met));
+  st = dpc_spmv_host(c, g, x, y, cfg, met);
+  dpc_dgraph_free(g);
+  return st;
+}
+
+dpc_status dpc_run_sssp(dpc_ctx* c, const dpc_csr* G, int32_t source, uint32_t* dist,
+                        const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!c || !G || !dist) return fail(DPC_E_INVALID, "NULL argument");
+  if (!G->w) return fail(DPC_E_INVALID, "SSSP needs edge weights (w)");
+  for (int64_t k = 0; k < G->m; k++)
+    if (G->w[k] < 0) return fail(DPC_E_INVALID, "SSSP weights must be >= 0");
+  dpc_dgraph* g = nullptr;
+  dpc_status st = dpc_dgraph_upload(c, G, &g);
+  if (st != DPC_OK) return st;
+  if (met) std::memset(met, 0, sizeof(*met));
+  st = dpc_sssp_device(c, g, source, cfg, met);
+  if (st == DPC_OK) st = dpc_copy_d2h(c, dist, g->dist, sizeof(unsigned) * static_cast<size_t>(G->n));
+  dpc_dgraph_free(g);
+  return st;
+}
+
+dpc_status dpc_run_color(dpc_ctx* c, const dpc_csr* G, uint64_t seed, int32_t* color,
+                         int32_t* ncolors, const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!c || !G || !color) return fail(DPC_E_INVALID, "NULL argument");
+  dpc_dgraph* g = nullptr;
+  dpc_status st = dpc_dgraph_upload(c, G, &g);
+  if (st != DPC_OK) return st;
+  dpc_metrics local{};
+  dpc_metrics* mp = met ? met : &local;
+  std::memset(mp, 0, sizeof(*mp));
+  st = dpc_color_device(c, g, seed, cfg, mp);
+  if (st == DPC_OK) st = dpc_copy_d2h(c, color, g->color, sizeof(int) * static_cast<size_t>(G->n));
+  if (st == DPC_OK && ncolors) *ncolors = mp->result_count;
+  dpc_dgraph_free(g);
+  return st;
+}
+
+static dpc_status run_tree(dpc_ctx* c, const dpc_tree* t, int which, int32_t* out,
+                           const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!c || !t || !out) return fail(DPC_E_INVALID, "NULL argument");
+  dpc_dtree* d = nullptr;
+  dpc_status st = dpc_dtree_upload(c, t, &d);
+  if (st != DPC_OK) return st;
+  if (met) std::memset(met, 0, sizeof(*met));
+  st = dpc_tree_device(c, d, which, cfg, met);
+  if (st == DPC_OK) st = dpc_copy_d2h(c, out, d->result, sizeof(int) * static_cast<size_t>(t->n));
+  dpc_dtree_free(d);
+  return st;
+}
+
+dpc_status dpc_run_tree_desc(dpc_ctx* c, const dpc_tree* t, int32_t* desc,
+                             const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  return run_tree(c, t, DPC_APP_TREE_DESC, desc, cfg, met);
+}
+
+dpc_status dpc_run_tree_height(dpc_ctx* c, const dpc_tree* t, int32_t* height,
+                               const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  return run_tree(c, t, DPC_APP_TREE_HEIGHT, height, cfg, met);
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// Host-side definitions of the opaque ABI handles (dpc_ctx, dpc_dgraph,
+// dpc_dtree) shared by the CUDA translation units.  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+#include "dpc.h"
+#include "dpc_internal.h"
+
+struct dpc_ctx {
+  int device = 0;
+  int sms = 148;
+  int max_threads_per_sm = 2048;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[64] = {};
+  size_t pending_limit = 0;  // current cudaLimitDevRuntimePendingLaunchCount
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+  int coop = 0;  // cooperative launch supported
+};
+
+// Device-resident graph plus every buffer its apps need.
+struct dpc_dgraph {
+  dpc_ctx* ctx = nullptr;
+  int64_t n = 0, m = 0;
+  unsigned* rowptr = nullptr;  // n+1 (uint32; m < 2^32)
+  int* col = nullptr;
+  int* w = nullptr;
+  float* val = nullptr;
+  float* x = nullptr;
+  float* y = nullptr;
+  unsigned* dist = nullptr;
+  int* color = nullptr;
+  // frontier / worklist buffers (SSSP, GC)
+  unsigned* front[2] = {nullptr, nullptr};
+  unsigned* stamp = nullptr;  // SSSP dedup stamp / GC pending counts
+  dpc::dev::RunHeader* hdr = nullptr;  // device counters
+  dpc::dev::RunHeader* hdr_host = nullptr;  // pinned mirror
+  // consolidation pool
+  dpc::dev::Item* items = nullptr;
+  unsigned cap = 0;
+  // host copies used to size pools: degree array
+  std::vector<int64_t> host_rowptr;
+  std::map<std::pair<int, int>, uint64_t> need_cache;
+  int64_t max_deg = 0;
+};
+
+struct dpc_dtree {
+  dpc_ctx* ctx = nullptr;
+  int64_t n = 0;
+  int root = 0;
+  int depth = 0;
+  int* parent = nullptr;
+  unsigned* cstart = nullptr;  // n+1
+  int* clist = nullptr;
+  int* result = nullptr;
+  unsigned* level_nodes = nullptr;   // nodes in visit order (level by level)
+  unsigned* level_off = nullptr;     // per-level offsets (device, depth+2)
+  dpc::dev::RunHeader* hdr = nullptr;
+  dpc::dev::RunHeader* hdr_host = nullptr;
+  dpc::dev::Item* items = nullptr;
+  unsigned cap = 0;
+  std::vector<int64_t> host_cstart;
+  int64_t max_children = 0;
+};
+
+namespace dpc {
+
+// CUDA error -> dpc_status with a message naming the call site.
+dpc_status cuda_fail(cudaError_t e, const char* what);
+#define DPC_CUDA(call)                                         \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return ::dpc::cuda_fail(_e, #call); \
+  } while (0)
+
+// Resolved launch configuration for one run.
+struct Cfg {
+  int variant;
+  unsigned threshold;
+  unsigned parent_threads;
+  unsigned child_threads;
+  unsigned child_blocks;  // cap (0 = none)
+  unsigned chunk;
+  int grid_persistent;  // grid variant as one cooperative persistent kernel
+};
+
+dpc_status resolve_cfg(dpc_ctx* ctx, int app, const dpc_launch_cfg* in, Cfg* out);
+
+// Ensures the device runtime pending-launch pool can hold `need` launches.
+// A large pool slows every device launch (tools/probes: 15 us -> 28 us per
+// link), so it is set back to the default for the consolidated variants.
+dpc_status ensure_pending_limit(dpc_ctx* ctx, size_t need);
+
+// Pool slots needed for (threshold, chunk): sum over rows with
+// deg > threshold of ceil(deg / chunk).  Cached per graph.
+uint64_t pool_need(dpc_dgraph* g, unsigned threshold, unsigned chunk);
+dpc_status ensure_pool(dpc_dgraph* g, uint64_t need);
+
+dpc_status begin_run(dpc_ctx* ctx, dpc::dev::RunHeader* hdr);
+dpc_status finish_metrics(dpc_ctx* ctx, dpc::dev::RunHeader* hdr, dpc::dev::RunHeader* hdr_host,
+                          dpc_metrics* met);
+
+}  // namespace dpc

@@ -1,0 +1,121 @@
+"""SpMV parity on the B200: every variant against the fp64 CPU oracle.
+
+Tolerance (BASELINE.json north_star): per row |y - y64| <= 1e-5 * |y64|
+(values and x are positive, so there is no cancellation; empty rows must be 0).
+"""
+import numpy as np
+import pytest
+
+import paper_1606_08150_b200 as dpc
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ["flat", "basic", "warp", "block", "grid"]
+RTOL = 1e-5
+
+
+def _x(n, seed=7):
+    rng = np.random.default_rng(seed)
+    return (rng.integers(1, 1 << 24, n) / float(1 << 24)).astype(np.float32)
+
+
+def _check(orc, g, x, y):
+    y64 = orc.spmv_f64(g.rowptr, g.col, g.val, x)
+    err = np.abs(y.astype(np.float64) - y64)
+    bad = err > RTOL * np.abs(y64)
+    assert not bad.any(), f"{bad.sum()} rows off; worst rel {np.max(err / np.maximum(np.abs(y64), 1e-300))}"
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("scale", [8, 12, 14])
+def test_spmv_rmat(ctx, orc, variant, scale):
+    g = dpc.gen_rmat(scale, 16, seed=scale, weights=False, values=True)
+    x = _x(g.n)
+    y, met = dpc.run_spmv(g, x, variant, ctx=ctx)
+    _check(orc, g, x, y)
+    heavy = int((g.degrees() > 32).sum())
+    if variant == "flat":
+        assert met.child_launch_count == 0
+    elif variant == "basic":
+        assert met.child_launch_count == heavy
+    elif variant == "grid":
+        assert met.child_launch_count == 0  # persistent default: one cooperative kernel
+
+
+@pytest.mark.parametrize("variant", ["warp", "block", "grid"])
+def test_spmv_launch_laws(ctx, variant):
+    """Launch-count law (corrected per SURVEY §4): warp <= #warps
+    with a heavy row, block <= #blocks with one, grid == 1."""
+    g = dpc.gen_rmat(13, 16, seed=3, weights=False, values=True)
+    deg = g.degrees()
+    heavy = deg > 32
+    cfg = dpc.launch_cfg("spmv", variant, grid_cdp=True)
+    y, met = dpc.run_spmv(g, _x(g.n), variant, cfg=cfg, ctx=ctx)
+    pad = np.zeros((-len(heavy)) % 256, bool)
+    h = np.concatenate([heavy, pad])
+    if variant == "warp":
+        assert met.child_launch_count == int(h.reshape(-1, 32).any(1).sum())
+    elif variant == "block":
+        assert met.child_launch_count == int(h.reshape(-1, 256).any(1).sum())
+    else:
+        assert met.child_launch_count == 1
+
+
+def test_spmv_grid_cdp(ctx, orc):
+    g = dpc.gen_rmat(14, 16, seed=5, weights=False, values=True)
+    x = _x(g.n)
+    y, met = dpc.run_spmv(g, x, "grid", cfg=dpc.launch_cfg("spmv", "grid", grid_cdp=True), ctx=ctx)
+    _check(orc, g, x, y)
+    assert met.child_launch_count == 1
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("chunk,threshold", [(32, 0), (64, 32), (1000, 5), (4096, 32)])
+def test_spmv_cfg_sweep(ctx, orc, variant, chunk, threshold):
+    """Moldability: results independent of the configuration."""
+    g = dpc.gen_graph(3000, powerlaw=(1.6, 2500), seed=11, weights=False, values=True)
+    x = _x(g.n)
+    cfg = dpc.launch_cfg("spmv", variant, chunk=chunk, threshold=threshold)
+    y, _ = dpc.run_spmv(g, x, variant, cfg=cfg, ctx=ctx)
+    _check(orc, g, x, y)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_spmv_edge_cases(ctx, orc, variant):
+    # empty matrix, single empty row
+    g = dpc.csr_from_arrays([0], [], val=[])
+    assert g.n == 0
+    g = dpc.csr_from_arrays([0, 0], [], val=[])
+    y, _ = dpc.run_spmv(g, np.ones(1, np.float32), variant, ctx=ctx)
+    assert y.tolist() == [0.0]
+    # SPEC.md:459 identity example
+    g = dpc.csr_from_arrays([0, 1, 2], [0, 1], val=[1.0, 1.0])
+    y, _ = dpc.run_spmv(g, np.array([3, 7], np.float32), variant, ctx=ctx)
+    assert y.tolist() == [3.0, 7.0]
+    # ragged: rows of every length 0..300 (unaligned starts), plus one hub row
+    lens = np.concatenate([np.arange(0, 301), [100_003]])
+    rowptr = np.concatenate([[0], np.cumsum(lens)])
+    n = len(lens)
+    rng = np.random.default_rng(1)
+    col = rng.integers(0, n, rowptr[-1]).astype(np.int32)
+    val = (rng.integers(1, 1 << 24, rowptr[-1]) / float(1 << 24)).astype(np.float32)
+    g = dpc.csr_from_arrays(rowptr, col, val=val)
+    x = _x(n)
+    y, _ = dpc.run_spmv(g, x, variant, ctx=ctx)
+    _check(orc, g, x, y)
+
+
+def test_spmv_config2_full_size(ctx, orc):
+    """BASELINE config 2 at full size (R-MAT scale 20, 16.8M nnz), grid variant
+    via the device-resident path, plus the end-to-end host path."""
+    g = dpc.gen_rmat(20, 16, seed=1, weights=False, values=True)
+    x = _x(g.n)
+    dg = dpc.DeviceGraph(ctx, g)
+    dg.set_x(x)
+    for variant in ["flat", "warp", "block", "grid"]:
+        met = dg.spmv(variant, metrics=True)
+        _check(orc, g, x, dg.get_y())
+    y = np.empty(g.n, np.float32)
+    dg.spmv_host(x, y, "grid")
+    _check(orc, g, x, y)
+    dg.close()
