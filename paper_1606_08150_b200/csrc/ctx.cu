@@ -92,6 +92,19 @@ uint64_t pool_need(dpc_dgraph* g, unsigned threshold, unsigned chunk) {
   return need;
 }
 
+dpc_status ensure_pending_for(dpc_ctx* ctx, dpc_dgraph* g, int variant, unsigned threshold,
+                              unsigned parent_threads) {
+  // Outstanding device launches one parent grid can create: basic = one per
+  // heavy vertex, warp = one per warp holding one, block = one per block.
+  const uint64_t heavy = pool_need(g, threshold, 1u << 30);
+  const uint64_t items = static_cast<uint64_t>(g->n);
+  uint64_t need = 1;
+  if (variant == DPC_BASIC) need = heavy;
+  else if (variant == DPC_WARP) need = std::min<uint64_t>(heavy, (items + 31) / 32);
+  else if (variant == DPC_BLOCK) need = std::min<uint64_t>(heavy, (items + parent_threads - 1) / parent_threads);
+  return ensure_pending_limit(ctx, static_cast<size_t>(need) + 1024);
+}
+
 dpc_status ensure_pool(dpc_dgraph* g, uint64_t need) {
   if (need < 1) need = 1;
   if (need > 0xffffffffull) return fail(DPC_E_OVERFLOW, "consolidation pool exceeds 2^32 items");
@@ -260,10 +273,11 @@ void dpc_dgraph_free(dpc_dgraph* g) {
   }
   void* bufs[] = {g->rowptr, g->col,      g->w,        g->val,   g->x,    g->y,
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
-                  g->items};
+                  g->items, g->ctr};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->hdr_host) cudaFreeHost(g->hdr_host);
+  if (g->ctr_host) cudaFreeHost(g->ctr_host);
   delete g;
 }
 

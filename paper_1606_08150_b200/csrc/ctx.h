@@ -41,6 +41,8 @@ struct dpc_dgraph {
   // frontier / worklist buffers (SSSP, GC)
   unsigned* front[2] = {nullptr, nullptr};
   unsigned* stamp = nullptr;  // SSSP dedup stamp / GC pending counts
+  unsigned* ctr = nullptr;    // per-iteration counters (app-specific layout, 64 B)
+  void* ctr_host = nullptr;   // pinned mirror of ctr
   dpc::dev::RunHeader* hdr = nullptr;  // device counters
   dpc::dev::RunHeader* hdr_host = nullptr;  // pinned mirror
   // consolidation pool
@@ -67,8 +69,11 @@ struct dpc_dtree {
   dpc::dev::RunHeader* hdr_host = nullptr;
   dpc::dev::Item* items = nullptr;
   unsigned cap = 0;
-  std::vector<int64_t> host_cstart;
+  unsigned* off_host = nullptr;      // pinned level offsets
   int64_t max_children = 0;
+  int64_t root_children = 0;
+  int64_t internal = 0;              // nodes with >= 1 child
+  unsigned group = 1;                // lanes per work item (mean fan-out)
 };
 
 namespace dpc {
@@ -102,6 +107,9 @@ dpc_status ensure_pending_limit(dpc_ctx* ctx, size_t need);
 // Pool slots needed for (threshold, chunk): sum over rows with
 // deg > threshold of ceil(deg / chunk).  Cached per graph.
 uint64_t pool_need(dpc_dgraph* g, unsigned threshold, unsigned chunk);
+// Sizes the pending-launch pool for the worst case of one parent grid.
+dpc_status ensure_pending_for(dpc_ctx* ctx, dpc_dgraph* g, int variant, unsigned threshold,
+                              unsigned parent_threads);
 dpc_status ensure_pool(dpc_dgraph* g, uint64_t need);
 
 dpc_status begin_run(dpc_ctx* ctx, dpc::dev::RunHeader* hdr);

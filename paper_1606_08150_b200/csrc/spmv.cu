@@ -317,11 +317,7 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
     if (st != DPC_OK) return st;
   }
   a.pool = dev::Pool{g->items, g->cap};
-  if (c.variant == DPC_BASIC) {
-    st = ensure_pending_limit(ctx, static_cast<size_t>(pool_need(g, c.threshold, 1u << 30)) + 1024);
-  } else {
-    st = ensure_pending_limit(ctx, 2048);
-  }
+  st = ensure_pending_for(ctx, g, c.variant, c.threshold, c.parent_threads);
   if (st != DPC_OK) return st;
   st = begin_run(ctx, g->hdr);
   if (st != DPC_OK) return st;

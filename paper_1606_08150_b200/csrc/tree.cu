@@ -1,0 +1,483 @@
+// Tree descendants (TD) and tree heights (TH) — the paper's parallel-recursion
+// apps (Fig. 1(c)): tree_traversal(node) <<<1, nc(node)>>>
+// gives each thread one child; a child with children recurses, a leaf does
+// leaf work; postwork folds the children's results into the node:
+//     TD: desc[v]   = sum_c (desc[c] + 1)
+//     TH: height[v] = max_c (height[c] + 1)
+//
+// CDP1's parent-side cudaDeviceSynchronize is gone on sm_100,
+// so postwork runs in TAIL-launched grids: a tail launch starts only after
+// the launching grid and all its descendant work have completed
+// (tools/probes/cdp2_probe Q1), which is exactly "after the subtree is done".
+//
+//   flat   : host loop over levels; thread per node, serial child loops;
+//            then a reverse level loop gathers results (no device launches)
+//   basic  : Fig. 1(c) literally: one <<<ceil(nc/T), T>>> grid per internal
+//            node (CDP2 fire-and-forget) + one tail-launched postwork grid
+//   warp / block / grid : recursive consolidation (transform.hpp:874-964):
+//            <k>_cons drains a buffer of internal nodes, inserts their
+//            internal children into owner buffers (warp / block / grid), the
+//            owner launches one <k>_cons per buffer, and every <k>_cons grid
+//            tail-launches one <k>_post over its own items
+//   grid (persistent) : one cooperative kernel: top-down levels with a
+//            device-wide barrier between them, then the bottom-up levels in
+//            reverse (PAPER.md:244-250 global barrier), zero launches.
+//
+// Work items are internal nodes; a group of g lanes (g = power of two <= 32
+// sized to the mean fan-out) handles one item's children.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+#include "ctx.h"
+
+namespace cg = cooperative_groups;
+
+namespace dpc {
+namespace tree {
+
+using dev::RunHeader;
+
+struct Args {
+  const unsigned* __restrict__ cstart;
+  const int* __restrict__ clist;
+  int* res;
+  unsigned* nodes;  // pool / level lists of internal nodes
+  unsigned* cnt;    // [0] bump pointer of `nodes`, [1..] level offsets (persistent/flat)
+  unsigned cap;
+  RunHeader* hdr;
+  unsigned n;
+  unsigned group;  // lanes per item (1, 2, 4, ..., 32)
+  unsigned child_threads;
+  unsigned child_blocks;
+  int is_max;      // TH (max) vs TD (sum)
+};
+
+__device__ __forceinline__ unsigned nkids(const Args& a, unsigned v) {
+  return __ldg(a.cstart + v + 1) - __ldg(a.cstart + v);
+}
+
+// Postwork for one node over a g-lane group: gather children's results.
+__device__ __forceinline__ void fold_node(const Args& a, unsigned v, unsigned sub, unsigned g,
+                                          bool active) {
+  int acc = 0;
+  if (active) {
+    unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
+    for (unsigned k = b + sub; k < e; k += g) {
+      int r = __ldcg(a.res + __ldg(a.clist + k)) + 1;
+      acc = a.is_max ? max(acc, r) : acc + r;
+    }
+  }
+  for (unsigned o = g >> 1; o > 0; o >>= 1) {
+    int t = __shfl_xor_sync(dev::kFull, acc, o);
+    acc = a.is_max ? max(acc, t) : acc + t;
+  }
+  if (active && sub == 0) a.res[v] = acc;
+}
+
+// Top-down expansion of one node: returns (per lane) how many internal
+// children this lane owns; they are written by write_kids once slots exist.
+__device__ __forceinline__ unsigned count_kids(const Args& a, unsigned v, unsigned sub, unsigned g,
+                                               bool active) {
+  unsigned c = 0;
+  if (active) {
+    unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
+    for (unsigned k = b + sub; k < e; k += g) c += nkids(a, static_cast<unsigned>(__ldg(a.clist + k))) > 0;
+  }
+  return c;
+}
+
+__device__ __forceinline__ void write_kids(const Args& a, unsigned v, unsigned sub, unsigned g,
+                                           bool active, unsigned at) {
+  if (!active) return;
+  unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
+  for (unsigned k = b + sub; k < e; k += g) {
+    unsigned c = static_cast<unsigned>(__ldg(a.clist + k));
+    if (nkids(a, c) > 0) {
+      if (at < a.cap) a.nodes[at] = c;
+      else atomicOr(&a.hdr->overflow, 1u);
+      at++;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- flat
+__global__ void __launch_bounds__(256) flat_down(Args a, unsigned lo, unsigned hi) {
+  unsigned i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  bool active = i < hi;
+  unsigned v = active ? a.nodes[i] : 0;
+  unsigned want = count_kids(a, v, 0, 1, active);
+  unsigned wb, wt;
+  unsigned at = dev::warp_reserve(&a.cnt[0], want, &wb, &wt);
+  write_kids(a, v, 0, 1, active && want, at);
+}
+
+__global__ void __launch_bounds__(256) flat_up(Args a, unsigned lo, unsigned hi) {
+  unsigned i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  bool active = i < hi;
+  fold_node(a, active ? a.nodes[i] : 0, 0, 1, active);
+}
+
+// ---------------------------------------------------------------- basic
+__global__ void __launch_bounds__(256) basic_post(Args a, unsigned v) {
+  unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
+  int r = 0;
+  if (b + k < e) r = __ldcg(a.res + __ldg(a.clist + b + k)) + 1;
+  for (int o = 16; o > 0; o >>= 1) {
+    int t = __shfl_xor_sync(dev::kFull, r, o);
+    r = a.is_max ? max(r, t) : r + t;
+  }
+  if (dev::lane_id() == 0 && r) {
+    if (a.is_max) atomicMax(a.res + v, r);
+    else atomicAdd(a.res + v, r);
+  }
+}
+
+// tree_traversal(node) <<<ceil(nc/T), T>>>: thread per child.
+__global__ void __launch_bounds__(256) basic_traverse(Args a, unsigned v) {
+  unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
+  if (b + k < e) {
+    unsigned c = static_cast<unsigned>(__ldg(a.clist + b + k));
+    unsigned nc = nkids(a, c);
+    if (nc > 0) {
+      basic_traverse<<<dev::ceil_div(nc, a.child_threads), a.child_threads, 0,
+                       cudaStreamFireAndForget>>>(a, c);
+      dev::note_launch(a.hdr);
+    }
+    // leaf work: res[c] stays 0
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    basic_post<<<dev::ceil_div(e - b, a.child_threads), a.child_threads, 0,
+                 cudaStreamTailLaunch>>>(a, v);
+    dev::note_launch(a.hdr);
+  }
+}
+
+// ---------------------------------------------------------------- consolidated
+enum Gran { kWarp = 2, kBlock = 3, kGrid = 4 };
+
+__global__ void __launch_bounds__(256) cons_post(Args a, const unsigned* items, unsigned count) {
+  const unsigned g = a.group;
+  const unsigned gid = (blockIdx.x * blockDim.x + threadIdx.x) / g, sub = threadIdx.x & (g - 1);
+  const unsigned ngroups = (gridDim.x * blockDim.x) / g;
+  // uniform trip count across the warp so the group shuffles stay converged
+  const unsigned base = gid - (threadIdx.x & 31u) / g;
+  for (unsigned i0 = base; i0 < count; i0 += ngroups) {
+    unsigned i = i0 + (threadIdx.x & 31u) / g;
+    bool active = i < count;
+    fold_node(a, active ? items[i] : 0, sub, g, active);
+  }
+}
+
+__device__ __forceinline__ unsigned cons_blocks(const Args& a, unsigned count) {
+  unsigned per_block = a.child_threads / a.group;
+  unsigned b = dev::ceil_div(count, per_block);
+  if (a.child_blocks && b > a.child_blocks) b = a.child_blocks;
+  return b ? b : 1u;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) cons_kernel(Args a, const unsigned* items, unsigned count) {
+  __shared__ unsigned s_base;
+  const unsigned g = a.group;
+  const unsigned lane = threadIdx.x & 31u, sub = threadIdx.x & (g - 1);
+  const unsigned gpw = 32 / g;  // groups per warp
+  const unsigned warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+  // Block-level and grid-level owners need every block to take part in the
+  // insert; a single pass over the items keeps the barrier count uniform.
+  unsigned rounds = dev::ceil_div(count, nwarps * gpw);
+  for (unsigned r = 0; r < rounds; r++) {
+    unsigned i = (r * nwarps + warp_g) * gpw + lane / g;
+    bool active = i < count;
+    unsigned v = active ? items[i] : 0;
+    unsigned want = count_kids(a, v, sub, g, active);
+    if (G == kWarp || G == kGrid) {
+      unsigned wb, wt;
+      unsigned at = dev::warp_reserve(&a.cnt[0], want, &wb, &wt);
+      write_kids(a, v, sub, g, active && want, at);
+      if (G == kWarp && wt) {
+        __threadfence();
+        unsigned leader = __ffs(__ballot_sync(dev::kFull, want != 0)) - 1;
+        __syncwarp();
+        if (lane == leader && wb < a.cap) {
+          unsigned cnt = min(wt, a.cap - wb);
+          cons_kernel<kWarp><<<cons_blocks(a, cnt), a.child_threads, 0, cudaStreamFireAndForget>>>(
+              a, a.nodes + wb, cnt);
+          dev::note_launch(a.hdr);
+        }
+      }
+    } else {  // block owner
+      unsigned bt;
+      unsigned off = dev::block_excl_scan(want, &bt);
+      if (threadIdx.x == 0 && bt) s_base = atomicAdd(&a.cnt[0], bt);
+      __syncthreads();
+      write_kids(a, v, sub, g, active && want, s_base + off);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0 && bt && s_base < a.cap) {
+        unsigned cnt = min(bt, a.cap - s_base);
+        cons_kernel<kBlock><<<cons_blocks(a, cnt), a.child_threads, 0, cudaStreamFireAndForget>>>(
+            a, a.nodes + s_base, cnt);
+        dev::note_launch(a.hdr);
+      }
+      __syncthreads();
+    }
+  }
+  if (G == kGrid) {
+    // next level = every item inserted by this grid: [level_end, cnt[0])
+    __threadfence();
+    if (dev::grid_last_block(&a.hdr->ticket) && threadIdx.x == 0) {
+      unsigned lo = static_cast<unsigned>(items - a.nodes) + count;
+      unsigned hi = min(*reinterpret_cast<volatile unsigned*>(&a.cnt[0]), a.cap);
+      if (hi > lo) {
+        cons_kernel<kGrid><<<cons_blocks(a, hi - lo), a.child_threads, 0, cudaStreamFireAndForget>>>(
+            a, a.nodes + lo, hi - lo);
+        dev::note_launch(a.hdr);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // consolidated postwork over this grid's items, after all descendants
+    cons_post<<<cons_blocks(a, count), a.child_threads, 0, cudaStreamTailLaunch>>>(a, items, count);
+    dev::note_launch(a.hdr);
+  }
+}
+
+// ---------------------------------------------------------------- persistent
+__global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_levels) {
+  cg::grid_group grid = cg::this_grid();
+  const unsigned g = a.group, lane = threadIdx.x & 31u, sub = threadIdx.x & (g - 1);
+  const unsigned gpw = 32 / g;
+  const unsigned warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned* off = a.cnt + 1;  // off[L] = start of level L in nodes[]
+  unsigned lo = 0, hi = off[1], levels = 0;
+  // top-down
+  while (hi > lo && levels < max_levels) {
+    for (unsigned base = lo + warp_g * gpw; base < hi; base += nwarps * gpw) {
+      unsigned i = base + lane / g;
+      bool active = i < hi;
+      unsigned v = active ? a.nodes[i] : 0;
+      unsigned want = count_kids(a, v, sub, g, active);
+      unsigned wb, wt;
+      unsigned at = dev::warp_reserve(&a.cnt[0], want, &wb, &wt);
+      write_kids(a, v, sub, g, active && want, at);
+    }
+    grid.sync();
+    levels++;
+    lo = hi;
+    hi = min(*reinterpret_cast<volatile unsigned*>(&a.cnt[0]), a.cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) off[levels + 1] = hi;
+  }
+  // bottom-up in reverse level order
+  for (int L = static_cast<int>(levels) - 1; L >= 0; L--) {
+    unsigned l0 = off[L], l1 = off[L + 1];
+    if (L == static_cast<int>(levels) - 1) l1 = lo;
+    for (unsigned base = l0 + warp_g * gpw; base < l1; base += nwarps * gpw) {
+      unsigned i = base + lane / g;
+      bool active = i < l1;
+      fold_node(a, active ? a.nodes[i] : 0, sub, g, active);
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->iter = levels;
+}
+
+}  // namespace tree
+}  // namespace dpc
+
+using namespace dpc;
+
+extern "C" {
+
+dpc_status dpc_dtree_upload(dpc_ctx* c, const dpc_tree* t, dpc_dtree** out) {
+  clear_error();
+  if (!c || !t || !out) return fail(DPC_E_INVALID, "NULL argument");
+  if (t->n < 1 || !t->cstart || !t->clist || t->root < 0 || t->root >= t->n)
+    return fail(DPC_E_INVALID, "invalid tree");
+  auto* d = new (std::nothrow) dpc_dtree();
+  if (!d) return fail(DPC_E_OOM, "dtree allocation failed");
+  d->ctx = c;
+  d->n = t->n;
+  d->root = t->root;
+  d->depth = t->depth;
+  const size_t n = static_cast<size_t>(t->n);
+  std::vector<unsigned> cs(n + 1);
+  int64_t internal = 0;
+  for (size_t v = 0; v <= n; v++) cs[v] = static_cast<unsigned>(t->cstart[v]);
+  for (size_t v = 0; v < n; v++) {
+    int64_t k = t->cstart[v + 1] - t->cstart[v];
+    d->max_children = std::max(d->max_children, k);
+    internal += k > 0;
+  }
+  d->internal = internal;
+  d->root_children = t->cstart[t->root + 1] - t->cstart[t->root];
+  double mean = internal ? static_cast<double>(n - 1) / static_cast<double>(internal) : 1.0;
+  unsigned g = 1;
+  while (g < 32 && g < mean) g <<= 1;
+  d->group = g;
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t x) {
+    if (e == cudaSuccess) e = x;
+  };
+  chk(cudaMalloc(&d->parent, sizeof(int) * n));
+  chk(cudaMalloc(&d->cstart, sizeof(unsigned) * (n + 1)));
+  chk(cudaMalloc(&d->clist, sizeof(int) * n));
+  chk(cudaMalloc(&d->result, sizeof(int) * n));
+  chk(cudaMalloc(&d->level_nodes, sizeof(unsigned) * std::max<size_t>(1, static_cast<size_t>(internal))));
+  chk(cudaMalloc(&d->level_off, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 4)));
+  chk(cudaMalloc(&d->hdr, sizeof(dev::RunHeader)));
+  chk(cudaMallocHost(&d->hdr_host, sizeof(dev::RunHeader)));
+  chk(cudaMallocHost(&d->off_host, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 4)));
+  if (e == cudaSuccess) {
+    cudaStream_t s = c->stream;
+    chk(cudaMemcpyAsync(d->parent, t->parent, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    chk(cudaMemcpyAsync(d->cstart, cs.data(), sizeof(unsigned) * (n + 1), cudaMemcpyHostToDevice, s));
+    chk(cudaMemcpyAsync(d->clist, t->clist, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    chk(cudaStreamSynchronize(s));
+  }
+  if (e != cudaSuccess) {
+    dpc_dtree_free(d);
+    return cuda_fail(e, "dpc_dtree_upload");
+  }
+  d->cap = static_cast<unsigned>(std::max<int64_t>(1, internal));
+  *out = d;
+  return DPC_OK;
+}
+
+void dpc_dtree_free(dpc_dtree* d) {
+  if (!d) return;
+  if (d->ctx) cudaStreamSynchronize(d->ctx->stream);
+  void* bufs[] = {d->parent, d->cstart, d->clist, d->result, d->level_nodes, d->level_off, d->hdr};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (d->hdr_host) cudaFreeHost(d->hdr_host);
+  if (d->off_host) cudaFreeHost(d->off_host);
+  delete d;
+}
+
+int32_t* dpc_dtree_result(dpc_dtree* d) { return d ? d->result : nullptr; }
+
+dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_launch_cfg* cfg,
+                           dpc_metrics* met) {
+  clear_error();
+  if (!c || !d) return fail(DPC_E_INVALID, "NULL argument");
+  if (which != DPC_APP_TREE_DESC && which != DPC_APP_TREE_HEIGHT)
+    return fail(DPC_E_INVALID, "which must be DPC_APP_TREE_DESC or DPC_APP_TREE_HEIGHT");
+  Cfg k;
+  dpc_status st = resolve_cfg(c, which, cfg, &k);
+  if (st != DPC_OK) return st;
+  if (k.child_threads > 256 || k.parent_threads != 256)
+    return fail(DPC_E_INVALID, "tree kernels are built for parent_threads = 256, child_threads <= 256");
+  tree::Args a;
+  a.cstart = d->cstart;
+  a.clist = d->clist;
+  a.res = d->result;
+  a.nodes = d->level_nodes;
+  a.cnt = d->level_off;
+  a.cap = d->cap;
+  a.hdr = d->hdr;
+  a.n = static_cast<unsigned>(d->n);
+  a.group = d->group;
+  a.child_threads = k.child_threads;
+  a.child_blocks = k.child_blocks;
+  a.is_max = which == DPC_APP_TREE_HEIGHT;
+  cudaStream_t s = c->stream;
+  size_t need = 2048;
+  if (k.variant == DPC_BASIC) need = 2 * static_cast<size_t>(d->internal) + 1024;
+  else if (k.variant == DPC_WARP || k.variant == DPC_BLOCK) need = 2 * static_cast<size_t>(d->internal) + 1024;
+  else if (k.variant == DPC_GRID) need = 4 * static_cast<size_t>(d->depth) + 1024;
+  st = ensure_pending_limit(c, need);
+  if (st != DPC_OK) return st;
+  DPC_CUDA(cudaMemsetAsync(d->hdr, 0, sizeof(dev::RunHeader), s));
+  DPC_CUDA(cudaMemsetAsync(d->result, 0, sizeof(int) * static_cast<size_t>(d->n), s));
+  const unsigned root = static_cast<unsigned>(d->root);
+  const bool root_internal = d->internal > 0;
+  // level_off[0] = bump pointer, level_off[1 + L] = start of level L
+  unsigned init[3] = {root_internal ? 1u : 0u, 0u, root_internal ? 1u : 0u};
+  DPC_CUDA(cudaMemcpyAsync(d->level_off, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  if (root_internal)
+    DPC_CUDA(cudaMemcpyAsync(d->level_nodes, &root, sizeof(unsigned), cudaMemcpyHostToDevice, s));
+  int64_t host_launches = 0, levels = 0;
+  if (root_internal) {
+    switch (k.variant) {
+      case DPC_FLAT: {
+        // host loop: level ranges come back through a pinned counter
+        std::vector<unsigned> off{0, 1};
+        unsigned lo = 0, hi = 1;
+        while (hi > lo) {
+          unsigned nb = std::max(1u, dev::ceil_div(hi - lo, 256u));
+          tree::flat_down<<<nb, 256, 0, s>>>(a, lo, hi);
+          host_launches++;
+          DPC_CUDA(cudaGetLastError());
+          DPC_CUDA(cudaMemcpyAsync(d->off_host, d->level_off, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+          DPC_CUDA(cudaStreamSynchronize(s));
+          lo = hi;
+          hi = std::min(d->off_host[0], d->cap);
+          off.push_back(hi);
+          levels++;
+        }
+        for (int64_t L = levels - 1; L >= 0; L--) {
+          unsigned l0 = off[L], l1 = off[L + 1];
+          unsigned nb = std::max(1u, dev::ceil_div(l1 - l0, 256u));
+          tree::flat_up<<<nb, 256, 0, s>>>(a, l0, l1);
+          host_launches++;
+        }
+        DPC_CUDA(cudaGetLastError());
+        break;
+      }
+      case DPC_BASIC: {
+        const unsigned nc = static_cast<unsigned>(d->root_children);
+        tree::basic_traverse<<<dev::ceil_div(nc, k.child_threads), k.child_threads, 0, s>>>(a, root);
+        host_launches++;
+        DPC_CUDA(cudaGetLastError());
+        break;
+      }
+      case DPC_WARP:
+        tree::cons_kernel<tree::kWarp><<<1, k.child_threads, 0, s>>>(a, d->level_nodes, 1);
+        host_launches++;
+        break;
+      case DPC_BLOCK:
+        tree::cons_kernel<tree::kBlock><<<1, k.child_threads, 0, s>>>(a, d->level_nodes, 1);
+        host_launches++;
+        break;
+      case DPC_GRID:
+        if (k.grid_persistent) {
+          int per_sm = 0;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+              &per_sm, reinterpret_cast<const void*>(tree::grid_persistent), 256, 0);
+          int blocks = std::max(1, per_sm) * c->sms;
+          unsigned max_levels = static_cast<unsigned>(d->depth) + 1;
+          void* args[] = {&a, &max_levels};
+          DPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tree::grid_persistent),
+                                               dim3(blocks), dim3(256), args, 0, s));
+        } else {
+          tree::cons_kernel<tree::kGrid><<<1, k.child_threads, 0, s>>>(a, d->level_nodes, 1);
+        }
+        host_launches++;
+        break;
+    }
+    DPC_CUDA(cudaGetLastError());
+  }
+  DPC_CUDA(cudaMemcpyAsync(d->hdr_host, d->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
+  DPC_CUDA(cudaStreamSynchronize(s));
+  if (d->hdr_host->overflow & 2u) return fail(DPC_E_CUDA, "a device-side (CDP2) launch failed");
+  if (d->hdr_host->overflow & 1u) return fail(DPC_E_OVERFLOW, "tree node buffer overflow");
+  if (met) {
+    met->child_launch_count += d->hdr_host->launches;
+    met->host_launches += host_launches;
+    met->iterations += levels ? levels : d->hdr_host->iter;
+    met->edges_processed += d->n - 1;
+    met->buffer_items_inserted += d->internal;
+  }
+  return DPC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+"""SSSP parity on the B200: every variant bit-exact against Dijkstra
+(oracle/oracle.c), including edge cases (unreachable vertices, zero weights,
+self loops, duplicate edges, a single hub)."""
+import numpy as np
+import pytest
+
+import paper_1606_08150_b200 as dpc
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ["flat", "basic", "warp", "block", "grid"]
+
+
+def _source(g):
+    return int(np.argmax(g.degrees()))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("scale", [8, 12, 14])
+def test_sssp_rmat(ctx, orc, variant, scale):
+    g = dpc.gen_rmat(scale, 16, seed=scale + 100)
+    s = _source(g)
+    d, met = dpc.run_sssp(g, s, variant, ctx=ctx)
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, s))
+    if variant == "flat":
+        assert met.child_launch_count == 0
+
+
+def test_sssp_grid_cdp(ctx, orc):
+    g = dpc.gen_rmat(13, 16, seed=9)
+    s = _source(g)
+    cfg = dpc.launch_cfg("sssp", "grid", grid_cdp=True)
+    d, met = dpc.run_sssp(g, s, cfg=cfg, ctx=ctx)
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, s))
+    assert 1 <= met.child_launch_count <= met.iterations  # <= 1 launch per parent grid
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("chunk,threshold", [(32, 0), (100, 7), (4096, 32)])
+def test_sssp_cfg_sweep(ctx, orc, variant, chunk, threshold):
+    g = dpc.gen_graph(4000, powerlaw=(1.5, 3000), seed=5, wmin=0, wmax=20)
+    cfg = dpc.launch_cfg("sssp", variant, chunk=chunk, threshold=threshold)
+    d, _ = dpc.run_sssp(g, 0, cfg=cfg, ctx=ctx)
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, 0))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_sssp_edge_cases(ctx, orc, variant):
+    # single vertex, no edges
+    g = dpc.csr_from_arrays([0, 0], [], w=[])
+    d, _ = dpc.run_sssp(g, 0, variant, ctx=ctx)
+    assert d.tolist() == [0]
+    # disconnected + self loop + duplicate edges + zero weight
+    g = dpc.csr_from_arrays([0, 3, 4, 4, 5], [0, 1, 1, 2, 3], w=[5, 0, 7, 1, 2])
+    d, _ = dpc.run_sssp(g, 0, variant, ctx=ctx)
+    assert d.tolist() == [0, 0, 1, 2**32 - 1]
+    # hub with 50k out-edges into a chain
+    n = 50_001
+    rowptr = np.concatenate([[0], np.full(n, n - 1)]).astype(np.int64)
+    col = np.arange(1, n, dtype=np.int32)
+    w = (np.arange(1, n) % 13 + 1).astype(np.int32)
+    g = dpc.csr_from_arrays(rowptr, col, w=w)
+    d, _ = dpc.run_sssp(g, 0, variant, ctx=ctx)
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, 0))
+
+
+def test_sssp_config1_full(ctx, orc):
+    """BASELINE config 1: R-MAT scale 16, int weights [1,255], all variants."""
+    g = dpc.gen_rmat(16, 16, seed=1)
+    s = _source(g)
+    ref = orc.sssp(g.rowptr, g.col, g.w, s)
+    dg = dpc.DeviceGraph(ctx, g)
+    for v in VARIANTS:
+        met = dg.sssp(s, v)
+        assert np.array_equal(dg.get_dist(), ref), v
+        assert met.iterations > 0
+    dg.close()
+
+
+def test_sssp_invalid(ctx):
+    g = dpc.gen_rmat(6, 4, seed=1)
+    with pytest.raises(dpc.DpcError) as e:
+        dpc.run_sssp(g, g.n + 5, "grid", ctx=ctx)
+    assert e.value.kind == "invalid"
+    g2 = dpc.gen_rmat(6, 4, seed=1, weights=False, values=True)
+    with pytest.raises(dpc.DpcError):
+        dpc.run_sssp(g2, 0, "grid", ctx=ctx)
