@@ -393,6 +393,16 @@ dpc_status dpc_run_color(dpc_ctx* c, const dpc_csr* G, uint64_t seed, int32_t* c
   std::memset(mp, 0, sizeof(*mp));
   st = dpc_color_device(c, g, seed, cfg, mp);
   if (st == DPC_OK) st = dpc_copy_d2h(c, color, g->color, sizeof(int) * static_cast<size_t>(G->n));
+  if (st == DPC_OK) {
+    // Jones-Plassmann counts down higher-priority neighbours through the
+    // reverse arcs: an uncolored vertex means the input was not symmetric.
+    for (int64_t v = 0; v < G->n; v++)
+      if (color[v] < 0) {
+        st = fail(DPC_E_INVALID, "coloring needs a symmetric graph (vertex " + std::to_string(v) +
+                                     " has an arc without its reverse)");
+        break;
+      }
+  }
   if (st == DPC_OK && ncolors) *ncolors = mp->result_count;
   dpc_dgraph_free(g);
   return st;

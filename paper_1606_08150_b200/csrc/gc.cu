@@ -1,0 +1,563 @@
+// Graph coloring (GC) in five variants: greedy first-fit in descending
+// priority order, priority(v) = (mix64(v ^ seed), v) ("greedy
+// first-fit coloring under canonical node order"; :468 determinism).
+//
+// Parallel form: data-driven Jones-Plassmann.  cnt[v] = number of
+// higher-priority neighbours not yet colored.  A vertex is ready when
+// cnt[v] == 0; it takes color mex{color[u] : u higher neighbour} — exactly the
+// color sequential greedy gives it, because in sequential order the colored
+// neighbours of v are precisely its higher neighbours — and decrements cnt[]
+// of its lower neighbours, appending those that reach 0 to the next round's
+// frontier.  Output is therefore bit-identical to the sequential oracle for
+// every variant and schedule.
+//
+// Two irregular loops per vertex, both consolidated:
+//   init pass  : count higher neighbours  (chunk items, warp per chunk, sum)
+//   color pass : mex + decrements         (vertex items, block per item with a
+//                shared-memory color bitmap — the SoloBlock drain shape,
+//                transform.hpp:545-563, because mex does not split across
+//                chunks)
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "ctx.h"
+
+namespace cg = cooperative_groups;
+
+namespace dpc {
+namespace gc {
+
+using dev::Item;
+using dev::kFull;
+using dev::Pool;
+using dev::RunHeader;
+
+constexpr unsigned kBitmapWords = 1024;  // 32768 colors per window in the block drain
+
+struct Ctr {
+  unsigned fsize[3];
+  unsigned pool[3];
+  unsigned iters;
+  int maxcolor;
+  unsigned pad[8];
+};
+
+struct Args {
+  const unsigned* __restrict__ rowptr;
+  const int* __restrict__ col;
+  int* color;
+  unsigned* cnt;
+  unsigned* front0;
+  unsigned* front1;
+  Ctr* ctr;
+  Pool pool;
+  RunHeader* hdr;
+  unsigned long long seed;
+  unsigned n;
+  unsigned threshold;
+  unsigned chunk;
+  unsigned child_threads;
+  unsigned child_blocks;
+  unsigned it;
+  unsigned fsize;
+};
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ unsigned long long prio(const Args& a, unsigned v) {
+  return mix64(static_cast<unsigned long long>(v) ^ a.seed);
+}
+
+// u precedes v in the greedy order
+__device__ __forceinline__ bool higher(unsigned u, unsigned long long pu, unsigned v,
+                                       unsigned long long pv) {
+  return pu > pv || (pu == pv && u > v);
+}
+
+__device__ __forceinline__ unsigned* cur_front(const Args& a, unsigned it) {
+  return (it & 1) ? a.front1 : a.front0;
+}
+__device__ __forceinline__ unsigned* next_front(const Args& a, unsigned it) {
+  return (it & 1) ? a.front0 : a.front1;
+}
+
+__device__ __forceinline__ void push(const Args& a, unsigned it, unsigned v) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(&a.ctr->fsize[(it + 1) % 3], g.size());
+  base = g.shfl(base, 0);
+  next_front(a, it)[base + g.thread_rank()] = v;
+}
+
+// --------------------------------------------------------------- init pass
+__device__ __forceinline__ unsigned count_higher(const Args& a, unsigned v, unsigned b, unsigned e,
+                                                 unsigned step, unsigned start) {
+  const unsigned long long pv = prio(a, v);
+  unsigned c = 0;
+  for (unsigned k = b + start; k < e; k += step) {
+    unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+    if (u != v && higher(u, prio(a, u), v, pv)) c++;
+  }
+  return c;
+}
+
+__device__ __forceinline__ void init_drain(const Args& a, const Item* items, unsigned count,
+                                           unsigned gwarp, unsigned nwarps) {
+  for (unsigned i = gwarp; i < count; i += nwarps) {
+    Item t = items[i];
+    unsigned e = min(t.begin + a.chunk, __ldg(a.rowptr + t.v + 1));
+    unsigned c = dev::warp_sum(count_higher(a, t.v, t.begin, e, 32, dev::lane_id()));
+    if (dev::lane_id() == 0 && c) atomicAdd(a.cnt + t.v, c);
+  }
+}
+
+__global__ void __launch_bounds__(256) init_child(Args a, const Item* items, unsigned count) {
+  init_drain(a, items, count, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+             (gridDim.x * blockDim.x) >> 5);
+}
+
+// basic-dp init child: <<<ceil(deg/T), T>>>, one arc per thread
+__global__ void __launch_bounds__(256) init_basic_child(Args a, unsigned v, unsigned b, unsigned e) {
+  unsigned k = b + blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned c = 0;
+  if (k < e) {
+    unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+    c = (u != v && higher(u, prio(a, u), v, prio(a, v))) ? 1u : 0u;
+  }
+  c = dev::warp_sum(c);
+  if (dev::lane_id() == 0 && c) atomicAdd(a.cnt + v, c);
+}
+
+// variant: 0 flat, 1 basic, 2 warp, 3 block, 4 grid(CDP) — one parent for the
+// init pass over all vertices.
+template <int V>
+__global__ void __launch_bounds__(256) init_parent(Args a) {
+  __shared__ unsigned s_base;
+  unsigned v = blockIdx.x * blockDim.x + threadIdx.x, b = 0, e = 0, want = 0;
+  if (v < a.n) {
+    b = __ldg(a.rowptr + v);
+    e = __ldg(a.rowptr + v + 1);
+    if (V == 0 || e - b <= a.threshold) {
+      a.cnt[v] = count_higher(a, v, b, e, 1, 0);
+    } else if (V == 1) {
+      init_basic_child<<<dev::ceil_div(e - b, a.child_threads), a.child_threads, 0,
+                         cudaStreamFireAndForget>>>(a, v, b, e);
+      dev::note_launch(a.hdr);
+    } else {
+      want = dev::nchunks(e - b, a.chunk);
+    }
+  }
+  if (V == 0 || V == 1) return;
+  if (V == 3) {
+    unsigned bt;
+    unsigned off = dev::block_excl_scan(want, &bt);
+    if (threadIdx.x == 0 && bt) s_base = atomicAdd(&a.ctr->pool[0], bt);
+    __syncthreads();
+    if (want) {
+      dev::write_chunks(a.pool, a.hdr, s_base + off, v, b, e, a.chunk);
+      __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && bt && s_base < a.pool.cap) {
+      unsigned c = min(bt, a.pool.cap - s_base);
+      init_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
+                   cudaStreamFireAndForget>>>(a, a.pool.items + s_base, c);
+      dev::note_launch(a.hdr);
+    }
+    return;
+  }
+  unsigned wb, wt;
+  unsigned at = dev::warp_reserve(&a.ctr->pool[0], want, &wb, &wt);
+  if (want) {
+    dev::write_chunks(a.pool, a.hdr, at, v, b, e, a.chunk);
+    __threadfence();
+  }
+  if (V == 2) {
+    if (wt) {
+      unsigned leader = __ffs(__ballot_sync(kFull, want != 0)) - 1;
+      __syncwarp();
+      if (dev::lane_id() == leader && wb < a.pool.cap) {
+        unsigned c = min(wt, a.pool.cap - wb);
+        init_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
+                     cudaStreamFireAndForget>>>(a, a.pool.items + wb, c);
+        dev::note_launch(a.hdr);
+      }
+    }
+    return;
+  }
+  // V == 4: grid-level
+  if (dev::grid_last_block(&a.hdr->ticket) && threadIdx.x == 0) {
+    unsigned c = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[0]), a.pool.cap);
+    if (c) {
+      init_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
+                   cudaStreamFireAndForget>>>(a, a.pool.items, c);
+      dev::note_launch(a.hdr);
+    }
+  }
+}
+
+// frontier 0 = vertices with no higher neighbour
+__global__ void __launch_bounds__(256) seed_kernel(Args a) {
+  unsigned v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < a.n && a.cnt[v] == 0) push(a, 0xffffffffu /* it = -1 -> next = 0 */, v);
+}
+
+// --------------------------------------------------------------- color pass
+// Thread-serial color of v (light vertices; the flat variant for all).
+__device__ __forceinline__ void color_serial(const Args& a, unsigned it, unsigned v, unsigned b,
+                                             unsigned e) {
+  const unsigned long long pv = prio(a, v);
+  unsigned long long used = 0;
+  for (unsigned k = b; k < e; k++) {
+    unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+    if (u == v) continue;
+    if (higher(u, prio(a, u), v, pv)) {
+      int c = __ldcg(a.color + u);
+      if (c < 64) used |= 1ull << c;
+    } else if (atomicSub(a.cnt + u, 1u) == 1u) {
+      push(a, it, u);
+    }
+  }
+  int mex;
+  if (~used) {
+    mex = __ffsll(static_cast<long long>(~used)) - 1;
+  } else {  // windowed mex: colors >= 64 (only for high-degree vertices)
+    mex = -1;
+    for (int base = 64; mex < 0; base += 64) {
+      unsigned long long w = 0;
+      for (unsigned k = b; k < e; k++) {
+        unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+        if (u != v && higher(u, prio(a, u), v, pv)) {
+          int c = __ldcg(a.color + u) - base;
+          if (c >= 0 && c < 64) w |= 1ull << c;
+        }
+      }
+      if (~w) mex = base + __ffsll(static_cast<long long>(~w)) - 1;
+    }
+  }
+  a.color[v] = mex;
+  atomicMax(&a.ctr->maxcolor, mex);
+}
+
+// Block-cooperative color of v (SoloBlock drain).  All threads call.
+__device__ void color_block(const Args& a, unsigned it, unsigned v, unsigned* bm, int* s_mex) {
+  const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+  const unsigned long long pv = prio(a, v);
+  int mex = -1;
+  for (int base = 0; mex < 0; base += kBitmapWords * 32) {
+    for (unsigned i = threadIdx.x; i < kBitmapWords; i += blockDim.x) bm[i] = 0;
+    if (threadIdx.x == 0) *s_mex = 0x7fffffff;
+    __syncthreads();
+    for (unsigned k = b + threadIdx.x; k < e; k += blockDim.x) {
+      unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+      if (u == v) continue;
+      if (higher(u, prio(a, u), v, pv)) {
+        int c = __ldcg(a.color + u) - base;
+        if (c >= 0 && c < static_cast<int>(kBitmapWords * 32)) atomicOr(bm + (c >> 5), 1u << (c & 31));
+      } else if (base == 0 && atomicSub(a.cnt + u, 1u) == 1u) {
+        push(a, it, u);
+      }
+    }
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < kBitmapWords; i += blockDim.x) {
+      unsigned free_bits = ~bm[i];
+      if (free_bits) atomicMin(s_mex, static_cast<int>(i * 32 + __ffs(free_bits) - 1));
+    }
+    __syncthreads();
+    if (*s_mex != 0x7fffffff) mex = base + *s_mex;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.color[v] = mex;
+    atomicMax(&a.ctr->maxcolor, mex);
+  }
+}
+
+__device__ __forceinline__ void color_drain(const Args& a, unsigned it, const Item* items,
+                                            unsigned count, unsigned first, unsigned stride) {
+  __shared__ unsigned bm[kBitmapWords];
+  __shared__ int s_mex;
+  for (unsigned i = first; i < count; i += stride) color_block(a, it, items[i].v, bm, &s_mex);
+}
+
+__global__ void __launch_bounds__(256) color_child(Args a, const Item* items, unsigned count) {
+  color_drain(a, a.it, items, count, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(256) color_basic_child(Args a, unsigned v) {
+  __shared__ unsigned bm[kBitmapWords];
+  __shared__ int s_mex;
+  color_block(a, a.it, v, bm, &s_mex);
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) color_parent(Args a) {
+  __shared__ unsigned s_base;
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x, v = 0, want = 0;
+  if (i < a.fsize) {
+    v = cur_front(a, a.it)[i];
+    unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+    if (V == 0 || e - b <= a.threshold) {
+      color_serial(a, a.it, v, b, e);
+    } else if (V == 1) {
+      color_basic_child<<<1, a.child_threads, 0, cudaStreamFireAndForget>>>(a, v);
+      dev::note_launch(a.hdr);
+    } else {
+      want = 1;
+    }
+  }
+  if (V == 0 || V == 1) return;
+  const unsigned slot = a.it % 3;
+  if (V == 3) {
+    unsigned bt;
+    unsigned off = dev::block_excl_scan(want, &bt);
+    if (threadIdx.x == 0 && bt) s_base = atomicAdd(&a.ctr->pool[slot], bt);
+    __syncthreads();
+    if (want) {
+      if (s_base + off < a.pool.cap) a.pool.items[s_base + off] = Item{v, 0};
+      else atomicOr(&a.hdr->overflow, 1u);
+      __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && bt && s_base < a.pool.cap) {
+      unsigned c = min(bt, a.pool.cap - s_base);
+      unsigned nb = a.child_blocks ? min(c, a.child_blocks) : c;
+      color_child<<<nb, a.child_threads, 0, cudaStreamFireAndForget>>>(a, a.pool.items + s_base, c);
+      dev::note_launch(a.hdr);
+    }
+    return;
+  }
+  unsigned wb, wt;
+  unsigned at = dev::warp_reserve(&a.ctr->pool[slot], want, &wb, &wt);
+  if (want) {
+    if (at < a.pool.cap) a.pool.items[at] = Item{v, 0};
+    else atomicOr(&a.hdr->overflow, 1u);
+    __threadfence();
+  }
+  if (V == 2) {
+    if (wt) {
+      unsigned leader = __ffs(__ballot_sync(kFull, want != 0)) - 1;
+      __syncwarp();
+      if (dev::lane_id() == leader && wb < a.pool.cap) {
+        unsigned c = min(wt, a.pool.cap - wb);
+        unsigned nb = a.child_blocks ? min(c, a.child_blocks) : c;
+        color_child<<<nb, a.child_threads, 0, cudaStreamFireAndForget>>>(a, a.pool.items + wb, c);
+        dev::note_launch(a.hdr);
+      }
+    }
+    return;
+  }
+  if (dev::grid_last_block(&a.hdr->ticket) && threadIdx.x == 0) {
+    unsigned c = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[slot]), a.pool.cap);
+    if (c) {
+      unsigned nb = a.child_blocks ? min(c, a.child_blocks) : c;
+      color_child<<<nb, a.child_threads, 0, cudaStreamFireAndForget>>>(a, a.pool.items, c);
+      dev::note_launch(a.hdr);
+    }
+  }
+}
+
+__device__ __forceinline__ void rotate(const Args& a, unsigned it) {
+  unsigned used = a.ctr->pool[it % 3];
+  atomicAdd(&a.hdr->aux1, used);
+  atomicMax(&a.hdr->count, used);
+  a.ctr->fsize[(it + 2) % 3] = 0;
+  a.ctr->pool[(it + 2) % 3] = 0;
+}
+
+__global__ void __launch_bounds__(32) rotate_kernel(Args a) {
+  if (threadIdx.x == 0) rotate(a, a.it);
+}
+
+__global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iters) {
+  __shared__ unsigned bm[kBitmapWords];
+  __shared__ int s_mex;
+  cg::grid_group grid = cg::this_grid();
+  const unsigned stride = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  // init pass: light vertices inline, heavy -> chunk items in pool[0]
+  for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
+    unsigned v = base + threadIdx.x, b = 0, e = 0, want = 0;
+    if (v < a.n) {
+      b = __ldg(a.rowptr + v);
+      e = __ldg(a.rowptr + v + 1);
+      if (e - b <= a.threshold) a.cnt[v] = count_higher(a, v, b, e, 1, 0);
+      else want = dev::nchunks(e - b, a.chunk);
+    }
+    unsigned wb, wt;
+    unsigned at = dev::warp_reserve(&a.ctr->pool[0], want, &wb, &wt);
+    if (want) dev::write_chunks(a.pool, a.hdr, at, v, b, e, a.chunk);
+  }
+  grid.sync();
+  init_drain(a, a.pool.items, min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[0]), a.pool.cap),
+             gtid >> 5, stride >> 5);
+  grid.sync();
+  if (gtid == 0) {
+    atomicAdd(&a.hdr->aux1, a.ctr->pool[0]);
+    a.ctr->pool[0] = 0;
+  }
+  for (unsigned v = gtid; v < a.n; v += stride)
+    if (a.cnt[v] == 0) push(a, 0xffffffffu, v);
+  grid.sync();
+  unsigned it = 0;
+  for (; it < max_iters; it++) {
+    const unsigned fs = *reinterpret_cast<volatile unsigned*>(&a.ctr->fsize[it % 3]);
+    if (fs == 0) break;
+    for (unsigned base = blockIdx.x * blockDim.x; base < fs; base += stride) {
+      unsigned i = base + threadIdx.x, v = 0, want = 0;
+      if (i < fs) {
+        v = cur_front(a, it)[i];
+        unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+        if (e - b <= a.threshold) color_serial(a, it, v, b, e);
+        else want = 1;
+      }
+      unsigned wb, wt;
+      unsigned at = dev::warp_reserve(&a.ctr->pool[it % 3], want, &wb, &wt);
+      if (want) {
+        if (at < a.pool.cap) a.pool.items[at] = Item{v, 0};
+        else atomicOr(&a.hdr->overflow, 1u);
+      }
+    }
+    grid.sync();
+    unsigned c = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[it % 3]), a.pool.cap);
+    for (unsigned i = blockIdx.x; i < c; i += gridDim.x) color_block(a, it, a.pool.items[i].v, bm, &s_mex);
+    if (gtid == 0) rotate(a, it);
+    grid.sync();
+  }
+  if (gtid == 0) a.ctr->iters = it;
+}
+
+}  // namespace gc
+}  // namespace dpc
+
+using namespace dpc;
+
+extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t seed,
+                                       const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
+  Cfg c;
+  dpc_status st = resolve_cfg(ctx, DPC_APP_COLOR, cfg, &c);
+  if (st != DPC_OK) return st;
+  if (c.parent_threads != 256 || c.child_threads > 256)
+    return fail(DPC_E_INVALID, "GC kernels are built for parent_threads = 256, child_threads <= 256");
+  if (!g->ctr) {
+    DPC_CUDA(cudaMalloc(&g->ctr, 64));
+    DPC_CUDA(cudaMallocHost(&g->ctr_host, 64));
+  }
+  static_assert(sizeof(gc::Ctr) == 64, "Ctr must fit the 64-byte counter block");
+  gc::Args a;
+  a.rowptr = g->rowptr;
+  a.col = g->col;
+  a.color = g->color;
+  a.cnt = g->stamp;
+  a.front0 = g->front[0];
+  a.front1 = g->front[1];
+  a.ctr = reinterpret_cast<gc::Ctr*>(g->ctr);
+  a.hdr = g->hdr;
+  a.seed = seed;
+  a.n = static_cast<unsigned>(g->n);
+  a.threshold = c.threshold;
+  a.chunk = c.chunk;
+  a.child_threads = c.child_threads;
+  a.child_blocks = c.child_blocks;
+  a.it = 0;
+  a.fsize = 0;
+  if (c.variant != DPC_FLAT && c.variant != DPC_BASIC) {
+    // init pass uses chunk items, color pass one item per heavy vertex
+    uint64_t need = std::max(pool_need(g, c.threshold, c.chunk), pool_need(g, c.threshold, 1u << 30));
+    st = ensure_pool(g, need);
+    if (st != DPC_OK) return st;
+  }
+  a.pool = dev::Pool{g->items, g->cap};
+  st = ensure_pending_for(ctx, g, c.variant, c.threshold, c.parent_threads);
+  if (st != DPC_OK) return st;
+  st = begin_run(ctx, g->hdr);
+  if (st != DPC_OK) return st;
+  cudaStream_t s = ctx->stream;
+  const size_t nv = static_cast<size_t>(std::max<int64_t>(g->n, 1));
+  DPC_CUDA(cudaMemsetAsync(g->ctr, 0, 64, s));
+  DPC_CUDA(cudaMemsetAsync(g->stamp, 0, sizeof(unsigned) * nv, s));
+  DPC_CUDA(cudaMemsetAsync(g->color, 0xff, sizeof(int) * nv, s));
+  auto* ctr_host = reinterpret_cast<gc::Ctr*>(g->ctr_host);
+  int64_t host_launches = 0, iters = 0;
+  const unsigned nb = std::max(1u, dev::ceil_div(a.n, 256u));
+  if (a.n == 0) {
+    ctr_host->maxcolor = -1;
+  } else if (c.variant == DPC_GRID && c.grid_persistent) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(gc::grid_persistent),
+                                                  256, 0);
+    int blocks = std::max(1, per_sm) * ctx->sms;
+    unsigned max_iters = a.n + 1;
+    void* args[] = {&a, &max_iters};
+    DPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(gc::grid_persistent),
+                                         dim3(blocks), dim3(256), args, 0, s));
+    host_launches = 1;
+    DPC_CUDA(cudaMemcpyAsync(ctr_host, a.ctr, sizeof(gc::Ctr), cudaMemcpyDeviceToHost, s));
+    DPC_CUDA(cudaStreamSynchronize(s));
+    iters = ctr_host->iters;
+  } else {
+    switch (c.variant) {
+      case DPC_FLAT: gc::init_parent<0><<<nb, 256, 0, s>>>(a); break;
+      case DPC_BASIC: gc::init_parent<1><<<nb, 256, 0, s>>>(a); break;
+      case DPC_WARP: gc::init_parent<2><<<nb, 256, 0, s>>>(a); break;
+      case DPC_BLOCK: gc::init_parent<3><<<nb, 256, 0, s>>>(a); break;
+      default: gc::init_parent<4><<<nb, 256, 0, s>>>(a); break;
+    }
+    DPC_CUDA(cudaGetLastError());
+    // pool slot 0 is reused by round 0: clear it after the init children ran
+    DPC_CUDA(cudaMemsetAsync(&a.ctr->pool[0], 0, sizeof(unsigned), s));
+    gc::seed_kernel<<<nb, 256, 0, s>>>(a);
+    host_launches += 2;
+    DPC_CUDA(cudaGetLastError());
+    DPC_CUDA(cudaMemcpyAsync(&ctr_host->fsize[0], &a.ctr->fsize[0], sizeof(unsigned),
+                             cudaMemcpyDeviceToHost, s));
+    DPC_CUDA(cudaStreamSynchronize(s));
+    unsigned fsize = ctr_host->fsize[0];
+    for (unsigned it = 0; fsize > 0 && it <= a.n; it++) {
+      a.it = it;
+      a.fsize = fsize;
+      const unsigned pb = std::max(1u, dev::ceil_div(fsize, 256u));
+      switch (c.variant) {
+        case DPC_FLAT: gc::color_parent<0><<<pb, 256, 0, s>>>(a); break;
+        case DPC_BASIC: gc::color_parent<1><<<pb, 256, 0, s>>>(a); break;
+        case DPC_WARP: gc::color_parent<2><<<pb, 256, 0, s>>>(a); break;
+        case DPC_BLOCK: gc::color_parent<3><<<pb, 256, 0, s>>>(a); break;
+        default: gc::color_parent<4><<<pb, 256, 0, s>>>(a); break;
+      }
+      gc::rotate_kernel<<<1, 32, 0, s>>>(a);
+      host_launches += 2;
+      DPC_CUDA(cudaGetLastError());
+      DPC_CUDA(cudaMemcpyAsync(&ctr_host->fsize[(it + 1) % 3], &a.ctr->fsize[(it + 1) % 3],
+                               sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      DPC_CUDA(cudaStreamSynchronize(s));
+      fsize = ctr_host->fsize[(it + 1) % 3];
+      iters = it + 1;
+    }
+    DPC_CUDA(cudaMemcpyAsync(ctr_host, a.ctr, sizeof(gc::Ctr), cudaMemcpyDeviceToHost, s));
+    DPC_CUDA(cudaStreamSynchronize(s));
+  }
+  DPC_CUDA(cudaMemcpyAsync(g->hdr_host, g->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
+  DPC_CUDA(cudaStreamSynchronize(s));
+  if (g->hdr_host->overflow & 2u) return fail(DPC_E_CUDA, "a device-side (CDP2) launch failed");
+  if (g->hdr_host->overflow & 1u) return fail(DPC_E_OVERFLOW, "consolidation pool overflow");
+  if (met) {
+    met->child_launch_count += g->hdr_host->launches;
+    met->host_launches += host_launches;
+    met->iterations += iters;
+    met->edges_processed += 2 * g->m;
+    met->buffer_items_inserted += g->hdr_host->aux1;
+    met->pool_peak = std::max<int64_t>(met->pool_peak, g->hdr_host->count);
+    met->result_count = ctr_host->maxcolor + 1;
+  }
+  return DPC_OK;
+}

@@ -2,7 +2,6 @@
 #include "ctx.h"
 using namespace dpc;
 extern "C" {
-dpc_status dpc_color_device(dpc_ctx*, dpc_dgraph*, uint64_t, const dpc_launch_cfg*, dpc_metrics*) { return fail(DPC_E_INVALID, "GC not implemented yet"); }
 dpc_status dpc_comm_unique_id(uint8_t*) { return fail(DPC_E_INVALID, "multi-GPU not implemented yet"); }
 dpc_status dpc_comm_init(dpc_ctx*, int32_t, int32_t, const uint8_t*, dpc_comm**) { return fail(DPC_E_INVALID, "multi-GPU not implemented yet"); }
 void dpc_comm_destroy(dpc_comm*) {}

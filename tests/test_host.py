@@ -1,0 +1,214 @@
+"""Host layer (CPU only): the C ABI library loads and exports every symbol
+include/dpc.h declares; generators, loaders and validators behave as the
+reference's workloads spec says; errors are typed."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1606_08150_b200 as dpc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "dpc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dpc_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_abi_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", dpc.lib_path()], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (dpc_[a-z0-9_]+)", out))
+    declared = _declared()
+    assert len(declared) > 40
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    # the Python binding covers them too
+    assert set(dpc.exported_symbols()) <= exported
+
+
+def test_libdpc_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", dpc.lib_path()], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_no_cuda_device_is_loud():
+    """Without a GPU the run path fails with a typed CUDA error — no CPU fallback."""
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if has_gpu:
+        pytest.skip("GPU present")
+    with pytest.raises(dpc.DpcError) as e:
+        dpc.Context(0)
+    assert e.value.kind == "cuda"
+
+
+def test_rmat_shape_and_determinism():
+    g1 = dpc.gen_rmat(10, 16, seed=5, values=True)
+    g2 = dpc.gen_rmat(10, 16, seed=5, values=True)
+    assert g1.n == 1024 and g1.m == 16384
+    for a, b in [(g1.rowptr, g2.rowptr), (g1.col, g2.col), (g1.w, g2.w), (g1.val, g2.val)]:
+        assert np.array_equal(a, b)
+    g1.validate()
+    assert g1.w.min() >= 1 and g1.w.max() <= 255
+    assert g1.val.min() > 0 and g1.val.max() <= 1.0
+    # rows sorted by column (deterministic order for any thread count)
+    for v in range(0, g1.n, 97):
+        r = g1.col[g1.rowptr[v]:g1.rowptr[v + 1]]
+        assert np.all(np.diff(r) >= 0)
+    g3 = dpc.gen_rmat(10, 16, seed=6)
+    assert not np.array_equal(g1.col, g3.col)
+
+
+def test_rmat_is_skewed():
+    g = dpc.gen_rmat(14, 16, seed=1)
+    deg = g.degrees()
+    assert deg.max() > 50 * deg.mean()          # power-law hub
+    assert (deg == 0).mean() > 0.2               # R-MAT leaves many isolated ids
+
+
+def test_rmat_thread_count_independent(tmp_path):
+    code = ("import paper_1606_08150_b200 as d, hashlib;"
+            "g=d.gen_rmat(12,16,seed=3,values=True,symmetric=True);"
+            "print(hashlib.sha1(g.col.tobytes()+g.rowptr.tobytes()).hexdigest())")
+    outs = []
+    for t in ("1", "3"):
+        env = dict(os.environ, DPC_HOST_THREADS=t, PYTHONPATH=ROOT)
+        outs.append(subprocess.run(["python", "-c", code], env=env, capture_output=True, text=True,
+                                   check=True).stdout)
+    assert outs[0] == outs[1]
+
+
+def test_symmetric_generator():
+    g = dpc.gen_rmat(9, 8, seed=2, weights=True, symmetric=True)
+    src = np.repeat(np.arange(g.n), g.degrees())
+    pairs = set(zip(src.tolist(), g.col.tolist()))
+    assert all((b, a) in pairs for a, b in pairs)
+    assert all(a != b for a, b in pairs)                      # no self loops
+    assert len(pairs) == g.m                                  # no duplicates
+    wmap = dict(zip(zip(src.tolist(), g.col.tolist()), g.w.tolist()))
+    assert all(wmap[(a, b)] == wmap[(b, a)] for a, b in pairs)  # one weight per edge
+
+
+def test_gen_graph_spec_examples():
+    g = dpc.gen_graph(1, uniform=(0, 0), seed=1)
+    assert g.n == 1 and g.m == 0
+    g = dpc.gen_graph(1000, powerlaw=(2.0, 500), seed=1)
+    assert g.degrees().max() <= 500 and g.degrees().min() >= 1
+    h = np.bincount(g.degrees())
+    assert h[1] > h[2] > h[4] > h[16]                          # skewed histogram
+    g = dpc.gen_graph(500, uniform=(3, 9), seed=4)
+    assert g.degrees().min() >= 3 and g.degrees().max() <= 9
+    a = dpc.gen_graph(800, powerlaw=(1.5, 100), seed=9)
+    b = dpc.gen_graph(800, powerlaw=(1.5, 100), seed=9)
+    assert np.array_equal(a.col, b.col)
+    with pytest.raises(dpc.DpcError):
+        dpc.gen_graph(0, uniform=(1, 2))
+    with pytest.raises(dpc.DpcError):
+        dpc.gen_graph(10, uniform=(1, 2), powerlaw=(2, 3))
+
+
+def test_gen_tree_spec():
+    t = dpc.gen_tree(1, 4, 8, 0.5, seed=1)
+    assert t.n == 1 and t.depth == 1 and t.parent.tolist() == [-1]
+    t = dpc.gen_tree(5, 4, 8, 0.5, seed=1)                     # SPEC.md:430 desk scale
+    assert t.depth == 5
+    assert np.array_equal(dpc.gen_tree(5, 4, 8, 0.5, seed=1).parent, t.parent)   # :431
+    kids = np.diff(t.cstart)
+    assert set(kids[kids > 0].tolist()) <= set(range(4, 9))
+    t = dpc.gen_tree(24, 1, 4, 0.84, seed=1)                   # BASELINE config 4
+    assert t.depth == 24 and 3_000_000 < t.n < 6_000_000
+    with pytest.raises(dpc.DpcError):
+        dpc.gen_tree(0, 1, 2, 0.5)
+    with pytest.raises(dpc.DpcError):
+        dpc.gen_tree(3, 5, 2, 0.5)
+
+
+def test_tree_validation():
+    t = dpc.tree_from_parent([2, 2, -1, 0])
+    assert t.root == 2 and t.depth == 3
+    assert sorted(t.children(2).tolist()) == [0, 1]
+    for bad in ([-1, -1], [1, 0], [-1, 5], [0]):
+        with pytest.raises(dpc.DpcError) as e:
+            dpc.tree_from_parent(bad)
+        assert e.value.kind == "invalid"
+
+
+def test_csr_validation():
+    with pytest.raises(dpc.DpcError):
+        dpc.csr_from_arrays([0, 2, 1], [0, 1])                 # decreasing
+    with pytest.raises(dpc.DpcError):
+        dpc.csr_from_arrays([0, 1], [3])                       # col out of range
+    with pytest.raises(dpc.DpcError):
+        dpc.csr_from_arrays([1, 1], [])                        # rowptr[0] != 0
+    g = dpc.csr_from_arrays([0], [])
+    assert g.n == 0 and g.m == 0
+
+
+def test_csr_io_roundtrip(tmp_path):
+    g = dpc.gen_rmat(8, 8, seed=1, values=True)
+    for name in ("g.txt", "g.bin"):
+        p = str(tmp_path / name)
+        dpc.save_csr(g, p)
+        h = dpc.load_csr(p)
+        assert np.array_equal(g.rowptr, h.rowptr) and np.array_equal(g.col, h.col)
+        assert np.array_equal(g.w, h.w)
+        if name.endswith(".bin"):
+            assert np.array_equal(g.val, h.val)
+    # SPEC.md:473 text format, hand-written; empty graph
+    p = tmp_path / "e.txt"
+    p.write_text("1 0\n0 0\n\n")
+    assert dpc.load_csr(str(p)).n == 1
+    p.write_text("3 2 weighted\n0 1 2 2\n1 2\n5 6\n")
+    h = dpc.load_csr(str(p))
+    assert h.col.tolist() == [1, 2] and h.w.tolist() == [5, 6]
+
+
+@pytest.mark.parametrize("text", ["3 2\n0 1 2 3\n0 1\n",     # rowptr not ending at m
+                                  "2 1\n0 1\n",               # missing columns
+                                  "2 1\n0 1 1\n5\n",          # column out of range
+                                  "x y\n",                    # junk header
+                                  "2 1 weighted\n0 1 1\n0\n"])  # missing weights
+def test_csr_load_errors(tmp_path, text):
+    p = tmp_path / "bad.txt"
+    p.write_text(text)
+    with pytest.raises(dpc.DpcError) as e:
+        dpc.load_csr(str(p))
+    assert e.value.kind == "io"
+
+
+def test_tree_io_roundtrip(tmp_path):
+    t = dpc.gen_tree(6, 1, 4, 0.7, seed=2)
+    p = str(tmp_path / "t.txt")
+    dpc.save_tree(t, p)
+    u = dpc.load_tree(p)
+    assert np.array_equal(t.parent, u.parent) and u.depth == t.depth
+    (tmp_path / "b.txt").write_text("3\n-1 0 7\n")
+    with pytest.raises(dpc.DpcError):
+        dpc.load_tree(str(tmp_path / "b.txt"))
+
+
+def test_launch_cfg_defaults():
+    for app in dpc.APPS:
+        for v, idx in dpc.VARIANTS.items():
+            c = dpc.launch_cfg(app, v)
+            assert c.variant == idx and c.threshold == 32 and c.child_threads % 32 == 0
+    assert dpc.launch_cfg("spmv", "grid").kc_x == 1
+    assert dpc.launch_cfg("spmv", "block").kc_x == 16
+    assert dpc.launch_cfg("spmv", "warp").kc_x == 32
+    c = dpc.launch_cfg("spmv", "grid", grid_cdp=True, chunk=256)
+    assert c.flags & 1 and c.chunk == 256
+
+
+def test_benchmark_registry():
+    for name in ("SSSP", "SpMV", "GC", "TD", "TH"):
+        assert dpc.benchmark(name).name.lower() == name.lower()
+    with pytest.raises(dpc.DpcError):
+        dpc.benchmark("PR")
