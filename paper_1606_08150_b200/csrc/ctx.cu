@@ -61,6 +61,7 @@ dpc_status resolve_cfg(dpc_ctx* ctx, int app, const dpc_launch_cfg* in, Cfg* out
   out->child_threads = static_cast<unsigned>(c.child_threads);
   out->chunk = static_cast<unsigned>(c.chunk);
   out->grid_persistent = !(c.flags & DPC_CFG_GRID_CDP);
+  out->flags = static_cast<unsigned>(c.flags);
   // KC_X: B = max(1, B_occ / X); X = 0 selects "1-1" (no cap).
   unsigned b_occ = static_cast<unsigned>(ctx->sms) *
                    static_cast<unsigned>(ctx->max_threads_per_sm / c.child_threads);

@@ -95,6 +95,7 @@ struct Cfg {
   unsigned child_blocks;  // cap (0 = none)
   unsigned chunk;
   int grid_persistent;  // grid variant as one cooperative persistent kernel
+  unsigned flags;       // raw dpc_launch_cfg.flags (bits >= 8: experiment switches)
 };
 
 dpc_status resolve_cfg(dpc_ctx* ctx, int app, const dpc_launch_cfg* in, Cfg* out);

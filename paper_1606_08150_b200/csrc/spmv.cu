@@ -34,6 +34,13 @@ using dev::kFull;
 using dev::Pool;
 using dev::RunHeader;
 
+// Resident 256-thread blocks per SM requested from ptxas for the drain
+// kernels (latency-bound gathers want warps in flight: 8 -> 64 warps/SM).
+#ifndef DPC_SPMV_MIN_BLOCKS
+#define DPC_SPMV_MIN_BLOCKS 8
+#endif
+constexpr int kMinBlocks = DPC_SPMV_MIN_BLOCKS;
+
 struct Args {
   const unsigned* __restrict__ rowptr;
   const int* __restrict__ col;
@@ -121,19 +128,61 @@ __device__ __forceinline__ float warp_range_dot(const Args& a, unsigned b, unsig
   return dev::warp_sum(s + s1);
 }
 
-// Drains chunk items [0, count) with one warp per item (grid-stride).
+// Drains chunk items [0, count).  A warp takes a batch of 32 items (one
+// descriptor per lane, so the item and rowptr loads are paid once per batch),
+// then streams two items at a time with every lane owning two nonzeros of
+// each: eight independent loads in flight per lane before the x gathers.
+// Per-item overhead is what bounds the drain (most heavy rows are short,
+// 33..1024 nonzeros), so it is amortised instead of vectorising the body.
 __device__ __forceinline__ void drain_items(const Args& a, const Item* items, unsigned count,
                                             unsigned gwarp, unsigned nwarps) {
-  for (unsigned i = gwarp; i < count; i += nwarps) {
-    Item it = items[i];
-    unsigned e = min(it.begin + a.chunk, __ldg(a.rowptr + it.v + 1));
-    float s = warp_range_dot(a, it.begin, e);
-    if (dev::lane_id() == 0) atomicAdd(a.y + it.v, s);
+  const unsigned lane = dev::lane_id();
+  // this warp owns items gwarp, gwarp + nwarps, ... (strided, so the
+  // consecutive chunks of one hub row land on different warps)
+  const unsigned mine = count > gwarp ? (count - gwarp + nwarps - 1) / nwarps : 0;
+  for (unsigned r0 = 0; r0 < mine; r0 += 32) {
+    unsigned v = 0, b = 0, e = 0;
+    if (r0 + lane < mine) {
+      Item t = items[(r0 + lane) * nwarps + gwarp];
+      v = t.v;
+      b = t.begin;
+      e = min(b + a.chunk, __ldg(a.rowptr + v + 1));
+    }
+    const unsigned nb = min(32u, mine - r0);
+    for (unsigned p = 0; p < nb; p += 2) {
+      const unsigned q = p + 1 < nb ? p + 1 : p;
+      const unsigned v0 = __shfl_sync(kFull, v, p), b0 = __shfl_sync(kFull, b, p);
+      const unsigned e0 = __shfl_sync(kFull, e, p);
+      const unsigned v1 = __shfl_sync(kFull, v, q), b1 = __shfl_sync(kFull, b, q);
+      const unsigned e1 = q != p ? __shfl_sync(kFull, e, q) : b1;
+      const unsigned n0 = e0 - b0, n1 = e1 - b1, nm = max(n0, n1);
+      float s0 = 0.f, s1 = 0.f;
+      for (unsigned o = lane; o < nm; o += 64) {
+        const bool p00 = o < n0, p01 = o + 32 < n0, p10 = o < n1, p11 = o + 32 < n1;
+        int c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+        float w00 = 0.f, w01 = 0.f, w10 = 0.f, w11 = 0.f;
+        if (p00) c00 = __ldg(a.col + b0 + o), w00 = __ldg(a.val + b0 + o);
+        if (p01) c01 = __ldg(a.col + b0 + o + 32), w01 = __ldg(a.val + b0 + o + 32);
+        if (p10) c10 = __ldg(a.col + b1 + o), w10 = __ldg(a.val + b1 + o);
+        if (p11) c11 = __ldg(a.col + b1 + o + 32), w11 = __ldg(a.val + b1 + o + 32);
+        float x00 = p00 ? __ldg(a.x + c00) : 0.f, x01 = p01 ? __ldg(a.x + c01) : 0.f;
+        float x10 = p10 ? __ldg(a.x + c10) : 0.f, x11 = p11 ? __ldg(a.x + c11) : 0.f;
+        s0 += w00 * x00 + w01 * x01;
+        s1 += w10 * x10 + w11 * x11;
+      }
+      s0 = dev::warp_sum(s0);
+      s1 = dev::warp_sum(s1);
+      if (lane == 0) {
+        atomicAdd(a.y + v0, s0);
+        if (q != p) atomicAdd(a.y + v1, s1);
+      }
+    }
   }
 }
 
 // <child>_cons: the consolidated child kernel (buffer-draining form).
-__global__ void __launch_bounds__(256) cons_child(Args a, const Item* items, unsigned count) {
+__global__ void __launch_bounds__(256, kMinBlocks) cons_child(Args a, const Item* items,
+                                                              unsigned count) {
   const unsigned nw = (gridDim.x * blockDim.x) >> 5;
   const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   drain_items(a, items, count, gw, nw);
@@ -159,33 +208,90 @@ __global__ void __launch_bounds__(256) basic_child(Args a, unsigned row, unsigne
   }
 }
 
+__device__ __forceinline__ float warp_light_rows(const Args& a, unsigned b, unsigned dl);
+
 __global__ void __launch_bounds__(256) basic_parent(Args a) {
-  unsigned row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= a.n) return;
-  unsigned b = __ldg(a.rowptr + row), e = __ldg(a.rowptr + row + 1);
-  if (e - b > a.threshold) {
+  unsigned row = blockIdx.x * blockDim.x + threadIdx.x, b = 0, e = 0, dl = 0;
+  bool heavy = false;
+  if (row < a.n) {
+    b = __ldg(a.rowptr + row);
+    e = __ldg(a.rowptr + row + 1);
+    heavy = e - b > a.threshold;
+    if (!heavy) dl = e - b;
+  }
+  if (heavy) {
     a.y[row] = 0.f;
     basic_child<<<dev::ceil_div(e - b, a.child_threads), a.child_threads, 0,
                   cudaStreamFireAndForget>>>(a, row, b, e);
     dev::note_launch(a.hdr);
-  } else {
-    a.y[row] = row_serial(a, b, e);
   }
+  float s = warp_light_rows(a, b, dl);
+  if (row < a.n && !heavy) a.y[row] = s;
 }
 
-// Common parent prework for the consolidated variants: inline light rows,
-// zero heavy rows' y, return how many chunk items this thread inserts.
+// Warp-cooperative inline work ("else work(item)" of Fig. 1) for the light
+// rows owned by the 32 lanes of a warp.  The lanes' light nonzeros are
+// concatenated (heavy rows contribute nothing) and swept 32 at a time: every
+// lane finds the row of its element by a 5-step shuffle binary search, the
+// products are summed per row with a segmented shuffle scan, and the segment
+// head hands the partial to the owning lane.  Same result as the thread's
+// serial loop, without the per-thread serial latency chain.  All lanes call;
+// `dl` is this lane's light degree (0 for heavy / out-of-range rows).
+__device__ __forceinline__ float warp_light_rows(const Args& a, unsigned b, unsigned dl) {
+  const unsigned lane = dev::lane_id();
+  const unsigned incl = dev::warp_incl_scan(dl);
+  const unsigned total = __shfl_sync(kFull, incl, 31);
+  const unsigned lo = incl - dl;  // my row's start in the concatenation
+  float acc = 0.f;
+  for (unsigned base = 0; base < total; base += 32) {
+    const unsigned j = base + lane;
+    unsigned l = 0;
+#pragma unroll
+    for (unsigned s = 16; s > 0; s >>= 1) {
+      unsigned c = l + s;
+      if (__shfl_sync(kFull, lo, c) <= j) l = c;
+    }
+    const unsigned bl = __shfl_sync(kFull, b, l), lol = __shfl_sync(kFull, lo, l);
+    float v = 0.f;
+    if (j < total) {
+      unsigned k = bl + (j - lol);
+      v = __ldg(a.val + k) * __ldg(a.x + __ldg(a.col + k));
+    }
+    // segmented suffix sum over lanes holding the same row
+#pragma unroll
+    for (unsigned s = 1; s < 32; s <<= 1) {
+      float ov = __shfl_down_sync(kFull, v, s);
+      unsigned ol = __shfl_down_sync(kFull, l, s);
+      if (lane + s < 32 && ol == l) v += ov;
+    }
+    // the owner lane picks up its segment's sum from the segment head
+    unsigned head = (lo > base ? lo : base) - base;
+    bool mine = dl > 0 && lo < base + 32 && lo + dl > base;
+    float got = __shfl_sync(kFull, v, head & 31u);
+    if (mine) acc += got;
+  }
+  return acc;
+}
+
+// Common parent prework for the DP variants: zero heavy rows' y, do the light
+// rows' inline work warp-cooperatively, return how many chunk items this
+// thread inserts.  All lanes call.
 __device__ __forceinline__ unsigned parent_prework(const Args& a, unsigned row, unsigned* b,
                                                    unsigned* e) {
-  if (row >= a.n) return 0;
-  *b = __ldg(a.rowptr + row);
-  *e = __ldg(a.rowptr + row + 1);
-  if (*e - *b > a.threshold) {
-    a.y[row] = 0.f;
-    return dev::nchunks(*e - *b, a.chunk);
+  unsigned dl = 0, want = 0;
+  if (row < a.n) {
+    *b = __ldg(a.rowptr + row);
+    *e = __ldg(a.rowptr + row + 1);
+    if (*e - *b > a.threshold) {
+      a.y[row] = 0.f;
+      want = dev::nchunks(*e - *b, a.chunk);
+    } else {
+      dl = *e - *b;
+    }
   }
-  a.y[row] = row_serial(a, *b, *e);
-  return 0;
+  float s = warp_light_rows(a, *b, dl);
+  if (row < a.n && !want) a.y[row] = s;
+  return want;
 }
 
 __device__ __forceinline__ unsigned clamp_count(const Args& a, unsigned base, unsigned total) {
@@ -258,21 +364,61 @@ __global__ void __launch_bounds__(256) grid_parent(Args a) {
   }
 }
 
+// Thread-serial prework (experiment switch: the light rows' inline work as
+// the paper's per-thread loop instead of the warp-cooperative sweep).
+__device__ __forceinline__ unsigned parent_prework_serial(const Args& a, unsigned row,
+                                                          unsigned* b, unsigned* e) {
+  if (row >= a.n) return 0;
+  *b = __ldg(a.rowptr + row);
+  *e = __ldg(a.rowptr + row + 1);
+  if (*e - *b > a.threshold) {
+    a.y[row] = 0.f;
+    return dev::nchunks(*e - *b, a.chunk);
+  }
+  a.y[row] = row_serial(a, *b, *e);
+  return 0;
+}
+
+// One warp per item (experiment switch: the unbatched drain).
+__device__ __forceinline__ void drain_items_warp(const Args& a, const Item* items, unsigned count,
+                                                 unsigned gwarp, unsigned nwarps) {
+  for (unsigned i = gwarp; i < count; i += nwarps) {
+    Item it = items[i];
+    unsigned e = min(it.begin + a.chunk, __ldg(a.rowptr + it.v + 1));
+    float s = warp_range_dot(a, it.begin, e);
+    if (dev::lane_id() == 0) atomicAdd(a.y + it.v, s);
+  }
+}
+
 // Grid-level consolidation as one persistent cooperative kernel: insert
 // phase, device-wide barrier, drain phase.  Zero device launches.
-__global__ void __launch_bounds__(256) grid_persistent(Args a) {
+// LM: 1 = warp-cooperative light rows, 0 = thread-serial; DM: 1 = batched
+// drain, 0 = warp per item; MB: min resident blocks for ptxas.
+template <int LM, int DM, int MB>
+__global__ void __launch_bounds__(256, MB) grid_persistent(Args a) {
   cg::grid_group grid = cg::this_grid();
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
     unsigned row = base + threadIdx.x, b = 0, e = 0;
-    unsigned want = parent_prework(a, row, &b, &e);
+    unsigned want = LM ? parent_prework(a, row, &b, &e) : parent_prework_serial(a, row, &b, &e);
     unsigned wbase, wtotal;
     unsigned at = dev::warp_reserve(&a.hdr->count, want, &wbase, &wtotal);
     if (want) dev::write_chunks(a.pool, a.hdr, at, row, b, e, a.chunk);
   }
   grid.sync();
   unsigned cnt = min(*reinterpret_cast<volatile unsigned*>(&a.hdr->count), a.pool.cap);
-  drain_items(a, a.pool.items, cnt, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, stride >> 5);
+  if (DM) drain_items(a, a.pool.items, cnt, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, stride >> 5);
+  else drain_items_warp(a, a.pool.items, cnt, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, stride >> 5);
+}
+
+using PersistentFn = void (*)(Args);
+// [LM][DM][MB == 8]
+static PersistentFn persistent_fn(unsigned flags) {
+  const bool serial = flags & (1u << 8), warp_drain = flags & (1u << 9), low_occ = flags & (1u << 10);
+  static const PersistentFn table[2][2][2] = {
+      {{grid_persistent<0, 0, 4>, grid_persistent<0, 0, 8>}, {grid_persistent<0, 1, 4>, grid_persistent<0, 1, 8>}},
+      {{grid_persistent<1, 0, 4>, grid_persistent<1, 0, 8>}, {grid_persistent<1, 1, 4>, grid_persistent<1, 1, 8>}}};
+  return table[serial ? 0 : 1][warp_drain ? 0 : 1][low_occ ? 0 : 1];
 }
 
 }  // namespace spmv
@@ -331,10 +477,10 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
       case DPC_BLOCK: spmv::block_parent<<<blocks, 256, 0, s>>>(a); break;
       case DPC_GRID:
         if (c.grid_persistent) {
-          int nb = coop_blocks(ctx, reinterpret_cast<const void*>(spmv::grid_persistent), 256);
+          const void* fn = reinterpret_cast<const void*>(spmv::persistent_fn(c.flags));
+          int nb = coop_blocks(ctx, fn, 256);
           void* args[] = {&a};
-          DPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(spmv::grid_persistent),
-                                               dim3(nb), dim3(256), args, 0, s));
+          DPC_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nb), dim3(256), args, 0, s));
         } else {
           spmv::grid_parent<<<blocks, 256, 0, s>>>(a);
         }

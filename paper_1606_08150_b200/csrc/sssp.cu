@@ -132,16 +132,50 @@ __global__ void __launch_bounds__(256) init_kernel(Args a, unsigned source) {
 
 // Prework shared by all parents: returns the vertex's chunk count when its
 // edges are child work, else relaxes them inline and returns 0.
+// Warp-cooperative inline relaxation of the light vertices held by the 32
+// lanes (the parent's "else work(item)"): their edges are concatenated and
+// swept 32 at a time; each lane locates its edge's vertex by a shuffle binary
+// search.  All lanes call; dl = this lane's light degree (0 otherwise).
+__device__ __forceinline__ void warp_light_relax(const Args& a, unsigned it, unsigned b,
+                                                 unsigned du, unsigned dl) {
+  const unsigned lane = dev::lane_id();
+  const unsigned incl = dev::warp_incl_scan(dl);
+  const unsigned total = __shfl_sync(kFull, incl, 31);
+  const unsigned lo = incl - dl;
+  for (unsigned base = 0; base < total; base += 32) {
+    const unsigned j = base + lane;
+    unsigned l = 0;
+#pragma unroll
+    for (unsigned s = 16; s > 0; s >>= 1) {
+      unsigned c = l + s;
+      if (__shfl_sync(kFull, lo, c) <= j) l = c;
+    }
+    const unsigned bl = __shfl_sync(kFull, b, l), lol = __shfl_sync(kFull, lo, l);
+    const unsigned dul = __shfl_sync(kFull, du, l);
+    if (j < total) {
+      unsigned k = bl + (j - lol);
+      unsigned long long nd = static_cast<unsigned long long>(dul) + static_cast<unsigned>(__ldg(a.w + k));
+      if (nd < kInf) relax(a, it, static_cast<unsigned>(__ldg(a.col + k)), static_cast<unsigned>(nd));
+    }
+  }
+}
+
+// Prework shared by the DP parents: returns the vertex's chunk count when its
+// edges are child work; light vertices are relaxed inline (warp-cooperative).
+// All lanes call.
 __device__ __forceinline__ unsigned prework(const Args& a, unsigned it, unsigned i, unsigned fsize,
                                             unsigned* u, unsigned* b, unsigned* e, unsigned* du) {
-  if (i >= fsize) return 0;
-  *u = cur_front(a, it)[i];
-  *b = __ldg(a.rowptr + *u);
-  *e = __ldg(a.rowptr + *u + 1);
-  *du = __ldcg(a.dist + *u);
-  if (*e - *b > a.threshold) return dev::nchunks(*e - *b, a.chunk);
-  relax_serial(a, it, *du, *b, *e);
-  return 0;
+  unsigned want = 0, dl = 0;
+  if (i < fsize) {
+    *u = cur_front(a, it)[i];
+    *b = __ldg(a.rowptr + *u);
+    *e = __ldg(a.rowptr + *u + 1);
+    *du = __ldcg(a.dist + *u);
+    if (*e - *b > a.threshold) want = dev::nchunks(*e - *b, a.chunk);
+    else dl = *e - *b;
+  }
+  warp_light_relax(a, it, *b, *du, dl);
+  return want;
 }
 
 __device__ __forceinline__ void count_work(const Args& a, unsigned deg) {
@@ -175,22 +209,27 @@ __global__ void __launch_bounds__(256) basic_child(Args a, unsigned du, unsigned
   }
 }
 
+__device__ __forceinline__ void warp_light_relax(const Args& a, unsigned it, unsigned b,
+                                                 unsigned du, unsigned dl);
+
 __global__ void __launch_bounds__(256) basic_parent(Args a) {
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned deg = 0;
+  unsigned deg = 0, b = 0, du = 0, dl = 0;
   if (i < a.fsize) {
     unsigned u = cur_front(a, a.it)[i];
-    unsigned b = __ldg(a.rowptr + u), e = __ldg(a.rowptr + u + 1);
-    unsigned du = __ldcg(a.dist + u);
+    b = __ldg(a.rowptr + u);
+    unsigned e = __ldg(a.rowptr + u + 1);
+    du = __ldcg(a.dist + u);
     deg = e - b;
     if (deg > a.threshold) {
       basic_child<<<dev::ceil_div(deg, a.child_threads), a.child_threads, 0,
                     cudaStreamFireAndForget>>>(a, du, b, e);
       dev::note_launch(a.hdr);
     } else {
-      relax_serial(a, a.it, du, b, e);
+      dl = deg;
     }
   }
+  warp_light_relax(a, a.it, b, du, dl);
   count_work(a, deg);
 }
 

@@ -257,23 +257,30 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
   const unsigned gpw = 32 / g;
   const unsigned warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
-  unsigned* off = a.cnt + 1;  // off[L] = start of level L in nodes[]
+  // cnt[0..2]: per-level append counters, triple-buffered so that the
+  // counter read after a level's barrier is never reset or appended to by a
+  // block that already raced ahead (same rotation as sssp::rotate).
+  // off[L] (= cnt + 3) = start of level L in nodes[].
+  unsigned* ctr = a.cnt;
+  unsigned* off = a.cnt + 3;
   unsigned lo = 0, hi = off[1], levels = 0;
   // top-down
   while (hi > lo && levels < max_levels) {
+    unsigned* app = ctr + levels % 3;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(levels + 1) % 3] = 0;
     for (unsigned base = lo + warp_g * gpw; base < hi; base += nwarps * gpw) {
       unsigned i = base + lane / g;
       bool active = i < hi;
       unsigned v = active ? a.nodes[i] : 0;
       unsigned want = count_kids(a, v, sub, g, active);
       unsigned wb, wt;
-      unsigned at = dev::warp_reserve(&a.cnt[0], want, &wb, &wt);
+      unsigned at = hi + dev::warp_reserve(app, want, &wb, &wt);
       write_kids(a, v, sub, g, active && want, at);
     }
     grid.sync();
     levels++;
     lo = hi;
-    hi = min(*reinterpret_cast<volatile unsigned*>(&a.cnt[0]), a.cap);
+    hi = min(hi + *reinterpret_cast<volatile unsigned*>(app), a.cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) off[levels + 1] = hi;
   }
   // bottom-up in reverse level order
@@ -332,10 +339,10 @@ dpc_status dpc_dtree_upload(dpc_ctx* c, const dpc_tree* t, dpc_dtree** out) {
   chk(cudaMalloc(&d->clist, sizeof(int) * n));
   chk(cudaMalloc(&d->result, sizeof(int) * n));
   chk(cudaMalloc(&d->level_nodes, sizeof(unsigned) * std::max<size_t>(1, static_cast<size_t>(internal))));
-  chk(cudaMalloc(&d->level_off, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 4)));
+  chk(cudaMalloc(&d->level_off, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 8)));
   chk(cudaMalloc(&d->hdr, sizeof(dev::RunHeader)));
   chk(cudaMallocHost(&d->hdr_host, sizeof(dev::RunHeader)));
-  chk(cudaMallocHost(&d->off_host, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 4)));
+  chk(cudaMallocHost(&d->off_host, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 8)));
   if (e == cudaSuccess) {
     cudaStream_t s = c->stream;
     chk(cudaMemcpyAsync(d->parent, t->parent, sizeof(int) * n, cudaMemcpyHostToDevice, s));
@@ -401,7 +408,12 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
   const unsigned root = static_cast<unsigned>(d->root);
   const bool root_internal = d->internal > 0;
   // level_off[0] = bump pointer, level_off[1 + L] = start of level L
-  unsigned init[3] = {root_internal ? 1u : 0u, 0u, root_internal ? 1u : 0u};
+  // CDP / flat variants: cnt[0] = bump pointer of nodes[] (root at slot 0).
+  // persistent grid: cnt[0..2] = per-level append counters, cnt[3 + L] =
+  // start of level L.
+  const unsigned r = root_internal ? 1u : 0u;
+  const bool persistent = k.variant == DPC_GRID && k.grid_persistent;
+  unsigned init[5] = {persistent ? 0u : r, 0u, 0u, 0u, r};
   DPC_CUDA(cudaMemcpyAsync(d->level_off, init, sizeof(init), cudaMemcpyHostToDevice, s));
   if (root_internal)
     DPC_CUDA(cudaMemcpyAsync(d->level_nodes, &root, sizeof(unsigned), cudaMemcpyHostToDevice, s));

@@ -1,0 +1,132 @@
+"""Times every app x variant at its BASELINE configuration (device-resident,
+CUDA events, L2 flushed) and checks each result against the CPU oracle.
+
+usage: python tools/prof_apps.py [--apps sssp gc td th spmv] [--reps N] [--json out.json]
+Also importable: run_apps(ctx, apps, reps) -> dict (used by bench.py)."""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1606_08150_b200 as dpc  # noqa: E402
+
+VARIANTS = ["flat", "basic", "warp", "block", "grid"]
+TREE = dict(depth=24, lo=1, hi=4, fill=0.84, seed=1)   # ~3.35M nodes, depth 24
+
+
+def _time(ctx, fn, reps):
+    ts = []
+    for _ in range(reps):
+        ctx.flush_l2()
+        ctx.synchronize()
+        ctx.record(4)
+        fn()
+        ctx.record(5)
+        ts.append(ctx.elapsed_ms(4, 5))
+    return float(np.median(ts)), ts
+
+
+def _summ(res, unit_count, unit):
+    for v, r in res.items():
+        r["g" + unit] = round(unit_count / (r["ms"] * 1e-3) / 1e9, 4)
+    out = {"variants": res}
+    best = min((r["ms"], v) for v, r in res.items() if v in ("warp", "block", "grid"))
+    out["best_consolidated"] = best[1]
+    if "basic" in res:
+        out["best_vs_basic"] = round(res["basic"]["ms"] / best[0], 2)
+    if "flat" in res:
+        out["best_vs_flat"] = round(res["flat"]["ms"] / best[0], 2)
+    return out
+
+
+def app_sssp(ctx, orc, reps, scale=16):
+    g = dpc.gen_rmat(scale, 16, seed=1)
+    s = int(np.argmax(g.degrees()))
+    ref = orc.sssp(g.rowptr, g.col, g.w, s)
+    reached = ref != np.uint32(0xFFFFFFFF)
+    m_reached = int(g.degrees()[reached].sum())
+    dg = dpc.DeviceGraph(ctx, g)
+    res = {}
+    for v in VARIANTS:
+        met = dg.sssp(s, v)  # warm + metrics
+        ok = bool(np.array_equal(dg.get_dist(), ref))
+        ms, _ = _time(ctx, lambda: dg.sssp(s, v, metrics=False), reps if v != "basic" else 1)
+        res[v] = {"ms": round(ms, 4), "bit_exact": ok, "device_launches": met.child_launch_count,
+                  "iterations": met.iterations, "relaxed_edges": met.edges_processed}
+    dg.close()
+    out = _summ(res, m_reached, "teps")
+    out.update({"workload": f"SSSP R-MAT scale {scale}, int weights [1,255], source = max-degree vertex",
+                "unit": "GTEPS (edges of the reached component / time, Graph500)",
+                "m_reached": m_reached})
+    return out
+
+
+def app_gc(ctx, orc, reps, scale=20):
+    g = dpc.gen_rmat(scale, 16, seed=1, weights=False, symmetric=True)
+    ref, k = orc.color(g.rowptr, g.col, 1)
+    dg = dpc.DeviceGraph(ctx, g)
+    res = {}
+    for v in VARIANTS:
+        met = dg.color(1, v)
+        ok = bool(np.array_equal(dg.get_color(), ref))
+        ms, _ = _time(ctx, lambda: dg.color(1, v, metrics=False), reps if v != "basic" else 1)
+        res[v] = {"ms": round(ms, 4), "bit_exact": ok, "colors": met.result_count,
+                  "device_launches": met.child_launch_count, "rounds": met.iterations}
+    dg.close()
+    out = _summ(res, 2 * g.m, "teps")
+    out.update({"workload": f"GC R-MAT scale {scale} symmetrized ({g.m} arcs), JP priorities mix64(v^1)",
+                "unit": "G scanned arcs/s (2 scans per arc)", "colors": k, "arcs": g.m})
+    return out
+
+
+def app_tree(ctx, orc, reps, which):
+    t = dpc.gen_tree(TREE["depth"], TREE["lo"], TREE["hi"], TREE["fill"], TREE["seed"])
+    ref = orc.tree_desc(t.parent) if which == "tree_desc" else orc.tree_height(t.parent)
+    dt = dpc.DeviceTree(ctx, t)
+    res = {}
+    for v in VARIANTS:
+        met = dt.run(which, v)
+        ok = bool(np.array_equal(dt.result(), ref))
+        ms, _ = _time(ctx, lambda: dt.run(which, v, metrics=False), reps if v != "basic" else 1)
+        res[v] = {"ms": round(ms, 4), "bit_exact": ok, "device_launches": met.child_launch_count,
+                  "levels": met.iterations}
+    dt.close()
+    out = _summ(res, t.n - 1, "edges_per_s")
+    out.update({"workload": f"{which} random tree gen_tree(24, 1, 4, 0.84, 1): {t.n} nodes, depth {t.depth}",
+                "unit": "G tree edges/s"})
+    return out
+
+
+def run_apps(ctx, apps, reps=3):
+    from tests._oracle import Oracle
+    orc = Oracle()
+    out = {}
+    for a in apps:
+        t0 = time.time()
+        if a == "sssp":
+            out[a] = app_sssp(ctx, orc, reps)
+        elif a == "gc":
+            out[a] = app_gc(ctx, orc, reps)
+        elif a in ("td", "th"):
+            out[a] = app_tree(ctx, orc, reps, "tree_desc" if a == "td" else "tree_height")
+        out[a]["wall_s"] = round(time.time() - t0, 1)
+    return out
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--apps", nargs="*", default=["sssp", "gc", "td", "th"])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--json", default=None)
+    a = ap.parse_args()
+    ctx = dpc.Context(0)
+    r = run_apps(ctx, a.apps, a.reps)
+    print(json.dumps(r, indent=1))
+    if a.json:
+        with open(a.json, "w") as f:
+            json.dump(r, f, indent=1)
