@@ -82,6 +82,8 @@ typedef struct dpc_csr {
   int32_t* col;
   int32_t* w;
   float* val;
+  int64_t ncols; /* columns; 0 = square (n).  Row slices of a partitioned
+                    matrix keep global column ids and set ncols. */
 } dpc_csr;
 
 /* Rooted tree.  parent[root] = -1.  Children of v are
@@ -108,6 +110,14 @@ typedef struct dpc_tree {
 dpc_status dpc_gen_rmat(int scale, int edgefactor, double a, double b, double c,
                         int32_t wmin, int32_t wmax, uint64_t seed, uint32_t flags,
                         dpc_csr** out);
+
+/* Rows [r0, r1) of exactly the graph dpc_gen_rmat(scale, ...) returns (same
+ * arguments; DPC_GEN_SYMMETRIC not supported), with global column ids:
+ * out->n = r1 - r0, out->ncols = 2^scale.  Each rank of a row-partitioned run
+ * generates only its slice (BASELINE config 5). */
+dpc_status dpc_gen_rmat_rows(int scale, int edgefactor, double a, double b, double c,
+                             int32_t wmin, int32_t wmax, uint64_t seed, uint32_t flags,
+                             int64_t r0, int64_t r1, dpc_csr** out);
 
 /* SPEC.md:435-444 gen_graph(nodeCount, uniform(min,max), seed). */
 dpc_status dpc_gen_graph_uniform(int64_t n, int32_t dmin, int32_t dmax, int32_t wmin,
@@ -237,6 +247,10 @@ float* dpc_dgraph_y(dpc_dgraph* dg);
 uint32_t* dpc_dgraph_dist(dpc_dgraph* dg);
 int32_t* dpc_dgraph_color(dpc_dgraph* dg);
 
+/* %globaltimer stamps (ns) of the last persistent-kernel run whose metrics
+ * were read: kernel start, device-wide barrier, end (phase split). */
+dpc_status dpc_dgraph_phase_ns(dpc_dgraph* dg, uint64_t out[3]);
+
 /* Asynchronous on the context stream (no host sync, no copies). */
 dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* dg, const float* d_x, float* d_y,
                            const dpc_launch_cfg* cfg, dpc_metrics* met);
@@ -277,15 +291,18 @@ dpc_status dpc_comm_unique_id(uint8_t id[128]);
 dpc_status dpc_comm_init(dpc_ctx* ctx, int32_t rank, int32_t world, const uint8_t id[128],
                          dpc_comm** out);
 void dpc_comm_destroy(dpc_comm* comm);
-/* Equal-nnz row split of a CSR with n rows into `world` parts; bounds has
- * world+1 entries. */
+int32_t dpc_comm_rank(dpc_comm* comm);
+int32_t dpc_comm_world(dpc_comm* comm);
+/* Equal-nnz row split of a CSR into `world` parts: bounds[0..world]. */
 dpc_status dpc_partition_rows(const dpc_csr* g, int32_t world, int64_t* bounds);
-/* Distributed SpMV power step: each rank holds rows [r0, r1) of A (global
- * column ids) uploaded as a dgraph; x_full is all-gathered over NCCL from
- * the ranks' y slices, then y_local = A_local x_full.  iters steps. */
-dpc_status dpc_multi_spmv(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, int64_t r0,
-                          int64_t r1, int64_t n_global, int32_t iters,
-                          const dpc_launch_cfg* cfg, dpc_metrics* met);
+/* One distributed SpMV step on a 1-D row partition with equal row blocks
+ * (rank p owns rows / x entries [p*R, (p+1)*R), R = local->n,
+ * local->ncols = R * world): ncclAllGather of every rank's x slice (d_x_local,
+ * R floats) into the handle's x (R * world floats) over NVLink, then
+ * y_local = A_local x with the variant in cfg.  Asynchronous on the context
+ * stream. */
+dpc_status dpc_multi_spmv(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, const float* d_x_local,
+                          float* d_y_local, const dpc_launch_cfg* cfg, dpc_metrics* met);
 
 #ifdef __cplusplus
 }

@@ -28,7 +28,7 @@ import numpy as np
 
 __all__ = [
     "DpcError", "VARIANTS", "APPS", "LaunchCfg", "Metrics", "CsrGraph", "Tree",
-    "gen_rmat", "gen_graph", "gen_tree", "csr_from_arrays", "tree_from_parent",
+    "gen_rmat", "gen_rmat_rows", "partition_rows", "Comm", "gen_graph", "gen_tree", "csr_from_arrays", "tree_from_parent",
     "load_csr", "save_csr", "load_tree", "save_tree", "Context", "DeviceGraph",
     "DeviceTree", "default_context", "run_spmv", "run_sssp", "run_color",
     "run_tree_desc", "run_tree_height", "benchmark", "lib_path",
@@ -69,7 +69,7 @@ class DpcError(RuntimeError):
 class _Csr(C.Structure):
     _fields_ = [("n", C.c_int64), ("m", C.c_int64), ("rowptr", C.POINTER(C.c_int64)),
                 ("col", C.POINTER(C.c_int32)), ("w", C.POINTER(C.c_int32)),
-                ("val", C.POINTER(C.c_float))]
+                ("val", C.POINTER(C.c_float)), ("ncols", C.c_int64)]
 
 
 class _Tree(C.Structure):
@@ -109,6 +109,8 @@ _SIGS = {
     "dpc_abi_version": (C.c_int, []),
     "dpc_gen_rmat": (C.c_int, [C.c_int, C.c_int, _f64, _f64, _f64, _i32, _i32, _u64, _u32,
                                C.POINTER(_CsrP)]),
+    "dpc_gen_rmat_rows": (C.c_int, [C.c_int, C.c_int, _f64, _f64, _f64, _i32, _i32, _u64, _u32,
+                                    _i64, _i64, C.POINTER(_CsrP)]),
     "dpc_gen_graph_uniform": (C.c_int, [_i64, _i32, _i32, _i32, _i32, _u64, _u32, C.POINTER(_CsrP)]),
     "dpc_gen_graph_powerlaw": (C.c_int, [_i64, _f64, _i32, _i32, _i32, _u64, _u32, C.POINTER(_CsrP)]),
     "dpc_gen_tree": (C.c_int, [_i32, _i32, _i32, _f64, _u64, C.POINTER(_TreeP)]),
@@ -142,6 +144,7 @@ _SIGS = {
     "dpc_dgraph_y": (_P, [_P]),
     "dpc_dgraph_dist": (_P, [_P]),
     "dpc_dgraph_color": (_P, [_P]),
+    "dpc_dgraph_phase_ns": (C.c_int, [_P, _P]),
     "dpc_spmv_device": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_sssp_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
@@ -157,9 +160,10 @@ _SIGS = {
     "dpc_comm_unique_id": (C.c_int, [_P]),
     "dpc_comm_init": (C.c_int, [_P, _i32, _i32, _P, C.POINTER(_P)]),
     "dpc_comm_destroy": (None, [_P]),
+    "dpc_comm_rank": (_i32, [_P]),
+    "dpc_comm_world": (_i32, [_P]),
     "dpc_partition_rows": (C.c_int, [_CsrP, _i32, _P]),
-    "dpc_multi_spmv": (C.c_int, [_P, _P, _P, _i64, _i64, _i64, _i32, C.POINTER(LaunchCfg),
-                                 C.POINTER(Metrics)]),
+    "dpc_multi_spmv": (C.c_int, [_P, _P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -202,6 +206,7 @@ class CsrGraph:
         c = handle.contents
         self.n = int(c.n)
         self.m = int(c.m)
+        self.ncols = int(c.ncols) or self.n
         self.rowptr = _view(c.rowptr, self.n + 1, C.c_int64, np.int64)
         self.col = _view(c.col, self.m, C.c_int32, np.int32)
         self.w = _view(c.w, self.m, C.c_int32, np.int32) if c.w else None
@@ -257,6 +262,23 @@ def gen_rmat(scale: int, edgefactor: int = 16, a: float = 0.57, b: float = 0.19,
     _check(_lib.dpc_gen_rmat(scale, edgefactor, a, b, c, wmin, wmax, seed & (2**64 - 1),
                              _gen_flags(weights, values, permute, symmetric), C.byref(h)))
     return CsrGraph(h)
+
+
+def gen_rmat_rows(scale: int, r0: int, r1: int, edgefactor: int = 16, a: float = 0.57,
+                  b: float = 0.19, c: float = 0.19, wmin: int = 1, wmax: int = 255, seed: int = 1,
+                  weights: bool = True, values: bool = False, permute: bool = False) -> CsrGraph:
+    """Rows [r0, r1) of gen_rmat(scale, ...) with global column ids (ncols = 2**scale)."""
+    h = _CsrP()
+    _check(_lib.dpc_gen_rmat_rows(scale, edgefactor, a, b, c, wmin, wmax, seed & (2**64 - 1),
+                                  _gen_flags(weights, values, permute, False), r0, r1, C.byref(h)))
+    return CsrGraph(h)
+
+
+def partition_rows(g: CsrGraph, world: int) -> np.ndarray:
+    """Equal-nnz row split: bounds[0..world]."""
+    b = np.zeros(world + 1, np.int64)
+    _check(_lib.dpc_partition_rows(g._h, world, _ptr(b)))
+    return b
 
 
 def gen_graph(node_count: int, uniform: tuple | None = None, powerlaw: tuple | None = None,
@@ -422,6 +444,12 @@ class DeviceGraph:
         _check(_lib.dpc_copy_d2h(self.ctx.handle, _ptr(d), _lib.dpc_dgraph_color(self._h), d.nbytes))
         return d
 
+    def phase_ns(self):
+        """(start, barrier, end) %globaltimer stamps of the last persistent run read with metrics."""
+        t = np.zeros(3, np.uint64)
+        _check(_lib.dpc_dgraph_phase_ns(self._h, _ptr(t)))
+        return [int(v) for v in t]
+
     def spmv(self, variant="grid", cfg=None, metrics: bool = False):
         """y = A x on the resident vectors (asynchronous unless metrics)."""
         met = Metrics() if metrics else None
@@ -454,6 +482,34 @@ class DeviceGraph:
         h, self._h = getattr(self, "_h", None), None
         if h:
             _lib.dpc_dgraph_free(h)
+
+    __del__ = close
+
+
+class Comm:
+    """dpc_comm: an NCCL communicator for one rank (one process per GPU)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(_lib.dpc_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, ctx: Context, rank: int, world: int, uid: bytes):
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(_lib.dpc_comm_init(ctx.handle, rank, world, buf, C.byref(h)))
+        self._h, self.ctx, self.rank, self.world = h, ctx, rank, world
+
+    def spmv(self, local: "DeviceGraph", d_x_local: int, d_y_local: int, variant="grid", cfg=None):
+        """AllGather x slices over NCCL, then y_local = A_local x (async)."""
+        _check(_lib.dpc_multi_spmv(self.ctx.handle, self._h, local._h, d_x_local, d_y_local,
+                                   _cfg_arg("spmv", variant, cfg), None))
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _lib.dpc_comm_destroy(h)
 
     __del__ = close
 

@@ -32,7 +32,7 @@ struct RunHeader {
   unsigned aux0;       // app-specific
   unsigned aux1;
   unsigned long long work; // edges processed (diagnostic)
-  unsigned pad[6];
+  unsigned long long t[3]; // %globaltimer stamps (ns): start, barrier, end (persistent kernels)
 };
 static_assert(sizeof(RunHeader) == 64, "RunHeader must be 64 bytes");
 
@@ -144,11 +144,22 @@ __device__ __forceinline__ bool grid_last_block(unsigned* ticket) {
   return s_last;
 }
 
-// Records a device-side launch, flags a failed one.
+// Records a device-side launch, flags a failed one (first error code kept in
+// aux0 so the host can name it).
 __device__ __forceinline__ void note_launch(RunHeader* hdr) {
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) atomicOr(&hdr->overflow, 2u);
-  else atomicAdd(&hdr->launches, 1u);
+  if (e != cudaSuccess) {
+    atomicOr(&hdr->overflow, 2u);
+    atomicCAS(&hdr->aux0, 0u, static_cast<unsigned>(e));
+  } else {
+    atomicAdd(&hdr->launches, 1u);
+  }
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 __host__ __device__ __forceinline__ unsigned ceil_div(unsigned a, unsigned b) { return (a + b - 1) / b; }

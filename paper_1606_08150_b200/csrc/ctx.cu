@@ -119,6 +119,14 @@ dpc_status ensure_pool(dpc_dgraph* g, uint64_t need) {
   return DPC_OK;
 }
 
+dpc_status check_header(const RunHeader* h) {
+  if (h->overflow & 2u)
+    return fail(DPC_E_CUDA, std::string("a device-side (CDP2) launch failed: ") +
+                                cudaGetErrorString(static_cast<cudaError_t>(h->aux0)));
+  if (h->overflow & 1u) return fail(DPC_E_OVERFLOW, "consolidation pool overflow");
+  return DPC_OK;
+}
+
 dpc_status begin_run(dpc_ctx* ctx, RunHeader* hdr) {
   DPC_CUDA(cudaMemsetAsync(hdr, 0, sizeof(RunHeader), ctx->stream));
   return DPC_OK;
@@ -127,9 +135,8 @@ dpc_status begin_run(dpc_ctx* ctx, RunHeader* hdr) {
 dpc_status finish_metrics(dpc_ctx* ctx, RunHeader* hdr, RunHeader* hdr_host, dpc_metrics* met) {
   DPC_CUDA(cudaMemcpyAsync(hdr_host, hdr, sizeof(RunHeader), cudaMemcpyDeviceToHost, ctx->stream));
   DPC_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (hdr_host->overflow & 2u)
-    return fail(DPC_E_CUDA, "a device-side (CDP2) launch failed (pending-launch pool exhausted?)");
-  if (hdr_host->overflow & 1u) return fail(DPC_E_OVERFLOW, "consolidation pool overflow");
+  dpc_status st = check_header(hdr_host);
+  if (st != DPC_OK) return st;
   if (met) {
     met->child_launch_count += hdr_host->launches;
     met->buffer_items_inserted += hdr_host->aux1;
@@ -293,7 +300,9 @@ dpc_status dpc_dgraph_upload(dpc_ctx* c, const dpc_csr* h, dpc_dgraph** out) {
   g->ctx = c;
   g->n = h->n;
   g->m = h->m;
+  g->ncols = h->ncols ? h->ncols : h->n;
   const size_t n = static_cast<size_t>(h->n), m = static_cast<size_t>(h->m);
+  const size_t nx = std::max<size_t>(static_cast<size_t>(g->ncols), 1);
   auto cleanup = [&](cudaError_t e, const char* w) {
     dpc_dgraph_free(g);
     return cuda_fail(e, w);
@@ -308,7 +317,7 @@ dpc_status dpc_dgraph_upload(dpc_ctx* c, const dpc_csr* h, dpc_dgraph** out) {
   if ((e = cudaMalloc(&g->col, sizeof(int) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc col");
   if (h->w && (e = cudaMalloc(&g->w, sizeof(int) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc w");
   if (h->val && (e = cudaMalloc(&g->val, sizeof(float) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc val");
-  if ((e = cudaMalloc(&g->x, sizeof(float) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc x");
+  if ((e = cudaMalloc(&g->x, sizeof(float) * nx)) != cudaSuccess) return cleanup(e, "cudaMalloc x");
   if ((e = cudaMalloc(&g->y, sizeof(float) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc y");
   if ((e = cudaMalloc(&g->dist, sizeof(unsigned) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc dist");
   if ((e = cudaMalloc(&g->color, sizeof(int) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc color");
@@ -322,12 +331,18 @@ dpc_status dpc_dgraph_upload(dpc_ctx* c, const dpc_csr* h, dpc_dgraph** out) {
   if (e == cudaSuccess && m) e = cudaMemcpyAsync(g->col, h->col, sizeof(int) * m, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess && m && h->w) e = cudaMemcpyAsync(g->w, h->w, sizeof(int) * m, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess && m && h->val) e = cudaMemcpyAsync(g->val, h->val, sizeof(float) * m, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(g->x, 0, sizeof(float) * nv, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->x, 0, sizeof(float) * nx, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(g->y, 0, sizeof(float) * nv, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(g->hdr, 0, sizeof(RunHeader) * 2, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cleanup(e, "dpc_dgraph_upload copy");
   *out = g;
+  return DPC_OK;
+}
+
+dpc_status dpc_dgraph_phase_ns(dpc_dgraph* g, uint64_t out[3]) {
+  if (!g || !out) return fail(DPC_E_INVALID, "NULL argument");
+  for (int i = 0; i < 3; i++) out[i] = g->hdr_host->t[i];
   return DPC_OK;
 }
 
@@ -342,11 +357,12 @@ dpc_status dpc_spmv_host(dpc_ctx* c, dpc_dgraph* g, const float* x, float* y,
                          const dpc_launch_cfg* cfg, dpc_metrics* met) {
   clear_error();
   if (!c || !g || !x || !y) return fail(DPC_E_INVALID, "NULL argument");
-  const size_t bytes = sizeof(float) * static_cast<size_t>(g->n);
-  DPC_CUDA(cudaMemcpyAsync(g->x, x, bytes, cudaMemcpyHostToDevice, c->stream));
+  const size_t xbytes = sizeof(float) * static_cast<size_t>(g->ncols);
+  const size_t ybytes = sizeof(float) * static_cast<size_t>(g->n);
+  DPC_CUDA(cudaMemcpyAsync(g->x, x, xbytes, cudaMemcpyHostToDevice, c->stream));
   dpc_status st = dpc_spmv_device(c, g, g->x, g->y, cfg, met);
   if (st != DPC_OK) return st;
-  DPC_CUDA(cudaMemcpyAsync(y, g->y, bytes, cudaMemcpyDeviceToHost, c->stream));
+  DPC_CUDA(cudaMemcpyAsync(y, g->y, ybytes, cudaMemcpyDeviceToHost, c->stream));
   DPC_CUDA(cudaStreamSynchronize(c->stream));
   return DPC_OK;
 }

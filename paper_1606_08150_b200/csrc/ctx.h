@@ -30,6 +30,7 @@ struct dpc_ctx {
 struct dpc_dgraph {
   dpc_ctx* ctx = nullptr;
   int64_t n = 0, m = 0;
+  int64_t ncols = 0;           // columns (= n for square graphs); x has ncols entries
   unsigned* rowptr = nullptr;  // n+1 (uint32; m < 2^32)
   int* col = nullptr;
   int* w = nullptr;
@@ -114,6 +115,8 @@ dpc_status ensure_pending_for(dpc_ctx* ctx, dpc_dgraph* g, int variant, unsigned
 dpc_status ensure_pool(dpc_dgraph* g, uint64_t need);
 
 dpc_status begin_run(dpc_ctx* ctx, dpc::dev::RunHeader* hdr);
+// Maps the device-side fault bits of a run header to a status + message.
+dpc_status check_header(const dpc::dev::RunHeader* h);
 dpc_status finish_metrics(dpc_ctx* ctx, dpc::dev::RunHeader* hdr, dpc::dev::RunHeader* hdr_host,
                           dpc_metrics* met);
 

@@ -444,6 +444,7 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
                                        const dpc_launch_cfg* cfg, dpc_metrics* met) {
   clear_error();
   if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
+  if (g->ncols != g->n) return fail(DPC_E_INVALID, "coloring needs a square graph (not a row slice)");
   Cfg c;
   dpc_status st = resolve_cfg(ctx, DPC_APP_COLOR, cfg, &c);
   if (st != DPC_OK) return st;
@@ -548,8 +549,8 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   }
   DPC_CUDA(cudaMemcpyAsync(g->hdr_host, g->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
   DPC_CUDA(cudaStreamSynchronize(s));
-  if (g->hdr_host->overflow & 2u) return fail(DPC_E_CUDA, "a device-side (CDP2) launch failed");
-  if (g->hdr_host->overflow & 1u) return fail(DPC_E_OVERFLOW, "consolidation pool overflow");
+  st = check_header(g->hdr_host);
+  if (st != DPC_OK) return st;
   if (met) {
     met->child_launch_count += g->hdr_host->launches;
     met->host_launches += host_launches;

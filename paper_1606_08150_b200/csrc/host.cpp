@@ -90,9 +90,13 @@ struct EdgeSrc {
   std::function<void(int64_t, uint32_t*, uint32_t*)> edge;
 };
 
+// Rows [r0, r1) only (r1 < 0: all rows); a slice keeps global column ids.
 static dpc_csr* build_csr(const EdgeSrc& es, int32_t wmin, int32_t wmax, uint64_t seed,
-                          uint32_t flags) {
-  const int64_t n = es.n;
+                          uint32_t flags, int64_t r0 = 0, int64_t r1 = -1) {
+  if (r1 < 0) r1 = es.n;
+  const int64_t n = r1 - r0;
+  const uint32_t lo32 = static_cast<uint32_t>(r0), hi32 = static_cast<uint32_t>(r1);
+  auto in_slice = [&](uint32_t s) { return s >= lo32 && s < hi32; };
   const bool sym = flags & DPC_GEN_SYMMETRIC;
   const int64_t arcs = sym ? 2 * es.m : es.m;
   std::vector<uint32_t> src(static_cast<size_t>(arcs)), dst(static_cast<size_t>(arcs));
@@ -117,8 +121,8 @@ static dpc_csr* build_csr(const EdgeSrc& es, int32_t wmin, int32_t wmax, uint64_
     });
     parallel_for(arcs, [&](int64_t lo, int64_t hi) {
       for (int64_t e = lo; e < hi; e++) {
-        if (sym && src[e] == dst[e]) continue;
-        deg[src[e]].fetch_add(1, std::memory_order_relaxed);
+        if ((sym && src[e] == dst[e]) || !in_slice(src[e])) continue;
+        deg[src[e] - lo32].fetch_add(1, std::memory_order_relaxed);
       }
     });
     for (int64_t i = 0; i < n; i++) rowptr[i + 1] = rowptr[i] + deg[i].load();
@@ -132,8 +136,8 @@ static dpc_csr* build_csr(const EdgeSrc& es, int32_t wmin, int32_t wmax, uint64_
     });
     parallel_for(arcs, [&](int64_t lo, int64_t hi) {
       for (int64_t e = lo; e < hi; e++) {
-        if (sym && src[e] == dst[e]) continue;
-        int64_t p = cur[src[e]].fetch_add(1, std::memory_order_relaxed);
+        if ((sym && src[e] == dst[e]) || !in_slice(src[e])) continue;
+        int64_t p = cur[src[e] - lo32].fetch_add(1, std::memory_order_relaxed);
         keys[p] = (static_cast<uint64_t>(dst[e]) << 32) | static_cast<uint64_t>(e);
       }
     });
@@ -159,6 +163,7 @@ static dpc_csr* build_csr(const EdgeSrc& es, int32_t wmin, int32_t wmax, uint64_
   });
   dpc_csr* g = new_csr();
   g->n = n;
+  if (n != es.n) g->ncols = es.n;
   g->rowptr = xalloc<int64_t>(n + 1);
   g->rowptr[0] = 0;
   for (int64_t i = 0; i < n; i++) g->rowptr[i + 1] = g->rowptr[i] + newdeg[i];
@@ -216,8 +221,9 @@ extern "C" {
 const char* dpc_last_error(void) { return g_last_error.c_str(); }
 int dpc_abi_version(void) { return DPC_ABI_VERSION; }
 
-dpc_status dpc_gen_rmat(int scale, int edgefactor, double a, double b, double c, int32_t wmin,
-                        int32_t wmax, uint64_t seed, uint32_t flags, dpc_csr** out) {
+dpc_status dpc_gen_rmat_rows(int scale, int edgefactor, double a, double b, double c,
+                             int32_t wmin, int32_t wmax, uint64_t seed, uint32_t flags, int64_t r0,
+                             int64_t r1, dpc_csr** out) {
   DPC_TRY_BEGIN
   if (!out) return fail(DPC_E_INVALID, "out is NULL");
   if (scale < 1 || scale > 31) return fail(DPC_E_INVALID, "scale must be in [1, 31]");
@@ -250,9 +256,18 @@ dpc_status dpc_gen_rmat(int scale, int edgefactor, double a, double b, double c,
     *s = si;
     *d = di;
   };
-  *out = build_csr(es, wmin, wmax, seed, flags);
+  if (r1 < 0) r1 = n;
+  if (r0 < 0 || r0 > r1 || r1 > n) return fail(DPC_E_INVALID, "row slice out of range");
+  if ((flags & DPC_GEN_SYMMETRIC) && (r0 != 0 || r1 != n))
+    return fail(DPC_E_INVALID, "row slices of symmetrized graphs are not supported");
+  *out = build_csr(es, wmin, wmax, seed, flags, r0, r1);
   return DPC_OK;
   DPC_TRY_END
+}
+
+dpc_status dpc_gen_rmat(int scale, int edgefactor, double a, double b, double c, int32_t wmin,
+                        int32_t wmax, uint64_t seed, uint32_t flags, dpc_csr** out) {
+  return dpc_gen_rmat_rows(scale, edgefactor, a, b, c, wmin, wmax, seed, flags, 0, -1, out);
 }
 
 dpc_status dpc_gen_graph_uniform(int64_t n, int32_t dmin, int32_t dmax, int32_t wmin, int32_t wmax,
@@ -328,8 +343,10 @@ dpc_status dpc_csr_validate(const dpc_csr* g) {
     if (g->rowptr[i + 1] < g->rowptr[i])
       return fail(DPC_E_INVALID, "rowOffsets must be nondecreasing (row " + std::to_string(i) + ")");
   if (g->rowptr[g->n] != g->m) return fail(DPC_E_INVALID, "rowOffsets[nodeCount] must equal edgeCount");
+  if (g->ncols < 0 || g->ncols >= (int64_t{1} << 31)) return fail(DPC_E_INVALID, "bad column count");
+  const int64_t nc = g->ncols ? g->ncols : g->n;
   for (int64_t k = 0; k < g->m; k++)
-    if (g->col[k] < 0 || g->col[k] >= g->n)
+    if (g->col[k] < 0 || g->col[k] >= nc)
       return fail(DPC_E_INVALID, "column index out of range at " + std::to_string(k));
   return DPC_OK;
 }
@@ -338,7 +355,7 @@ dpc_status dpc_csr_create(int64_t n, int64_t m, const int64_t* rowptr, const int
                           const int32_t* w, const float* val, dpc_csr** out) {
   DPC_TRY_BEGIN
   if (!out) return fail(DPC_E_INVALID, "out is NULL");
-  dpc_csr tmp{n, m, const_cast<int64_t*>(rowptr), const_cast<int32_t*>(col), nullptr, nullptr};
+  dpc_csr tmp{n, m, const_cast<int64_t*>(rowptr), const_cast<int32_t*>(col), nullptr, nullptr, 0};
   dpc_status st = dpc_csr_validate(&tmp);
   if (st != DPC_OK) return st;
   std::unique_ptr<dpc_csr, void (*)(dpc_csr*)> g(new_csr(), dpc_csr_free);

@@ -398,6 +398,7 @@ template <int LM, int DM, int MB>
 __global__ void __launch_bounds__(256, MB) grid_persistent(Args a) {
   cg::grid_group grid = cg::this_grid();
   const unsigned stride = gridDim.x * blockDim.x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[0] = dev::global_ns();
   for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
     unsigned row = base + threadIdx.x, b = 0, e = 0;
     unsigned want = LM ? parent_prework(a, row, &b, &e) : parent_prework_serial(a, row, &b, &e);
@@ -406,9 +407,12 @@ __global__ void __launch_bounds__(256, MB) grid_persistent(Args a) {
     if (want) dev::write_chunks(a.pool, a.hdr, at, row, b, e, a.chunk);
   }
   grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[1] = dev::global_ns();
   unsigned cnt = min(*reinterpret_cast<volatile unsigned*>(&a.hdr->count), a.pool.cap);
   if (DM) drain_items(a, a.pool.items, cnt, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, stride >> 5);
   else drain_items_warp(a, a.pool.items, cnt, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, stride >> 5);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&a.hdr->t[2], dev::global_ns());
 }
 
 using PersistentFn = void (*)(Args);

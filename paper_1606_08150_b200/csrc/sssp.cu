@@ -365,6 +365,7 @@ extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t sourc
   clear_error();
   if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
   if (g->m > 0 && !g->w) return fail(DPC_E_INVALID, "graph was uploaded without weights (w)");
+  if (g->ncols != g->n) return fail(DPC_E_INVALID, "SSSP needs a square graph (not a row slice)");
   if (source < 0 || source >= g->n) return fail(DPC_E_INVALID, "source out of range");
   Cfg c;
   dpc_status st = resolve_cfg(ctx, DPC_APP_SSSP, cfg, &c);
@@ -451,7 +452,5 @@ extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t sourc
   }
   DPC_CUDA(cudaMemcpyAsync(g->hdr_host, g->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
   DPC_CUDA(cudaStreamSynchronize(s));
-  if (g->hdr_host->overflow) return fail(g->hdr_host->overflow & 2u ? DPC_E_CUDA : DPC_E_OVERFLOW,
-                                         "SSSP: device launch failure or pool overflow");
-  return DPC_OK;
+  return check_header(g->hdr_host);
 }

@@ -480,8 +480,8 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
   }
   DPC_CUDA(cudaMemcpyAsync(d->hdr_host, d->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
   DPC_CUDA(cudaStreamSynchronize(s));
-  if (d->hdr_host->overflow & 2u) return fail(DPC_E_CUDA, "a device-side (CDP2) launch failed");
-  if (d->hdr_host->overflow & 1u) return fail(DPC_E_OVERFLOW, "tree node buffer overflow");
+  st = check_header(d->hdr_host);
+  if (st != DPC_OK) return st;
   if (met) {
     met->child_launch_count += d->hdr_host->launches;
     met->host_launches += host_launches;

@@ -15,6 +15,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--scale", type=int, default=20)
 ap.add_argument("--cdp", action="store_true")
 ap.add_argument("--chunk", type=int, default=0)
+ap.add_argument("--flags", type=int, default=0)
 a = ap.parse_args()
 ctx = dpc.Context(0)
 g = dpc.gen_rmat(a.scale, 16, seed=1, weights=False, values=True)
@@ -27,10 +28,16 @@ for v in a.variants:
     if a.chunk:
         over["chunk"] = a.chunk
     cfg = dpc.launch_cfg("spmv", v, **over)
+    cfg.flags |= a.flags
     for _ in range(a.reps):
         ctx.flush_l2()
         ctx.record(0)
         dg.spmv(v, cfg=cfg)
         ctx.record(1)
         print(v, f"{ctx.elapsed_ms(0, 1):.4f} ms")
+    if v == "grid" and not a.cdp:
+        ctx.flush_l2()
+        dg.spmv(v, cfg=cfg, metrics=True)
+        t0, t1, t2 = dg.phase_ns()
+        print(f"  phase split: insert+inline {(t1 - t0) / 1e3:.1f} us, drain {(t2 - t1) / 1e3:.1f} us")
 ctx.synchronize()
