@@ -170,10 +170,124 @@ def time_variant(ctx, dg, variant, steps, warmup, cfg=None):
     return total / steps
 
 
+def _x_global(n):
+    """x in (0, 1], a pure function of the global index (same on every rank)."""
+    rng = np.random.default_rng(SEED)
+    return (rng.integers(1, 1 << 24, n) / float(1 << 24)).astype(np.float32)
+
+
+def run_multi(args, dist, rank, world, local):
+    """BASELINE config 5 shape, weak scaling: a vertex-permuted R-MAT of scale
+    20 + log2(N) split into N equal row blocks (2^20 rows, ~16.8M nnz per
+    GPU).  One step = ncclAllGather of the x slices over NVLink + the local
+    grid-consolidated SpMV (dpc_multi_spmv), max over ranks."""
+    import math
+
+    import paper_1606_08150_b200 as dpc
+    from tests._oracle import Oracle
+    if world & (world - 1):
+        raise SystemExit("--gpus must be a power of two")
+    scale = SCALE + int(math.log2(world))
+    R = 1 << SCALE
+    r0 = rank * R
+    ctx = dpc.Context(local)
+    t0 = time.time()
+    A = dpc.gen_rmat_rows(scale, r0, r0 + R, EDGEFACTOR, seed=SEED, weights=False, values=True,
+                          permute=True)
+    gen_s = time.time() - t0
+    dg = dpc.DeviceGraph(ctx, A)
+    x_full = _x_global(A.ncols)
+    dx = ctx.alloc(4 * R)
+    ctx.h2d(dx, x_full[r0:r0 + R])
+    uid = [dpc.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = dpc.Comm(ctx, rank, world, uid[0])
+    comm.spmv(dg, dx, dg.y_ptr)
+    y = dg.get_y().astype(np.float64)
+    y64 = Oracle().spmv_f64(A.rowptr, A.col, A.val, x_full)
+    parity_ok = bool(np.all(np.abs(y - y64) <= 1e-5 * np.abs(y64)))
+    for _ in range(args.warmup):
+        comm.spmv(dg, dx, dg.y_ptr)
+    ctx.synchronize()
+    _barrier(dist)
+    ts = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            ctx.flush_l2()
+            ctx.record(0)
+            comm.spmv(dg, dx, dg.y_ptr)
+            ctx.record(1)
+            ts.append(ctx.elapsed_ms(0, 1))
+    ctx.synchronize()
+    _barrier(dist)
+    ms = float(np.mean(ts))
+    ms_max = _max_over_ranks(dist, ms)
+    total_nnz = _sum_over_ranks(dist, float(A.m))
+    # e2e: host x slice in (pinned), all-gather + SpMV, host y slice out
+    import ctypes as C
+    xh = dpc._lib.dpc_host_alloc(4 * R)
+    xa = np.frombuffer((C.c_float * R).from_address(xh), np.float32)
+    xa[:] = x_full[r0:r0 + R]
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        _barrier(dist) if i == args.warmup else None
+        ctx.record(2)
+        ctx.h2d(dx, xa)
+        comm.spmv(dg, dx, dg.y_ptr)
+        yl = dg.get_y()
+        ctx.record(3)
+        if i >= args.warmup:
+            e2e.append(ctx.elapsed_ms(2, 3))
+    e2e_max = _max_over_ranks(dist, float(np.mean(e2e)))
+    e2e_ok = bool(np.all(np.abs(yl.astype(np.float64) - y64) <= 1e-5 * np.abs(y64)))
+    ok_all = _sum_over_ranks(dist, float(parity_ok and e2e_ok)) == world
+    peak = _peak_hbm()
+    alg = spmv_bytes(R, A.m) + 4 * (A.ncols - R)  # + the gathered remote x slices
+    out = {
+        "metric": "SSSP/SpMV GTEPS per B200 (1-8 GPU) & speedup vs basic-DP and flat kernels",
+        "value": round(total_nnz / (ms_max * 1e-3) / 1e9, 3), "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"BASELINE config 5 shape: SpMV on a vertex-permuted R-MAT scale-{scale} "
+                               f"matrix, {world} equal row blocks of 2^20 rows (~16.8M nnz) per GPU",
+                   "parallelism": f"row-partition x{world}, ncclAllGather of x over NVLink",
+                   "l2": "flushed before every timed step", "generate_s": round(gen_s, 2)},
+        "parity": {"all_ranks_vs_fp64_rtol_1e-5": ok_all},
+        "e2e": {"value": round(total_nnz / (e2e_max * 1e-3) / 1e9, 3), "unit": "GTEPS",
+                "h2d_bytes_per_step": 4 * R, "d2h_bytes_per_step": 4 * R,
+                "ms_per_step": round(e2e_max, 4),
+                "api": "dpc_copy_h2d + dpc_multi_spmv + dpc_copy_d2h (C ABI), per rank"},
+        "roofline": {"bound": "hbm", "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / peak, 4),
+                     "traffic": None, "algorithmic_bytes": alg,
+                     "kernel": "ncclAllGather + spmv::grid_persistent (rank 0)"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    comm.close()
+    ctx.free(dx)
+    dg.close()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def _peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f).get("hbm_gbs", 6650.0))
+    except (OSError, ValueError):
+        return 6650.0
+
+
 def run_ours(args):
     import paper_1606_08150_b200 as dpc
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
     dist = _dist_init(world)
+    if world > 1:
+        return run_multi(args, dist, rank, world, local)
     ctx = dpc.Context(local)
     t0 = time.time()
     g = dpc.gen_rmat(SCALE, EDGEFACTOR, seed=SEED + rank, weights=False, values=True)

@@ -273,6 +273,11 @@ int32_t* dpc_dtree_result(dpc_dtree* dt);
 dpc_status dpc_spmv_host(dpc_ctx* ctx, dpc_dgraph* dg, const float* x_host, float* y_host,
                          const dpc_launch_cfg* cfg, dpc_metrics* met);
 
+/* Device memory on the context's GPU (caller-owned vectors for the
+ * device-pointer entry points). */
+void* dpc_dev_alloc(dpc_ctx* ctx, size_t bytes);
+void dpc_dev_free(dpc_ctx* ctx, void* p);
+
 /* Pinned host memory (for copy bandwidth on the end-to-end path). */
 void* dpc_host_alloc(size_t bytes);
 void dpc_host_free(void* p);

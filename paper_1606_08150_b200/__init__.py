@@ -153,6 +153,8 @@ _SIGS = {
     "dpc_dtree_free": (None, [_P]),
     "dpc_tree_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_dtree_result": (_P, [_P]),
+    "dpc_dev_alloc": (_P, [_P, C.c_size_t]),
+    "dpc_dev_free": (None, [_P, _P]),
     "dpc_host_alloc": (_P, [C.c_size_t]),
     "dpc_host_free": (None, [_P]),
     "dpc_copy_h2d": (C.c_int, [_P, _P, _P, C.c_size_t]),
@@ -389,6 +391,25 @@ class Context:
 
     def synchronize(self):
         _check(_lib.dpc_ctx_synchronize(self._h))
+
+    def alloc(self, nbytes: int) -> int:
+        """Device buffer on this context's GPU (free with free())."""
+        p = _lib.dpc_dev_alloc(self._h, nbytes)
+        if not p:
+            raise DpcError(6, f"device allocation of {nbytes} bytes failed")
+        return p
+
+    def free(self, p: int):
+        _lib.dpc_dev_free(self._h, p)
+
+    def h2d(self, dst: int, a: np.ndarray):
+        a = np.ascontiguousarray(a)
+        _check(_lib.dpc_copy_h2d(self._h, dst, _ptr(a), a.nbytes))
+
+    def d2h(self, src: int, count: int, dtype=np.float32) -> np.ndarray:
+        out = np.empty(count, dtype)
+        _check(_lib.dpc_copy_d2h(self._h, _ptr(out), src, out.nbytes))
+        return out
 
     def flush_l2(self):
         _check(_lib.dpc_ctx_flush_l2(self._h))

@@ -244,6 +244,24 @@ dpc_status dpc_ctx_flush_l2(dpc_ctx* c) {
   return DPC_OK;
 }
 
+void* dpc_dev_alloc(dpc_ctx* c, size_t bytes) {
+  if (!c) return nullptr;
+  void* p = nullptr;
+  cudaSetDevice(c->device);
+  if (cudaMalloc(&p, bytes ? bytes : 1) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dpc_dev_free(dpc_ctx* c, void* p) {
+  if (c && p) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(p);
+  }
+}
+
 void* dpc_host_alloc(size_t bytes) {
   void* p = nullptr;
   if (cudaMallocHost(&p, bytes) != cudaSuccess) {

@@ -273,6 +273,112 @@ __device__ __forceinline__ float warp_light_rows(const Args& a, unsigned b, unsi
   return acc;
 }
 
+__device__ __forceinline__ int ld_stream_i(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_stream_f(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
+// Segmented dot product over a warp: lane i owns the nonzero segment
+// [b_i, b_i + len_i); returns sum(val * x[col]) over lane i's segment.  The
+// concatenated segments are swept U*32 elements per step: all U col/val
+// loads of a step are issued before any x gather (memory-level parallelism),
+// col/val bypass L1 (x keeps it), each element finds its owner with a 5-step
+// shuffle binary search and partial sums reach the owner through a segmented
+// shuffle reduction.  Balanced however the lengths are distributed.
+template <int U>
+__device__ __forceinline__ float warp_segments_dot(const Args& a, unsigned b, unsigned len) {
+  const unsigned lane = dev::lane_id();
+  const unsigned incl = dev::warp_incl_scan(len);
+  const unsigned total = __shfl_sync(kFull, incl, 31);
+  const unsigned lo = incl - len;
+  float acc = 0.f;
+  for (unsigned base = 0; base < total; base += 32 * U) {
+    unsigned l[U];
+    int c[U];
+    float w[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const unsigned j = base + u * 32 + lane;
+      unsigned s = 0;
+#pragma unroll
+      for (unsigned st = 16; st > 0; st >>= 1) {
+        unsigned cand = s + st;
+        if (__shfl_sync(kFull, lo, cand) <= j) s = cand;
+      }
+      l[u] = s;
+      const unsigned k = __shfl_sync(kFull, b, s) + (j - __shfl_sync(kFull, lo, s));
+      const bool ok = j < total;
+      c[u] = ok ? ld_stream_i(a.col + k) : 0;
+      w[u] = ok ? ld_stream_f(a.val + k) : 0.f;
+    }
+    float p[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) p[u] = w[u] * __ldg(a.x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      float v = p[u];
+      const unsigned lu = l[u];
+#pragma unroll
+      for (unsigned s = 1; s < 32; s <<= 1) {
+        float ov = __shfl_down_sync(kFull, v, s);
+        unsigned ol = __shfl_down_sync(kFull, lu, s);
+        if (lane + s < 32 && ol == lu) v += ov;
+      }
+      const unsigned j0 = base + u * 32;
+      const unsigned first = lo > j0 ? lo : j0;
+      const bool mine = len > 0 && lo < j0 + 32 && lo + len > j0;
+      const float got = __shfl_sync(kFull, v, (first - j0) & 31u);
+      if (mine) acc += got;
+    }
+  }
+  return acc;
+}
+
+// Light rows of a 32-row tile through the segmented sweep (4 elements per lane
+// per step covers the typical tile in one step).  All lanes call.
+__device__ __forceinline__ unsigned parent_prework_stream(const Args& a, unsigned row, unsigned* b,
+                                                          unsigned* e) {
+  unsigned dl = 0, want = 0;
+  if (row < a.n) {
+    *b = __ldg(a.rowptr + row);
+    *e = __ldg(a.rowptr + row + 1);
+    if (*e - *b > a.threshold) {
+      a.y[row] = 0.f;
+      want = dev::nchunks(*e - *b, a.chunk);
+    } else {
+      dl = *e - *b;
+    }
+  }
+  float s = warp_segments_dot<4>(a, *b, dl);
+  if (row < a.n && !want) a.y[row] = s;
+  return want;
+}
+
+// Drain through the segmented sweep: a warp's batch of up to 32 items (lane i
+// holds item i) is one concatenated stream, 8 elements per lane per step.
+__device__ __forceinline__ void drain_items_stream(const Args& a, const Item* items, unsigned count,
+                                                   unsigned gwarp, unsigned nwarps) {
+  const unsigned lane = dev::lane_id();
+  const unsigned mine = count > gwarp ? (count - gwarp + nwarps - 1) / nwarps : 0;
+  for (unsigned r0 = 0; r0 < mine; r0 += 32) {
+    unsigned v = 0, b = 0, len = 0;
+    if (r0 + lane < mine) {
+      Item t = items[(r0 + lane) * nwarps + gwarp];
+      v = t.v;
+      b = t.begin;
+      len = min(b + a.chunk, __ldg(a.rowptr + v + 1)) - b;
+    }
+    float s = warp_segments_dot<8>(a, b, len);
+    if (len) atomicAdd(a.y + v, s);
+  }
+}
+
 // Common parent prework for the DP variants: zero heavy rows' y, do the light
 // rows' inline work warp-cooperatively, return how many chunk items this
 // thread inserts.  All lanes call.
@@ -401,7 +507,9 @@ __global__ void __launch_bounds__(256, MB) grid_persistent(Args a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[0] = dev::global_ns();
   for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
     unsigned row = base + threadIdx.x, b = 0, e = 0;
-    unsigned want = LM ? parent_prework(a, row, &b, &e) : parent_prework_serial(a, row, &b, &e);
+    unsigned want = LM == 2   ? parent_prework_stream(a, row, &b, &e)
+                    : LM == 1 ? parent_prework(a, row, &b, &e)
+                              : parent_prework_serial(a, row, &b, &e);
     unsigned wbase, wtotal;
     unsigned at = dev::warp_reserve(&a.hdr->count, want, &wbase, &wtotal);
     if (want) dev::write_chunks(a.pool, a.hdr, at, row, b, e, a.chunk);
@@ -409,8 +517,10 @@ __global__ void __launch_bounds__(256, MB) grid_persistent(Args a) {
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[1] = dev::global_ns();
   unsigned cnt = min(*reinterpret_cast<volatile unsigned*>(&a.hdr->count), a.pool.cap);
-  if (DM) drain_items(a, a.pool.items, cnt, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, stride >> 5);
-  else drain_items_warp(a, a.pool.items, cnt, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, stride >> 5);
+  const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = stride >> 5;
+  if (DM == 2) drain_items_stream(a, a.pool.items, cnt, gw, nw);
+  else if (DM == 1) drain_items(a, a.pool.items, cnt, gw, nw);
+  else drain_items_warp(a, a.pool.items, cnt, gw, nw);
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&a.hdr->t[2], dev::global_ns());
 }
@@ -419,6 +529,9 @@ using PersistentFn = void (*)(Args);
 // [LM][DM][MB == 8]
 static PersistentFn persistent_fn(unsigned flags) {
   const bool serial = flags & (1u << 8), warp_drain = flags & (1u << 9), low_occ = flags & (1u << 10);
+  if (flags & (1u << 11)) return low_occ ? grid_persistent<2, 2, 4> : grid_persistent<2, 2, 8>;
+  if (flags & (1u << 12)) return low_occ ? grid_persistent<2, 1, 4> : grid_persistent<2, 1, 8>;
+  if (flags & (1u << 13)) return low_occ ? grid_persistent<1, 2, 4> : grid_persistent<1, 2, 8>;
   static const PersistentFn table[2][2][2] = {
       {{grid_persistent<0, 0, 4>, grid_persistent<0, 0, 8>}, {grid_persistent<0, 1, 4>, grid_persistent<0, 1, 8>}},
       {{grid_persistent<1, 0, 4>, grid_persistent<1, 0, 8>}, {grid_persistent<1, 1, 4>, grid_persistent<1, 1, 8>}}};
