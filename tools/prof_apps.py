@@ -1,7 +1,7 @@
 """Times every app x variant at its BASELINE configuration (device-resident,
 CUDA events, L2 flushed) and checks each result against the CPU oracle.
 
-usage: python tools/prof_apps.py [--apps sssp gc td th spmv] [--reps N] [--json out.json]
+usage: python tools/prof_apps.py [--apps sssp gc td th] [--reps N] [--json out.json]
 Also importable: run_apps(ctx, apps, reps) -> dict (used by bench.py)."""
 import argparse
 import json
@@ -28,19 +28,37 @@ def _time(ctx, fn, reps):
         fn()
         ctx.record(5)
         ts.append(ctx.elapsed_ms(4, 5))
-    return float(np.median(ts)), ts
+    return float(np.median(ts))
+
+
+def _variants(ctx, reps, run, check, extra):
+    """run(variant, metrics) -> Metrics; check() -> bool; extra(Metrics) -> dict."""
+    res = {}
+    for v in VARIANTS:
+        try:
+            met = run(v, True)
+            ok = bool(check())
+            ms = _time(ctx, lambda: run(v, False), reps if v != "basic" else 1)
+            res[v] = {"ms": round(ms, 4), "bit_exact": ok, "device_launches": met.child_launch_count,
+                      **extra(met)}
+        except dpc.DpcError as e:
+            res[v] = {"error": str(e)}
+    return res
 
 
 def _summ(res, unit_count, unit):
-    for v, r in res.items():
-        r["g" + unit] = round(unit_count / (r["ms"] * 1e-3) / 1e9, 4)
+    for r in res.values():
+        if "ms" in r:
+            r["g" + unit] = round(unit_count / (r["ms"] * 1e-3) / 1e9, 4)
     out = {"variants": res}
-    best = min((r["ms"], v) for v, r in res.items() if v in ("warp", "block", "grid"))
-    out["best_consolidated"] = best[1]
-    if "basic" in res:
-        out["best_vs_basic"] = round(res["basic"]["ms"] / best[0], 2)
-    if "flat" in res:
-        out["best_vs_flat"] = round(res["flat"]["ms"] / best[0], 2)
+    timed = [(r["ms"], v) for v, r in res.items() if "ms" in r and v in ("warp", "block", "grid")]
+    if timed:
+        best = min(timed)
+        out["best_consolidated"] = best[1]
+        if "ms" in res.get("basic", {}):
+            out["best_vs_basic"] = round(res["basic"]["ms"] / best[0], 2)
+        if "ms" in res.get("flat", {}):
+            out["best_vs_flat"] = round(res["flat"]["ms"] / best[0], 2)
     return out
 
 
@@ -48,16 +66,11 @@ def app_sssp(ctx, orc, reps, scale=16):
     g = dpc.gen_rmat(scale, 16, seed=1)
     s = int(np.argmax(g.degrees()))
     ref = orc.sssp(g.rowptr, g.col, g.w, s)
-    reached = ref != np.uint32(0xFFFFFFFF)
-    m_reached = int(g.degrees()[reached].sum())
+    m_reached = int(g.degrees()[ref != np.uint32(0xFFFFFFFF)].sum())
     dg = dpc.DeviceGraph(ctx, g)
-    res = {}
-    for v in VARIANTS:
-        met = dg.sssp(s, v)  # warm + metrics
-        ok = bool(np.array_equal(dg.get_dist(), ref))
-        ms, _ = _time(ctx, lambda: dg.sssp(s, v, metrics=False), reps if v != "basic" else 1)
-        res[v] = {"ms": round(ms, 4), "bit_exact": ok, "device_launches": met.child_launch_count,
-                  "iterations": met.iterations, "relaxed_edges": met.edges_processed}
+    res = _variants(ctx, reps, lambda v, m: dg.sssp(s, v, metrics=m),
+                    lambda: np.array_equal(dg.get_dist(), ref),
+                    lambda met: {"iterations": met.iterations, "relaxed_edges": met.edges_processed})
     dg.close()
     out = _summ(res, m_reached, "teps")
     out.update({"workload": f"SSSP R-MAT scale {scale}, int weights [1,255], source = max-degree vertex",
@@ -70,13 +83,9 @@ def app_gc(ctx, orc, reps, scale=20):
     g = dpc.gen_rmat(scale, 16, seed=1, weights=False, symmetric=True)
     ref, k = orc.color(g.rowptr, g.col, 1)
     dg = dpc.DeviceGraph(ctx, g)
-    res = {}
-    for v in VARIANTS:
-        met = dg.color(1, v)
-        ok = bool(np.array_equal(dg.get_color(), ref))
-        ms, _ = _time(ctx, lambda: dg.color(1, v, metrics=False), reps if v != "basic" else 1)
-        res[v] = {"ms": round(ms, 4), "bit_exact": ok, "colors": met.result_count,
-                  "device_launches": met.child_launch_count, "rounds": met.iterations}
+    res = _variants(ctx, reps, lambda v, m: dg.color(1, v, metrics=m),
+                    lambda: np.array_equal(dg.get_color(), ref),
+                    lambda met: {"colors": met.result_count, "rounds": met.iterations})
     dg.close()
     out = _summ(res, 2 * g.m, "teps")
     out.update({"workload": f"GC R-MAT scale {scale} symmetrized ({g.m} arcs), JP priorities mix64(v^1)",
@@ -88,16 +97,12 @@ def app_tree(ctx, orc, reps, which):
     t = dpc.gen_tree(TREE["depth"], TREE["lo"], TREE["hi"], TREE["fill"], TREE["seed"])
     ref = orc.tree_desc(t.parent) if which == "tree_desc" else orc.tree_height(t.parent)
     dt = dpc.DeviceTree(ctx, t)
-    res = {}
-    for v in VARIANTS:
-        met = dt.run(which, v)
-        ok = bool(np.array_equal(dt.result(), ref))
-        ms, _ = _time(ctx, lambda: dt.run(which, v, metrics=False), reps if v != "basic" else 1)
-        res[v] = {"ms": round(ms, 4), "bit_exact": ok, "device_launches": met.child_launch_count,
-                  "levels": met.iterations}
+    res = _variants(ctx, reps, lambda v, m: dt.run(which, v, metrics=m),
+                    lambda: np.array_equal(dt.result(), ref),
+                    lambda met: {"levels": met.iterations})
     dt.close()
     out = _summ(res, t.n - 1, "edges_per_s")
-    out.update({"workload": f"{which} random tree gen_tree(24, 1, 4, 0.84, 1): {t.n} nodes, depth {t.depth}",
+    out.update({"workload": f"{which}: gen_tree(24, 1, 4, 0.84, 1) = {t.n} nodes, depth {t.depth}",
                 "unit": "G tree edges/s"})
     return out
 
