@@ -108,6 +108,66 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned want, unsigned* bto
   return off;
 }
 
+// Block-aggregated reservation (dp_insert with one global atomic per block):
+// same-address global atomics serialise at ~0.7 ns each on B200
+// (tools/probes/atomics_sync), so a per-warp atomic on one counter costs
+// ~20 us per 30K warps.  Returns this thread's first slot; *bbase / *btotal
+// receive the block's slice.  All threads call; ends with a barrier.
+__device__ __forceinline__ unsigned block_reserve(unsigned* counter, unsigned want,
+                                                  unsigned* bbase, unsigned* btotal) {
+  __shared__ unsigned s_base;
+  unsigned off = block_excl_scan(want, btotal);
+  if (threadIdx.x == 0) s_base = *btotal ? atomicAdd(counter, *btotal) : 0u;
+  __syncthreads();
+  *bbase = s_base;
+  unsigned at = s_base + off;
+  __syncthreads();  // s_base is reused by the next call
+  return at;
+}
+
+// Block-local append queue in shared memory: pushes are shared-memory
+// atomics; flush() publishes the block's items with ONE global atomic.  A
+// push that finds the queue full spills straight to global memory.
+template <unsigned CAP>
+struct BlockQueue {
+  unsigned n;
+  unsigned base;
+  unsigned items[CAP];
+
+  __device__ __forceinline__ void init() {
+    if (threadIdx.x == 0) n = 0;
+  }
+  __device__ __forceinline__ void push(unsigned v, unsigned* gcount, unsigned* gdst) {
+    cooperative_groups::coalesced_group g = cooperative_groups::coalesced_threads();
+    unsigned s = 0;
+    if (g.thread_rank() == 0) s = atomicAdd(&n, g.size());
+    s = g.shfl(s, 0) + g.thread_rank();
+    if (s < CAP) {
+      items[s] = v;
+    } else {
+      unsigned gs = atomicAdd(gcount, 1u);
+      gdst[gs] = v;
+    }
+  }
+  // All threads of the block call (uniform control flow).
+  __device__ __forceinline__ void flush(unsigned* gcount, unsigned* gdst) {
+    __syncthreads();
+    const unsigned cnt = n < CAP ? n : CAP;
+    if (threadIdx.x == 0) base = cnt ? atomicAdd(gcount, cnt) : 0u;
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) gdst[base + i] = items[i];
+    __syncthreads();
+    if (threadIdx.x == 0) n = 0;
+    __syncthreads();
+  }
+};
+
+// Block-level sum / max accumulators flushed with one global atomic.
+__device__ __forceinline__ void block_add_u64(unsigned long long* smem_acc, unsigned v) {
+  unsigned s = warp_sum(v);
+  if (lane_id() == 0 && s) atomicAdd(smem_acc, static_cast<unsigned long long>(s));
+}
+
 // Writes the chunk items of vertex v (edges [b, e)) starting at slot `at`.
 // Slots past the pool capacity set the overflow flag (sim.hpp:1512-1517
 // turns overflow into a fault; we report it as DPC_E_OVERFLOW).

@@ -299,7 +299,7 @@ void dpc_dgraph_free(dpc_dgraph* g) {
   }
   void* bufs[] = {g->rowptr, g->col,      g->w,        g->val,   g->x,    g->y,
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
-                  g->items, g->ctr};
+                  g->items, g->ctr, g->gc_state};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->hdr_host) cudaFreeHost(g->hdr_host);

@@ -42,6 +42,8 @@ struct dpc_dgraph {
   // frontier / worklist buffers (SSSP, GC)
   unsigned* front[2] = {nullptr, nullptr};
   unsigned* stamp = nullptr;  // SSSP dedup stamp / GC pending counts
+  unsigned* gc_state = nullptr;  // GC heavy-vertex bitmaps (36 words per pool slot)
+  size_t gc_state_slots = 0;
   unsigned* ctr = nullptr;    // per-iteration counters (app-specific layout, 64 B)
   void* ctr_host = nullptr;   // pinned mirror of ctr
   dpc::dev::RunHeader* hdr = nullptr;  // device counters

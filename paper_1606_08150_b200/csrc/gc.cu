@@ -12,11 +12,16 @@
 // every variant and schedule.
 //
 // Two irregular loops per vertex, both consolidated:
-//   init pass  : count higher neighbours  (chunk items, warp per chunk, sum)
-//   color pass : mex + decrements         (vertex items, block per item with a
-//                shared-memory color bitmap — the SoloBlock drain shape,
-//                transform.hpp:545-563, because mex does not split across
-//                chunks)
+//   init pass  : count higher neighbours (chunk items, warp per chunk, sum)
+//   color pass : mex + decrements.  Heavy vertices are split into chunk
+//                items too: a warp ORs its chunk's neighbour colors into a
+//                shared-memory bitmap and then into the vertex's global
+//                bitmap; the warp that finishes the vertex's LAST chunk
+//                (per-vertex countdown — the paper's last-block protocol at
+//                item granularity) computes the mex and writes the color.
+//                basic-dp keeps the paper's per-vertex child (<<<1, T>>>,
+//                SoloBlock, shared-memory bitmap).
+// Frontier appends and the color-count maximum are block-aggregated.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -35,7 +40,11 @@ using dev::kFull;
 using dev::Pool;
 using dev::RunHeader;
 
-constexpr unsigned kBitmapWords = 1024;  // 32768 colors per window in the block drain
+constexpr unsigned kBitmapWords = 1024;  // SoloBlock window: 32768 colors
+constexpr unsigned kVW = 32;             // chunked heavy vertex: 1024-color window
+constexpr unsigned kStateWords = 36;     // per heavy vertex: 32 bitmap + remaining + overflow + pad
+constexpr unsigned kQueue = 2048;
+using Queue = dev::BlockQueue<kQueue>;
 
 struct Ctr {
   unsigned fsize[3];
@@ -52,6 +61,7 @@ struct Args {
   unsigned* cnt;
   unsigned* front0;
   unsigned* front1;
+  unsigned* state;  // kStateWords per pool slot (heavy-vertex bitmaps)
   Ctr* ctr;
   Pool pool;
   RunHeader* hdr;
@@ -63,6 +73,12 @@ struct Args {
   unsigned child_blocks;
   unsigned it;
   unsigned fsize;
+};
+
+struct Block {
+  Queue q;
+  int maxc;
+  unsigned wbm[8][kVW];  // per-warp chunk bitmaps
 };
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
@@ -88,13 +104,33 @@ __device__ __forceinline__ unsigned* cur_front(const Args& a, unsigned it) {
 __device__ __forceinline__ unsigned* next_front(const Args& a, unsigned it) {
   return (it & 1) ? a.front0 : a.front1;
 }
+__device__ __forceinline__ unsigned* next_count(const Args& a, unsigned it) {
+  return &a.ctr->fsize[(it + 1) % 3];
+}
 
-__device__ __forceinline__ void push(const Args& a, unsigned it, unsigned v) {
-  cg::coalesced_group g = cg::coalesced_threads();
-  unsigned base = 0;
-  if (g.thread_rank() == 0) base = atomicAdd(&a.ctr->fsize[(it + 1) % 3], g.size());
-  base = g.shfl(base, 0);
-  next_front(a, it)[base + g.thread_rank()] = v;
+__device__ __forceinline__ void block_begin(Block& s) {
+  s.q.init();
+  if (threadIdx.x == 0) s.maxc = -1;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void block_end(const Args& a, unsigned it, Block& s) {
+  s.q.flush(next_count(a, it), next_front(a, it));
+  if (threadIdx.x == 0 && s.maxc >= 0) {
+    atomicMax(&a.ctr->maxcolor, s.maxc);
+    s.maxc = -1;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void set_color(const Args& a, Block& s, unsigned v, int c) {
+  a.color[v] = c;
+  atomicMax(&s.maxc, c);
+}
+
+// Lower neighbour u of a vertex being colored: count down, append when ready.
+__device__ __forceinline__ void release(const Args& a, unsigned it, Block& s, unsigned u) {
+  if (atomicSub(a.cnt + u, 1u) == 1u) s.q.push(u, next_count(a, it), next_front(a, it));
 }
 
 // --------------------------------------------------------------- init pass
@@ -136,11 +172,9 @@ __global__ void __launch_bounds__(256) init_basic_child(Args a, unsigned v, unsi
   if (dev::lane_id() == 0 && c) atomicAdd(a.cnt + v, c);
 }
 
-// variant: 0 flat, 1 basic, 2 warp, 3 block, 4 grid(CDP) — one parent for the
-// init pass over all vertices.
+// variant: 0 flat, 1 basic, 2 warp, 3 block, 4 grid(CDP) — the init pass
 template <int V>
 __global__ void __launch_bounds__(256) init_parent(Args a) {
-  __shared__ unsigned s_base;
   unsigned v = blockIdx.x * blockDim.x + threadIdx.x, b = 0, e = 0, want = 0;
   if (v < a.n) {
     b = __ldg(a.rowptr + v);
@@ -156,31 +190,22 @@ __global__ void __launch_bounds__(256) init_parent(Args a) {
     }
   }
   if (V == 0 || V == 1) return;
-  if (V == 3) {
-    unsigned bt;
-    unsigned off = dev::block_excl_scan(want, &bt);
-    if (threadIdx.x == 0 && bt) s_base = atomicAdd(&a.ctr->pool[0], bt);
-    __syncthreads();
-    if (want) {
-      dev::write_chunks(a.pool, a.hdr, s_base + off, v, b, e, a.chunk);
-      __threadfence();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && bt && s_base < a.pool.cap) {
-      unsigned c = min(bt, a.pool.cap - s_base);
-      init_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
-                   cudaStreamFireAndForget>>>(a, a.pool.items + s_base, c);
-      dev::note_launch(a.hdr);
-    }
-    return;
-  }
-  unsigned wb, wt;
-  unsigned at = dev::warp_reserve(&a.ctr->pool[0], want, &wb, &wt);
+  unsigned bbase, bt;
+  unsigned at = dev::block_reserve(&a.ctr->pool[0], want, &bbase, &bt);
   if (want) {
     dev::write_chunks(a.pool, a.hdr, at, v, b, e, a.chunk);
     __threadfence();
   }
-  if (V == 2) {
+  if (V == 3) {
+    __syncthreads();
+    if (threadIdx.x == 0 && bt && bbase < a.pool.cap) {
+      unsigned c = min(bt, a.pool.cap - bbase);
+      init_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
+                   cudaStreamFireAndForget>>>(a, a.pool.items + bbase, c);
+      dev::note_launch(a.hdr);
+    }
+  } else if (V == 2) {
+    const unsigned wb = __shfl_sync(kFull, at, 0), wt = dev::warp_sum(want);
     if (wt) {
       unsigned leader = __ffs(__ballot_sync(kFull, want != 0)) - 1;
       __syncwarp();
@@ -191,10 +216,7 @@ __global__ void __launch_bounds__(256) init_parent(Args a) {
         dev::note_launch(a.hdr);
       }
     }
-    return;
-  }
-  // V == 4: grid-level
-  if (dev::grid_last_block(&a.hdr->ticket) && threadIdx.x == 0) {
+  } else if (dev::grid_last_block(&a.hdr->ticket) && threadIdx.x == 0) {
     unsigned c = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[0]), a.pool.cap);
     if (c) {
       init_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
@@ -206,14 +228,17 @@ __global__ void __launch_bounds__(256) init_parent(Args a) {
 
 // frontier 0 = vertices with no higher neighbour
 __global__ void __launch_bounds__(256) seed_kernel(Args a) {
-  unsigned v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < a.n && a.cnt[v] == 0) push(a, 0xffffffffu /* it = -1 -> next = 0 */, v);
+  __shared__ Block s;
+  block_begin(s);
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += gridDim.x * blockDim.x)
+    if (a.cnt[v] == 0) s.q.push(v, next_count(a, 0xffffffffu), next_front(a, 0xffffffffu));
+  block_end(a, 0xffffffffu, s);
 }
 
 // --------------------------------------------------------------- color pass
 // Thread-serial color of v (light vertices; the flat variant for all).
-__device__ __forceinline__ void color_serial(const Args& a, unsigned it, unsigned v, unsigned b,
-                                             unsigned e) {
+__device__ __forceinline__ void color_serial(const Args& a, unsigned it, Block& s, unsigned v,
+                                             unsigned b, unsigned e) {
   const unsigned long long pv = prio(a, v);
   unsigned long long used = 0;
   for (unsigned k = b; k < e; k++) {
@@ -222,8 +247,8 @@ __device__ __forceinline__ void color_serial(const Args& a, unsigned it, unsigne
     if (higher(u, prio(a, u), v, pv)) {
       int c = __ldcg(a.color + u);
       if (c < 64) used |= 1ull << c;
-    } else if (atomicSub(a.cnt + u, 1u) == 1u) {
-      push(a, it, u);
+    } else {
+      release(a, it, s, u);
     }
   }
   int mex;
@@ -243,12 +268,12 @@ __device__ __forceinline__ void color_serial(const Args& a, unsigned it, unsigne
       if (~w) mex = base + __ffsll(static_cast<long long>(~w)) - 1;
     }
   }
-  a.color[v] = mex;
-  atomicMax(&a.ctr->maxcolor, mex);
+  set_color(a, s, v, mex);
 }
 
-// Block-cooperative color of v (SoloBlock drain).  All threads call.
-__device__ void color_block(const Args& a, unsigned it, unsigned v, unsigned* bm, int* s_mex) {
+// Block-cooperative color of v (basic-dp SoloBlock child).  All threads call.
+__device__ void color_block(const Args& a, unsigned it, Block& s, unsigned v, unsigned* bm,
+                            int* s_mex) {
   const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
   const unsigned long long pv = prio(a, v);
   int mex = -1;
@@ -262,8 +287,8 @@ __device__ void color_block(const Args& a, unsigned it, unsigned v, unsigned* bm
       if (higher(u, prio(a, u), v, pv)) {
         int c = __ldcg(a.color + u) - base;
         if (c >= 0 && c < static_cast<int>(kBitmapWords * 32)) atomicOr(bm + (c >> 5), 1u << (c & 31));
-      } else if (base == 0 && atomicSub(a.cnt + u, 1u) == 1u) {
-        push(a, it, u);
+      } else if (base == 0) {
+        release(a, it, s, u);
       }
     }
     __syncthreads();
@@ -275,91 +300,169 @@ __device__ void color_block(const Args& a, unsigned it, unsigned v, unsigned* bm
     if (*s_mex != 0x7fffffff) mex = base + *s_mex;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    a.color[v] = mex;
-    atomicMax(&a.ctr->maxcolor, mex);
-  }
-}
-
-__device__ __forceinline__ void color_drain(const Args& a, unsigned it, const Item* items,
-                                            unsigned count, unsigned first, unsigned stride) {
-  __shared__ unsigned bm[kBitmapWords];
-  __shared__ int s_mex;
-  for (unsigned i = first; i < count; i += stride) color_block(a, it, items[i].v, bm, &s_mex);
-}
-
-__global__ void __launch_bounds__(256) color_child(Args a, const Item* items, unsigned count) {
-  color_drain(a, a.it, items, count, blockIdx.x, gridDim.x);
+  if (threadIdx.x == 0) set_color(a, s, v, mex);
 }
 
 __global__ void __launch_bounds__(256) color_basic_child(Args a, unsigned v) {
+  __shared__ Block s;
   __shared__ unsigned bm[kBitmapWords];
   __shared__ int s_mex;
-  color_block(a, a.it, v, bm, &s_mex);
+  block_begin(s);
+  color_block(a, a.it, s, v, bm, &s_mex);
+  block_end(a, a.it, s);
 }
 
+// Per-vertex state of a chunked heavy vertex: 32-word color bitmap (colors
+// < 1024), chunks remaining, overflow flag.  Initialised by the inserting
+// thread, owned by the vertex's first chunk slot.
+__device__ __forceinline__ void state_init(const Args& a, unsigned slot, unsigned nch) {
+  if (slot >= a.pool.cap) return;
+  unsigned* st = a.state + static_cast<size_t>(slot) * kStateWords;
+  for (unsigned i = 0; i < kVW; i++) st[i] = 0;
+  st[kVW] = nch;
+  st[kVW + 1] = 0;
+}
+
+// Finishes a heavy vertex whose chunks have all been scanned (one warp):
+// mex over the global bitmap, or a windowed warp scan when every color
+// below 1024 is taken.
+__device__ void finish_vertex(const Args& a, Block& s, unsigned v, unsigned* st) {
+  const unsigned lane = dev::lane_id();
+  unsigned word = __ldcg(st + lane);
+  unsigned freeb = ~word;
+  unsigned ball = __ballot_sync(kFull, freeb != 0);
+  int mex = -1;
+  if (ball) {
+    unsigned l = __ffs(ball) - 1;
+    unsigned fw = __shfl_sync(kFull, freeb, l);
+    mex = static_cast<int>(l * 32 + __ffs(fw) - 1);
+  } else {
+    const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+    const unsigned long long pv = prio(a, v);
+    for (int base = kVW * 32; mex < 0; base += 32) {
+      unsigned w = 0;
+      for (unsigned k = b + lane; k < e; k += 32) {
+        unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+        if (u != v && higher(u, prio(a, u), v, pv)) {
+          int c = __ldcg(a.color + u) - base;
+          if (c >= 0 && c < 32) w |= 1u << c;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) w |= __shfl_xor_sync(kFull, w, o);
+      if (~w) mex = base + __ffs(~w) - 1;
+    }
+  }
+  if (lane == 0) set_color(a, s, v, mex);
+}
+
+// Chunked color drain: warp per chunk item; the last chunk of a vertex
+// finishes it.  Uses the block's per-warp shared bitmaps.
+__device__ __forceinline__ void color_chunks(const Args& a, unsigned it, Block& s, const Item* items,
+                                             unsigned count, unsigned gwarp, unsigned nwarps) {
+  const unsigned lane = dev::lane_id(), wib = dev::warp_in_block();
+  unsigned* wbm = s.wbm[wib & 7];
+  for (unsigned i = gwarp; i < count; i += nwarps) {
+    const Item t = items[i];
+    const unsigned b0 = __ldg(a.rowptr + t.v), e0 = __ldg(a.rowptr + t.v + 1);
+    const unsigned e = min(t.begin + a.chunk, e0);
+    // the vertex's first chunk (absolute pool slot: `items` may be a slice)
+    const unsigned slot = static_cast<unsigned>(items - a.pool.items) + i - (t.begin - b0) / a.chunk;
+    unsigned* st = a.state + static_cast<size_t>(slot) * kStateWords;
+    wbm[lane] = 0;
+    __syncwarp();
+    const unsigned long long pv = prio(a, t.v);
+    bool over = false;
+    for (unsigned k = t.begin + lane; k < e; k += 32) {
+      unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+      if (u == t.v) continue;
+      if (higher(u, prio(a, u), t.v, pv)) {
+        int c = __ldcg(a.color + u);
+        if (c < static_cast<int>(kVW * 32)) atomicOr(wbm + (c >> 5), 1u << (c & 31));
+        else over = true;
+      } else {
+        release(a, it, s, u);
+      }
+    }
+    __syncwarp();
+    unsigned wv = wbm[lane];
+    if (wv) atomicOr(st + lane, wv);
+    if (__any_sync(kFull, over) && lane == 0) atomicOr(st + kVW + 1, 1u);
+    __threadfence();
+    unsigned last = 0;
+    if (lane == 0) last = atomicSub(st + kVW, 1u) == 1u;
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+      __threadfence();
+      finish_vertex(a, s, t.v, st);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(256) color_child(Args a, const Item* items, unsigned count) {
+  __shared__ Block s;
+  block_begin(s);
+  color_chunks(a, a.it, s, items, count, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+               (gridDim.x * blockDim.x) >> 5);
+  block_end(a, a.it, s);
+}
+
+// Parent of one color round.  Heavy vertices -> chunk items + vertex state.
 template <int V>
 __global__ void __launch_bounds__(256) color_parent(Args a) {
-  __shared__ unsigned s_base;
-  unsigned i = blockIdx.x * blockDim.x + threadIdx.x, v = 0, want = 0;
+  __shared__ Block s;
+  block_begin(s);
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x, v = 0, want = 0, b = 0, e = 0;
   if (i < a.fsize) {
     v = cur_front(a, a.it)[i];
-    unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+    b = __ldg(a.rowptr + v);
+    e = __ldg(a.rowptr + v + 1);
     if (V == 0 || e - b <= a.threshold) {
-      color_serial(a, a.it, v, b, e);
+      color_serial(a, a.it, s, v, b, e);
     } else if (V == 1) {
       color_basic_child<<<1, a.child_threads, 0, cudaStreamFireAndForget>>>(a, v);
       dev::note_launch(a.hdr);
     } else {
-      want = 1;
+      want = dev::nchunks(e - b, a.chunk);
     }
   }
-  if (V == 0 || V == 1) return;
-  const unsigned slot = a.it % 3;
-  if (V == 3) {
-    unsigned bt;
-    unsigned off = dev::block_excl_scan(want, &bt);
-    if (threadIdx.x == 0 && bt) s_base = atomicAdd(&a.ctr->pool[slot], bt);
-    __syncthreads();
+  if (V >= 2) {
+    const unsigned slot = a.it % 3;
+    unsigned bbase, bt;
+    unsigned at = dev::block_reserve(&a.ctr->pool[slot], want, &bbase, &bt);
     if (want) {
-      if (s_base + off < a.pool.cap) a.pool.items[s_base + off] = Item{v, 0};
-      else atomicOr(&a.hdr->overflow, 1u);
+      state_init(a, at, want);
+      dev::write_chunks(a.pool, a.hdr, at, v, b, e, a.chunk);
       __threadfence();
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && bt && s_base < a.pool.cap) {
-      unsigned c = min(bt, a.pool.cap - s_base);
-      unsigned nb = a.child_blocks ? min(c, a.child_blocks) : c;
-      color_child<<<nb, a.child_threads, 0, cudaStreamFireAndForget>>>(a, a.pool.items + s_base, c);
-      dev::note_launch(a.hdr);
-    }
-    return;
-  }
-  unsigned wb, wt;
-  unsigned at = dev::warp_reserve(&a.ctr->pool[slot], want, &wb, &wt);
-  if (want) {
-    if (at < a.pool.cap) a.pool.items[at] = Item{v, 0};
-    else atomicOr(&a.hdr->overflow, 1u);
-    __threadfence();
-  }
-  if (V == 2) {
-    if (wt) {
-      unsigned leader = __ffs(__ballot_sync(kFull, want != 0)) - 1;
-      __syncwarp();
-      if (dev::lane_id() == leader && wb < a.pool.cap) {
-        unsigned c = min(wt, a.pool.cap - wb);
-        unsigned nb = a.child_blocks ? min(c, a.child_blocks) : c;
-        color_child<<<nb, a.child_threads, 0, cudaStreamFireAndForget>>>(a, a.pool.items + wb, c);
+    if (V == 3) {
+      __syncthreads();
+      if (threadIdx.x == 0 && bt && bbase < a.pool.cap) {
+        unsigned c = min(bt, a.pool.cap - bbase);
+        color_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
+                      cudaStreamFireAndForget>>>(a, a.pool.items + bbase, c);
         dev::note_launch(a.hdr);
       }
+    } else if (V == 2) {
+      const unsigned wb = __shfl_sync(kFull, at, 0), wt = dev::warp_sum(want);
+      if (wt) {
+        unsigned leader = __ffs(__ballot_sync(kFull, want != 0)) - 1;
+        __syncwarp();
+        if (dev::lane_id() == leader && wb < a.pool.cap) {
+          unsigned c = min(wt, a.pool.cap - wb);
+          color_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
+                        cudaStreamFireAndForget>>>(a, a.pool.items + wb, c);
+          dev::note_launch(a.hdr);
+        }
+      }
     }
-    return;
   }
-  if (dev::grid_last_block(&a.hdr->ticket) && threadIdx.x == 0) {
-    unsigned c = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[slot]), a.pool.cap);
+  block_end(a, a.it, s);
+  if (V == 4 && dev::grid_last_block(&a.hdr->ticket) && threadIdx.x == 0) {
+    unsigned c = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[a.it % 3]), a.pool.cap);
     if (c) {
-      unsigned nb = a.child_blocks ? min(c, a.child_blocks) : c;
-      color_child<<<nb, a.child_threads, 0, cudaStreamFireAndForget>>>(a, a.pool.items, c);
+      color_child<<<dev::child_blocks(c, a.child_threads, a.child_blocks), a.child_threads, 0,
+                    cudaStreamFireAndForget>>>(a, a.pool.items, c);
       dev::note_launch(a.hdr);
     }
   }
@@ -378,11 +481,11 @@ __global__ void __launch_bounds__(32) rotate_kernel(Args a) {
 }
 
 __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iters) {
-  __shared__ unsigned bm[kBitmapWords];
-  __shared__ int s_mex;
+  __shared__ Block s;
   cg::grid_group grid = cg::this_grid();
   const unsigned stride = gridDim.x * blockDim.x;
   const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  block_begin(s);
   // init pass: light vertices inline, heavy -> chunk items in pool[0]
   for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
     unsigned v = base + threadIdx.x, b = 0, e = 0, want = 0;
@@ -392,8 +495,8 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iter
       if (e - b <= a.threshold) a.cnt[v] = count_higher(a, v, b, e, 1, 0);
       else want = dev::nchunks(e - b, a.chunk);
     }
-    unsigned wb, wt;
-    unsigned at = dev::warp_reserve(&a.ctr->pool[0], want, &wb, &wt);
+    unsigned bbase, bt;
+    unsigned at = dev::block_reserve(&a.ctr->pool[0], want, &bbase, &bt);
     if (want) dev::write_chunks(a.pool, a.hdr, at, v, b, e, a.chunk);
   }
   grid.sync();
@@ -405,30 +508,33 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iter
     a.ctr->pool[0] = 0;
   }
   for (unsigned v = gtid; v < a.n; v += stride)
-    if (a.cnt[v] == 0) push(a, 0xffffffffu, v);
+    if (a.cnt[v] == 0) s.q.push(v, next_count(a, 0xffffffffu), next_front(a, 0xffffffffu));
+  block_end(a, 0xffffffffu, s);
   grid.sync();
   unsigned it = 0;
   for (; it < max_iters; it++) {
     const unsigned fs = *reinterpret_cast<volatile unsigned*>(&a.ctr->fsize[it % 3]);
     if (fs == 0) break;
     for (unsigned base = blockIdx.x * blockDim.x; base < fs; base += stride) {
-      unsigned i = base + threadIdx.x, v = 0, want = 0;
+      unsigned i = base + threadIdx.x, v = 0, want = 0, b = 0, e = 0;
       if (i < fs) {
         v = cur_front(a, it)[i];
-        unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
-        if (e - b <= a.threshold) color_serial(a, it, v, b, e);
-        else want = 1;
+        b = __ldg(a.rowptr + v);
+        e = __ldg(a.rowptr + v + 1);
+        if (e - b <= a.threshold) color_serial(a, it, s, v, b, e);
+        else want = dev::nchunks(e - b, a.chunk);
       }
-      unsigned wb, wt;
-      unsigned at = dev::warp_reserve(&a.ctr->pool[it % 3], want, &wb, &wt);
+      unsigned bbase, bt;
+      unsigned at = dev::block_reserve(&a.ctr->pool[it % 3], want, &bbase, &bt);
       if (want) {
-        if (at < a.pool.cap) a.pool.items[at] = Item{v, 0};
-        else atomicOr(&a.hdr->overflow, 1u);
+        state_init(a, at, want);
+        dev::write_chunks(a.pool, a.hdr, at, v, b, e, a.chunk);
       }
     }
     grid.sync();
     unsigned c = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[it % 3]), a.pool.cap);
-    for (unsigned i = blockIdx.x; i < c; i += gridDim.x) color_block(a, it, a.pool.items[i].v, bm, &s_mex);
+    color_chunks(a, it, s, a.pool.items, c, gtid >> 5, stride >> 5);
+    block_end(a, it, s);
     if (gtid == 0) rotate(a, it);
     grid.sync();
   }
@@ -448,8 +554,8 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   Cfg c;
   dpc_status st = resolve_cfg(ctx, DPC_APP_COLOR, cfg, &c);
   if (st != DPC_OK) return st;
-  if (c.parent_threads != 256 || c.child_threads > 256)
-    return fail(DPC_E_INVALID, "GC kernels are built for parent_threads = 256, child_threads <= 256");
+  if (c.parent_threads != 256 || c.child_threads != 256)
+    return fail(DPC_E_INVALID, "GC kernels are built for parent_threads = child_threads = 256");
   if (!g->ctr) {
     DPC_CUDA(cudaMalloc(&g->ctr, 64));
     DPC_CUDA(cudaMallocHost(&g->ctr_host, 64));
@@ -472,11 +578,19 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   a.child_blocks = c.child_blocks;
   a.it = 0;
   a.fsize = 0;
+  a.state = nullptr;
   if (c.variant != DPC_FLAT && c.variant != DPC_BASIC) {
-    // init pass uses chunk items, color pass one item per heavy vertex
-    uint64_t need = std::max(pool_need(g, c.threshold, c.chunk), pool_need(g, c.threshold, 1u << 30));
-    st = ensure_pool(g, need);
+    st = ensure_pool(g, pool_need(g, c.threshold, c.chunk));
     if (st != DPC_OK) return st;
+    if (g->gc_state_slots < g->cap) {
+      DPC_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (g->gc_state) cudaFree(g->gc_state);
+      g->gc_state = nullptr;
+      g->gc_state_slots = 0;
+      DPC_CUDA(cudaMalloc(&g->gc_state, sizeof(unsigned) * gc::kStateWords * g->cap));
+      g->gc_state_slots = g->cap;
+    }
+    a.state = g->gc_state;
   }
   a.pool = dev::Pool{g->items, g->cap};
   st = ensure_pending_for(ctx, g, c.variant, c.threshold, c.parent_threads);
@@ -517,7 +631,7 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
     DPC_CUDA(cudaGetLastError());
     // pool slot 0 is reused by round 0: clear it after the init children ran
     DPC_CUDA(cudaMemsetAsync(&a.ctr->pool[0], 0, sizeof(unsigned), s));
-    gc::seed_kernel<<<nb, 256, 0, s>>>(a);
+    gc::seed_kernel<<<std::min(nb, 4u * static_cast<unsigned>(ctx->sms)), 256, 0, s>>>(a);
     host_launches += 2;
     DPC_CUDA(cudaGetLastError());
     DPC_CUDA(cudaMemcpyAsync(&ctr_host->fsize[0], &a.ctr->fsize[0], sizeof(unsigned),
@@ -562,3 +676,4 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   }
   return DPC_OK;
 }
+

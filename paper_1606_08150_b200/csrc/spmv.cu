@@ -408,12 +408,14 @@ __device__ __forceinline__ unsigned clamp_count(const Args& a, unsigned base, un
 __global__ void __launch_bounds__(256) warp_parent(Args a) {
   unsigned row = blockIdx.x * blockDim.x + threadIdx.x, b = 0, e = 0;
   unsigned want = parent_prework(a, row, &b, &e);
-  unsigned wbase, wtotal;
-  unsigned at = dev::warp_reserve(&a.hdr->count, want, &wbase, &wtotal);
+  unsigned bbase, btotal;
+  unsigned at = dev::block_reserve(&a.hdr->count, want, &bbase, &btotal);
   if (want) {
     dev::write_chunks(a.pool, a.hdr, at, row, b, e, a.chunk);
     __threadfence();
   }
+  // this warp's slice of the block slice: starts at lane 0's slot
+  const unsigned wbase = __shfl_sync(kFull, at, 0), wtotal = dev::warp_sum(want);
   if (wtotal) {
     unsigned leader = __ffs(__ballot_sync(kFull, want != 0)) - 1;  // a live inserting lane
     __syncwarp();
@@ -454,8 +456,8 @@ __global__ void __launch_bounds__(256) block_parent(Args a) {
 __global__ void __launch_bounds__(256) grid_parent(Args a) {
   unsigned row = blockIdx.x * blockDim.x + threadIdx.x, b = 0, e = 0;
   unsigned want = parent_prework(a, row, &b, &e);
-  unsigned wbase, wtotal;
-  unsigned at = dev::warp_reserve(&a.hdr->count, want, &wbase, &wtotal);
+  unsigned bbase, btotal;
+  unsigned at = dev::block_reserve(&a.hdr->count, want, &bbase, &btotal);
   if (want) {
     dev::write_chunks(a.pool, a.hdr, at, row, b, e, a.chunk);
     __threadfence();
@@ -510,8 +512,8 @@ __global__ void __launch_bounds__(256, MB) grid_persistent(Args a) {
     unsigned want = LM == 2   ? parent_prework_stream(a, row, &b, &e)
                     : LM == 1 ? parent_prework(a, row, &b, &e)
                               : parent_prework_serial(a, row, &b, &e);
-    unsigned wbase, wtotal;
-    unsigned at = dev::warp_reserve(&a.hdr->count, want, &wbase, &wtotal);
+    unsigned bbase, btotal;
+    unsigned at = dev::block_reserve(&a.hdr->count, want, &bbase, &btotal);
     if (want) dev::write_chunks(a.pool, a.hdr, at, row, b, e, a.chunk);
   }
   grid.sync();

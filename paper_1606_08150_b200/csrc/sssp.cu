@@ -16,6 +16,10 @@
 // The persistent grid variant runs all iterations inside one cooperative
 // kernel: insert phase, device-wide barrier, drain phase, barrier — the
 // paper's custom global barrier with zero launches.
+//
+// Frontier appends go through a shared-memory BlockQueue and reach the
+// global frontier with one atomic per block (same-address global atomics
+// serialise at ~0.7 ns each, tools/probes/atomics_sync).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -35,6 +39,8 @@ using dev::Pool;
 using dev::RunHeader;
 
 constexpr unsigned kInf = 0xffffffffu;
+constexpr unsigned kQueue = 2048;  // shared-memory frontier queue per block
+using Queue = dev::BlockQueue<kQueue>;
 
 // Per-iteration counters (device): frontier sizes and pool bump pointers,
 // triple-buffered by iteration so no reset has to race a reader.
@@ -65,53 +71,71 @@ struct Args {
   unsigned fsize;  // |F_it| (host-loop variants)
 };
 
+// Per-block state every relaxing kernel carries in shared memory.
+struct Block {
+  Queue q;
+  unsigned long long work;
+};
+
 __device__ __forceinline__ unsigned* cur_front(const Args& a, unsigned it) {
   return (it & 1) ? a.front1 : a.front0;
 }
 __device__ __forceinline__ unsigned* next_front(const Args& a, unsigned it) {
   return (it & 1) ? a.front0 : a.front1;
 }
-
-// Appends v to F_{it+1}: aggregated over the currently converged lanes.
-__device__ __forceinline__ void push(const Args& a, unsigned it, unsigned v) {
-  cg::coalesced_group g = cg::coalesced_threads();
-  unsigned base = 0;
-  if (g.thread_rank() == 0) base = atomicAdd(&a.ctr->fsize[(it + 1) % 3], g.size());
-  base = g.shfl(base, 0);
-  next_front(a, it)[base + g.thread_rank()] = v;
+__device__ __forceinline__ unsigned* next_count(const Args& a, unsigned it) {
+  return &a.ctr->fsize[(it + 1) % 3];
 }
 
-__device__ __forceinline__ void relax(const Args& a, unsigned it, unsigned v, unsigned nd) {
+__device__ __forceinline__ void block_begin(Block& s) {
+  s.q.init();
+  if (threadIdx.x == 0) s.work = 0;
+  __syncthreads();
+}
+
+// Publishes the block's frontier appends and edge count.  All threads call.
+__device__ __forceinline__ void block_end(const Args& a, unsigned it, Block& s) {
+  s.q.flush(next_count(a, it), next_front(a, it));
+  if (threadIdx.x == 0 && s.work) {
+    atomicAdd(&a.hdr->work, s.work);
+    s.work = 0;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void relax(const Args& a, unsigned it, Block& s, unsigned v,
+                                      unsigned nd) {
   if (nd < __ldcg(a.dist + v)) {
     unsigned old = atomicMin(a.dist + v, nd);
-    if (nd < old && atomicExch(a.stamp + v, it + 1) != it + 1) push(a, it, v);
+    if (nd < old && atomicExch(a.stamp + v, it + 1) != it + 1)
+      s.q.push(v, next_count(a, it), next_front(a, it));
   }
 }
 
-__device__ __forceinline__ void relax_serial(const Args& a, unsigned it, unsigned du, unsigned b,
-                                             unsigned e) {
-  for (unsigned k = b; k < e; k++) {
-    unsigned long long nd = static_cast<unsigned long long>(du) + static_cast<unsigned>(__ldg(a.w + k));
-    if (nd < kInf) relax(a, it, static_cast<unsigned>(__ldg(a.col + k)), static_cast<unsigned>(nd));
-  }
+__device__ __forceinline__ void relax_edge(const Args& a, unsigned it, Block& s, unsigned du,
+                                           unsigned k) {
+  unsigned long long nd = static_cast<unsigned long long>(du) + static_cast<unsigned>(__ldg(a.w + k));
+  if (nd < kInf) relax(a, it, s, static_cast<unsigned>(__ldg(a.col + k)), static_cast<unsigned>(nd));
+}
+
+__device__ __forceinline__ void relax_serial(const Args& a, unsigned it, Block& s, unsigned du,
+                                             unsigned b, unsigned e) {
+  for (unsigned k = b; k < e; k++) relax_edge(a, it, s, du, k);
 }
 
 // Warp-cooperative relaxation of edges [b, e) of a vertex at distance du.
-__device__ __forceinline__ void relax_warp(const Args& a, unsigned it, unsigned du, unsigned b,
-                                           unsigned e) {
-  for (unsigned k = b + dev::lane_id(); k < e; k += 32) {
-    unsigned long long nd = static_cast<unsigned long long>(du) + static_cast<unsigned>(__ldg(a.w + k));
-    if (nd < kInf) relax(a, it, static_cast<unsigned>(__ldg(a.col + k)), static_cast<unsigned>(nd));
-  }
+__device__ __forceinline__ void relax_warp(const Args& a, unsigned it, Block& s, unsigned du,
+                                           unsigned b, unsigned e) {
+  for (unsigned k = b + dev::lane_id(); k < e; k += 32) relax_edge(a, it, s, du, k);
 }
 
-__device__ __forceinline__ void drain_items(const Args& a, unsigned it, const Item* items,
+__device__ __forceinline__ void drain_items(const Args& a, unsigned it, Block& s, const Item* items,
                                             unsigned count, unsigned gwarp, unsigned nwarps) {
   for (unsigned i = gwarp; i < count; i += nwarps) {
     Item t = items[i];
     unsigned e = min(t.begin + a.chunk, __ldg(a.rowptr + t.v + 1));
     unsigned du = __ldcg(a.dist + t.v);
-    relax_warp(a, it, du, t.begin, e);
+    relax_warp(a, it, s, du, t.begin, e);
   }
 }
 
@@ -130,13 +154,11 @@ __global__ void __launch_bounds__(256) init_kernel(Args a, unsigned source) {
   }
 }
 
-// Prework shared by all parents: returns the vertex's chunk count when its
-// edges are child work, else relaxes them inline and returns 0.
 // Warp-cooperative inline relaxation of the light vertices held by the 32
 // lanes (the parent's "else work(item)"): their edges are concatenated and
 // swept 32 at a time; each lane locates its edge's vertex by a shuffle binary
 // search.  All lanes call; dl = this lane's light degree (0 otherwise).
-__device__ __forceinline__ void warp_light_relax(const Args& a, unsigned it, unsigned b,
+__device__ __forceinline__ void warp_light_relax(const Args& a, unsigned it, Block& s, unsigned b,
                                                  unsigned du, unsigned dl) {
   const unsigned lane = dev::lane_id();
   const unsigned incl = dev::warp_incl_scan(dl);
@@ -146,73 +168,72 @@ __device__ __forceinline__ void warp_light_relax(const Args& a, unsigned it, uns
     const unsigned j = base + lane;
     unsigned l = 0;
 #pragma unroll
-    for (unsigned s = 16; s > 0; s >>= 1) {
-      unsigned c = l + s;
+    for (unsigned st = 16; st > 0; st >>= 1) {
+      unsigned c = l + st;
       if (__shfl_sync(kFull, lo, c) <= j) l = c;
     }
     const unsigned bl = __shfl_sync(kFull, b, l), lol = __shfl_sync(kFull, lo, l);
     const unsigned dul = __shfl_sync(kFull, du, l);
-    if (j < total) {
-      unsigned k = bl + (j - lol);
-      unsigned long long nd = static_cast<unsigned long long>(dul) + static_cast<unsigned>(__ldg(a.w + k));
-      if (nd < kInf) relax(a, it, static_cast<unsigned>(__ldg(a.col + k)), static_cast<unsigned>(nd));
-    }
+    if (j < total) relax_edge(a, it, s, dul, bl + (j - lol));
   }
 }
 
 // Prework shared by the DP parents: returns the vertex's chunk count when its
 // edges are child work; light vertices are relaxed inline (warp-cooperative).
-// All lanes call.
-__device__ __forceinline__ unsigned prework(const Args& a, unsigned it, unsigned i, unsigned fsize,
-                                            unsigned* u, unsigned* b, unsigned* e, unsigned* du) {
-  unsigned want = 0, dl = 0;
+// All lanes call.  Adds the vertex degree to the block's work counter.
+__device__ __forceinline__ unsigned prework(const Args& a, unsigned it, Block& s, unsigned i,
+                                            unsigned fsize, unsigned* u, unsigned* b, unsigned* e,
+                                            unsigned* du) {
+  unsigned want = 0, dl = 0, deg = 0;
   if (i < fsize) {
     *u = cur_front(a, it)[i];
     *b = __ldg(a.rowptr + *u);
     *e = __ldg(a.rowptr + *u + 1);
     *du = __ldcg(a.dist + *u);
-    if (*e - *b > a.threshold) want = dev::nchunks(*e - *b, a.chunk);
-    else dl = *e - *b;
+    deg = *e - *b;
+    if (deg > a.threshold) want = dev::nchunks(deg, a.chunk);
+    else dl = deg;
   }
-  warp_light_relax(a, it, *b, *du, dl);
+  dev::block_add_u64(&s.work, deg);
+  warp_light_relax(a, it, s, *b, *du, dl);
   return want;
 }
 
-__device__ __forceinline__ void count_work(const Args& a, unsigned deg) {
-  unsigned s = dev::warp_sum(deg);
-  if (dev::lane_id() == 0 && s) atomicAdd(&a.hdr->work, static_cast<unsigned long long>(s));
-}
-
 __global__ void __launch_bounds__(256) cons_child(Args a, const Item* items, unsigned count) {
-  drain_items(a, a.it, items, count, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+  __shared__ Block s;
+  block_begin(s);
+  drain_items(a, a.it, s, items, count, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
               (gridDim.x * blockDim.x) >> 5);
+  block_end(a, a.it, s);
 }
 
 __global__ void __launch_bounds__(256) flat_kernel(Args a) {
+  __shared__ Block s;
+  block_begin(s);
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned deg = 0;
   if (i < a.fsize) {
     unsigned u = cur_front(a, a.it)[i];
     unsigned b = __ldg(a.rowptr + u), e = __ldg(a.rowptr + u + 1);
     deg = e - b;
-    relax_serial(a, a.it, __ldcg(a.dist + u), b, e);
+    relax_serial(a, a.it, s, __ldcg(a.dist + u), b, e);
   }
-  count_work(a, deg);
+  dev::block_add_u64(&s.work, deg);
+  block_end(a, a.it, s);
 }
 
 // Fig. 1(b) child: one edge per thread.
 __global__ void __launch_bounds__(256) basic_child(Args a, unsigned du, unsigned b, unsigned e) {
+  __shared__ Block s;
+  block_begin(s);
   unsigned k = b + blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < e) {
-    unsigned long long nd = static_cast<unsigned long long>(du) + static_cast<unsigned>(__ldg(a.w + k));
-    if (nd < kInf) relax(a, a.it, static_cast<unsigned>(__ldg(a.col + k)), static_cast<unsigned>(nd));
-  }
+  if (k < e) relax_edge(a, a.it, s, du, k);
+  block_end(a, a.it, s);
 }
 
-__device__ __forceinline__ void warp_light_relax(const Args& a, unsigned it, unsigned b,
-                                                 unsigned du, unsigned dl);
-
 __global__ void __launch_bounds__(256) basic_parent(Args a) {
+  __shared__ Block s;
+  block_begin(s);
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned deg = 0, b = 0, du = 0, dl = 0;
   if (i < a.fsize) {
@@ -229,8 +250,9 @@ __global__ void __launch_bounds__(256) basic_parent(Args a) {
       dl = deg;
     }
   }
-  warp_light_relax(a, a.it, b, du, dl);
-  count_work(a, deg);
+  dev::block_add_u64(&s.work, deg);
+  warp_light_relax(a, a.it, s, b, du, dl);
+  block_end(a, a.it, s);
 }
 
 __device__ __forceinline__ unsigned clamp_count(const Args& a, unsigned base, unsigned total) {
@@ -239,15 +261,17 @@ __device__ __forceinline__ unsigned clamp_count(const Args& a, unsigned base, un
 }
 
 __global__ void __launch_bounds__(256) warp_parent(Args a) {
+  __shared__ Block s;
+  block_begin(s);
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x, u = 0, b = 0, e = 0, du = 0;
-  unsigned want = prework(a, a.it, i, a.fsize, &u, &b, &e, &du);
-  count_work(a, e - b);
-  unsigned wbase, wtotal;
-  unsigned at = dev::warp_reserve(&a.ctr->pool[a.it % 3], want, &wbase, &wtotal);
+  unsigned want = prework(a, a.it, s, i, a.fsize, &u, &b, &e, &du);
+  unsigned bbase, btotal;
+  unsigned at = dev::block_reserve(&a.ctr->pool[a.it % 3], want, &bbase, &btotal);
   if (want) {
     dev::write_chunks(a.pool, a.hdr, at, u, b, e, a.chunk);
     __threadfence();
   }
+  const unsigned wbase = __shfl_sync(kFull, at, 0), wtotal = dev::warp_sum(want);
   if (wtotal) {
     unsigned leader = __ffs(__ballot_sync(kFull, want != 0)) - 1;
     __syncwarp();
@@ -260,42 +284,44 @@ __global__ void __launch_bounds__(256) warp_parent(Args a) {
       }
     }
   }
+  block_end(a, a.it, s);
 }
 
 __global__ void __launch_bounds__(256) block_parent(Args a) {
-  __shared__ unsigned s_base;
+  __shared__ Block s;
+  block_begin(s);
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x, u = 0, b = 0, e = 0, du = 0;
-  unsigned want = prework(a, a.it, i, a.fsize, &u, &b, &e, &du);
-  count_work(a, e - b);
-  unsigned btotal;
-  unsigned off = dev::block_excl_scan(want, &btotal);
-  if (threadIdx.x == 0 && btotal) s_base = atomicAdd(&a.ctr->pool[a.it % 3], btotal);
-  __syncthreads();
-  if (want) {
-    dev::write_chunks(a.pool, a.hdr, s_base + off, u, b, e, a.chunk);
-    __threadfence();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && btotal) {
-    unsigned cnt = clamp_count(a, s_base, btotal);
-    if (cnt) {
-      cons_child<<<dev::child_blocks(cnt, a.child_threads, a.child_blocks), a.child_threads, 0,
-                   cudaStreamFireAndForget>>>(a, a.pool.items + s_base, cnt);
-      dev::note_launch(a.hdr);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) grid_parent(Args a) {
-  unsigned i = blockIdx.x * blockDim.x + threadIdx.x, u = 0, b = 0, e = 0, du = 0;
-  unsigned want = prework(a, a.it, i, a.fsize, &u, &b, &e, &du);
-  count_work(a, e - b);
-  unsigned wbase, wtotal;
-  unsigned at = dev::warp_reserve(&a.ctr->pool[a.it % 3], want, &wbase, &wtotal);
+  unsigned want = prework(a, a.it, s, i, a.fsize, &u, &b, &e, &du);
+  unsigned bbase, btotal;
+  unsigned at = dev::block_reserve(&a.ctr->pool[a.it % 3], want, &bbase, &btotal);
   if (want) {
     dev::write_chunks(a.pool, a.hdr, at, u, b, e, a.chunk);
     __threadfence();
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && btotal) {
+    unsigned cnt = clamp_count(a, bbase, btotal);
+    if (cnt) {
+      cons_child<<<dev::child_blocks(cnt, a.child_threads, a.child_blocks), a.child_threads, 0,
+                   cudaStreamFireAndForget>>>(a, a.pool.items + bbase, cnt);
+      dev::note_launch(a.hdr);
+    }
+  }
+  block_end(a, a.it, s);
+}
+
+__global__ void __launch_bounds__(256) grid_parent(Args a) {
+  __shared__ Block s;
+  block_begin(s);
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x, u = 0, b = 0, e = 0, du = 0;
+  unsigned want = prework(a, a.it, s, i, a.fsize, &u, &b, &e, &du);
+  unsigned bbase, btotal;
+  unsigned at = dev::block_reserve(&a.ctr->pool[a.it % 3], want, &bbase, &btotal);
+  if (want) {
+    dev::write_chunks(a.pool, a.hdr, at, u, b, e, a.chunk);
+    __threadfence();
+  }
+  block_end(a, a.it, s);  // this block's inline pushes are published first
   if (dev::grid_last_block(&a.hdr->ticket) && threadIdx.x == 0) {
     unsigned cnt = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[a.it % 3]), a.pool.cap);
     if (cnt) {
@@ -321,24 +347,26 @@ __global__ void __launch_bounds__(32) rotate_kernel(Args a) {
 }
 
 __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iters) {
+  __shared__ Block s;
   cg::grid_group grid = cg::this_grid();
   const unsigned stride = gridDim.x * blockDim.x;
   const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  block_begin(s);
   unsigned it = 0;
   for (; it < max_iters; it++) {
     const unsigned fs = *reinterpret_cast<volatile unsigned*>(&a.ctr->fsize[it % 3]);
     if (fs == 0) break;
     for (unsigned base = blockIdx.x * blockDim.x; base < fs; base += stride) {
       unsigned i = base + threadIdx.x, u = 0, b = 0, e = 0, du = 0;
-      unsigned want = prework(a, it, i, fs, &u, &b, &e, &du);
-      count_work(a, e - b);
-      unsigned wbase, wtotal;
-      unsigned at = dev::warp_reserve(&a.ctr->pool[it % 3], want, &wbase, &wtotal);
+      unsigned want = prework(a, it, s, i, fs, &u, &b, &e, &du);
+      unsigned bbase, btotal;
+      unsigned at = dev::block_reserve(&a.ctr->pool[it % 3], want, &bbase, &btotal);
       if (want) dev::write_chunks(a.pool, a.hdr, at, u, b, e, a.chunk);
     }
     grid.sync();
     unsigned cnt = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[it % 3]), a.pool.cap);
-    drain_items(a, it, a.pool.items, cnt, gtid >> 5, stride >> 5);
+    drain_items(a, it, s, a.pool.items, cnt, gtid >> 5, stride >> 5);
+    block_end(a, it, s);
     if (gtid == 0) rotate(a, it);
     grid.sync();
   }

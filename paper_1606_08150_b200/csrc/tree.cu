@@ -111,8 +111,8 @@ __global__ void __launch_bounds__(256) flat_down(Args a, unsigned lo, unsigned h
   bool active = i < hi;
   unsigned v = active ? a.nodes[i] : 0;
   unsigned want = count_kids(a, v, 0, 1, active);
-  unsigned wb, wt;
-  unsigned at = dev::warp_reserve(&a.cnt[0], want, &wb, &wt);
+  unsigned bb, bt;
+  unsigned at = dev::block_reserve(&a.cnt[0], want, &bb, &bt);
   write_kids(a, v, 0, 1, active && want, at);
 }
 
@@ -199,9 +199,10 @@ __global__ void __launch_bounds__(256) cons_kernel(Args a, const unsigned* items
     unsigned v = active ? items[i] : 0;
     unsigned want = count_kids(a, v, sub, g, active);
     if (G == kWarp || G == kGrid) {
-      unsigned wb, wt;
-      unsigned at = dev::warp_reserve(&a.cnt[0], want, &wb, &wt);
+      unsigned bb, bt;
+      unsigned at = dev::block_reserve(&a.cnt[0], want, &bb, &bt);
       write_kids(a, v, sub, g, active && want, at);
+      const unsigned wb = __shfl_sync(dev::kFull, at, 0), wt = dev::warp_sum(want);
       if (G == kWarp && wt) {
         __threadfence();
         unsigned leader = __ffs(__ballot_sync(dev::kFull, want != 0)) - 1;
@@ -268,13 +269,15 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
   while (hi > lo && levels < max_levels) {
     unsigned* app = ctr + levels % 3;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(levels + 1) % 3] = 0;
-    for (unsigned base = lo + warp_g * gpw; base < hi; base += nwarps * gpw) {
-      unsigned i = base + lane / g;
+    // block-uniform trip count (block_reserve synchronises the block)
+    const unsigned per_block = (blockDim.x >> 5) * gpw;
+    for (unsigned base = lo + blockIdx.x * per_block; base < hi; base += nwarps * gpw) {
+      unsigned i = base + dev::warp_in_block() * gpw + lane / g;
       bool active = i < hi;
       unsigned v = active ? a.nodes[i] : 0;
       unsigned want = count_kids(a, v, sub, g, active);
-      unsigned wb, wt;
-      unsigned at = hi + dev::warp_reserve(app, want, &wb, &wt);
+      unsigned bb, bt;
+      unsigned at = hi + dev::block_reserve(app, want, &bb, &bt);
       write_kids(a, v, sub, g, active && want, at);
     }
     grid.sync();

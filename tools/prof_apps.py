@@ -16,7 +16,8 @@ sys.path.insert(0, ROOT)
 import paper_1606_08150_b200 as dpc  # noqa: E402
 
 VARIANTS = ["flat", "basic", "warp", "block", "grid"]
-TREE = dict(depth=24, lo=1, hi=4, fill=0.84, seed=1)   # ~3.35M nodes, depth 24
+TREE = dict(depth=24, lo=1, hi=4, fill=0.84, seed=1)      # ~3.35M nodes, depth 24
+TREE_PAPER = dict(depth=5, lo=32, hi=128, fill=0.4, seed=1)  # paper-shaped, ~2.7M nodes
 
 
 def _time(ctx, fn, reps):
@@ -93,8 +94,8 @@ def app_gc(ctx, orc, reps, scale=20):
     return out
 
 
-def app_tree(ctx, orc, reps, which):
-    t = dpc.gen_tree(TREE["depth"], TREE["lo"], TREE["hi"], TREE["fill"], TREE["seed"])
+def app_tree(ctx, orc, reps, which, shape=TREE):
+    t = dpc.gen_tree(shape["depth"], shape["lo"], shape["hi"], shape["fill"], shape["seed"])
     ref = orc.tree_desc(t.parent) if which == "tree_desc" else orc.tree_height(t.parent)
     dt = dpc.DeviceTree(ctx, t)
     res = _variants(ctx, reps, lambda v, m: dt.run(which, v, metrics=m),
@@ -102,7 +103,8 @@ def app_tree(ctx, orc, reps, which):
                     lambda met: {"levels": met.iterations})
     dt.close()
     out = _summ(res, t.n - 1, "edges_per_s")
-    out.update({"workload": f"{which}: gen_tree(24, 1, 4, 0.84, 1) = {t.n} nodes, depth {t.depth}",
+    out.update({"workload": f"{which}: gen_tree({shape['depth']}, {shape['lo']}, {shape['hi']}, "
+                            f"{shape['fill']}, {shape['seed']}) = {t.n} nodes, depth {t.depth}",
                 "unit": "G tree edges/s"})
     return out
 
@@ -119,13 +121,16 @@ def run_apps(ctx, apps, reps=3):
             out[a] = app_gc(ctx, orc, reps)
         elif a in ("td", "th"):
             out[a] = app_tree(ctx, orc, reps, "tree_desc" if a == "td" else "tree_height")
+        elif a in ("td_paper", "th_paper"):
+            out[a] = app_tree(ctx, orc, reps, "tree_desc" if a == "td_paper" else "tree_height",
+                              TREE_PAPER)
         out[a]["wall_s"] = round(time.time() - t0, 1)
     return out
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--apps", nargs="*", default=["sssp", "gc", "td", "th"])
+    ap.add_argument("--apps", nargs="*", default=["sssp", "gc", "td", "th", "td_paper", "th_paper"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--json", default=None)
     a = ap.parse_args()
