@@ -408,6 +408,13 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_spmv(g, x, args.cpu_budget)
+    if rank == 0 and world == 1 and args.apps:
+        # the other BASELINE apps, every variant, each checked against the
+        # oracle (speed-ups vs basic-DP and flat per app; tools/prof_apps.py)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from prof_apps import run_apps
+        dg.close()
+        out["apps"] = run_apps(ctx, args.apps, reps=2)
     if rank == 0:
         print(json.dumps(out), flush=True)
     dg.close()
@@ -490,6 +497,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--ref-stride", type=int, default=256)
+    ap.add_argument("--apps", nargs="*",
+                    default=["sssp", "gc", "td", "th", "td_paper", "th_paper"],
+                    help="other BASELINE apps timed in the same run (empty list: none)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
