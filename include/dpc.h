@@ -172,6 +172,9 @@ typedef struct dpc_launch_cfg {
 #define DPC_CFG_GRID_CDP 1 /* grid variant: last block launches the child via
                               CDP2 (else: one persistent cooperative kernel
                               with a device-wide barrier) */
+#define DPC_CFG_GRID_CHUNKED 2 /* SpMV persistent grid variant: drain fixed-size
+                                  chunk items warp by warp instead of the
+                                  stream-balanced drain (comparison only) */
 
 /* Fills the measured default for (app, variant) (configs/launch_cfg.json,
  * compiled in).  Replaces resolve_config, transform.hpp:417-475. */

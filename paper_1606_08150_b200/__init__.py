@@ -55,6 +55,7 @@ VARIANTS = {"flat": 0, "basic": 1, "warp": 2, "block": 3, "grid": 4}
 APPS = {"sssp": 0, "spmv": 1, "color": 2, "tree_desc": 3, "tree_height": 4}
 GEN_WEIGHTS, GEN_VALUES, GEN_PERMUTE, GEN_SYMMETRIC = 1, 2, 4, 8
 CFG_GRID_CDP = 1
+CFG_GRID_CHUNKED = 2
 
 
 class DpcError(RuntimeError):
@@ -354,6 +355,8 @@ def launch_cfg(app: str, variant: str, **overrides) -> LaunchCfg:
     for k, v in overrides.items():
         if k == "grid_cdp":
             cfg.flags = (cfg.flags | CFG_GRID_CDP) if v else (cfg.flags & ~CFG_GRID_CDP)
+        elif k == "grid_chunked":
+            cfg.flags = (cfg.flags | CFG_GRID_CHUNKED) if v else (cfg.flags & ~CFG_GRID_CHUNKED)
         else:
             setattr(cfg, k, int(v))
     return cfg

@@ -299,7 +299,7 @@ void dpc_dgraph_free(dpc_dgraph* g) {
   }
   void* bufs[] = {g->rowptr, g->col,      g->w,        g->val,   g->x,    g->y,
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
-                  g->items, g->ctr, g->gc_state};
+                  g->items, g->ctr, g->gc_state, g->soff, g->smark};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->hdr_host) cudaFreeHost(g->hdr_host);
@@ -332,9 +332,9 @@ dpc_status dpc_dgraph_upload(dpc_ctx* c, const dpc_csr* h, dpc_dgraph** out) {
   for (size_t i = 0; i < n; i++) g->max_deg = std::max<int64_t>(g->max_deg, h->rowptr[i + 1] - h->rowptr[i]);
   const size_t nv = std::max<size_t>(n, 1), mv = std::max<size_t>(m, 1);
   if ((e = cudaMalloc(&g->rowptr, sizeof(unsigned) * (n + 1))) != cudaSuccess) return cleanup(e, "cudaMalloc rowptr");
-  if ((e = cudaMalloc(&g->col, sizeof(int) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc col");
-  if (h->w && (e = cudaMalloc(&g->w, sizeof(int) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc w");
-  if (h->val && (e = cudaMalloc(&g->val, sizeof(float) * mv)) != cudaSuccess) return cleanup(e, "cudaMalloc val");
+  if ((e = cudaMalloc(&g->col, sizeof(int) * (mv + 4))) != cudaSuccess) return cleanup(e, "cudaMalloc col");
+  if (h->w && (e = cudaMalloc(&g->w, sizeof(int) * (mv + 4))) != cudaSuccess) return cleanup(e, "cudaMalloc w");
+  if (h->val && (e = cudaMalloc(&g->val, sizeof(float) * (mv + 4))) != cudaSuccess) return cleanup(e, "cudaMalloc val");
   if ((e = cudaMalloc(&g->x, sizeof(float) * nx)) != cudaSuccess) return cleanup(e, "cudaMalloc x");
   if ((e = cudaMalloc(&g->y, sizeof(float) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc y");
   if ((e = cudaMalloc(&g->dist, sizeof(unsigned) * nv)) != cudaSuccess) return cleanup(e, "cudaMalloc dist");

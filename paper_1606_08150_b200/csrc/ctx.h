@@ -51,6 +51,11 @@ struct dpc_dgraph {
   // consolidation pool
   dpc::dev::Item* items = nullptr;
   unsigned cap = 0;
+  // stream-balanced drain (SpMV grid): per-item stream offsets and the
+  // item index at every kMark-th stream position
+  unsigned* soff = nullptr;
+  unsigned* smark = nullptr;
+  size_t soff_cap = 0, smark_cap = 0;
   // host copies used to size pools: degree array
   std::vector<int64_t> host_rowptr;
   std::map<std::pair<int, int>, uint64_t> need_cache;

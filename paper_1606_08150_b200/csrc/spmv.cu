@@ -54,6 +54,7 @@ struct Args {
   unsigned chunk;
   unsigned child_threads;
   unsigned child_blocks;  // cap, 0 = none
+  unsigned xflags;        // experiment switches (dpc_launch_cfg.flags >> 24), 0 in production
 };
 
 __device__ __forceinline__ int4 ldg_stream(const int4* p) {
@@ -581,6 +582,293 @@ __global__ void __launch_bounds__(256, MB) grid_persistent(Args a) {
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&a.hdr->t[2], dev::global_ns());
 }
+// ------------------------------------------------------------------------
+// Stream-balanced grid consolidation (the default grid variant).
+//
+// The consolidated child of the grid variant is the reference's MultiBlock
+// drain (transform.hpp:564-598): every thread of the grid cooperates on the
+// buffered items.  Here the buffered rows form ONE virtual stream of
+// nonzeros and the drain cuts that stream into equal slices, one per warp,
+// so every warp streams the same number of nonzeros and the grid finishes
+// together (no per-item tail, whatever the degree distribution).
+//
+// dp_insert (transform.hpp:501-508; sim.hpp:1492-1528): a row with
+// deg > threshold reserves its item slot AND its stream range with ONE
+// 64-bit atomic per block (slot << 38 | positions), so slot order is stream
+// order.  A row's stream range is its CSR range widened to 16-byte
+// boundaries ([b & ~3, (e + 3) & ~3)), so every stream offset is a multiple
+// of 4 and an aligned 4-position group of the stream lies inside ONE item
+// and maps onto ONE aligned int4 of col / float4 of val; the widening
+// elements are masked (their sectors are fetched by the neighbour rows
+// anyway).
+//
+// Drain: a warp sweeps its slice in windows of 128 positions (4 per lane), V
+// windows per step (2V vector loads + 4V x gathers in flight per lane).  The
+// items of a window are located with one ballot and one OR-reduction (the
+// lanes where an item starts), partial sums are combined per item with a
+// 5-step segmented shuffle scan, and each item segment is written with a
+// plain store when the item lies inside the window, else with atomicAdd.
+constexpr int kPackShift = 38;  // packed reservation: items << 38 | positions
+constexpr unsigned long long kNnzMask = (1ull << kPackShift) - 1;
+constexpr int kStreamV = 4;
+constexpr unsigned kWin = 128;  // stream positions per window (32 lanes x 4)
+
+struct Stream {
+  uint2* seg;  // per item: {stream offset, CSR end}; Item {row, CSR begin} in the pool
+  unsigned long long* sctr;
+};
+
+__device__ __forceinline__ unsigned long long warp_incl_scan64(unsigned long long v) {
+  const unsigned lane = dev::lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long t = __shfl_up_sync(kFull, v, o);
+    if (lane >= static_cast<unsigned>(o)) v += t;
+  }
+  return v;
+}
+
+__device__ __forceinline__ unsigned stream_len(unsigned b, unsigned e) {
+  return ((e + 3u) & ~3u) - (b & ~3u);
+}
+
+// Insert of row `row` (CSR range [b, e)) at packed position `at`.
+__device__ __forceinline__ void stream_insert(const Args& a, const Stream& st, unsigned long long at,
+                                              unsigned row, unsigned b, unsigned e) {
+  const unsigned slot = static_cast<unsigned>(at >> kPackShift);
+  if (slot >= a.pool.cap) {
+    atomicOr(&a.hdr->overflow, 1u);
+    return;
+  }
+  if (!(a.xflags & 4u)) {
+    a.pool.items[slot] = Item{row, b};
+    st.seg[slot] = make_uint2(static_cast<unsigned>(at & kNnzMask), e);
+  }
+}
+
+// Per-warp shared-memory window onto the item list: kBatch consecutive
+// items {stream offset, CSR end, CSR begin, row}.
+constexpr unsigned kBatch = 128;
+
+__device__ __forceinline__ void load_items(const Args& a, const Stream& st, unsigned ni, unsigned base,
+                                           uint4* buf) {
+  const unsigned lane = dev::lane_id();
+#pragma unroll
+  for (unsigned i = 0; i < kBatch / 32; i++) {
+    const unsigned idx = base + lane + 32 * i;
+    uint4 v = make_uint4(0xffffffffu, 0, 0, 0);
+    if (idx < ni) {
+      const uint2 sg = __ldcg(st.seg + idx);
+      const Item it = a.pool.items[idx];
+      v = make_uint4(sg.x, sg.y, it.begin, it.v);
+    }
+    buf[lane + 32 * i] = v;
+  }
+  __syncwarp();
+}
+
+// Drains this warp's slice [s0, s1) of the stream (s0 a multiple of kWin,
+// s1 a multiple of kWin or the stream end).  All lanes call.
+//   start: 32-ary search of the item covering s0 (log32(items) L2 rounds)
+//   window: its items are ja .. ja+31 at most (items are >= 4 positions and
+//     start on 4-aligned positions); each lane reads item ja+lane from the
+//     shared-memory batch, the lanes where an item starts form a bit mask
+//     (one OR-reduction), and each lane's item is ja + popc(mask below it).
+//     ja of the next window follows from the mask; the batch is refilled
+//     from L2 when the window could run past it.
+template <int V>
+__device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, unsigned ni,
+                                             unsigned s0, unsigned s1, uint4* buf) {
+  const unsigned lane = dev::lane_id();
+  const unsigned lt_mask = (2u << lane) - 1u;  // lanes <= this one
+  unsigned lo = 0, hi = ni;  // seg[lo].x <= s0 < seg[hi].x (hi = ni: end)
+  while (hi - lo > 1) {
+    const unsigned step = (hi - lo + 31) / 32;
+    const unsigned probe = lo + lane * step;
+    const unsigned v = probe < hi ? __ldcg(&st.seg[probe].x) : 0xffffffffu;
+    const unsigned c = __popc(__ballot_sync(kFull, v <= s0));  // >= 1: lane 0 probes lo
+    const unsigned nlo = lo + (c - 1) * step;
+    hi = min(hi, nlo + step);
+    lo = nlo;
+  }
+  unsigned ja = lo, bb = lo;
+  load_items(a, st, ni, bb, buf);
+  for (unsigned p0 = s0; p0 < s1; p0 += kWin * V) {
+    unsigned kk[V], info[V], rw[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      const unsigned pw = p0 + kWin * v;
+      info[v] = 0;
+      kk[v] = 0;
+      rw[v] = 0;
+      if (pw < s1) {
+        if (ja + 33 > bb + kBatch) {
+          bb = ja;
+          load_items(a, st, ni, bb, buf);
+        }
+        const unsigned last = min(pw + kWin, s1) - 1;
+        const unsigned off = buf[ja - bb + lane].x;
+        // lanes where an item starts inside the window (lane 0 excluded)
+        const bool starts = off > pw && off <= last;
+        const unsigned smask = __reduce_or_sync(kFull, starts ? 1u << ((off - pw) >> 2) : 0u);
+        const uint4 it = buf[ja - bb + __popc(smask & lt_mask)];
+        rw[v] = it.w;
+        const unsigned q = pw + 4 * lane;
+        if (q < s1) {
+          const unsigned oj = it.x, ej = it.y, bj = it.z;
+          const unsigned k = (bj & ~3u) + (q - oj);
+          kk[v] = k;
+          unsigned m = 0;
+#pragma unroll
+          for (int e = 0; e < 4; e++) m |= (k + e >= bj && k + e < ej) ? 1u << e : 0u;
+          const unsigned ls = 31 - __clz((smask | 1u) & lt_mask);  // segment start lane
+          const bool seg_end = lane == 31 || ((smask >> (lane + 1)) & 1u) || q + 4 >= s1;
+          const bool whole = oj >= pw && oj + stream_len(bj, ej) <= pw + kWin;  // item inside the window
+          info[v] = m | (ls << 4) | (seg_end ? 1u << 9 : 0u) | (whole ? 1u << 10 : 0u);
+        }
+        // first item of the next window
+        ja += __popc(smask);
+        if (buf[ja + 1 - bb].x == pw + kWin) ja++;
+      }
+    }
+    int4 c[V];
+    float4 w[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      c[v] = make_int4(0, 0, 0, 0);
+      w[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (info[v] & 15u) {
+        c[v] = ldg_stream(reinterpret_cast<const int4*>(a.col + kk[v]));
+        w[v] = ldg_stream(reinterpret_cast<const float4*>(a.val + kk[v]));
+      }
+    }
+    float s[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      // masked lanes contribute exact zeros (the widening may read padding)
+      const unsigned m = info[v];
+      float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+      if (m & 1u) q0 = w[v].x * __ldg(a.x + c[v].x);
+      if (m & 2u) q1 = w[v].y * __ldg(a.x + c[v].y);
+      if (m & 4u) q2 = w[v].z * __ldg(a.x + c[v].z);
+      if (m & 8u) q3 = w[v].w * __ldg(a.x + c[v].w);
+      s[v] = (q0 + q1) + (q2 + q3);
+    }
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      if (p0 + kWin * v >= s1) break;
+      const unsigned ls = (info[v] >> 4) & 31u;
+      float t = s[v];
+#pragma unroll
+      for (unsigned d = 1; d < 32; d <<= 1) {
+        const float u = __shfl_up_sync(kFull, t, d);
+        if (lane >= ls + d) t += u;
+      }
+      if (info[v] & (1u << 9)) {
+        if (info[v] & (1u << 10)) a.y[rw[v]] = t;
+        else atomicAdd(a.y + rw[v], t);
+      }
+    }
+  }
+}
+
+// Persistent grid-consolidated SpMV.
+//   insert: 256-row tiles are dealt to blocks round-robin (tile k*G + b of a
+//     round goes to block b, row = lane), kRound tiles per thread per round.
+//     The round's stream lengths of the rows with deg > threshold are
+//     scanned per tile (slots in tile-major, then row order, so the item
+//     stores of a warp are contiguous), ONE 64-bit atomic per block and
+//     round reserves the slots and positions; lighter rows are done inline
+//     (warp-cooperative).
+//   one device-wide barrier (the paper's custom global barrier,
+//     PAPER.md:244-250; legal because a cooperative launch co-schedules
+//     the whole grid)
+//   drain: stream-balanced, every warp the same number of positions.
+constexpr int kRound = 8;
+
+template <bool INLINE, int V, int MINB>
+__global__ void __launch_bounds__(256, MINB) grid_stream(Args a, Stream st) {
+  __shared__ unsigned long long s_w[kRound * 8];
+  __shared__ unsigned long long s_base;
+  __shared__ uint4 s_items[8][kBatch];
+  cg::grid_group grid = cg::this_grid();
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[0] = dev::global_ns();
+  const unsigned lane = dev::lane_id(), wib = dev::warp_in_block();
+  const unsigned lt_excl = (1u << lane) - 1u;
+  const unsigned G = gridDim.x, ntiles = (a.n + 255) / 256;
+  for (unsigned t0 = blockIdx.x; t0 < ntiles; t0 += G * kRound) {
+    unsigned bb[kRound], ee[kRound], inc[kRound];
+#pragma unroll
+    for (int k = 0; k < kRound; k++) {
+      const unsigned r = (t0 + k * G) * 256 + threadIdx.x;
+      bb[k] = ee[k] = 0;
+      if (t0 + k * G < ntiles && r < a.n) bb[k] = __ldg(a.rowptr + r), ee[k] = __ldg(a.rowptr + r + 1);
+    }
+#pragma unroll
+    for (int k = 0; k < kRound; k++) {
+      const bool cons = ee[k] - bb[k] > a.threshold;
+      const unsigned len = cons ? stream_len(bb[k], ee[k]) : 0u;
+      inc[k] = dev::warp_incl_scan(len);
+      const unsigned cnt = __popc(__ballot_sync(kFull, cons));
+      if (lane == 31) s_w[k * 8 + wib] = (static_cast<unsigned long long>(cnt) << kPackShift) | inc[k];
+    }
+    __syncthreads();
+    if (wib == 0) {  // tile-major scan of the kRound x 8 warp totals, one reservation
+      const unsigned long long x0 = s_w[2 * lane], x1 = s_w[2 * lane + 1];
+      const unsigned long long pi = warp_incl_scan64(x0 + x1);
+      s_w[2 * lane] = pi - x0 - x1;
+      s_w[2 * lane + 1] = pi - x1;
+      if (lane == 31) s_base = pi ? atomicAdd(st.sctr, pi) : 0ull;
+    }
+    __syncthreads();
+    const unsigned long long base = s_base;
+#pragma unroll
+    for (int k = 0; k < kRound; k++) {
+      const unsigned r = (t0 + k * G) * 256 + threadIdx.x;
+      const bool in = t0 + k * G < ntiles && r < a.n;
+      const unsigned b = bb[k], e = ee[k];
+      const bool cons = e - b > a.threshold;
+      const unsigned ball = __ballot_sync(kFull, cons);
+      float sl = 0.f;
+      if (INLINE) sl = warp_light_rows(a, b, in && !cons ? e - b : 0u);
+      if (in && !(a.xflags & 8u)) a.y[r] = cons ? 0.f : sl;
+      if (cons) {
+        const unsigned len = stream_len(b, e);
+        const unsigned long long at = base + s_w[k * 8 + wib] +
+                                      ((static_cast<unsigned long long>(__popc(ball & lt_excl)) << kPackShift) |
+                                       (inc[k] - len));
+        stream_insert(a, st, at, r, b, e);
+      }
+    }
+    __syncthreads();  // s_w / s_base are reused by the next round
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[1] = dev::global_ns();
+  const unsigned long long tot = *reinterpret_cast<volatile unsigned long long*>(st.sctr);
+  const unsigned ni = min(static_cast<unsigned>(tot >> kPackShift), a.pool.cap);
+  const unsigned total = static_cast<unsigned>(tot & kNnzMask);
+  const unsigned nw = (gridDim.x * blockDim.x) >> 5, gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long per = ((static_cast<unsigned long long>(total) + nw - 1) / nw + kWin - 1) /
+                                 kWin * kWin;
+  const unsigned long long s0 = static_cast<unsigned long long>(gw) * per;
+  if (ni > 0 && s0 < total && !(a.xflags & 1u))
+    stream_drain<V>(a, st, ni, static_cast<unsigned>(s0),
+                    static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
+                    s_items[wib]);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&a.hdr->t[2], dev::global_ns());
+}
+
+// [INLINE][shape]: shape 0 = V4 x 4 blocks/SM, 1 = V2 x 6, 2 = V2 x 8 (flag bits 20-21)
+static const void* stream_fn(bool inl, unsigned flags) {
+  static const void* t[2][3] = {
+      {reinterpret_cast<const void*>(grid_stream<false, 4, 4>), reinterpret_cast<const void*>(grid_stream<false, 2, 6>),
+       reinterpret_cast<const void*>(grid_stream<false, 2, 8>)},
+      {reinterpret_cast<const void*>(grid_stream<true, 4, 4>), reinterpret_cast<const void*>(grid_stream<true, 2, 6>),
+       reinterpret_cast<const void*>(grid_stream<true, 2, 8>)}};
+  const unsigned shape = (flags >> 20) & 3u;
+  return t[inl ? 1 : 0][shape > 2 ? 0 : shape];
+}
 
 using PersistentFn = void (*)(Args);
 // [LM][DM][MB == 8]
@@ -600,6 +888,18 @@ static PersistentFn persistent_fn(unsigned flags) {
 }
 
 }  // namespace spmv
+
+static dpc_status ensure_stream(dpc_dgraph* g, uint64_t items) {
+  if (items > g->soff_cap) {
+    DPC_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    if (g->soff) cudaFree(g->soff);
+    g->soff = nullptr;
+    g->soff_cap = 0;
+    DPC_CUDA(cudaMalloc(&g->soff, sizeof(uint2) * std::max<uint64_t>(items, 1)));
+    g->soff_cap = items;
+  }
+  return DPC_OK;
+}
 
 static int coop_blocks(dpc_ctx* ctx, const void* fn, int threads) {
   int per_sm = 0;
@@ -636,11 +936,24 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
   a.chunk = c.chunk;
   a.child_threads = c.child_threads;
   a.child_blocks = c.child_blocks;
-  if (c.variant != DPC_FLAT && c.variant != DPC_BASIC) {
+  a.xflags = c.flags >> 24;
+  // stream-balanced grid drain (grid_stream)
+  const bool use_stream = c.variant == DPC_GRID && c.grid_persistent && !(c.flags & DPC_CFG_GRID_CHUNKED);
+  spmv::Stream sa{};
+  if (use_stream) {
+    const uint64_t heavy = pool_need(g, c.threshold, 1u << 30);
+    st = ensure_pool(g, heavy);
+    if (st != DPC_OK) return st;
+    // stream positions <= m + 6 per item (16-byte widening)
+    st = ensure_stream(g, heavy);
+    if (st != DPC_OK) return st;
+    sa = spmv::Stream{reinterpret_cast<uint2*>(g->soff), &g->hdr->work};
+  } else if (c.variant != DPC_FLAT && c.variant != DPC_BASIC) {
     st = ensure_pool(g, pool_need(g, c.threshold, c.chunk));
     if (st != DPC_OK) return st;
   }
-  a.pool = dev::Pool{g->items, g->cap};
+  a.pool = dev::Pool{g->items, use_stream ? static_cast<unsigned>(std::min<uint64_t>(g->cap, g->soff_cap))
+                                          : g->cap};
   st = ensure_pending_for(ctx, g, c.variant, c.threshold, c.parent_threads);
   if (st != DPC_OK) return st;
   st = begin_run(ctx, g->hdr);
@@ -654,7 +967,12 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
       case DPC_WARP: spmv::warp_parent<<<blocks, 256, 0, s>>>(a); break;
       case DPC_BLOCK: spmv::block_parent<<<blocks, 256, 0, s>>>(a); break;
       case DPC_GRID:
-        if (c.grid_persistent) {
+        if (use_stream) {
+          const void* fn = spmv::stream_fn(c.threshold > 0, c.flags);
+          int nb = coop_blocks(ctx, fn, 256);
+          void* args[] = {&a, &sa};
+          DPC_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nb), dim3(256), args, 0, s));
+        } else if (c.grid_persistent) {
           const void* fn = reinterpret_cast<const void*>(spmv::persistent_fn(c.flags));
           int nb = coop_blocks(ctx, fn, 256);
           void* args[] = {&a};

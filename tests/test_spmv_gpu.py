@@ -49,7 +49,7 @@ def test_spmv_launch_laws(ctx, variant):
     g = dpc.gen_rmat(13, 16, seed=3, weights=False, values=True)
     deg = g.degrees()
     heavy = deg > 32
-    cfg = dpc.launch_cfg("spmv", variant, grid_cdp=True)
+    cfg = dpc.launch_cfg("spmv", variant, grid_cdp=True, threshold=32)
     y, met = dpc.run_spmv(g, _x(g.n), variant, cfg=cfg, ctx=ctx)
     pad = np.zeros((-len(heavy)) % 256, bool)
     h = np.concatenate([heavy, pad])
@@ -119,3 +119,37 @@ def test_spmv_config2_full_size(ctx, orc):
     dg.spmv_host(x, y, "grid")
     _check(orc, g, x, y)
     dg.close()
+
+
+def _ragged(seed=1, hub=100_003):
+    lens = np.concatenate([np.arange(0, 301), [hub], np.arange(300, -1, -7), [4] * 500, [1] * 777])
+    rowptr = np.concatenate([[0], np.cumsum(lens)])
+    n = len(lens)
+    rng = np.random.default_rng(seed)
+    col = rng.integers(0, n, rowptr[-1]).astype(np.int32)
+    val = (rng.integers(1, 1 << 24, rowptr[-1]) / float(1 << 24)).astype(np.float32)
+    return dpc.csr_from_arrays(rowptr, col, val=val)
+
+
+@pytest.mark.parametrize("shape", [0, 1, 2])
+@pytest.mark.parametrize("threshold", [0, 3, 7, 31, 32, 100])
+def test_spmv_grid_stream_forms(ctx, orc, shape, threshold):
+    """Stream-balanced grid drain: every kernel shape x consolidation
+    threshold on ragged rows (unaligned starts, window-boundary items, a hub)
+    and on an R-MAT matrix."""
+    for g in (_ragged(), dpc.gen_rmat(13, 16, seed=4, weights=False, values=True)):
+        x = _x(g.n)
+        cfg = dpc.launch_cfg("spmv", "grid", threshold=threshold)
+        cfg.flags |= shape << 20
+        y, met = dpc.run_spmv(g, x, "grid", cfg=cfg, ctx=ctx)
+        _check(orc, g, x, y)
+        assert met.child_launch_count == 0
+
+
+@pytest.mark.parametrize("threshold", [0, 32])
+def test_spmv_grid_chunked_form(ctx, orc, threshold):
+    g = _ragged(seed=3)
+    x = _x(g.n)
+    cfg = dpc.launch_cfg("spmv", "grid", grid_chunked=True, threshold=threshold)
+    y, _ = dpc.run_spmv(g, x, "grid", cfg=cfg, ctx=ctx)
+    _check(orc, g, x, y)

@@ -16,6 +16,7 @@ ap.add_argument("--scale", type=int, default=20)
 ap.add_argument("--cdp", action="store_true")
 ap.add_argument("--chunk", type=int, default=0)
 ap.add_argument("--flags", type=int, default=0)
+ap.add_argument("--threshold", type=int, default=-1)
 a = ap.parse_args()
 ctx = dpc.Context(0)
 g = dpc.gen_rmat(a.scale, 16, seed=1, weights=False, values=True)
@@ -27,6 +28,8 @@ for v in a.variants:
         over["grid_cdp"] = True
     if a.chunk:
         over["chunk"] = a.chunk
+    if a.threshold >= 0:
+        over["threshold"] = a.threshold
     cfg = dpc.launch_cfg("spmv", v, **over)
     cfg.flags |= a.flags
     for _ in range(a.reps):

@@ -47,7 +47,13 @@ def timeit(cfg):
         ctx.record(1)
         ts.append(ctx.elapsed_ms(0, 1))
     y = dg.get_y().astype(np.float64)
-    ok = bool(np.all(np.abs(y - y64) <= 1e-5 * np.abs(y64)))
+    err = np.abs(y - y64) / np.maximum(np.abs(y64), 1e-300)
+    ok = bool(np.all(err <= 1e-5))
+    if not ok:
+        bad = np.argsort(-err)[:5]
+        deg = np.diff(g.rowptr)
+        print("  worst rows", [(int(r), int(deg[r]), float(y[r]), float(y64[r])) for r in bad],
+              "nbad", int((err > 1e-5).sum()), flush=True)
     return float(np.median(ts)), ok
 
 
