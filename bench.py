@@ -261,7 +261,7 @@ def run_multi(args, dist, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / peak, 4),
                      "traffic": None, "algorithmic_bytes": alg,
-                     "kernel": "ncclAllGather + spmv::grid_persistent (rank 0)"},
+                     "kernel": "ncclAllGather + spmv::grid_stream (rank 0)"},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
@@ -385,7 +385,8 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "BASELINE config 2: SpMV CSR, synthetic R-MAT scale-20 matrix "
                                "(1,048,576 rows, 16,777,216 nnz, fp32 values/x in (0,1], seed 1)",
-                   "variant": "grid-consolidated (persistent cooperative kernel)",
+                   "variant": "grid-consolidated: one persistent cooperative kernel, insert phase + "
+                              "device-wide barrier + stream-balanced drain (threshold 0, measured)",
                    "n": n, "nnz": nnz, "l2": "flushed (512 MB memset) before every timed step",
                    "parallelism": f"replicas{world}" if world > 1 else "single GPU",
                    "generate_s": round(gen_s, 2)},
@@ -403,7 +404,7 @@ def run_ours(args):
                 "api": "dpc_spmv_host (C ABI), pinned host x/y, A resident"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None,
-                     "algorithmic_bytes": alg, "kernel": "spmv::grid_persistent",
+                     "algorithmic_bytes": alg, "kernel": "spmv::grid_stream (whole step)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"},
         "gpu_launches": args.steps * (1 + int(met.child_launch_count)),
         "clocks": clk.summary(),

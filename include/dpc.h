@@ -175,6 +175,9 @@ typedef struct dpc_launch_cfg {
 #define DPC_CFG_GRID_CHUNKED 2 /* SpMV persistent grid variant: drain fixed-size
                                   chunk items warp by warp instead of the
                                   stream-balanced drain (comparison only) */
+#define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
+                                 + grid.sync instead of a normal launch of a
+                                 co-resident grid + software barrier */
 
 /* Fills the measured default for (app, variant) (configs/launch_cfg.json,
  * compiled in).  Replaces resolve_config, transform.hpp:417-475. */

@@ -204,6 +204,24 @@ __device__ __forceinline__ bool grid_last_block(unsigned* ticket) {
   return s_last;
 }
 
+// Device-wide barrier for a grid whose blocks are all co-resident (checked
+// by the host with the occupancy calculator before a normal launch): the
+// paper's custom global barrier without the cooperative
+// launch's extra setup cost.  `count` is zero at kernel start and used once.
+__device__ __forceinline__ void soft_grid_barrier(unsigned* count) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(count, 1u);
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(count) : "memory");
+      if (seen < gridDim.x) __nanosleep(20);
+    } while (seen < gridDim.x);
+  }
+  __syncthreads();
+}
+
 // Records a device-side launch, flags a failed one (first error code kept in
 // aux0 so the host can name it).
 __device__ __forceinline__ void note_launch(RunHeader* hdr) {

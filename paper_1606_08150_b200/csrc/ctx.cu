@@ -299,7 +299,7 @@ void dpc_dgraph_free(dpc_dgraph* g) {
   }
   void* bufs[] = {g->rowptr, g->col,      g->w,        g->val,   g->x,    g->y,
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
-                  g->items, g->ctr, g->gc_state, g->soff, g->smark};
+                  g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->hdr_host) cudaFreeHost(g->hdr_host);
@@ -349,6 +349,11 @@ dpc_status dpc_dgraph_upload(dpc_ctx* c, const dpc_csr* h, dpc_dgraph** out) {
   if (e == cudaSuccess && m) e = cudaMemcpyAsync(g->col, h->col, sizeof(int) * m, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess && m && h->w) e = cudaMemcpyAsync(g->w, h->w, sizeof(int) * m, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess && m && h->val) e = cudaMemcpyAsync(g->val, h->val, sizeof(float) * m, cudaMemcpyHostToDevice, s);
+  // 16 bytes of zero padding past the last nonzero: vector loads of the last
+  // aligned group may touch it (stream_drain widens rows to 16 bytes)
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->col + m, 0, 4 * sizeof(int), s);
+  if (e == cudaSuccess && g->w) e = cudaMemsetAsync(g->w + m, 0, 4 * sizeof(int), s);
+  if (e == cudaSuccess && g->val) e = cudaMemsetAsync(g->val + m, 0, 4 * sizeof(float), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(g->x, 0, sizeof(float) * nx, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(g->y, 0, sizeof(float) * nv, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(g->hdr, 0, sizeof(RunHeader) * 2, s);

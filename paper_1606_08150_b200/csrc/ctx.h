@@ -54,8 +54,11 @@ struct dpc_dgraph {
   // stream-balanced drain (SpMV grid): per-item stream offsets and the
   // item index at every kMark-th stream position
   unsigned* soff = nullptr;
-  unsigned* smark = nullptr;
-  size_t soff_cap = 0, smark_cap = 0;
+  size_t soff_cap = 0;
+  // SpMV hot-column cache plan (column per slot) and per-run x values
+  int* xhot_col = nullptr;
+  float* xhot_val = nullptr;
+  int xhot_log = 0;
   // host copies used to size pools: degree array
   std::vector<int64_t> host_rowptr;
   std::map<std::pair<int, int>, uint64_t> need_cache;

@@ -55,6 +55,7 @@ struct Args {
   unsigned child_threads;
   unsigned child_blocks;  // cap, 0 = none
   unsigned xflags;        // experiment switches (dpc_launch_cfg.flags >> 24), 0 in production
+  unsigned coop;          // launched cooperatively (grid.sync) vs normal launch + soft barrier
 };
 
 __device__ __forceinline__ int4 ldg_stream(const int4* p) {
@@ -616,7 +617,18 @@ constexpr unsigned kWin = 128;  // stream positions per window (32 lanes x 4)
 struct Stream {
   uint2* seg;  // per item: {stream offset, CSR end}; Item {row, CSR begin} in the pool
   unsigned long long* sctr;
+  const int* xhot_col;  // hot-column cache plan: column held by each slot (-1: none)
+  float* xhot_val;      // x at those columns, gathered once per run
 };
+
+// Hot-column cache of x in shared memory.  R-MAT / power-law matrices reuse
+// a few columns heavily (config 2: the 16K most popular columns take 59% of
+// the nonzeros), and scattered 4-byte x gathers are bound by L1 tag
+// throughput (~1 distinct line per SM clock), not by HBM.  A direct-mapped
+// table of S = 2^SLOG {column, value} slots (multiplicative hash; per slot
+// the most popular column, planned once per matrix on the device) serves the
+// hits from shared memory; misses go to L1/L2 as before.
+__device__ __forceinline__ unsigned xslot(unsigned c, int slog) { return (c * 2654435761u) >> (32 - slog); }
 
 __device__ __forceinline__ unsigned long long warp_incl_scan64(unsigned long long v) {
   const unsigned lane = dev::lane_id();
@@ -648,13 +660,12 @@ __device__ __forceinline__ void stream_insert(const Args& a, const Stream& st, u
 
 // Per-warp shared-memory window onto the item list: kBatch consecutive
 // items {stream offset, CSR end, CSR begin, row}.
-constexpr unsigned kBatch = 128;
-
+template <unsigned KB>
 __device__ __forceinline__ void load_items(const Args& a, const Stream& st, unsigned ni, unsigned base,
                                            uint4* buf) {
   const unsigned lane = dev::lane_id();
 #pragma unroll
-  for (unsigned i = 0; i < kBatch / 32; i++) {
+  for (unsigned i = 0; i < KB / 32; i++) {
     const unsigned idx = base + lane + 32 * i;
     uint4 v = make_uint4(0xffffffffu, 0, 0, 0);
     if (idx < ni) {
@@ -676,9 +687,9 @@ __device__ __forceinline__ void load_items(const Args& a, const Stream& st, unsi
 //     (one OR-reduction), and each lane's item is ja + popc(mask below it).
 //     ja of the next window follows from the mask; the batch is refilled
 //     from L2 when the window could run past it.
-template <int V>
+template <int V, unsigned KB, int SLOG>
 __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, unsigned ni,
-                                             unsigned s0, unsigned s1, uint4* buf) {
+                                             unsigned s0, unsigned s1, uint4* buf, const uint2* xc) {
   const unsigned lane = dev::lane_id();
   const unsigned lt_mask = (2u << lane) - 1u;  // lanes <= this one
   unsigned lo = 0, hi = ni;  // seg[lo].x <= s0 < seg[hi].x (hi = ni: end)
@@ -692,52 +703,116 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
     lo = nlo;
   }
   unsigned ja = lo, bb = lo;
-  load_items(a, st, ni, bb, buf);
+  load_items<KB>(a, st, ni, bb, buf);
+  float carry = 0.f;  // this lane's partial sum for item ja from fast steps
+  bool carrying = false;
   for (unsigned p0 = s0; p0 < s1; p0 += kWin * V) {
+    {
+      // Fast step: the V windows lie inside item ja (long rows): no lookup,
+      // no segmented scan; the lanes accumulate and flush once per item.
+      if (ja + 33 > bb + KB) {
+        bb = ja;
+        load_items<KB>(a, st, ni, bb, buf);
+      }
+      const uint4 it = buf[ja - bb];
+      const unsigned iend = it.x + stream_len(it.z, it.y);
+      if (p0 + kWin * V <= min(iend, s1)) {
+        const unsigned kb = (it.z & ~3u) + (p0 - it.x) + 4 * lane;
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+          const unsigned k = kb + kWin * v;
+          const int lo_e = max(static_cast<int>(it.z - k), 0);
+          const int hi_e = min(max(static_cast<int>(it.y - k), 0), 4);
+          const unsigned m = (0xfu << lo_e) & ((1u << hi_e) - 1u);
+          int4 cv;
+          float4 wv;
+          if (a.xflags & 32u) {
+            const int cs = static_cast<int>((k * 2654435761u) & 0xfffffu);
+            cv = make_int4(cs, cs ^ 1, cs ^ 2, cs ^ 3);
+            wv = make_float4(1.f, 1.f, 1.f, 1.f);
+          } else {
+            cv = ldg_stream(reinterpret_cast<const int4*>(a.col + k));
+            wv = ldg_stream(reinterpret_cast<const float4*>(a.val + k));
+          }
+          const int i0 = (m & 1u) ? cv.x : 0, i1 = (m & 2u) ? cv.y : 0;
+          const int i2 = (m & 4u) ? cv.z : 0, i3 = (m & 8u) ? cv.w : 0;
+          const float w0 = (m & 1u) ? wv.x : 0.f, w1 = (m & 2u) ? wv.y : 0.f;
+          const float w2 = (m & 4u) ? wv.z : 0.f, w3 = (m & 8u) ? wv.w : 0.f;
+          float x0, x1, x2, x3;
+          if (a.xflags & 16u) {
+            x0 = x1 = x2 = x3 = 1.f;
+          } else if (SLOG > 0) {
+            const uint2 t0 = xc[xslot(i0, SLOG)], t1 = xc[xslot(i1, SLOG)];
+            const uint2 t2 = xc[xslot(i2, SLOG)], t3 = xc[xslot(i3, SLOG)];
+            x0 = t0.x == static_cast<unsigned>(i0) ? __uint_as_float(t0.y) : __ldg(a.x + i0);
+            x1 = t1.x == static_cast<unsigned>(i1) ? __uint_as_float(t1.y) : __ldg(a.x + i1);
+            x2 = t2.x == static_cast<unsigned>(i2) ? __uint_as_float(t2.y) : __ldg(a.x + i2);
+            x3 = t3.x == static_cast<unsigned>(i3) ? __uint_as_float(t3.y) : __ldg(a.x + i3);
+          } else {
+            x0 = __ldg(a.x + i0);
+            x1 = __ldg(a.x + i1);
+            x2 = __ldg(a.x + i2);
+            x3 = __ldg(a.x + i3);
+          }
+          carry += (w0 * x0 + w1 * x1) + (w2 * x2 + w3 * x3);
+        }
+        carrying = true;
+        if (iend == p0 + kWin * V) {  // item ja ends exactly here: flush, move on
+          const float t = dev::warp_sum(carry);
+          if (lane == 0) atomicAdd(a.y + it.w, t);
+          carry = 0.f;
+          carrying = false;
+          ja++;
+        }
+        continue;
+      }
+      if (carrying) {  // leaving item ja's fast steps: flush its partial sum
+        const float t = dev::warp_sum(carry);
+        if (lane == 0) atomicAdd(a.y + it.w, t);
+        carry = 0.f;
+        carrying = false;
+      }
+    }
     unsigned kk[V], info[V], rw[V];
 #pragma unroll
     for (int v = 0; v < V; v++) {
-      const unsigned pw = p0 + kWin * v;
-      info[v] = 0;
-      kk[v] = 0;
-      rw[v] = 0;
-      if (pw < s1) {
-        if (ja + 33 > bb + kBatch) {
-          bb = ja;
-          load_items(a, st, ni, bb, buf);
-        }
-        const unsigned last = min(pw + kWin, s1) - 1;
-        const unsigned off = buf[ja - bb + lane].x;
-        // lanes where an item starts inside the window (lane 0 excluded)
-        const bool starts = off > pw && off <= last;
-        const unsigned smask = __reduce_or_sync(kFull, starts ? 1u << ((off - pw) >> 2) : 0u);
-        const uint4 it = buf[ja - bb + __popc(smask & lt_mask)];
-        rw[v] = it.w;
-        const unsigned q = pw + 4 * lane;
-        if (q < s1) {
-          const unsigned oj = it.x, ej = it.y, bj = it.z;
-          const unsigned k = (bj & ~3u) + (q - oj);
-          kk[v] = k;
-          unsigned m = 0;
-#pragma unroll
-          for (int e = 0; e < 4; e++) m |= (k + e >= bj && k + e < ej) ? 1u << e : 0u;
-          const unsigned ls = 31 - __clz((smask | 1u) & lt_mask);  // segment start lane
-          const bool seg_end = lane == 31 || ((smask >> (lane + 1)) & 1u) || q + 4 >= s1;
-          const bool whole = oj >= pw && oj + stream_len(bj, ej) <= pw + kWin;  // item inside the window
-          info[v] = m | (ls << 4) | (seg_end ? 1u << 9 : 0u) | (whole ? 1u << 10 : 0u);
-        }
-        // first item of the next window
-        ja += __popc(smask);
-        if (buf[ja + 1 - bb].x == pw + kWin) ja++;
+      const unsigned pw = p0 + kWin * v;  // may lie past s1 on the last step: no lane is valid then
+      if (ja + 33 > bb + KB) {
+        bb = ja;
+        load_items<KB>(a, st, ni, bb, buf);
       }
+      const unsigned last = min(pw + kWin, s1) - 1;
+      const unsigned off = buf[ja - bb + lane].x;
+      // lanes where an item starts inside the window (lane 0 excluded)
+      const unsigned bit = (off > pw && off <= last) ? 1u << ((off - pw) >> 2) : 0u;
+      const unsigned smask = __reduce_or_sync(kFull, bit);
+      const uint4 it = buf[ja - bb + __popc(smask & lt_mask)];  // {offset, end, begin, row}
+      const unsigned q = pw + 4 * lane;
+      const bool valid = q < s1;
+      const unsigned k = valid ? (it.z & ~3u) + (q - it.x) : 0u;
+      // elements of the aligned group inside [begin, end): a bit range
+      const int lo_e = max(static_cast<int>(it.z - k), 0);
+      const int hi_e = min(max(static_cast<int>(it.y - k), 0), 4);
+      const unsigned m = valid ? ((0xfu << lo_e) & ((1u << hi_e) - 1u)) : 0u;
+      const unsigned ls = 31 - __clz((smask | 1u) & lt_mask);  // segment start lane
+      const bool seg_end = valid && (lane == 31 || (((smask >> 1) >> lane) & 1u) || q + 4 >= s1);
+      const bool whole = it.x >= pw && it.x + stream_len(it.z, it.y) <= pw + kWin;
+      kk[v] = k;
+      rw[v] = it.w;
+      info[v] = m | (ls << 4) | (seg_end ? 1u << 9 : 0u) | (whole ? 1u << 10 : 0u);
+      // first item of the next window
+      ja += __popc(smask);
+      ja += buf[ja + 1 - bb].x == pw + kWin ? 1u : 0u;
     }
     int4 c[V];
     float4 w[V];
 #pragma unroll
     for (int v = 0; v < V; v++) {
-      c[v] = make_int4(0, 0, 0, 0);
-      w[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (info[v] & 15u) {
+      if (a.xflags & 32u) {  // probe: no col/val traffic (synthetic columns)
+        const int cs = static_cast<int>((kk[v] * 2654435761u) & 0xfffffu);
+        c[v] = make_int4(cs, cs ^ 1, cs ^ 2, cs ^ 3);
+        w[v] = make_float4(1.f, 1.f, 1.f, 1.f);
+      } else {
         c[v] = ldg_stream(reinterpret_cast<const int4*>(a.col + kk[v]));
         w[v] = ldg_stream(reinterpret_cast<const float4*>(a.val + kk[v]));
       }
@@ -745,14 +820,29 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
     float s[V];
 #pragma unroll
     for (int v = 0; v < V; v++) {
-      // masked lanes contribute exact zeros (the widening may read padding)
+      // masked elements (the widening, invalid lanes) gather x[0] and weigh 0
       const unsigned m = info[v];
-      float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
-      if (m & 1u) q0 = w[v].x * __ldg(a.x + c[v].x);
-      if (m & 2u) q1 = w[v].y * __ldg(a.x + c[v].y);
-      if (m & 4u) q2 = w[v].z * __ldg(a.x + c[v].z);
-      if (m & 8u) q3 = w[v].w * __ldg(a.x + c[v].w);
-      s[v] = (q0 + q1) + (q2 + q3);
+      const int i0 = (m & 1u) ? c[v].x : 0, i1 = (m & 2u) ? c[v].y : 0;
+      const int i2 = (m & 4u) ? c[v].z : 0, i3 = (m & 8u) ? c[v].w : 0;
+      const float w0 = (m & 1u) ? w[v].x : 0.f, w1 = (m & 2u) ? w[v].y : 0.f;
+      const float w2 = (m & 4u) ? w[v].z : 0.f, w3 = (m & 8u) ? w[v].w : 0.f;
+      float x0, x1, x2, x3;
+      if (a.xflags & 16u) {  // probe: no x gathers
+        x0 = x1 = x2 = x3 = 1.f;
+      } else if (SLOG > 0) {
+        const uint2 t0 = xc[xslot(i0, SLOG)], t1 = xc[xslot(i1, SLOG)];
+        const uint2 t2 = xc[xslot(i2, SLOG)], t3 = xc[xslot(i3, SLOG)];
+        x0 = t0.x == static_cast<unsigned>(i0) ? __uint_as_float(t0.y) : __ldg(a.x + i0);
+        x1 = t1.x == static_cast<unsigned>(i1) ? __uint_as_float(t1.y) : __ldg(a.x + i1);
+        x2 = t2.x == static_cast<unsigned>(i2) ? __uint_as_float(t2.y) : __ldg(a.x + i2);
+        x3 = t3.x == static_cast<unsigned>(i3) ? __uint_as_float(t3.y) : __ldg(a.x + i3);
+      } else {
+        x0 = __ldg(a.x + i0);
+        x1 = __ldg(a.x + i1);
+        x2 = __ldg(a.x + i2);
+        x3 = __ldg(a.x + i3);
+      }
+      s[v] = (w0 * x0 + w1 * x1) + (w2 * x2 + w3 * x3);
     }
 #pragma unroll
     for (int v = 0; v < V; v++) {
@@ -770,6 +860,10 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
       }
     }
   }
+  if (carrying) {
+    const float t = dev::warp_sum(carry);
+    if (lane == 0) atomicAdd(a.y + buf[ja - bb].w, t);
+  }
 }
 
 // Persistent grid-consolidated SpMV.
@@ -784,23 +878,29 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
 //     PAPER.md:244-250; legal because a cooperative launch co-schedules
 //     the whole grid)
 //   drain: stream-balanced, every warp the same number of positions.
-constexpr int kRound = 8;
-
-template <bool INLINE, int V, int MINB>
-__global__ void __launch_bounds__(256, MINB) grid_stream(Args a, Stream st) {
-  __shared__ unsigned long long s_w[kRound * 8];
+template <bool INLINE, int V, int NT, int MINB, int SLOG, unsigned KB>
+__global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
+  constexpr int NW = NT / 32;
+  constexpr int kRound = NT >= 1024 ? 4 : 8;  // tiles per thread per reservation round
+  __shared__ unsigned long long s_w[kRound * NW];
   __shared__ unsigned long long s_base;
-  __shared__ uint4 s_items[8][kBatch];
-  cg::grid_group grid = cg::this_grid();
+  extern __shared__ uint4 s_dyn[];  // [NW][KB] item windows, then 2^SLOG cache slots
+  uint4* s_items = s_dyn;
+  uint2* s_cache = reinterpret_cast<uint2*>(s_dyn + NW * KB);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[0] = dev::global_ns();
   const unsigned lane = dev::lane_id(), wib = dev::warp_in_block();
   const unsigned lt_excl = (1u << lane) - 1u;
-  const unsigned G = gridDim.x, ntiles = (a.n + 255) / 256;
+  const unsigned G = gridDim.x, ntiles = (a.n + NT - 1) / NT;
+  if (SLOG > 0)  // x at the planned hot columns, once per run
+    for (unsigned i = blockIdx.x * NT + threadIdx.x; i < (1u << SLOG); i += G * NT) {
+      const int c = st.xhot_col[i];
+      st.xhot_val[i] = c >= 0 ? __ldg(a.x + c) : 0.f;
+    }
   for (unsigned t0 = blockIdx.x; t0 < ntiles; t0 += G * kRound) {
     unsigned bb[kRound], ee[kRound], inc[kRound];
 #pragma unroll
     for (int k = 0; k < kRound; k++) {
-      const unsigned r = (t0 + k * G) * 256 + threadIdx.x;
+      const unsigned r = (t0 + k * G) * NT + threadIdx.x;
       bb[k] = ee[k] = 0;
       if (t0 + k * G < ntiles && r < a.n) bb[k] = __ldg(a.rowptr + r), ee[k] = __ldg(a.rowptr + r + 1);
     }
@@ -810,21 +910,25 @@ __global__ void __launch_bounds__(256, MINB) grid_stream(Args a, Stream st) {
       const unsigned len = cons ? stream_len(bb[k], ee[k]) : 0u;
       inc[k] = dev::warp_incl_scan(len);
       const unsigned cnt = __popc(__ballot_sync(kFull, cons));
-      if (lane == 31) s_w[k * 8 + wib] = (static_cast<unsigned long long>(cnt) << kPackShift) | inc[k];
+      if (lane == 31) s_w[k * NW + wib] = (static_cast<unsigned long long>(cnt) << kPackShift) | inc[k];
     }
     __syncthreads();
-    if (wib == 0) {  // tile-major scan of the kRound x 8 warp totals, one reservation
-      const unsigned long long x0 = s_w[2 * lane], x1 = s_w[2 * lane + 1];
-      const unsigned long long pi = warp_incl_scan64(x0 + x1);
-      s_w[2 * lane] = pi - x0 - x1;
-      s_w[2 * lane + 1] = pi - x1;
+    if (wib == 0) {  // tile-major scan of the kRound x NW warp totals, one reservation
+      constexpr int PER = kRound * NW / 32;
+      unsigned long long xs[PER], tsum = 0;
+#pragma unroll
+      for (int i = 0; i < PER; i++) xs[i] = s_w[PER * lane + i], tsum += xs[i];
+      const unsigned long long pi = warp_incl_scan64(tsum);
+      unsigned long long run = pi - tsum;
+#pragma unroll
+      for (int i = 0; i < PER; i++) s_w[PER * lane + i] = run, run += xs[i];
       if (lane == 31) s_base = pi ? atomicAdd(st.sctr, pi) : 0ull;
     }
     __syncthreads();
     const unsigned long long base = s_base;
 #pragma unroll
     for (int k = 0; k < kRound; k++) {
-      const unsigned r = (t0 + k * G) * 256 + threadIdx.x;
+      const unsigned r = (t0 + k * G) * NT + threadIdx.x;
       const bool in = t0 + k * G < ntiles && r < a.n;
       const unsigned b = bb[k], e = ee[k];
       const bool cons = e - b > a.threshold;
@@ -834,7 +938,7 @@ __global__ void __launch_bounds__(256, MINB) grid_stream(Args a, Stream st) {
       if (in && !(a.xflags & 8u)) a.y[r] = cons ? 0.f : sl;
       if (cons) {
         const unsigned len = stream_len(b, e);
-        const unsigned long long at = base + s_w[k * 8 + wib] +
+        const unsigned long long at = base + s_w[k * NW + wib] +
                                       ((static_cast<unsigned long long>(__popc(ball & lt_excl)) << kPackShift) |
                                        (inc[k] - len));
         stream_insert(a, st, at, r, b, e);
@@ -842,32 +946,54 @@ __global__ void __launch_bounds__(256, MINB) grid_stream(Args a, Stream st) {
     }
     __syncthreads();  // s_w / s_base are reused by the next round
   }
-  grid.sync();
+  if (a.coop) cg::this_grid().sync();
+  else dev::soft_grid_barrier(&a.hdr->ticket);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[1] = dev::global_ns();
+  if (SLOG > 0) {
+    for (unsigned i = threadIdx.x; i < (1u << SLOG); i += NT)
+      s_cache[i] = make_uint2(static_cast<unsigned>(__ldcg(st.xhot_col + i)), __float_as_uint(__ldcg(st.xhot_val + i)));
+    __syncthreads();
+  }
   const unsigned long long tot = *reinterpret_cast<volatile unsigned long long*>(st.sctr);
   const unsigned ni = min(static_cast<unsigned>(tot >> kPackShift), a.pool.cap);
   const unsigned total = static_cast<unsigned>(tot & kNnzMask);
-  const unsigned nw = (gridDim.x * blockDim.x) >> 5, gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nw = (gridDim.x * NT) >> 5, gw = (blockIdx.x * NT + threadIdx.x) >> 5;
   const unsigned long long per = ((static_cast<unsigned long long>(total) + nw - 1) / nw + kWin - 1) /
                                  kWin * kWin;
   const unsigned long long s0 = static_cast<unsigned long long>(gw) * per;
   if (ni > 0 && s0 < total && !(a.xflags & 1u))
-    stream_drain<V>(a, st, ni, static_cast<unsigned>(s0),
-                    static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
-                    s_items[wib]);
+    stream_drain<V, KB, SLOG>(a, st, ni, static_cast<unsigned>(s0),
+                              static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
+                              s_items + wib * KB, s_cache);
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&a.hdr->t[2], dev::global_ns());
 }
 
-// [INLINE][shape]: shape 0 = V4 x 4 blocks/SM, 1 = V2 x 6, 2 = V2 x 8 (flag bits 20-21)
-static const void* stream_fn(bool inl, unsigned flags) {
-  static const void* t[2][3] = {
-      {reinterpret_cast<const void*>(grid_stream<false, 4, 4>), reinterpret_cast<const void*>(grid_stream<false, 2, 6>),
-       reinterpret_cast<const void*>(grid_stream<false, 2, 8>)},
-      {reinterpret_cast<const void*>(grid_stream<true, 4, 4>), reinterpret_cast<const void*>(grid_stream<true, 2, 6>),
-       reinterpret_cast<const void*>(grid_stream<true, 2, 8>)}};
-  const unsigned shape = (flags >> 20) & 3u;
-  return t[inl ? 1 : 0][shape > 2 ? 0 : shape];
+// Stream kernel shapes (dpc_launch_cfg.flags bits 20-21), measured on config 2:
+//   0: 1024 threads x 1 block/SM, no cache                (default, best)
+//   1: 256 threads x 4 blocks/SM, no cache
+//   2: 1024 threads x 1 block/SM, hot-column cache of 2^14 slots
+struct StreamShape {
+  const void* fn;
+  int threads;
+  int slog;
+  size_t smem;  // dynamic shared memory bytes
+};
+constexpr int kHotLog = 14;
+static StreamShape stream_shape(bool inl, unsigned flags) {
+  const unsigned sh = (flags >> 20) & 3u;
+  const size_t c14 = sizeof(uint2) << kHotLog;
+  if (sh == 1)
+    return {inl ? reinterpret_cast<const void*>(grid_stream<true, 4, 256, 4, 0, 128>)
+                : reinterpret_cast<const void*>(grid_stream<false, 4, 256, 4, 0, 128>),
+            256, 0, 8 * 128 * sizeof(uint4)};
+  if (sh == 2)
+    return {inl ? reinterpret_cast<const void*>(grid_stream<true, 4, 1024, 1, kHotLog, 64>)
+                : reinterpret_cast<const void*>(grid_stream<false, 4, 1024, 1, kHotLog, 64>),
+            1024, kHotLog, 32 * 64 * sizeof(uint4) + c14};
+  return {inl ? reinterpret_cast<const void*>(grid_stream<true, 4, 1024, 1, 0, 128>)
+              : reinterpret_cast<const void*>(grid_stream<false, 4, 1024, 1, 0, 128>),
+          1024, 0, 32 * 128 * sizeof(uint4)};
 }
 
 using PersistentFn = void (*)(Args);
@@ -901,9 +1027,59 @@ static dpc_status ensure_stream(dpc_dgraph* g, uint64_t items) {
   return DPC_OK;
 }
 
-static int coop_blocks(dpc_ctx* ctx, const void* fn, int threads) {
+// Hot-column cache plan (once per matrix): per slot, the most used column
+// among those hashing to it (ties: the larger id).
+namespace spmv {
+__global__ void hot_count(const int* __restrict__ col, unsigned m, unsigned* cnt) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    atomicAdd(cnt + col[i], 1u);
+}
+__global__ void hot_pick(const unsigned* __restrict__ cnt, unsigned ncols, unsigned long long* best, int slog) {
+  for (unsigned c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x)
+    if (cnt[c]) atomicMax(best + xslot(c, slog), (static_cast<unsigned long long>(cnt[c]) << 32) | c);
+}
+__global__ void hot_final(const unsigned long long* __restrict__ best, int* hot_col, unsigned slots) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < slots; i += gridDim.x * blockDim.x)
+    hot_col[i] = best[i] ? static_cast<int>(best[i] & 0xffffffffu) : -1;
+}
+}  // namespace spmv
+
+static dpc_status ensure_xhot(dpc_ctx* ctx, dpc_dgraph* g, int slog) {
+  if (g->xhot_log == slog) return DPC_OK;
+  cudaStream_t s = ctx->stream;
+  DPC_CUDA(cudaStreamSynchronize(s));
+  if (g->xhot_col) cudaFree(g->xhot_col);
+  if (g->xhot_val) cudaFree(g->xhot_val);
+  g->xhot_col = nullptr;
+  g->xhot_val = nullptr;
+  g->xhot_log = 0;
+  const size_t slots = size_t{1} << slog, nc = static_cast<size_t>(std::max<int64_t>(g->ncols, 1));
+  unsigned* cnt = nullptr;
+  unsigned long long* best = nullptr;
+  DPC_CUDA(cudaMalloc(&g->xhot_col, sizeof(int) * slots));
+  DPC_CUDA(cudaMalloc(&g->xhot_val, sizeof(float) * slots));
+  DPC_CUDA(cudaMalloc(&cnt, sizeof(unsigned) * nc));
+  cudaError_t e = cudaMalloc(&best, sizeof(unsigned long long) * slots);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, sizeof(unsigned) * nc, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(best, 0, sizeof(unsigned long long) * slots, s);
+  if (e == cudaSuccess) {
+    const unsigned grid = 4u * static_cast<unsigned>(ctx->sms);
+    if (g->m > 0) spmv::hot_count<<<grid, 256, 0, s>>>(g->col, static_cast<unsigned>(g->m), cnt);
+    spmv::hot_pick<<<grid, 256, 0, s>>>(cnt, static_cast<unsigned>(nc), best, slog);
+    spmv::hot_final<<<grid, 256, 0, s>>>(best, g->xhot_col, static_cast<unsigned>(slots));
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(cnt);
+  if (best) cudaFree(best);
+  if (e != cudaSuccess) return cuda_fail(e, "SpMV hot-column plan");
+  g->xhot_log = slog;
+  return DPC_OK;
+}
+
+static int coop_blocks(dpc_ctx* ctx, const void* fn, int threads, size_t smem = 0) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) {
     cudaGetLastError();
     per_sm = 1;
   }
@@ -937,6 +1113,7 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
   a.child_threads = c.child_threads;
   a.child_blocks = c.child_blocks;
   a.xflags = c.flags >> 24;
+  a.coop = 1;
   // stream-balanced grid drain (grid_stream)
   const bool use_stream = c.variant == DPC_GRID && c.grid_persistent && !(c.flags & DPC_CFG_GRID_CHUNKED);
   spmv::Stream sa{};
@@ -947,7 +1124,7 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
     // stream positions <= m + 6 per item (16-byte widening)
     st = ensure_stream(g, heavy);
     if (st != DPC_OK) return st;
-    sa = spmv::Stream{reinterpret_cast<uint2*>(g->soff), &g->hdr->work};
+    sa = spmv::Stream{reinterpret_cast<uint2*>(g->soff), &g->hdr->work, nullptr, nullptr};
   } else if (c.variant != DPC_FLAT && c.variant != DPC_BASIC) {
     st = ensure_pool(g, pool_need(g, c.threshold, c.chunk));
     if (st != DPC_OK) return st;
@@ -968,10 +1145,25 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
       case DPC_BLOCK: spmv::block_parent<<<blocks, 256, 0, s>>>(a); break;
       case DPC_GRID:
         if (use_stream) {
-          const void* fn = spmv::stream_fn(c.threshold > 0, c.flags);
-          int nb = coop_blocks(ctx, fn, 256);
+          const spmv::StreamShape sh = spmv::stream_shape(c.threshold > 0, c.flags);
+          DPC_CUDA(cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sh.smem)));
+          if (sh.slog > 0) {
+            st = ensure_xhot(ctx, g, sh.slog);
+            if (st != DPC_OK) return st;
+          }
+          sa.xhot_col = g->xhot_col;
+          sa.xhot_val = g->xhot_val;
+          // one block per resident slot; all co-resident, so a normal launch
+          // with the software grid barrier is safe (cooperative on request)
+          int nb = coop_blocks(ctx, sh.fn, sh.threads, sh.smem);
+          a.coop = (c.flags & DPC_CFG_COOP_LAUNCH) ? 1u : 0u;
           void* args[] = {&a, &sa};
-          DPC_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nb), dim3(256), args, 0, s));
+          if (a.coop) {
+            DPC_CUDA(cudaLaunchCooperativeKernel(sh.fn, dim3(nb), dim3(sh.threads), args, sh.smem, s));
+          } else {
+            DPC_CUDA(cudaLaunchKernel(sh.fn, dim3(nb), dim3(sh.threads), args, sh.smem, s));
+          }
         } else if (c.grid_persistent) {
           const void* fn = reinterpret_cast<const void*>(spmv::persistent_fn(c.flags));
           int nb = coop_blocks(ctx, fn, 256);

@@ -17,6 +17,7 @@ ap.add_argument("--cdp", action="store_true")
 ap.add_argument("--chunk", type=int, default=0)
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--threshold", type=int, default=-1)
+ap.add_argument("--burst", type=int, default=0)
 a = ap.parse_args()
 ctx = dpc.Context(0)
 g = dpc.gen_rmat(a.scale, 16, seed=1, weights=False, values=True)
@@ -38,6 +39,14 @@ for v in a.variants:
         dg.spmv(v, cfg=cfg)
         ctx.record(1)
         print(v, f"{ctx.elapsed_ms(0, 1):.4f} ms")
+    if a.burst:
+        for nb in (1, a.burst):
+            ctx.flush_l2()
+            ctx.record(0)
+            for _ in range(nb):
+                dg.spmv(v, cfg=cfg)
+            ctx.record(1)
+            print(f"  burst {nb}: {ctx.elapsed_ms(0, 1) / nb * 1e3:.1f} us per run")
     if v == "grid" and not a.cdp:
         ctx.flush_l2()
         dg.spmv(v, cfg=cfg, metrics=True)
