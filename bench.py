@@ -47,11 +47,14 @@ def _env_int(k, d):
         return d
 
 
-def _dist_init(world):
-    if world <= 1:
+def _dist_init(world, force=False):
+    if world <= 1 and not force:
         return None
     import torch.distributed as dist
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    os.environ.setdefault("RANK", "0")
+    os.environ.setdefault("WORLD_SIZE", str(max(1, world)))
     dist.init_process_group("gloo")
     return dist
 
@@ -265,6 +268,7 @@ def run_multi(args, dist, rank, world, local):
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
+    out["sssp"] = run_multi_sssp(args, dist, rank, world, ctx, comm, scale, r0, R)
     if rank == 0:
         print(json.dumps(out), flush=True)
     comm.close()
@@ -272,6 +276,43 @@ def run_multi(args, dist, rank, world, local):
     dg.close()
     ctx.close()
     dist.destroy_process_group()
+
+
+def run_multi_sssp(args, dist, rank, world, ctx, comm, scale, r0, R):
+    """Vertex-partitioned SSSP on the same R-MAT shape (integer weights
+    [1, 255], source = vertex 0 of the permuted graph's largest block row):
+    dpc_multi_sssp = local consolidated relaxation + grouped NCCL send/recv of
+    {vertex, distance} pairs per iteration.  GTEPS = edges of the reached
+    vertices / device time (max over ranks)."""
+    import paper_1606_08150_b200 as dpc
+    n = 1 << scale
+    A = dpc.gen_rmat_rows(scale, r0, r0 + R, EDGEFACTOR, seed=SEED, weights=True, permute=True)
+    dg = dpc.DeviceGraph(ctx, A)
+    deg = A.degrees()
+    cand = np.array([r0 + int(np.argmax(deg)), int(deg.max())], dtype=np.float64)
+    t = __import__("torch").tensor(cand)
+    allc = [__import__("torch").zeros(2, dtype=__import__("torch").float64) for _ in range(world)]
+    dist.all_gather(allc, t)
+    source = int(max(allc, key=lambda x: float(x[1]))[0])
+    met = comm.sssp(dg, n, source)  # warm-up / correctness run
+    d = dg.get_dist()
+    reached = d != 0xFFFFFFFF
+    te = float(deg[reached].sum())
+    ts = []
+    for _ in range(max(1, min(args.steps, 5))):
+        _barrier(dist)
+        ctx.record(4)
+        comm.sssp(dg, n, source)
+        ctx.record(5)
+        ts.append(ctx.elapsed_ms(4, 5))
+    ms = _max_over_ranks(dist, float(np.median(ts)))
+    edges = _sum_over_ranks(dist, te)
+    dg.close()
+    return {"metric": "SSSP GTEPS (edges of reached vertices / time)", "value": round(edges / (ms * 1e-3) / 1e9, 3),
+            "unit": "GTEPS", "ms": round(ms, 3), "iterations": int(met.iterations), "source": source,
+            "workload": f"R-MAT scale {scale}, vertex-permuted, {world} row blocks, int weights [1,255]",
+            "exchange": "grouped ncclSend/ncclRecv of {vertex, distance} pairs + ncclAllGather counts + "
+                        "ncclAllReduce frontier size per iteration"}
 
 
 def _peak_hbm():
@@ -285,8 +326,8 @@ def _peak_hbm():
 def run_ours(args):
     import paper_1606_08150_b200 as dpc
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
-    dist = _dist_init(world)
-    if world > 1:
+    dist = _dist_init(world, args.multi)
+    if world > 1 or args.multi:
         return run_multi(args, dist, rank, world, local)
     ctx = dpc.Context(local)
     t0 = time.time()
@@ -500,6 +541,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--ref-stride", type=int, default=256)
+    ap.add_argument("--multi", action="store_true",
+                    help="run the partitioned (config 5) path even on one rank (testing)")
     ap.add_argument("--apps", nargs="*",
                     default=["sssp", "gc", "td", "th", "td_paper", "th_paper"],
                     help="other BASELINE apps timed in the same run (empty list: none)")

@@ -315,6 +315,44 @@ dpc_status dpc_partition_rows(const dpc_csr* g, int32_t world, int64_t* bounds);
 dpc_status dpc_multi_spmv(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, const float* d_x_local,
                           float* d_y_local, const dpc_launch_cfg* cfg, dpc_metrics* met);
 
+/* Vertex-partitioned SSSP (BASELINE config 5; the reference's Fig. 1(b)
+ * irregular loop, run level-synchronously across ranks).
+ * `local` is this rank's row block [rank*R, rank*R + local->n) of an
+ * n_global-vertex graph with global column ids (dpc_gen_rmat_rows), R =
+ * ceil(n_global / world).  Each iteration relaxes the local frontier with
+ * the cfg variant (the grid variant runs in its CDP form: one exchange per
+ * iteration), sends {vertex, distance} pairs for remote targets to their
+ * owners with grouped ncclSend/ncclRecv over NVLink, applies what it
+ * receives, and stops when the all-reduced next-frontier size is 0.
+ * Distances of the local vertices are left in the handle (dpc_dgraph_dist).
+ * met->result_count = pairs this rank sent. */
+dpc_status dpc_multi_sssp(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, int64_t n_global, int64_t source,
+                          const dpc_launch_cfg* cfg, dpc_metrics* met);
+
+/* The steps of dpc_multi_sssp, for callers that drive the exchange with
+ * their own transport (and for single-GPU tests of the partitioned path):
+ *   dpc_msssp_begin : init distances of the rank's block (r0 = rank * R,
+ *                     rows_per_rank = R), clear the remote filter
+ *   dpc_msssp_relax : relax the current frontier; send_counts[q] = pairs
+ *                     queued for owner q (host array of `world` entries)
+ *   dpc_msssp_send_buffer(q) : device pointer to those pairs
+ *                     ({uint32 global vertex, uint32 distance} each)
+ *   dpc_msssp_recv_buffer : device scratch large enough for every pair
+ *                     this rank can receive in one iteration
+ *   dpc_msssp_send_counts : device copy of send_counts (for collectives)
+ *   dpc_msssp_apply : apply `count` received pairs (device pointer), close
+ *                     the iteration; *next_fsize = local |F_it+1|
+ *   dpc_msssp_end   : fault check and metrics */
+dpc_status dpc_msssp_begin(dpc_ctx* ctx, dpc_dgraph* local, int64_t r0, int64_t rows_per_rank,
+                           int64_t n_global, int32_t world, int64_t source, const dpc_launch_cfg* cfg);
+dpc_status dpc_msssp_relax(dpc_ctx* ctx, dpc_dgraph* local, uint32_t* send_counts);
+const void* dpc_msssp_send_buffer(dpc_dgraph* local, int32_t owner);
+void* dpc_msssp_recv_buffer(dpc_dgraph* local);
+const uint32_t* dpc_msssp_send_counts(dpc_dgraph* local);
+dpc_status dpc_msssp_apply(dpc_ctx* ctx, dpc_dgraph* local, const void* d_pairs, uint64_t count,
+                           uint32_t* next_fsize);
+dpc_status dpc_msssp_end(dpc_ctx* ctx, dpc_dgraph* local, dpc_metrics* met);
+
 #ifdef __cplusplus
 }
 #endif

@@ -167,6 +167,14 @@ _SIGS = {
     "dpc_comm_world": (_i32, [_P]),
     "dpc_partition_rows": (C.c_int, [_CsrP, _i32, _P]),
     "dpc_multi_spmv": (C.c_int, [_P, _P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_multi_sssp": (C.c_int, [_P, _P, _P, _i64, _i64, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_msssp_begin": (C.c_int, [_P, _P, _i64, _i64, _i64, _i32, _i64, C.POINTER(LaunchCfg)]),
+    "dpc_msssp_relax": (C.c_int, [_P, _P, _P]),
+    "dpc_msssp_send_buffer": (_P, [_P, _i32]),
+    "dpc_msssp_recv_buffer": (_P, [_P]),
+    "dpc_msssp_send_counts": (_P, [_P]),
+    "dpc_msssp_apply": (C.c_int, [_P, _P, _P, _u64, C.POINTER(_u32)]),
+    "dpc_msssp_end": (C.c_int, [_P, _P, C.POINTER(Metrics)]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -530,12 +538,58 @@ class Comm:
         _check(_lib.dpc_multi_spmv(self.ctx.handle, self._h, local._h, d_x_local, d_y_local,
                                    _cfg_arg("spmv", variant, cfg), None))
 
+    def sssp(self, local: "DeviceGraph", n_global: int, source: int, variant="grid", cfg=None):
+        """Vertex-partitioned SSSP over NCCL; local distances stay in `local`."""
+        met = Metrics()
+        _check(_lib.dpc_multi_sssp(self.ctx.handle, self._h, local._h, n_global, source,
+                                   _cfg_arg("sssp", variant, cfg), C.byref(met)))
+        return met
+
     def close(self):
         h, self._h = getattr(self, "_h", None), None
         if h:
             _lib.dpc_comm_destroy(h)
 
     __del__ = close
+
+
+class PartitionedSSSP:
+    """The dpc_msssp_* steps of one rank's block (transport left to the
+    caller): begin -> [relax -> exchange -> apply]* -> end."""
+
+    def __init__(self, local: "DeviceGraph", rank: int, world: int, n_global: int, source: int,
+                 variant="grid", cfg=None):
+        self.g, self.ctx, self.world = local, local.ctx, world
+        R = -(-n_global // world)
+        _check(_lib.dpc_msssp_begin(self.ctx.handle, local._h, rank * R, R, n_global, world, source,
+                                    _cfg_arg("sssp", variant, cfg)))
+
+    def relax(self) -> np.ndarray:
+        cnt = np.zeros(self.world, np.uint32)
+        _check(_lib.dpc_msssp_relax(self.ctx.handle, self.g._h, _ptr(cnt)))
+        return cnt
+
+    def outgoing(self, owner: int, count: int) -> np.ndarray:
+        """The {vertex, distance} pairs queued for `owner` (host copy, (count, 2) uint32)."""
+        out = np.empty((count, 2), np.uint32)
+        if count:
+            _check(_lib.dpc_copy_d2h(self.ctx.handle, _ptr(out), _lib.dpc_msssp_send_buffer(self.g._h, owner),
+                                     out.nbytes))
+        return out
+
+    def apply(self, pairs: np.ndarray) -> int:
+        pairs = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        buf = _lib.dpc_msssp_recv_buffer(self.g._h)
+        if len(pairs):
+            _check(_lib.dpc_copy_h2d(self.ctx.handle, buf, _ptr(pairs), pairs.nbytes))
+        nxt = _u32()
+        _check(_lib.dpc_msssp_apply(self.ctx.handle, self.g._h, buf, len(pairs), C.byref(nxt)))
+        return int(nxt.value)
+
+    def end(self):
+        met = Metrics()
+        _check(_lib.dpc_msssp_end(self.ctx.handle, self.g._h, C.byref(met)))
+        return met
 
 
 class DeviceTree:

@@ -299,9 +299,11 @@ void dpc_dgraph_free(dpc_dgraph* g) {
   }
   void* bufs[] = {g->rowptr, g->col,      g->w,        g->val,   g->x,    g->y,
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
-                  g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val};
+                  g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val,
+                  g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  if (g->ms_state) dpc::sssp_state_free(g->ms_state);
   if (g->hdr_host) cudaFreeHost(g->hdr_host);
   if (g->ctr_host) cudaFreeHost(g->ctr_host);
   delete g;

@@ -56,6 +56,14 @@ struct dpc_dgraph {
   unsigned* soff = nullptr;
   size_t soff_cap = 0;
   // SpMV hot-column cache plan (column per slot) and per-run x values
+  // partitioned SSSP (dpc_msssp_*): remote-distance filter, send / receive
+  // pair buffers, per-owner counters, step state
+  unsigned* ms_rdist = nullptr;
+  void* ms_send = nullptr;
+  void* ms_recv = nullptr;
+  unsigned* ms_cnt = nullptr;
+  size_t ms_n = 0, ms_cap = 0;
+  void* ms_state = nullptr;
   int* xhot_col = nullptr;
   float* xhot_val = nullptr;
   int xhot_log = 0;
@@ -125,6 +133,8 @@ dpc_status ensure_pending_for(dpc_ctx* ctx, dpc_dgraph* g, int variant, unsigned
 dpc_status ensure_pool(dpc_dgraph* g, uint64_t need);
 
 dpc_status begin_run(dpc_ctx* ctx, dpc::dev::RunHeader* hdr);
+// Frees the partitioned-SSSP step state of a graph (sssp.cu).
+void sssp_state_free(void* state);
 // Maps the device-side fault bits of a run header to a status + message.
 dpc_status check_header(const dpc::dev::RunHeader* h);
 dpc_status finish_metrics(dpc_ctx* ctx, dpc::dev::RunHeader* hdr, dpc::dev::RunHeader* hdr_host,

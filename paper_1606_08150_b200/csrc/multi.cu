@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "ctx.h"
 
@@ -21,6 +22,10 @@ struct dpc_comm {
   int rank = 0;
   int world = 1;
   dpc_ctx* ctx = nullptr;
+  unsigned* d_counts = nullptr;   // world x world send counts (SSSP exchange)
+  unsigned* h_counts = nullptr;   // pinned mirror
+  unsigned* d_scalar = nullptr;   // all-reduce scratch
+  unsigned* h_scalar = nullptr;
 };
 
 namespace dpc {
@@ -74,6 +79,10 @@ dpc_status dpc_comm_init(dpc_ctx* ctx, int32_t rank, int32_t world, const uint8_
 void dpc_comm_destroy(dpc_comm* c) {
   if (!c) return;
   if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->d_counts) cudaFree(c->d_counts);
+  if (c->d_scalar) cudaFree(c->d_scalar);
+  if (c->h_counts) cudaFreeHost(c->h_counts);
+  if (c->h_scalar) cudaFreeHost(c->h_scalar);
   delete c;
 }
 
@@ -104,6 +113,58 @@ dpc_status dpc_multi_spmv(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, const
   DPC_NCCL(ncclAllGather(d_x_local, local->x, static_cast<size_t>(local->n), ncclFloat, comm->nccl,
                          ctx->stream));
   return dpc_spmv_device(ctx, local, local->x, d_y_local, cfg, met);
+}
+
+// Vertex-partitioned SSSP over NCCL (BASELINE config 5): the dpc_msssp_*
+// steps (sssp.cu) with the exchange done by grouped ncclSend / ncclRecv of
+// {vertex, distance} pairs over NVLink, the per-owner counts by one
+// ncclAllGather, and the stop test by an ncclAllReduce of |F_it+1|.
+dpc_status dpc_multi_sssp(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, int64_t n_global, int64_t source,
+                          const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!ctx || !comm || !local) return fail(DPC_E_INVALID, "NULL argument");
+  const int P = comm->world, me = comm->rank;
+  const int64_t R = (n_global + P - 1) / P;
+  cudaStream_t s = ctx->stream;
+  if (!comm->d_counts) {
+    DPC_CUDA(cudaMalloc(&comm->d_counts, sizeof(unsigned) * 64 * 64));
+    DPC_CUDA(cudaMallocHost(&comm->h_counts, sizeof(unsigned) * 64 * 64));
+    DPC_CUDA(cudaMalloc(&comm->d_scalar, sizeof(unsigned) * 2));
+    DPC_CUDA(cudaMallocHost(&comm->h_scalar, sizeof(unsigned) * 2));
+  }
+  dpc_status st = dpc_msssp_begin(ctx, local, me * R, R, n_global, P, source, cfg);
+  if (st != DPC_OK) return st;
+  std::vector<uint32_t> sc(static_cast<size_t>(P));
+  uint2* recv = static_cast<uint2*>(dpc_msssp_recv_buffer(local));
+  for (int64_t it = 0; it <= n_global; it++) {
+    st = dpc_msssp_relax(ctx, local, sc.data());
+    if (st != DPC_OK) return st;
+    // every rank learns the full count matrix (row q = what q sends)
+    DPC_NCCL(ncclAllGather(dpc_msssp_send_counts(local), comm->d_counts, static_cast<size_t>(P), ncclUint32,
+                           comm->nccl, s));
+    DPC_CUDA(cudaMemcpyAsync(comm->h_counts, comm->d_counts, sizeof(unsigned) * P * P, cudaMemcpyDeviceToHost, s));
+    DPC_CUDA(cudaStreamSynchronize(s));
+    uint64_t total = 0;
+    DPC_NCCL(ncclGroupStart());
+    for (int q = 0; q < P; q++) {
+      if (q == me) continue;
+      const size_t out = comm->h_counts[me * P + q], in = comm->h_counts[q * P + me];
+      if (out) DPC_NCCL(ncclSend(dpc_msssp_send_buffer(local, q), 2 * out, ncclUint32, q, comm->nccl, s));
+      if (in) DPC_NCCL(ncclRecv(recv + total, 2 * in, ncclUint32, q, comm->nccl, s));
+      total += in;
+    }
+    DPC_NCCL(ncclGroupEnd());
+    uint32_t next = 0;
+    st = dpc_msssp_apply(ctx, local, recv, total, &next);
+    if (st != DPC_OK) return st;
+    comm->h_scalar[0] = next;
+    DPC_CUDA(cudaMemcpyAsync(comm->d_scalar, comm->h_scalar, sizeof(unsigned), cudaMemcpyHostToDevice, s));
+    DPC_NCCL(ncclAllReduce(comm->d_scalar, comm->d_scalar + 1, 1, ncclUint32, ncclSum, comm->nccl, s));
+    DPC_CUDA(cudaMemcpyAsync(comm->h_scalar + 1, comm->d_scalar + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    DPC_CUDA(cudaStreamSynchronize(s));
+    if (comm->h_scalar[1] == 0) break;
+  }
+  return dpc_msssp_end(ctx, local, met);
 }
 
 }  // extern "C"

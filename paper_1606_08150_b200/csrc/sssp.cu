@@ -69,6 +69,14 @@ struct Args {
   unsigned child_blocks;
   unsigned it;     // iteration index (host-loop variants)
   unsigned fsize;  // |F_it| (host-loop variants)
+  // vertex partition (multi-GPU): this rank owns global
+  // vertices [r0, r0 + n); single GPU: r0 = 0 and nothing is remote.
+  unsigned r0;
+  unsigned rows_per_rank;  // owner(v) = v / rows_per_rank
+  unsigned* rdist;         // best distance sent so far per global vertex (remote filter)
+  uint2* sendbuf;          // [world][sendcap] {global vertex, distance}
+  unsigned* sendcnt;       // [world]
+  unsigned sendcap;
 };
 
 // Per-block state every relaxing kernel carries in shared memory.
@@ -103,8 +111,24 @@ __device__ __forceinline__ void block_end(const Args& a, unsigned it, Block& s) 
   __syncthreads();
 }
 
-__device__ __forceinline__ void relax(const Args& a, unsigned it, Block& s, unsigned v,
+// Remote relaxation (multi-GPU): the candidate distance of a vertex another
+// rank owns is min-filtered against the best one already sent and appended
+// to that rank's send buffer; the owner applies it after the exchange.
+__device__ __noinline__ void relax_remote(const Args& a, unsigned v, unsigned nd) {
+  if (nd >= __ldcg(a.rdist + v) || nd >= atomicMin(a.rdist + v, nd)) return;
+  const unsigned d = v / a.rows_per_rank;
+  const unsigned slot = atomicAdd(a.sendcnt + d, 1u);
+  if (slot < a.sendcap) a.sendbuf[static_cast<size_t>(d) * a.sendcap + slot] = make_uint2(v, nd);
+  else atomicOr(&a.hdr->overflow, 1u);
+}
+
+__device__ __forceinline__ void relax(const Args& a, unsigned it, Block& s, unsigned gv,
                                       unsigned nd) {
+  const unsigned v = gv - a.r0;  // local index (wraps for vertices below r0)
+  if (v >= a.n) {
+    relax_remote(a, gv, nd);
+    return;
+  }
   if (nd < __ldcg(a.dist + v)) {
     unsigned old = atomicMin(a.dist + v, nd);
     if (nd < old && atomicExch(a.stamp + v, it + 1) != it + 1)
@@ -139,15 +163,18 @@ __device__ __forceinline__ void drain_items(const Args& a, unsigned it, Block& s
   }
 }
 
+// `source` is a global vertex id; only its owner seeds the frontier.
 __global__ void __launch_bounds__(256) init_kernel(Args a, unsigned source) {
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned ls = source - a.r0;
+  const bool mine = ls < a.n;
   if (i < a.n) {
-    a.dist[i] = i == source ? 0u : kInf;
+    a.dist[i] = i == ls ? 0u : kInf;
     a.stamp[i] = 0;
   }
   if (i == 0) {
-    a.front0[0] = source;
-    a.ctr->fsize[0] = 1;
+    a.front0[0] = ls;
+    a.ctr->fsize[0] = mine ? 1u : 0u;
     a.ctr->fsize[1] = a.ctr->fsize[2] = 0;
     a.ctr->pool[0] = a.ctr->pool[1] = a.ctr->pool[2] = 0;
     a.ctr->iters = 0;
@@ -346,6 +373,19 @@ __global__ void __launch_bounds__(32) rotate_kernel(Args a) {
   if (threadIdx.x == 0) rotate(a, a.it);
 }
 
+// Applies the {global vertex, distance} pairs other ranks sent for the
+// vertices this rank owns (the exchange step of iteration a.it): improved
+// vertices join F_{it+1} like local relaxations do.
+__global__ void __launch_bounds__(256) apply_kernel(Args a, const uint2* __restrict__ recv, unsigned count) {
+  __shared__ Block s;
+  block_begin(s);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const uint2 p = recv[i];
+    relax(a, a.it, s, p.x, p.y);
+  }
+  block_end(a, a.it, s);
+}
+
 __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iters) {
   __shared__ Block s;
   cg::grid_group grid = cg::this_grid();
@@ -388,47 +428,94 @@ static int coop_blocks_sssp(dpc_ctx* ctx, const void* fn, int threads) {
 
 using namespace dpc;
 
-extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t source,
-                                      const dpc_launch_cfg* cfg, dpc_metrics* met) {
-  clear_error();
-  if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
+// Builds the kernel arguments of one SSSP run on `g` (a square graph, or the
+// row block [r0, r0 + g->n) of an n_global-vertex graph).
+static dpc_status sssp_setup(dpc_ctx* ctx, dpc_dgraph* g, const dpc_launch_cfg* cfg, sssp::Args* a,
+                             Cfg* c) {
   if (g->m > 0 && !g->w) return fail(DPC_E_INVALID, "graph was uploaded without weights (w)");
-  if (g->ncols != g->n) return fail(DPC_E_INVALID, "SSSP needs a square graph (not a row slice)");
-  if (source < 0 || source >= g->n) return fail(DPC_E_INVALID, "source out of range");
-  Cfg c;
-  dpc_status st = resolve_cfg(ctx, DPC_APP_SSSP, cfg, &c);
+  dpc_status st = resolve_cfg(ctx, DPC_APP_SSSP, cfg, c);
   if (st != DPC_OK) return st;
-  if (c.parent_threads != 256 || c.child_threads > 256)
+  if (c->parent_threads != 256 || c->child_threads > 256)
     return fail(DPC_E_INVALID, "SSSP kernels are built for parent_threads = 256, child_threads <= 256");
   if (!g->ctr) {
     DPC_CUDA(cudaMalloc(&g->ctr, sizeof(sssp::Ctr)));
     DPC_CUDA(cudaMallocHost(&g->ctr_host, sizeof(sssp::Ctr)));
   }
-  sssp::Args a;
-  a.rowptr = g->rowptr;
-  a.col = g->col;
-  a.w = g->w;
-  a.dist = g->dist;
-  a.stamp = g->stamp;
-  a.front0 = g->front[0];
-  a.front1 = g->front[1];
-  a.ctr = reinterpret_cast<sssp::Ctr*>(g->ctr);
-  a.hdr = g->hdr;
-  a.n = static_cast<unsigned>(g->n);
-  a.threshold = c.threshold;
-  a.chunk = c.chunk;
-  a.child_threads = c.child_threads;
-  a.child_blocks = c.child_blocks;
-  a.it = 0;
-  a.fsize = 1;
-  if (c.variant != DPC_FLAT && c.variant != DPC_BASIC) {
-    st = ensure_pool(g, pool_need(g, c.threshold, c.chunk));
+  *a = sssp::Args{};
+  a->rowptr = g->rowptr;
+  a->col = g->col;
+  a->w = g->w;
+  a->dist = g->dist;
+  a->stamp = g->stamp;
+  a->front0 = g->front[0];
+  a->front1 = g->front[1];
+  a->ctr = reinterpret_cast<sssp::Ctr*>(g->ctr);
+  a->hdr = g->hdr;
+  a->n = static_cast<unsigned>(g->n);
+  a->threshold = c->threshold;
+  a->chunk = c->chunk;
+  a->child_threads = c->child_threads;
+  a->child_blocks = c->child_blocks;
+  a->it = 0;
+  a->fsize = 1;
+  a->r0 = 0;
+  a->rows_per_rank = 0xffffffffu;
+  if (c->variant != DPC_FLAT && c->variant != DPC_BASIC) {
+    st = ensure_pool(g, pool_need(g, c->threshold, c->chunk));
     if (st != DPC_OK) return st;
   }
-  a.pool = dev::Pool{g->items, g->cap};
-  st = ensure_pending_for(ctx, g, c.variant, c.threshold, c.parent_threads);
+  a->pool = dev::Pool{g->items, g->cap};
+  st = ensure_pending_for(ctx, g, c->variant, c->threshold, c->parent_threads);
   if (st != DPC_OK) return st;
-  st = begin_run(ctx, g->hdr);
+  return begin_run(ctx, g->hdr);
+}
+
+// One host-loop iteration: relax F_it (the variant's parent grid + its
+// consolidated children) and rotate the per-iteration counters.
+static dpc_status sssp_iterate(dpc_ctx* ctx, const Cfg& c, sssp::Args& a, unsigned it, unsigned fsize) {
+  cudaStream_t s = ctx->stream;
+  a.it = it;
+  a.fsize = fsize;
+  const unsigned pb = std::max(1u, dev::ceil_div(fsize, 256u));
+  if (fsize > 0) {
+    switch (c.variant) {
+      case DPC_FLAT: sssp::flat_kernel<<<pb, 256, 0, s>>>(a); break;
+      case DPC_BASIC: sssp::basic_parent<<<pb, 256, 0, s>>>(a); break;
+      case DPC_WARP: sssp::warp_parent<<<pb, 256, 0, s>>>(a); break;
+      case DPC_BLOCK: sssp::block_parent<<<pb, 256, 0, s>>>(a); break;
+      default: sssp::grid_parent<<<pb, 256, 0, s>>>(a); break;
+    }
+  }
+  DPC_CUDA(cudaGetLastError());
+  return DPC_OK;
+}
+
+static dpc_status sssp_finish(dpc_ctx* ctx, dpc_dgraph* g, int64_t host_launches, int64_t iters,
+                              dpc_metrics* met) {
+  cudaStream_t s = ctx->stream;
+  if (met) {
+    met->host_launches += host_launches;
+    met->iterations += iters;
+    dpc_status st = finish_metrics(ctx, g->hdr, g->hdr_host, met);
+    if (st != DPC_OK) return st;
+    met->edges_processed += static_cast<int64_t>(g->hdr_host->work);
+    met->buffer_items_inserted = g->hdr_host->aux1;
+    return DPC_OK;
+  }
+  DPC_CUDA(cudaMemcpyAsync(g->hdr_host, g->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
+  DPC_CUDA(cudaStreamSynchronize(s));
+  return check_header(g->hdr_host);
+}
+
+extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t source,
+                                      const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
+  if (g->ncols != g->n) return fail(DPC_E_INVALID, "SSSP needs a square graph (not a row slice)");
+  if (source < 0 || source >= g->n) return fail(DPC_E_INVALID, "source out of range");
+  Cfg c;
+  sssp::Args a;
+  dpc_status st = sssp_setup(ctx, g, cfg, &a, &c);
   if (st != DPC_OK) return st;
   cudaStream_t s = ctx->stream;
   const unsigned nb = std::max(1u, dev::ceil_div(a.n, 256u));
@@ -449,16 +536,8 @@ extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t sourc
   } else {
     unsigned fsize = 1;
     for (unsigned it = 0; fsize > 0 && it <= a.n; it++) {
-      a.it = it;
-      a.fsize = fsize;
-      const unsigned pb = std::max(1u, dev::ceil_div(fsize, 256u));
-      switch (c.variant) {
-        case DPC_FLAT: sssp::flat_kernel<<<pb, 256, 0, s>>>(a); break;
-        case DPC_BASIC: sssp::basic_parent<<<pb, 256, 0, s>>>(a); break;
-        case DPC_WARP: sssp::warp_parent<<<pb, 256, 0, s>>>(a); break;
-        case DPC_BLOCK: sssp::block_parent<<<pb, 256, 0, s>>>(a); break;
-        default: sssp::grid_parent<<<pb, 256, 0, s>>>(a); break;
-      }
+      st = sssp_iterate(ctx, c, a, it, fsize);
+      if (st != DPC_OK) return st;
       sssp::rotate_kernel<<<1, 32, 0, s>>>(a);
       host_launches += 2;
       DPC_CUDA(cudaGetLastError());
@@ -469,16 +548,161 @@ extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t sourc
       iters = it + 1;
     }
   }
-  if (met) {
-    met->host_launches += host_launches;
-    met->iterations += iters;
-    st = finish_metrics(ctx, g->hdr, g->hdr_host, met);
-    if (st != DPC_OK) return st;
-    met->edges_processed += static_cast<int64_t>(g->hdr_host->work);
-    met->buffer_items_inserted = g->hdr_host->aux1;
-    return DPC_OK;
+  return sssp_finish(ctx, g, host_launches, iters, met);
+}
+
+// ---------------------------------------------------------------------------
+// Vertex-partitioned SSSP (BASELINE config 5).  Rank p owns
+// the global vertices [p*R, p*R + n_p) and their out-edges (a row block from
+// dpc_gen_rmat_rows); columns are global ids.  Each iteration:
+//   relax   : the local consolidated relaxation of F_it; targets this rank
+//             owns are atomicMin'd in place, others are min-filtered
+//             (rdist) into per-owner send buffers {vertex, distance}
+//   exchange: the send buffers go to their owners (NCCL send/recv over
+//             NVLink in dpc_multi_sssp; any transport through the step API)
+//   apply   : received pairs are atomicMin'd; improved vertices join F_it+1
+//   stop    : when the global |F_it+1| (sum over ranks) is 0
+// The step API (dpc_msssp_*) exposes relax / apply so the exchange can be
+// driven by any transport; dpc_multi_sssp composes them with NCCL.
+struct MsState {
+  sssp::Args a;
+  Cfg c;
+  int world = 1;
+  unsigned it = 0;
+  unsigned fsize = 0;
+  int64_t host_launches = 0;
+  int64_t remote_sent = 0;
+};
+
+static MsState* ms_state(dpc_dgraph* g) { return reinterpret_cast<MsState*>(g->ms_state); }
+
+namespace dpc {
+void sssp_state_free(void* state) { delete reinterpret_cast<MsState*>(state); }
+}  // namespace dpc
+
+extern "C" dpc_status dpc_msssp_begin(dpc_ctx* ctx, dpc_dgraph* g, int64_t r0, int64_t rows_per_rank,
+                                      int64_t n_global, int32_t world, int64_t source,
+                                      const dpc_launch_cfg* cfg) {
+  clear_error();
+  if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
+  if (world < 1 || rows_per_rank < 1 || r0 < 0 || r0 + g->n > n_global || g->ncols != n_global ||
+      n_global >= (int64_t{1} << 32) || (n_global + rows_per_rank - 1) / rows_per_rank > world ||
+      r0 % rows_per_rank != 0)
+    return fail(DPC_E_INVALID, "bad partition: need r0 = rank * rows_per_rank, ncols = n_global");
+  if (source < 0 || source >= n_global) return fail(DPC_E_INVALID, "source out of range");
+  if (!g->ms_state) g->ms_state = new (std::nothrow) MsState();
+  MsState* m = ms_state(g);
+  if (!m) return fail(DPC_E_OOM, "state allocation failed");
+  dpc_status st = sssp_setup(ctx, g, cfg, &m->a, &m->c);
+  if (st != DPC_OK) return st;
+  if (m->c.variant == DPC_GRID) m->c.grid_persistent = 0;  // one exchange per iteration
+  // buffers: rdist over all global vertices, one send segment per owner
+  // (a segment holds at most every local edge), one receive area
+  const size_t cap = static_cast<size_t>(std::max<int64_t>(g->m, 1));
+  const size_t need_send = cap * static_cast<size_t>(world);
+  if (g->ms_n < static_cast<size_t>(n_global) || g->ms_cap < need_send) {
+    DPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (void* p : {static_cast<void*>(g->ms_rdist), static_cast<void*>(g->ms_send),
+                    static_cast<void*>(g->ms_recv), static_cast<void*>(g->ms_cnt)})
+      if (p) cudaFree(p);
+    g->ms_rdist = nullptr, g->ms_send = nullptr, g->ms_recv = nullptr, g->ms_cnt = nullptr;
+    g->ms_n = g->ms_cap = 0;
+    DPC_CUDA(cudaMalloc(&g->ms_rdist, sizeof(unsigned) * static_cast<size_t>(n_global)));
+    DPC_CUDA(cudaMalloc(&g->ms_send, sizeof(uint2) * need_send));
+    DPC_CUDA(cudaMalloc(&g->ms_recv, sizeof(uint2) * need_send));
+    DPC_CUDA(cudaMalloc(&g->ms_cnt, sizeof(unsigned) * 2 * 64));
+    g->ms_n = static_cast<size_t>(n_global);
+    g->ms_cap = need_send;
   }
-  DPC_CUDA(cudaMemcpyAsync(g->hdr_host, g->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
+  if (world > 64) return fail(DPC_E_INVALID, "world > 64");
+  m->world = world;
+  m->a.r0 = static_cast<unsigned>(r0);
+  m->a.rows_per_rank = static_cast<unsigned>(rows_per_rank);
+  m->a.rdist = g->ms_rdist;
+  m->a.sendbuf = reinterpret_cast<uint2*>(g->ms_send);
+  m->a.sendcnt = g->ms_cnt;
+  m->a.sendcap = static_cast<unsigned>(cap);
+  m->it = 0;
+  m->host_launches = 0;
+  m->remote_sent = 0;
+  cudaStream_t s = ctx->stream;
+  DPC_CUDA(cudaMemsetAsync(g->ms_rdist, 0xff, sizeof(unsigned) * static_cast<size_t>(n_global), s));
+  DPC_CUDA(cudaMemsetAsync(g->ms_cnt, 0, sizeof(unsigned) * 64, s));
+  const unsigned nb = std::max(1u, dev::ceil_div(m->a.n, 256u));
+  sssp::init_kernel<<<nb, 256, 0, s>>>(m->a, static_cast<unsigned>(source));
+  DPC_CUDA(cudaGetLastError());
+  m->host_launches = 1;
+  m->fsize = (source >= r0 && source < r0 + g->n) ? 1u : 0u;
   DPC_CUDA(cudaStreamSynchronize(s));
-  return check_header(g->hdr_host);
+  return DPC_OK;
+}
+
+extern "C" dpc_status dpc_msssp_relax(dpc_ctx* ctx, dpc_dgraph* g, uint32_t* send_counts) {
+  clear_error();
+  if (!ctx || !g || !send_counts) return fail(DPC_E_INVALID, "NULL argument");
+  MsState* m = ms_state(g);
+  if (!m) return fail(DPC_E_INVALID, "dpc_msssp_begin was not called");
+  cudaStream_t s = ctx->stream;
+  DPC_CUDA(cudaMemsetAsync(m->a.sendcnt, 0, sizeof(unsigned) * static_cast<size_t>(m->world), s));
+  dpc_status st = sssp_iterate(ctx, m->c, m->a, m->it, m->fsize);
+  if (st != DPC_OK) return st;
+  m->host_launches += 1;
+  DPC_CUDA(cudaMemcpyAsync(send_counts, m->a.sendcnt, sizeof(unsigned) * static_cast<size_t>(m->world),
+                           cudaMemcpyDeviceToHost, s));
+  DPC_CUDA(cudaStreamSynchronize(s));
+  for (int p = 0; p < m->world; p++) {
+    if (send_counts[p] > m->a.sendcap) return fail(DPC_E_OVERFLOW, "send buffer overflow");
+    m->remote_sent += send_counts[p];
+  }
+  return DPC_OK;
+}
+
+extern "C" const void* dpc_msssp_send_buffer(dpc_dgraph* g, int32_t owner) {
+  MsState* m = g ? ms_state(g) : nullptr;
+  if (!m || owner < 0 || owner >= m->world) return nullptr;
+  return m->a.sendbuf + static_cast<size_t>(owner) * m->a.sendcap;
+}
+
+extern "C" void* dpc_msssp_recv_buffer(dpc_dgraph* g) { return g ? g->ms_recv : nullptr; }
+
+extern "C" const uint32_t* dpc_msssp_send_counts(dpc_dgraph* g) {
+  MsState* m = g ? ms_state(g) : nullptr;
+  return m ? m->a.sendcnt : nullptr;
+}
+
+extern "C" dpc_status dpc_msssp_apply(dpc_ctx* ctx, dpc_dgraph* g, const void* d_pairs, uint64_t count,
+                                      uint32_t* next_fsize) {
+  clear_error();
+  if (!ctx || !g || !next_fsize || (count && !d_pairs)) return fail(DPC_E_INVALID, "NULL argument");
+  MsState* m = ms_state(g);
+  if (!m) return fail(DPC_E_INVALID, "dpc_msssp_begin was not called");
+  cudaStream_t s = ctx->stream;
+  m->a.it = m->it;
+  if (count) {
+    const unsigned nb = std::min(4u * static_cast<unsigned>(ctx->sms),
+                                 std::max(1u, dev::ceil_div(static_cast<unsigned>(count), 256u)));
+    sssp::apply_kernel<<<nb, 256, 0, s>>>(m->a, static_cast<const uint2*>(d_pairs), static_cast<unsigned>(count));
+    m->host_launches += 1;
+  }
+  sssp::rotate_kernel<<<1, 32, 0, s>>>(m->a);
+  m->host_launches += 1;
+  DPC_CUDA(cudaGetLastError());
+  auto* ctr_host = reinterpret_cast<sssp::Ctr*>(g->ctr_host);
+  DPC_CUDA(cudaMemcpyAsync(&ctr_host->fsize[(m->it + 1) % 3], &m->a.ctr->fsize[(m->it + 1) % 3],
+                           sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  DPC_CUDA(cudaStreamSynchronize(s));
+  m->fsize = ctr_host->fsize[(m->it + 1) % 3];
+  m->it++;
+  *next_fsize = m->fsize;
+  return DPC_OK;
+}
+
+extern "C" dpc_status dpc_msssp_end(dpc_ctx* ctx, dpc_dgraph* g, dpc_metrics* met) {
+  clear_error();
+  if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
+  MsState* m = ms_state(g);
+  if (!m) return fail(DPC_E_INVALID, "dpc_msssp_begin was not called");
+  dpc_status st = sssp_finish(ctx, g, m->host_launches, m->it, met);
+  if (st == DPC_OK && met) met->result_count = m->remote_sent;
+  return st;
 }

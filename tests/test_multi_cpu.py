@@ -84,3 +84,64 @@ def test_row_slice_arguments():
         dpc.gen_rmat_rows(8, 10, 5, 8)            # r0 > r1
     with pytest.raises(dpc.DpcError):
         dpc.gen_rmat_rows(8, 0, 300, 8)           # past the last row
+
+
+def _sssp_worker(rank, world, port, out_dir):
+    """Level-synchronous partitioned Bellman-Ford with the dpc_multi_sssp
+    exchange pattern (owner-computes, min-filtered remote pairs, all-reduced
+    frontier size), ranks talking over gloo."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 1 << SCALE
+    R = -(-n // world)
+    r0 = rank * R
+    A = dpc.gen_rmat_rows(SCALE, r0, min(n, r0 + R), 16, seed=7, permute=True)
+    src = int(np.load(os.path.join(out_dir, "src.npy")))
+    INF = np.uint64(0xFFFFFFFF)
+    d = np.full(A.n, INF, np.uint64)
+    rdist = np.full(n, INF, np.uint64)
+    front = []
+    if r0 <= src < r0 + A.n:
+        d[src - r0] = 0
+        front = [src - r0]
+    while True:
+        out = [[] for _ in range(world)]
+        nxt = set()
+        for u in front:
+            for k in range(A.rowptr[u], A.rowptr[u + 1]):
+                v, nd = int(A.col[k]), d[u] + np.uint64(A.w[k])
+                if r0 <= v < r0 + A.n:
+                    if nd < d[v - r0]:
+                        d[v - r0] = nd
+                        nxt.add(v - r0)
+                elif nd < rdist[v]:
+                    rdist[v] = nd
+                    out[v // R].append((v, int(nd)))
+        gathered = [None] * world
+        dist.all_gather_object(gathered, out)          # the exchange step
+        for p in range(world):
+            for v, nd in gathered[p][rank]:
+                if nd < d[v - r0]:
+                    d[v - r0] = nd
+                    nxt.add(v - r0)
+        front = sorted(nxt)
+        tot = torch.tensor([len(front)], dtype=torch.int64)
+        dist.all_reduce(tot)                             # stop test
+        if int(tot) == 0:
+            break
+    parts = [None] * world
+    dist.all_gather_object(parts, d.astype(np.uint32))
+    if rank == 0:
+        np.save(os.path.join(out_dir, "d.npy"), np.concatenate(parts))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_sssp_gloo(tmp_path, orc, world):
+    g = dpc.gen_rmat(SCALE, 16, seed=7, permute=True)
+    src = int(np.argmax(g.degrees()))
+    np.save(tmp_path / "src.npy", np.array(src))
+    mp.spawn(_sssp_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    d = np.load(tmp_path / "d.npy")
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, src))
