@@ -172,9 +172,11 @@ typedef struct dpc_launch_cfg {
 #define DPC_CFG_GRID_CDP 1 /* grid variant: last block launches the child via
                               CDP2 (else: one persistent cooperative kernel
                               with a device-wide barrier) */
-#define DPC_CFG_GRID_CHUNKED 2 /* SpMV persistent grid variant: drain fixed-size
-                                  chunk items warp by warp instead of the
-                                  stream-balanced drain (comparison only) */
+#define DPC_CFG_GRID_CHUNKED 2 /* persistent grid variant, comparison form: SpMV
+                                  drains fixed-size chunk items warp by warp
+                                  instead of the stream-balanced drain; GC runs
+                                  round-synchronously (grid barriers) instead of
+                                  the asynchronous worklist */
 #define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */
@@ -292,6 +294,12 @@ void dpc_host_free(void* p);
  * context stream (synchronous). */
 dpc_status dpc_copy_h2d(dpc_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
 dpc_status dpc_copy_d2h(dpc_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+
+/* Diagnostics: with DPC_TRACE=1 in the environment, the coloring kernels
+ * record per vertex %globaltimer (ns) at its color write [0, n), at its
+ * enqueue [n, 2n) and at its dequeue [2n, 3n) (asynchronous form); copies
+ * the first `n` words of that record from the handle's last run. */
+dpc_status dpc_dgraph_trace(dpc_dgraph* g, uint64_t* out, int64_t n);
 
 /* ---- multi-GPU (one process per GPU; NCCL over NVLink) ------------------
  * Row / vertex partition of a graph across `world` ranks (BASELINE config 5).

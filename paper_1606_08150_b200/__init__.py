@@ -146,6 +146,7 @@ _SIGS = {
     "dpc_dgraph_dist": (_P, [_P]),
     "dpc_dgraph_color": (_P, [_P]),
     "dpc_dgraph_phase_ns": (C.c_int, [_P, _P]),
+    "dpc_dgraph_trace": (C.c_int, [_P, _P, _i64]),
     "dpc_spmv_device": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_sssp_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
@@ -470,6 +471,12 @@ class DeviceGraph:
         d = np.empty(self.n, dtype=np.uint32)
         _check(_lib.dpc_copy_d2h(self.ctx.handle, _ptr(d), _lib.dpc_dgraph_dist(self._h), d.nbytes))
         return d
+
+    def trace(self, words: int = 0) -> np.ndarray:
+        """Per-vertex timestamps (ns) of the last DPC_TRACE=1 run (see dpc.h)."""
+        t = np.empty(words or self.n, dtype=np.uint64)
+        _check(_lib.dpc_dgraph_trace(self._h, _ptr(t), len(t)))
+        return t
 
     def get_color(self) -> np.ndarray:
         d = np.empty(self.n, dtype=np.int32)

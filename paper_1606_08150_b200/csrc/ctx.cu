@@ -123,6 +123,9 @@ dpc_status check_header(const RunHeader* h) {
   if (h->overflow & 2u)
     return fail(DPC_E_CUDA, std::string("a device-side (CDP2) launch failed: ") +
                                 cudaGetErrorString(static_cast<cudaError_t>(h->aux0)));
+  if (h->overflow & 8u)
+    return fail(DPC_E_INVALID, "coloring needs a symmetric graph (the worklist drained with uncolored vertices)");
+  if (h->overflow & 4u) return fail(DPC_E_DEADLOCK, "worklist made no progress for 2 s (lost task)");
   if (h->overflow & 1u) return fail(DPC_E_OVERFLOW, "consolidation pool overflow");
   return DPC_OK;
 }
@@ -300,7 +303,7 @@ void dpc_dgraph_free(dpc_dgraph* g) {
   void* bufs[] = {g->rowptr, g->col,      g->w,        g->val,   g->x,    g->y,
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
                   g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val,
-                  g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt};
+                  g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt, g->gc_q, g->gc_hstate, g->trace};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->ms_state) dpc::sssp_state_free(g->ms_state);
@@ -368,6 +371,13 @@ dpc_status dpc_dgraph_upload(dpc_ctx* c, const dpc_csr* h, dpc_dgraph** out) {
 dpc_status dpc_dgraph_phase_ns(dpc_dgraph* g, uint64_t out[3]) {
   if (!g || !out) return fail(DPC_E_INVALID, "NULL argument");
   for (int i = 0; i < 3; i++) out[i] = g->hdr_host->t[i];
+  return DPC_OK;
+}
+
+dpc_status dpc_dgraph_trace(dpc_dgraph* g, uint64_t* out, int64_t n) {
+  if (!g || !out || n < 0 || n > 3 * g->n) return fail(DPC_E_INVALID, "bad arguments");
+  if (!g->trace) return fail(DPC_E_INVALID, "no traced run (set DPC_TRACE=1)");
+  DPC_CUDA(cudaMemcpy(out, g->trace, sizeof(uint64_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost));
   return DPC_OK;
 }
 

@@ -44,6 +44,11 @@ struct dpc_dgraph {
   unsigned* stamp = nullptr;  // SSSP dedup stamp / GC pending counts
   unsigned* gc_state = nullptr;  // GC heavy-vertex bitmaps (36 words per pool slot)
   size_t gc_state_slots = 0;
+  void* trace = nullptr;          // per-vertex timestamps of the last traced run (DPC_TRACE=1)
+  void* gc_q = nullptr;           // GC async task queue (+ 64 B of counters)
+  size_t gc_q_cap = 0;
+  unsigned* gc_hstate = nullptr;  // GC async heavy-vertex states
+  size_t gc_hstate_cap = 0;
   unsigned* ctr = nullptr;    // per-iteration counters (app-specific layout, 64 B)
   void* ctr_host = nullptr;   // pinned mirror of ctr
   dpc::dev::RunHeader* hdr = nullptr;  // device counters

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -73,6 +74,7 @@ struct Args {
   unsigned child_blocks;
   unsigned it;
   unsigned fsize;
+  unsigned long long* trace;  // optional: per-vertex %globaltimer at color write (DPC_TRACE=1)
 };
 
 struct Block {
@@ -541,6 +543,341 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iter
   if (gtid == 0) a.ctr->iters = it;
 }
 
+// ---------------------------------------------------------------------------
+// Asynchronous grid consolidation (the default grid form).
+//
+// The round-synchronous forms pay one or two device-wide barriers per JP
+// round, and config 3 has ~1700 rounds of a few hundred vertices each: the
+// barriers, not the arcs, bound them.  Here the grid-level buffer is a
+// device-wide FIFO of ready vertices drained by a persistent grid with no
+// barrier between rounds (position p served by warp p mod W): a vertex is colored as soon as its last
+// higher-priority neighbour is, so the run time is the longest dependency
+// chain times the per-link latency instead of rounds times barrier cost.
+//   task queue Q: u64 slots, written once, EMPTY = ~0; one tail counter
+//   light vertex (deg <= kAsyncHeavy): one warp: mex of the higher
+//     neighbours' colors (shared-memory bitmap), write the color, release
+//     the lower neighbours (the one taking a count to 0 enqueues it)
+//   heavy vertex: split into chunk tasks -- phase A chunks OR the higher
+//     colors into a per-vertex bitmap, the last one computes the mex and
+//     writes the color, then enqueues phase B chunks that release the lower
+//     neighbours (releases must follow the color write)
+// Same coloring as sequential greedy in priority order (see top of file).
+constexpr int kAsyncW = 4;               // edges per lane per step (loads in flight)
+constexpr unsigned kAsyncHeavy = 128;    // edges a single warp takes (one step)
+constexpr unsigned kAsyncChunk = 128;    // edges per heavy chunk task
+constexpr unsigned long long kEmpty = ~0ull;
+
+// Queue counters, one per 128-byte line: thousands of warps poll / bump
+// them, and sharing a line would serialise all of them on one L2 slice.
+constexpr unsigned kTail = 32, kSlots = 64, kColored = 96, kDeadlock = 128, kDone = 160;
+
+struct Async {
+  unsigned long long* q;   // task slots
+  unsigned* qctr;          // [kTail], [kSlots] heavy states used, [kColored] vertices colored
+  unsigned qcap;
+  unsigned* hstate;        // kStateWords per heavy vertex in flight
+  unsigned hcap;
+};
+
+// Release / acquire primitives (PTX memory model, gpu scope): a color
+// written before a release is visible to whoever acquires the queue slot
+// (cumulative through the acq_rel count-down chain), so no full fences sit
+// on the critical path.
+__device__ __forceinline__ unsigned atom_sub_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(0u - v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Task word: vertex (32) | chunk (12) | heavy-state slot + 1 (19) | phase (1).
+constexpr unsigned kChunkBits = 12, kSlotBits = 19;
+__device__ __forceinline__ unsigned long long task(unsigned v, unsigned chunk, unsigned slot, unsigned phase) {
+  return static_cast<unsigned long long>(v) | (static_cast<unsigned long long>(chunk) << 32) |
+         (static_cast<unsigned long long>(slot) << (32 + kChunkBits)) | (static_cast<unsigned long long>(phase) << 63);
+}
+
+// Warp-aggregated enqueue of the lanes' tasks (want = true).  All lanes call.
+__device__ __forceinline__ void enqueue(const Args& a, const Async& q, bool want, unsigned long long t) {
+  const unsigned ball = __ballot_sync(kFull, want);
+  if (!ball) return;
+  const unsigned lane = dev::lane_id();
+  unsigned base = 0;
+  if (lane == __ffs(ball) - 1) base = atomicAdd(q.qctr + kTail, __popc(ball));
+  base = __shfl_sync(kFull, base, __ffs(ball) - 1);
+  if (want) {
+    const unsigned at = base + __popc(ball & ((1u << lane) - 1u));
+    if (at < q.qcap) {
+      // the slot store depends on the count-down's returned value, which
+      // follows the (fenced) color stores of every higher neighbour
+      *reinterpret_cast<volatile unsigned long long*>(q.q + at) = t;
+      if (a.trace && (t >> 32) == 0) a.trace[a.n + static_cast<unsigned>(t)] = dev::global_ns();
+    } else {
+      atomicOr(&a.hdr->overflow, 1u);
+      atomicExch(q.qctr + kDeadlock, 1u);
+    }
+  }
+}
+
+// Lower neighbours of a colored vertex v among edges [b, e): release each
+// (relaxed count-down: the color store was fenced once before), and keep ONE
+// vertex that became ready as this warp's next task -- work-first: the
+// releaser serves it itself, without a queue round trip -- enqueueing the
+// rest.  Four edges per lane per step.  Returns the kept task or kEmpty.
+// All lanes call.
+__device__ __forceinline__ unsigned long long release_range(const Args& a, const Async& q, unsigned v,
+                                                            unsigned long long pv, unsigned b, unsigned e,
+                                                            unsigned long long keep) {
+  for (unsigned k0 = b; k0 < e; k0 += 32 * kAsyncW) {
+    unsigned u[kAsyncW];
+    bool low[kAsyncW], ready[kAsyncW];
+#pragma unroll
+    for (int j = 0; j < kAsyncW; j++) {
+      const unsigned k = k0 + 32 * j + dev::lane_id();
+      u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
+    }
+#pragma unroll
+    for (int j = 0; j < kAsyncW; j++) low[j] = u[j] != v && !higher(u[j], prio(a, u[j]), v, pv);
+#pragma unroll
+    for (int j = 0; j < kAsyncW; j++) ready[j] = low[j] && atomicSub(a.cnt + u[j], 1u) == 1u;
+#pragma unroll
+    for (int j = 0; j < kAsyncW; j++) {
+      if (keep == kEmpty) {
+        const unsigned ball = __ballot_sync(kFull, ready[j]);
+        if (ball) {
+          const unsigned l = __ffs(ball) - 1;
+          keep = task(__shfl_sync(kFull, u[j], l), 0, 0, 0);
+          if (dev::lane_id() == l) ready[j] = false;
+        }
+      }
+      enqueue(a, q, ready[j], task(u[j], 0, 0, 0));
+    }
+  }
+  return keep;
+}
+
+// ORs the colors of v's higher neighbours among [b, e) into the warp bitmap
+// (colors < 32 * kVW); returns true (warp-uniform) if a larger color was seen.
+__device__ __forceinline__ bool gather_colors(const Args& a, unsigned v, unsigned long long pv, unsigned b,
+                                              unsigned e, unsigned* wbm) {
+  bool over = false;
+  for (unsigned k0 = b; k0 < e; k0 += 32 * kAsyncW) {
+    unsigned u[kAsyncW];
+    int c[kAsyncW];
+#pragma unroll
+    for (int j = 0; j < kAsyncW; j++) {
+      const unsigned k = k0 + 32 * j + dev::lane_id();
+      u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
+    }
+#pragma unroll
+    for (int j = 0; j < kAsyncW; j++) c[j] = (u[j] != v && higher(u[j], prio(a, u[j]), v, pv)) ? __ldcg(a.color + u[j]) : -1;
+#pragma unroll
+    for (int j = 0; j < kAsyncW; j++) {
+      if (c[j] >= static_cast<int>(kVW * 32)) over = true;
+      else if (c[j] >= 0) atomicOr(wbm + (c[j] >> 5), 1u << (c[j] & 31));
+    }
+  }
+  return __any_sync(kFull, over);
+}
+
+// mex of a 32-word bitmap held one word per lane; -1 if all set.
+__device__ __forceinline__ int bitmap_mex(unsigned word) {
+  const unsigned freeb = ~word;
+  const unsigned ball = __ballot_sync(kFull, freeb != 0);
+  if (!ball) return -1;
+  const unsigned l = __ffs(ball) - 1;
+  return static_cast<int>(l * 32 + __ffs(__shfl_sync(kFull, freeb, l)) - 1);
+}
+
+// Colors >= 32 * kVW: windowed warp scan over all of v's higher neighbours.
+__device__ int mex_windowed(const Args& a, unsigned v, unsigned long long pv) {
+  const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+  for (int base = kVW * 32;; base += 32) {
+    unsigned w = 0;
+    for (unsigned k = b + dev::lane_id(); k < e; k += 32) {
+      const unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+      if (u != v && higher(u, prio(a, u), v, pv)) {
+        const int c = __ldcg(a.color + u) - base;
+        if (c >= 0 && c < 32) w |= 1u << c;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) w |= __shfl_xor_sync(kFull, w, o);
+    if (~w) return base + __ffs(~w) - 1;
+  }
+}
+
+__device__ __forceinline__ void set_color_async(const Args& a, const Async& q, Block& s, unsigned v, int c) {
+  if (dev::lane_id() == 0) {
+    __stcg(a.color + v, c);
+    if (a.trace) a.trace[v] = dev::global_ns();
+    atomicMax(&s.maxc, c);
+    __threadfence();  // the color is visible before any count-down it enables
+    atomicAdd(q.qctr + kColored, 1u);
+  }
+  __syncwarp();
+}
+
+// Serves one task with the whole warp.
+__device__ unsigned long long serve(const Args& a, const Async& q, Block& s, unsigned long long t) {
+  const unsigned lane = dev::lane_id();
+  unsigned* wbm = s.wbm[dev::warp_in_block() & 7];
+  const unsigned v = static_cast<unsigned>(t);
+  const unsigned chunk = static_cast<unsigned>(t >> 32) & ((1u << kChunkBits) - 1u);
+  const unsigned slot = static_cast<unsigned>(t >> (32 + kChunkBits)) & ((1u << kSlotBits) - 1u);
+  const bool phase_b = t >> 63;
+  const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+  const unsigned long long pv = prio(a, v);
+  if (e - b <= kAsyncHeavy && !phase_b && chunk == 0 && slot == 0) {
+    wbm[lane] = 0;
+    __syncwarp();
+    const bool over = gather_colors(a, v, pv, b, e, wbm);
+    __syncwarp();
+    int c = bitmap_mex(wbm[lane]);
+    if (c < 0 || over) {
+      const int cw = c < 0 ? mex_windowed(a, v, pv) : c;
+      c = cw;
+    }
+    __syncwarp();
+    set_color_async(a, q, s, v, c);
+    return release_range(a, q, v, pv, b, e, kEmpty);
+  }
+  const unsigned nch = (e - b + kAsyncChunk - 1) / kAsyncChunk;
+  if (!phase_b && chunk == 0 && slot == 0) {
+    // heavy vertex: take a state slot, fan out phase A chunks
+    unsigned sl = 0;
+    if (lane == 0) sl = atomicAdd(q.qctr + kSlots, 1u);
+    sl = __shfl_sync(kFull, sl, 0);
+    if (sl >= q.hcap) {
+      if (lane == 0) atomicOr(&a.hdr->overflow, 1u), atomicExch(q.qctr + kDeadlock, 1u);
+      return kEmpty;
+    }
+    unsigned* st = q.hstate + static_cast<size_t>(sl) * kStateWords;
+    if (lane < kVW) st[lane] = 0;
+    if (lane == 0) st[kVW] = nch, st[kVW + 1] = 0;
+    __threadfence();
+    for (unsigned c0 = 0; c0 < nch; c0 += 32)
+      enqueue(a, q, c0 + lane < nch, task(v, c0 + lane, sl + 1, 0));
+    return kEmpty;
+  }
+  const unsigned cb = b + chunk * kAsyncChunk, ce = min(e, cb + kAsyncChunk);
+  unsigned* st = q.hstate + static_cast<size_t>(slot - 1) * kStateWords;
+  if (!phase_b) {
+    wbm[lane] = 0;
+    __syncwarp();
+    const bool over = gather_colors(a, v, pv, cb, ce, wbm);
+    __syncwarp();
+    const unsigned wv = wbm[lane];
+    if (wv) atomicOr(st + lane, wv);
+    if (over && lane == 0) atomicOr(st + kVW + 1, 1u);
+    __threadfence();
+    unsigned last = 0;
+    if (lane == 0) last = atomicSub(st + kVW, 1u) == 1u;
+    if (!__shfl_sync(kFull, last, 0)) return kEmpty;
+    __threadfence();
+    int c = bitmap_mex(__ldcg(st + lane));
+    if (c < 0 || __ldcg(st + kVW + 1)) c = c < 0 ? mex_windowed(a, v, pv) : c;
+    set_color_async(a, q, s, v, c);
+    // phase B: chunk 0 released by this warp right away, the rest queued
+    for (unsigned c0 = 0; c0 < nch; c0 += 32)
+      enqueue(a, q, c0 + lane < nch && c0 + lane > 0, task(v, c0 + lane, slot, 1));
+    return release_range(a, q, v, pv, b, min(e, b + kAsyncChunk), kEmpty);
+  }
+  return release_range(a, q, v, pv, cb, ce, kEmpty);
+}
+
+__global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
+  __shared__ Block s;
+  cg::grid_group grid = cg::this_grid();
+  const unsigned stride = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned lane = dev::lane_id();
+  block_begin(s);
+  // init pass: cnt[v] = higher neighbours (light inline, heavy as chunk items)
+  for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
+    unsigned v = base + threadIdx.x, b = 0, e = 0, want = 0;
+    if (v < a.n) {
+      b = __ldg(a.rowptr + v);
+      e = __ldg(a.rowptr + v + 1);
+      if (e - b <= a.threshold) a.cnt[v] = count_higher(a, v, b, e, 1, 0);
+      else want = dev::nchunks(e - b, a.chunk);
+    }
+    unsigned bbase, bt;
+    unsigned at = dev::block_reserve(&a.ctr->pool[0], want, &bbase, &bt);
+    if (want) dev::write_chunks(a.pool, a.hdr, at, v, b, e, a.chunk);
+  }
+  grid.sync();
+  init_drain(a, a.pool.items, min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[0]), a.pool.cap),
+             gtid >> 5, stride >> 5);
+  grid.sync();
+  // seed: every vertex without a higher neighbour is ready
+  for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
+    const unsigned v = base + threadIdx.x;
+    const bool ready = v < a.n && __ldcg(a.cnt + v) == 0;
+    enqueue(a, q, ready, task(v, 0, 0, 0));
+  }
+  grid.sync();
+  // drain: queue position p is served by warp p mod W, in order (no claim
+  // atomics; consecutive tasks land on different warps).  A position is
+  // filled by the p-th enqueue, whose producer serves an earlier position,
+  // so in-order waiting cannot deadlock.  Stop once every vertex is colored
+  // (positions past the last task never fill).
+  const unsigned nwarps = stride >> 5, gw = gtid >> 5;
+  volatile unsigned* vq = q.qctr;
+  for (unsigned p = gw; p < q.qcap; p += nwarps) {
+    unsigned long long t = kEmpty;
+    unsigned spins = 0;
+    unsigned long long since = 0;
+    while (true) {
+      if (lane == 0) t = *reinterpret_cast<volatile unsigned long long*>(q.q + p);
+      t = __shfl_sync(kFull, t, 0);
+      if (t != kEmpty) break;
+      unsigned fin = 0;
+      if (lane == 0 && (++spins & 15) == 0) {
+        fin = vq[kColored] >= a.n;
+        // watchdog: no progress for 2 s means a lost task -- report the
+        // reference's "deadlock" fault (sim.hpp:946-955) instead of hanging
+        const unsigned long long now = dev::global_ns();
+        if (!since) since = now;
+        if (now - since > 2000000000ull) {
+          atomicOr(&a.hdr->overflow, 4u);
+          atomicExch(q.qctr + kDeadlock, 1u);
+          fin = 1;
+        }
+        if (vq[kDeadlock]) fin = 1;
+        // drained: every queued task served (done read before tail) yet
+        // uncolored vertices remain -- their counts never reach 0, which
+        // only an asymmetric adjacency produces
+        const unsigned d = vq[kDone];
+        if (!fin && d == vq[kTail] && vq[kColored] < a.n) {
+          atomicOr(&a.hdr->overflow, 8u);
+          atomicExch(q.qctr + kDeadlock, 1u);
+          fin = 1;
+        }
+      }
+      if (__shfl_sync(kFull, fin, 0)) break;
+      if (spins > 32) __nanosleep(64);
+    }
+    if (t == kEmpty) break;
+    // serve it, then the vertices it makes ready first (work-first chain)
+    while (t != kEmpty) {
+      if (a.trace && lane == 0 && (t >> 32) == 0) a.trace[2ull * a.n + static_cast<unsigned>(t)] = dev::global_ns();
+      t = serve(a, q, s, t);
+    }
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(q.qctr + kDone, 1u);
+    }
+  }
+  block_end(a, 0, s);
+}
+
 }  // namespace gc
 }  // namespace dpc
 
@@ -579,6 +916,13 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   a.it = 0;
   a.fsize = 0;
   a.state = nullptr;
+  a.trace = nullptr;
+  if (const char* tr = getenv("DPC_TRACE")) {
+    if (tr[0] == '1') {
+      if (!g->trace) DPC_CUDA(cudaMalloc(&g->trace, 3 * sizeof(unsigned long long) * std::max<int64_t>(g->n, 1)));
+      a.trace = static_cast<unsigned long long*>(g->trace);
+    }
+  }
   if (c.variant != DPC_FLAT && c.variant != DPC_BASIC) {
     st = ensure_pool(g, pool_need(g, c.threshold, c.chunk));
     if (st != DPC_OK) return st;
@@ -607,6 +951,47 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   const unsigned nb = std::max(1u, dev::ceil_div(a.n, 256u));
   if (a.n == 0) {
     ctr_host->maxcolor = -1;
+  } else if (c.variant == DPC_GRID && c.grid_persistent && !(c.flags & DPC_CFG_GRID_CHUNKED)) {
+    // asynchronous worklist form: task queue, heavy-vertex states
+    const uint64_t heavy = pool_need(g, gc::kAsyncHeavy, 1u << 30);
+    if (heavy + 1 >= (1ull << gc::kSlotBits) || static_cast<uint64_t>(g->max_deg) >= (uint64_t{gc::kAsyncChunk} << gc::kChunkBits))
+      return fail(DPC_E_OVERFLOW, "asynchronous GC task encoding exceeded (use DPC_CFG_GRID_CHUNKED)");
+    const uint64_t qcap = static_cast<uint64_t>(g->n) + 2 * pool_need(g, gc::kAsyncHeavy, gc::kAsyncChunk) + 32;
+    if (g->gc_q_cap < qcap) {
+      DPC_CUDA(cudaStreamSynchronize(s));
+      if (g->gc_q) cudaFree(g->gc_q);
+      g->gc_q = nullptr;
+      g->gc_q_cap = 0;
+      DPC_CUDA(cudaMalloc(&g->gc_q, sizeof(unsigned long long) * qcap + 1024));
+      g->gc_q_cap = qcap;
+    }
+    if (g->gc_hstate_cap < heavy + 1) {
+      DPC_CUDA(cudaStreamSynchronize(s));
+      if (g->gc_hstate) cudaFree(g->gc_hstate);
+      g->gc_hstate = nullptr;
+      g->gc_hstate_cap = 0;
+      DPC_CUDA(cudaMalloc(&g->gc_hstate, sizeof(unsigned) * gc::kStateWords * (heavy + 1)));
+      g->gc_hstate_cap = heavy + 1;
+    }
+    gc::Async q;
+    q.q = reinterpret_cast<unsigned long long*>(g->gc_q);
+    q.qctr = reinterpret_cast<unsigned*>(q.q + qcap);  // 128 words after the slots
+    q.qcap = static_cast<unsigned>(qcap);
+    q.hstate = g->gc_hstate;
+    q.hcap = static_cast<unsigned>(g->gc_hstate_cap);
+    DPC_CUDA(cudaMemsetAsync(q.q, 0xff, sizeof(unsigned long long) * qcap, s));
+    DPC_CUDA(cudaMemsetAsync(q.qctr, 0, 1024, s));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(gc::async_persistent),
+                                                  256, 0);
+    int blocks = std::max(1, per_sm) * ctx->sms;
+    void* args[] = {&a, &q};
+    DPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(gc::async_persistent), dim3(blocks),
+                                         dim3(256), args, 0, s));
+    host_launches = 1;
+    DPC_CUDA(cudaMemcpyAsync(ctr_host, a.ctr, sizeof(gc::Ctr), cudaMemcpyDeviceToHost, s));
+    DPC_CUDA(cudaStreamSynchronize(s));
+    iters = 1;
   } else if (c.variant == DPC_GRID && c.grid_persistent) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(gc::grid_persistent),

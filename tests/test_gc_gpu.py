@@ -78,3 +78,22 @@ def test_gc_config3_full(ctx, orc):
         assert np.array_equal(dg.get_color(), ref), v
         assert met.result_count == k
     dg.close()
+
+
+def _clique(n):
+    rows = [[j for j in range(n) if j != i] for i in range(n)]
+    rowptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])])
+    return dpc.csr_from_arrays(rowptr, np.concatenate(rows).astype(np.int32))
+
+
+@pytest.mark.parametrize("form", ["async", "rounds"])
+def test_gc_grid_forms(ctx, orc, form):
+    """The persistent grid variant's two forms: the asynchronous worklist
+    (default) and the round-synchronous one, on heavy vertices (chunk tasks),
+    a 1030-clique (colors >= 1024: windowed mex) and R-MAT."""
+    cfg = dpc.launch_cfg("color", "grid", grid_chunked=(form == "rounds"))
+    for g in (_clique(1030), dpc.gen_rmat(15, 16, seed=2, weights=False, symmetric=True),
+              dpc.gen_graph(5000, powerlaw=(1.3, 4900), seed=8, weights=False, symmetric=True)):
+        color, k, met = dpc.run_color(g, 11, cfg=cfg, ctx=ctx)
+        _check(orc, g, 11, color, k)
+        assert met.child_launch_count == 0
