@@ -172,11 +172,13 @@ typedef struct dpc_launch_cfg {
 #define DPC_CFG_GRID_CDP 1 /* grid variant: last block launches the child via
                               CDP2 (else: one persistent cooperative kernel
                               with a device-wide barrier) */
-#define DPC_CFG_GRID_CHUNKED 2 /* persistent grid variant, comparison form: SpMV
-                                  drains fixed-size chunk items warp by warp
-                                  instead of the stream-balanced drain; GC runs
-                                  round-synchronously (grid barriers) instead of
-                                  the asynchronous worklist */
+#define DPC_CFG_GRID_CHUNKED 2 /* SpMV persistent grid variant, comparison form:
+                                  drain fixed-size chunk items warp by warp
+                                  instead of the stream-balanced drain */
+#define DPC_CFG_GRID_ASYNC 8 /* GC / SSSP persistent grid variant: asynchronous
+                                worklist (device FIFO, no barrier between
+                                rounds) instead of round-synchronous grid
+                                barriers; GC default */
 #define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */

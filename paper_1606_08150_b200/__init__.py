@@ -56,6 +56,7 @@ APPS = {"sssp": 0, "spmv": 1, "color": 2, "tree_desc": 3, "tree_height": 4}
 GEN_WEIGHTS, GEN_VALUES, GEN_PERMUTE, GEN_SYMMETRIC = 1, 2, 4, 8
 CFG_GRID_CDP = 1
 CFG_GRID_CHUNKED = 2
+CFG_GRID_ASYNC = 8
 
 
 class DpcError(RuntimeError):
@@ -366,6 +367,8 @@ def launch_cfg(app: str, variant: str, **overrides) -> LaunchCfg:
             cfg.flags = (cfg.flags | CFG_GRID_CDP) if v else (cfg.flags & ~CFG_GRID_CDP)
         elif k == "grid_chunked":
             cfg.flags = (cfg.flags | CFG_GRID_CHUNKED) if v else (cfg.flags & ~CFG_GRID_CHUNKED)
+        elif k == "grid_async":
+            cfg.flags = (cfg.flags | CFG_GRID_ASYNC) if v else (cfg.flags & ~CFG_GRID_ASYNC)
         else:
             setattr(cfg, k, int(v))
     return cfg

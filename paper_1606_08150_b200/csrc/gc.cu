@@ -951,11 +951,11 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   const unsigned nb = std::max(1u, dev::ceil_div(a.n, 256u));
   if (a.n == 0) {
     ctr_host->maxcolor = -1;
-  } else if (c.variant == DPC_GRID && c.grid_persistent && !(c.flags & DPC_CFG_GRID_CHUNKED)) {
+  } else if (c.variant == DPC_GRID && c.grid_persistent && (c.flags & DPC_CFG_GRID_ASYNC)) {
     // asynchronous worklist form: task queue, heavy-vertex states
     const uint64_t heavy = pool_need(g, gc::kAsyncHeavy, 1u << 30);
     if (heavy + 1 >= (1ull << gc::kSlotBits) || static_cast<uint64_t>(g->max_deg) >= (uint64_t{gc::kAsyncChunk} << gc::kChunkBits))
-      return fail(DPC_E_OVERFLOW, "asynchronous GC task encoding exceeded (use DPC_CFG_GRID_CHUNKED)");
+      return fail(DPC_E_OVERFLOW, "asynchronous GC task encoding exceeded (clear DPC_CFG_GRID_ASYNC)");
     const uint64_t qcap = static_cast<uint64_t>(g->n) + 2 * pool_need(g, gc::kAsyncHeavy, gc::kAsyncChunk) + 32;
     if (g->gc_q_cap < qcap) {
       DPC_CUDA(cudaStreamSynchronize(s));

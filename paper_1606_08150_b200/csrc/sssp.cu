@@ -413,6 +413,158 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iter
   if (gtid == 0) a.ctr->iters = it;
 }
 
+// ---------------------------------------------------------------------------
+// Asynchronous grid consolidation (DPC_CFG_GRID_ASYNC; single GPU).  Measured
+// slower than the level-synchronous persistent form on R-MAT SSSP (the
+// relaxations, not the barriers, dominate), so it is not the default here.
+//
+// Level-synchronous Bellman-Ford pays a device-wide barrier (or a host round
+// trip) per level; here the grid-level buffer is a device-wide FIFO of
+// {vertex, distance} tasks drained by a persistent grid without barriers
+// (chaotic relaxation: same unique fixpoint = Dijkstra's distances).  Every
+// distance drop queues a task carrying the new distance; a task whose
+// vertex has since dropped further is stale and skipped (the drop queued its
+// own), so no dedup flags and no store-buffering fences are needed.  Queue
+// position p is served by warp p mod W in order; the warp that makes a
+// distance drop serves one such task itself next (work-first); heavy
+// vertices fan out into chunk tasks.  The run ends when the FIFO is drained
+// (every queued task served, none in flight).
+constexpr int kAW = 4;                      // edges per lane per step
+constexpr unsigned kAsyncHeavy = 128;       // edges one warp task takes
+constexpr unsigned kAsyncChunk = 128;       // edges per chunk task
+constexpr unsigned long long kEmpty = ~0ull;
+constexpr unsigned long long kChunkTask = 1ull << 63;
+constexpr unsigned kTail = 0, kDone = 32, kStop = 64;
+
+struct Async {
+  unsigned long long* q;  // vertex | dist << 32, or vertex | chunk << 32 | kChunkTask
+  unsigned* qctr;         // [kTail], [kDone], [kStop], one line each
+  unsigned qcap;
+};
+
+__device__ __forceinline__ unsigned long long vtask(unsigned v, unsigned d) {
+  return static_cast<unsigned long long>(v) | (static_cast<unsigned long long>(d) << 32);
+}
+
+__device__ __forceinline__ void a_enqueue(const Args& a, const Async& q, bool want, unsigned long long t) {
+  const unsigned ball = __ballot_sync(kFull, want);
+  if (!ball) return;
+  const unsigned lane = dev::lane_id(), lead = __ffs(ball) - 1;
+  unsigned base = 0;
+  if (lane == lead) base = atomicAdd(q.qctr + kTail, __popc(ball));
+  base = __shfl_sync(kFull, base, lead);
+  if (want) {
+    const unsigned at = base + __popc(ball & ((1u << lane) - 1u));
+    if (at < q.qcap) {
+      *reinterpret_cast<volatile unsigned long long*>(q.q + at) = t;
+    } else {
+      atomicOr(&a.hdr->overflow, 1u);
+      atomicExch(q.qctr + kStop, 1u);
+    }
+  }
+}
+
+// Relaxes edges [b, e) from distance du; each drop queues a task, one kept
+// as this warp's continuation.
+__device__ __forceinline__ unsigned long long a_relax(const Args& a, const Async& q, unsigned b, unsigned e,
+                                                      unsigned du, unsigned long long* work) {
+  unsigned long long keep = kEmpty;
+  for (unsigned k0 = b; k0 < e; k0 += 32 * kAW) {
+    unsigned v[kAW], nd[kAW];
+    bool drop[kAW];
+#pragma unroll
+    for (int j = 0; j < kAW; j++) {
+      const unsigned k = k0 + 32 * j + dev::lane_id();
+      nd[j] = kInf;
+      v[j] = 0;
+      if (k < e) {
+        v[j] = static_cast<unsigned>(__ldg(a.col + k));
+        const unsigned long long d = static_cast<unsigned long long>(du) + static_cast<unsigned>(__ldg(a.w + k));
+        nd[j] = d < 0x7fffffffull ? static_cast<unsigned>(d) : kInf;  // task words hold 31-bit distances
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kAW; j++)
+      drop[j] = nd[j] < kInf && nd[j] < __ldcg(a.dist + v[j]) && nd[j] < atomicMin(a.dist + v[j], nd[j]);
+#pragma unroll
+    for (int j = 0; j < kAW; j++) {
+      if (keep == kEmpty) {
+        const unsigned ball = __ballot_sync(kFull, drop[j]);
+        if (ball) {
+          const unsigned l = __ffs(ball) - 1;
+          keep = vtask(__shfl_sync(kFull, v[j], l), __shfl_sync(kFull, nd[j], l));
+          if (dev::lane_id() == l) drop[j] = false;
+        }
+      }
+      a_enqueue(a, q, drop[j], vtask(v[j], nd[j]));
+    }
+  }
+  if (dev::lane_id() == 0) *work += e - b;
+  return keep;
+}
+
+__device__ unsigned long long a_serve(const Args& a, const Async& q, unsigned long long t,
+                                      unsigned long long* work) {
+  const unsigned u = static_cast<unsigned>(t);
+  const unsigned b = __ldg(a.rowptr + u), e = __ldg(a.rowptr + u + 1);
+  const unsigned du = __ldcg(a.dist + u);
+  if (!(t & kChunkTask)) {
+    if (du != static_cast<unsigned>(t >> 32)) return kEmpty;  // stale: a later drop queued u again
+    if (e - b <= kAsyncHeavy) return a_relax(a, q, b, e, du, work);
+    const unsigned nch = (e - b + kAsyncChunk - 1) / kAsyncChunk;
+    for (unsigned c0 = 1; c0 < nch; c0 += 32)
+      a_enqueue(a, q, c0 + dev::lane_id() < nch,
+                u | (static_cast<unsigned long long>(c0 + dev::lane_id()) << 32) | kChunkTask);
+    return a_relax(a, q, b, b + kAsyncChunk, du, work);
+  }
+  const unsigned chunk = static_cast<unsigned>(t >> 32) & 0x7fffffffu;
+  const unsigned cb = b + chunk * kAsyncChunk, ce = min(e, cb + kAsyncChunk);
+  return a_relax(a, q, cb, ce, du, work);  // the freshest distance of u is as good
+}
+
+__global__ void __launch_bounds__(256) async_persistent(Args a, Async q, unsigned source) {
+  const unsigned stride = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x, lane = dev::lane_id();
+  const unsigned nwarps = stride >> 5, gw = gtid >> 5;
+  volatile unsigned* vq = q.qctr;
+  unsigned long long work = 0;
+  if (gtid == 0) {
+    atomicAdd(q.qctr + kTail, 1u);
+    *reinterpret_cast<volatile unsigned long long*>(q.q) = vtask(source, 0);
+  }
+  for (unsigned p = gw; p < q.qcap; p += nwarps) {
+    unsigned long long t = kEmpty;
+    unsigned spins = 0;
+    unsigned long long since = 0;
+    while (true) {
+      if (lane == 0) t = *reinterpret_cast<volatile unsigned long long*>(q.q + p);
+      t = __shfl_sync(kFull, t, 0);
+      if (t != kEmpty) break;
+      unsigned fin = 0;
+      if (lane == 0 && (++spins & 15) == 0) {
+        const unsigned d = vq[kDone];  // read before tail: equal means nothing in flight
+        fin = (d > 0 && d == vq[kTail]) || vq[kStop];
+        const unsigned long long now = dev::global_ns();
+        if (!since) since = now;
+        if (now - since > 2000000000ull) {
+          atomicOr(&a.hdr->overflow, 4u);
+          atomicExch(q.qctr + kStop, 1u);
+          fin = 1;
+        }
+      }
+      if (__shfl_sync(kFull, fin, 0)) break;
+      if (spins > 32) __nanosleep(64);
+    }
+    if (t == kEmpty) break;
+    while (t != kEmpty) t = a_serve(a, q, t, &work);
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(q.qctr + kDone, 1u);
+    }
+  }
+  if (lane == 0 && work) atomicAdd(&a.hdr->work, work);
+}
+
 }  // namespace sssp
 
 static int coop_blocks_sssp(dpc_ctx* ctx, const void* fn, int threads) {
@@ -523,7 +675,30 @@ extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t sourc
   DPC_CUDA(cudaGetLastError());
   int64_t host_launches = 1, iters = 0;
   auto* ctr_host = reinterpret_cast<sssp::Ctr*>(g->ctr_host);
-  if (c.variant == DPC_GRID && c.grid_persistent) {
+  if (c.variant == DPC_GRID && c.grid_persistent && (c.flags & DPC_CFG_GRID_ASYNC)) {
+    const uint64_t qcap = 8 * (static_cast<uint64_t>(g->n) + static_cast<uint64_t>(g->m)) + 64;
+    if (g->gc_q_cap < qcap) {
+      DPC_CUDA(cudaStreamSynchronize(s));
+      if (g->gc_q) cudaFree(g->gc_q);
+      g->gc_q = nullptr;
+      g->gc_q_cap = 0;
+      DPC_CUDA(cudaMalloc(&g->gc_q, sizeof(unsigned long long) * qcap + 1024));
+      g->gc_q_cap = qcap;
+    }
+    sssp::Async q;
+    q.q = reinterpret_cast<unsigned long long*>(g->gc_q);
+    q.qcap = static_cast<unsigned>(std::min<uint64_t>(g->gc_q_cap, 0xffffffffull));
+    q.qctr = reinterpret_cast<unsigned*>(q.q + g->gc_q_cap);
+    DPC_CUDA(cudaMemsetAsync(q.q, 0xff, sizeof(unsigned long long) * g->gc_q_cap, s));
+    DPC_CUDA(cudaMemsetAsync(q.qctr, 0, 1024, s));
+    int blocks = coop_blocks_sssp(ctx, reinterpret_cast<const void*>(sssp::async_persistent), 256);
+    unsigned src = static_cast<unsigned>(source);
+    void* args[] = {&a, &q, &src};
+    DPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(sssp::async_persistent),
+                                         dim3(blocks), dim3(256), args, 0, s));
+    host_launches += 1;
+    iters = 1;
+  } else if (c.variant == DPC_GRID && c.grid_persistent) {
     int blocks = coop_blocks_sssp(ctx, reinterpret_cast<const void*>(sssp::grid_persistent), 256);
     unsigned max_iters = a.n + 1;
     void* args[] = {&a, &max_iters};

@@ -91,7 +91,7 @@ def test_gc_grid_forms(ctx, orc, form):
     """The persistent grid variant's two forms: the asynchronous worklist
     (default) and the round-synchronous one, on heavy vertices (chunk tasks),
     a 1030-clique (colors >= 1024: windowed mex) and R-MAT."""
-    cfg = dpc.launch_cfg("color", "grid", grid_chunked=(form == "rounds"))
+    cfg = dpc.launch_cfg("color", "grid", grid_async=(form == "async"))
     for g in (_clique(1030), dpc.gen_rmat(15, 16, seed=2, weights=False, symmetric=True),
               dpc.gen_graph(5000, powerlaw=(1.3, 4900), seed=8, weights=False, symmetric=True)):
         color, k, met = dpc.run_color(g, 11, cfg=cfg, ctx=ctx)

@@ -85,3 +85,17 @@ def test_sssp_invalid(ctx):
     g2 = dpc.gen_rmat(6, 4, seed=1, weights=False, values=True)
     with pytest.raises(dpc.DpcError):
         dpc.run_sssp(g2, 0, "grid", ctx=ctx)
+
+
+@pytest.mark.parametrize("form", ["rounds", "async"])
+@pytest.mark.parametrize("scale", [10, 14])
+def test_sssp_grid_forms(ctx, orc, form, scale):
+    """The persistent grid variant's two forms (level-synchronous default and
+    the asynchronous worklist) are bit-exact against Dijkstra, including an
+    isolated source and zero-weight edges."""
+    g = dpc.gen_rmat(scale, 16, seed=scale + 1, wmin=0, wmax=3)
+    cfg = dpc.launch_cfg("sssp", "grid", grid_async=(form == "async"))
+    for s in (int(np.argmax(g.degrees())), int(np.flatnonzero(g.degrees() == 0)[0])):
+        d, met = dpc.run_sssp(g, s, "grid", cfg=cfg, ctx=ctx)
+        assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, s))
+        assert met.child_launch_count == 0
