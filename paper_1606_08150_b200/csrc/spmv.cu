@@ -611,8 +611,6 @@ __global__ void __launch_bounds__(256, MB) grid_persistent(Args a) {
 // plain store when the item lies inside the window, else with atomicAdd.
 constexpr int kPackShift = 38;  // packed reservation: items << 38 | positions
 constexpr unsigned long long kNnzMask = (1ull << kPackShift) - 1;
-constexpr int kStreamV = 4;
-constexpr unsigned kWin = 128;  // stream positions per window (32 lanes x 4)
 
 struct Stream {
   uint2* seg;  // per item: {stream offset, CSR end}; Item {row, CSR begin} in the pool
@@ -640,8 +638,78 @@ __device__ __forceinline__ unsigned long long warp_incl_scan64(unsigned long lon
   return v;
 }
 
+// Stream length of CSR range [b, e) widened to G-element (4G-byte) boundaries.
+template <int G>
 __device__ __forceinline__ unsigned stream_len(unsigned b, unsigned e) {
-  return ((e + 3u) & ~3u) - (b & ~3u);
+  return ((e + (G - 1u)) & ~(G - 1u)) - (b & ~(G - 1u));
+}
+
+// One lane's aligned group of G stream positions: G/4 int4 of col, G/4
+// float4 of val.
+template <int G>
+struct Grp {
+  int4 c[G / 4];
+  float4 w[G / 4];
+};
+
+template <int G>
+__device__ __forceinline__ void grp_load(const Args& a, unsigned k, Grp<G>& g) {
+#pragma unroll
+  for (int i = 0; i < G / 4; i++) {
+    if (a.xflags & 32u) {  // probe: no col/val traffic (synthetic columns)
+      const int cs = static_cast<int>(((k + 4 * i) * 2654435761u) & 0xfffffu);
+      g.c[i] = make_int4(cs, cs ^ 1, cs ^ 2, cs ^ 3);
+      g.w[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+    } else {
+      g.c[i] = ldg_stream(reinterpret_cast<const int4*>(a.col + k + 4 * i));
+      g.w[i] = ldg_stream(reinterpret_cast<const float4*>(a.val + k + 4 * i));
+    }
+  }
+}
+
+// Masked dot of a group with x: masked elements (the widening, invalid
+// lanes) gather x[0] and weigh exactly 0.
+template <int G, int SLOG>
+__device__ __forceinline__ float grp_dot(const Args& a, const Grp<G>& g, unsigned m, const uint2* xc) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < G / 4; i++) {
+    const int* cp = reinterpret_cast<const int*>(&g.c[i]);
+    const float* wp = reinterpret_cast<const float*>(&g.w[i]);
+    float part = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const bool on = (m >> (4 * i + e)) & 1u;
+      int idx = on ? cp[e] : 0;
+      if (a.xflags & 64u) idx &= 1023;      // probe: gathers confined to 4 KB of x
+      if (a.xflags & 128u) idx &= 0xffff;   // probe: gathers confined to 256 KB of x
+      const float wt = on ? wp[e] : 0.f;
+      float xv;
+      if (a.xflags & 16u) {
+        xv = 1.f;
+      } else if (SLOG > 0) {
+        const uint2 t = xc[xslot(static_cast<unsigned>(idx), SLOG)];
+        xv = t.x == static_cast<unsigned>(idx) ? __uint_as_float(t.y) : __ldg(a.x + idx);
+      } else if (a.xflags & 256u) {
+        xv = __ldcg(a.x + idx);  // probe: x gathers through L2 only
+      } else if (a.xflags & 512u) {
+        xv = ld_stream_f(a.x + idx);  // probe: x gathers without L1 allocation
+      } else {
+        xv = __ldg(a.x + idx);
+      }
+      part += wt * xv;
+    }
+    s += part;
+  }
+  return s;
+}
+
+// Bits of the aligned group at CSR index k that lie inside [b, e).
+template <int G>
+__device__ __forceinline__ unsigned grp_mask(unsigned k, unsigned b, unsigned e) {
+  const int lo_e = max(static_cast<int>(b - k), 0);
+  const int hi_e = min(max(static_cast<int>(e - k), 0), G);
+  return ((((1u << G) - 1u) << lo_e) & ((1u << hi_e) - 1u)) & ((1u << G) - 1u);
 }
 
 // Insert of row `row` (CSR range [b, e)) at packed position `at`.
@@ -678,18 +746,21 @@ __device__ __forceinline__ void load_items(const Args& a, const Stream& st, unsi
   __syncwarp();
 }
 
-// Drains this warp's slice [s0, s1) of the stream (s0 a multiple of kWin,
-// s1 a multiple of kWin or the stream end).  All lanes call.
+// Drains this warp's slice [s0, s1) of the stream (s0 a multiple of the
+// window 32G, s1 a multiple of it or the stream end).  All lanes call.
 //   start: 32-ary search of the item covering s0 (log32(items) L2 rounds)
-//   window: its items are ja .. ja+31 at most (items are >= 4 positions and
-//     start on 4-aligned positions); each lane reads item ja+lane from the
-//     shared-memory batch, the lanes where an item starts form a bit mask
-//     (one OR-reduction), and each lane's item is ja + popc(mask below it).
-//     ja of the next window follows from the mask; the batch is refilled
-//     from L2 when the window could run past it.
-template <int V, unsigned KB, int SLOG>
+//   window: 32 groups of G positions (one per lane); its items are ja ..
+//     ja+31 at most (items are >= G positions and start on G-aligned
+//     positions); each lane reads item ja+lane from the shared-memory batch,
+//     the lanes where an item starts form a bit mask (one OR-reduction), and
+//     each lane's item is ja + popc(mask below it).  ja of the next window
+//     follows from the mask; the batch is refilled from L2 when the window
+//     could run past it.
+//   fast step: V windows inside one long item need no lookup and no scan.
+template <int G, int V, unsigned KB, int SLOG>
 __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, unsigned ni,
                                              unsigned s0, unsigned s1, uint4* buf, const uint2* xc) {
+  constexpr unsigned W = 32u * G;  // stream positions per window
   const unsigned lane = dev::lane_id();
   const unsigned lt_mask = (2u << lane) - 1u;  // lanes <= this one
   unsigned lo = 0, hi = ni;  // seg[lo].x <= s0 < seg[hi].x (hi = ni: end)
@@ -706,58 +777,24 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
   load_items<KB>(a, st, ni, bb, buf);
   float carry = 0.f;  // this lane's partial sum for item ja from fast steps
   bool carrying = false;
-  for (unsigned p0 = s0; p0 < s1; p0 += kWin * V) {
+  for (unsigned p0 = s0; p0 < s1; p0 += W * V) {
     {
-      // Fast step: the V windows lie inside item ja (long rows): no lookup,
-      // no segmented scan; the lanes accumulate and flush once per item.
       if (ja + 33 > bb + KB) {
         bb = ja;
         load_items<KB>(a, st, ni, bb, buf);
       }
       const uint4 it = buf[ja - bb];
-      const unsigned iend = it.x + stream_len(it.z, it.y);
-      if (p0 + kWin * V <= min(iend, s1)) {
-        const unsigned kb = (it.z & ~3u) + (p0 - it.x) + 4 * lane;
+      const unsigned iend = it.x + stream_len<G>(it.z, it.y);
+      if (p0 + W * V <= min(iend, s1)) {
+        const unsigned kb = (it.z & ~(G - 1u)) + (p0 - it.x) + G * lane;
+        Grp<G> g[V];
 #pragma unroll
-        for (int v = 0; v < V; v++) {
-          const unsigned k = kb + kWin * v;
-          const int lo_e = max(static_cast<int>(it.z - k), 0);
-          const int hi_e = min(max(static_cast<int>(it.y - k), 0), 4);
-          const unsigned m = (0xfu << lo_e) & ((1u << hi_e) - 1u);
-          int4 cv;
-          float4 wv;
-          if (a.xflags & 32u) {
-            const int cs = static_cast<int>((k * 2654435761u) & 0xfffffu);
-            cv = make_int4(cs, cs ^ 1, cs ^ 2, cs ^ 3);
-            wv = make_float4(1.f, 1.f, 1.f, 1.f);
-          } else {
-            cv = ldg_stream(reinterpret_cast<const int4*>(a.col + k));
-            wv = ldg_stream(reinterpret_cast<const float4*>(a.val + k));
-          }
-          const int i0 = (m & 1u) ? cv.x : 0, i1 = (m & 2u) ? cv.y : 0;
-          const int i2 = (m & 4u) ? cv.z : 0, i3 = (m & 8u) ? cv.w : 0;
-          const float w0 = (m & 1u) ? wv.x : 0.f, w1 = (m & 2u) ? wv.y : 0.f;
-          const float w2 = (m & 4u) ? wv.z : 0.f, w3 = (m & 8u) ? wv.w : 0.f;
-          float x0, x1, x2, x3;
-          if (a.xflags & 16u) {
-            x0 = x1 = x2 = x3 = 1.f;
-          } else if (SLOG > 0) {
-            const uint2 t0 = xc[xslot(i0, SLOG)], t1 = xc[xslot(i1, SLOG)];
-            const uint2 t2 = xc[xslot(i2, SLOG)], t3 = xc[xslot(i3, SLOG)];
-            x0 = t0.x == static_cast<unsigned>(i0) ? __uint_as_float(t0.y) : __ldg(a.x + i0);
-            x1 = t1.x == static_cast<unsigned>(i1) ? __uint_as_float(t1.y) : __ldg(a.x + i1);
-            x2 = t2.x == static_cast<unsigned>(i2) ? __uint_as_float(t2.y) : __ldg(a.x + i2);
-            x3 = t3.x == static_cast<unsigned>(i3) ? __uint_as_float(t3.y) : __ldg(a.x + i3);
-          } else {
-            x0 = __ldg(a.x + i0);
-            x1 = __ldg(a.x + i1);
-            x2 = __ldg(a.x + i2);
-            x3 = __ldg(a.x + i3);
-          }
-          carry += (w0 * x0 + w1 * x1) + (w2 * x2 + w3 * x3);
-        }
+        for (int v = 0; v < V; v++) grp_load<G>(a, kb + W * v, g[v]);
+#pragma unroll
+        for (int v = 0; v < V; v++)
+          carry += grp_dot<G, SLOG>(a, g[v], grp_mask<G>(kb + W * v, it.z, it.y), xc);
         carrying = true;
-        if (iend == p0 + kWin * V) {  // item ja ends exactly here: flush, move on
+        if (iend == p0 + W * V) {  // item ja ends exactly here: flush, move on
           const float t = dev::warp_sum(carry);
           if (lane == 0) atomicAdd(a.y + it.w, t);
           carry = 0.f;
@@ -776,86 +813,49 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
     unsigned kk[V], info[V], rw[V];
 #pragma unroll
     for (int v = 0; v < V; v++) {
-      const unsigned pw = p0 + kWin * v;  // may lie past s1 on the last step: no lane is valid then
+      const unsigned pw = p0 + W * v;  // may lie past s1 on the last step: no lane is valid then
       if (ja + 33 > bb + KB) {
         bb = ja;
         load_items<KB>(a, st, ni, bb, buf);
       }
-      const unsigned last = min(pw + kWin, s1) - 1;
+      const unsigned last = min(pw + W, s1) - 1;
       const unsigned off = buf[ja - bb + lane].x;
       // lanes where an item starts inside the window (lane 0 excluded)
-      const unsigned bit = (off > pw && off <= last) ? 1u << ((off - pw) >> 2) : 0u;
+      const unsigned bit = (off > pw && off <= last) ? 1u << ((off - pw) / G) : 0u;
       const unsigned smask = __reduce_or_sync(kFull, bit);
       const uint4 it = buf[ja - bb + __popc(smask & lt_mask)];  // {offset, end, begin, row}
-      const unsigned q = pw + 4 * lane;
+      const unsigned q = pw + G * lane;
       const bool valid = q < s1;
-      const unsigned k = valid ? (it.z & ~3u) + (q - it.x) : 0u;
-      // elements of the aligned group inside [begin, end): a bit range
-      const int lo_e = max(static_cast<int>(it.z - k), 0);
-      const int hi_e = min(max(static_cast<int>(it.y - k), 0), 4);
-      const unsigned m = valid ? ((0xfu << lo_e) & ((1u << hi_e) - 1u)) : 0u;
+      const unsigned k = valid ? (it.z & ~(G - 1u)) + (q - it.x) : 0u;
+      const unsigned m = valid ? grp_mask<G>(k, it.z, it.y) : 0u;
       const unsigned ls = 31 - __clz((smask | 1u) & lt_mask);  // segment start lane
-      const bool seg_end = valid && (lane == 31 || (((smask >> 1) >> lane) & 1u) || q + 4 >= s1);
-      const bool whole = it.x >= pw && it.x + stream_len(it.z, it.y) <= pw + kWin;
+      const bool seg_end = valid && (lane == 31 || (((smask >> 1) >> lane) & 1u) || q + G >= s1);
+      const bool whole = it.x >= pw && it.x + stream_len<G>(it.z, it.y) <= pw + W;
       kk[v] = k;
       rw[v] = it.w;
-      info[v] = m | (ls << 4) | (seg_end ? 1u << 9 : 0u) | (whole ? 1u << 10 : 0u);
+      info[v] = m | (ls << 16) | (seg_end ? 1u << 21 : 0u) | (whole ? 1u << 22 : 0u);
       // first item of the next window
       ja += __popc(smask);
-      ja += buf[ja + 1 - bb].x == pw + kWin ? 1u : 0u;
+      ja += buf[ja + 1 - bb].x == pw + W ? 1u : 0u;
     }
-    int4 c[V];
-    float4 w[V];
+    Grp<G> g[V];
 #pragma unroll
-    for (int v = 0; v < V; v++) {
-      if (a.xflags & 32u) {  // probe: no col/val traffic (synthetic columns)
-        const int cs = static_cast<int>((kk[v] * 2654435761u) & 0xfffffu);
-        c[v] = make_int4(cs, cs ^ 1, cs ^ 2, cs ^ 3);
-        w[v] = make_float4(1.f, 1.f, 1.f, 1.f);
-      } else {
-        c[v] = ldg_stream(reinterpret_cast<const int4*>(a.col + kk[v]));
-        w[v] = ldg_stream(reinterpret_cast<const float4*>(a.val + kk[v]));
-      }
-    }
+    for (int v = 0; v < V; v++) grp_load<G>(a, kk[v], g[v]);
     float s[V];
 #pragma unroll
-    for (int v = 0; v < V; v++) {
-      // masked elements (the widening, invalid lanes) gather x[0] and weigh 0
-      const unsigned m = info[v];
-      const int i0 = (m & 1u) ? c[v].x : 0, i1 = (m & 2u) ? c[v].y : 0;
-      const int i2 = (m & 4u) ? c[v].z : 0, i3 = (m & 8u) ? c[v].w : 0;
-      const float w0 = (m & 1u) ? w[v].x : 0.f, w1 = (m & 2u) ? w[v].y : 0.f;
-      const float w2 = (m & 4u) ? w[v].z : 0.f, w3 = (m & 8u) ? w[v].w : 0.f;
-      float x0, x1, x2, x3;
-      if (a.xflags & 16u) {  // probe: no x gathers
-        x0 = x1 = x2 = x3 = 1.f;
-      } else if (SLOG > 0) {
-        const uint2 t0 = xc[xslot(i0, SLOG)], t1 = xc[xslot(i1, SLOG)];
-        const uint2 t2 = xc[xslot(i2, SLOG)], t3 = xc[xslot(i3, SLOG)];
-        x0 = t0.x == static_cast<unsigned>(i0) ? __uint_as_float(t0.y) : __ldg(a.x + i0);
-        x1 = t1.x == static_cast<unsigned>(i1) ? __uint_as_float(t1.y) : __ldg(a.x + i1);
-        x2 = t2.x == static_cast<unsigned>(i2) ? __uint_as_float(t2.y) : __ldg(a.x + i2);
-        x3 = t3.x == static_cast<unsigned>(i3) ? __uint_as_float(t3.y) : __ldg(a.x + i3);
-      } else {
-        x0 = __ldg(a.x + i0);
-        x1 = __ldg(a.x + i1);
-        x2 = __ldg(a.x + i2);
-        x3 = __ldg(a.x + i3);
-      }
-      s[v] = (w0 * x0 + w1 * x1) + (w2 * x2 + w3 * x3);
-    }
+    for (int v = 0; v < V; v++) s[v] = grp_dot<G, SLOG>(a, g[v], info[v] & 0xffffu, xc);
 #pragma unroll
     for (int v = 0; v < V; v++) {
-      if (p0 + kWin * v >= s1) break;
-      const unsigned ls = (info[v] >> 4) & 31u;
+      if (p0 + W * v >= s1) break;
+      const unsigned ls = (info[v] >> 16) & 31u;
       float t = s[v];
 #pragma unroll
       for (unsigned d = 1; d < 32; d <<= 1) {
         const float u = __shfl_up_sync(kFull, t, d);
         if (lane >= ls + d) t += u;
       }
-      if (info[v] & (1u << 9)) {
-        if (info[v] & (1u << 10)) a.y[rw[v]] = t;
+      if (info[v] & (1u << 21)) {
+        if (info[v] & (1u << 22)) a.y[rw[v]] = t;
         else atomicAdd(a.y + rw[v], t);
       }
     }
@@ -878,8 +878,9 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
 //     PAPER.md:244-250; legal because a cooperative launch co-schedules
 //     the whole grid)
 //   drain: stream-balanced, every warp the same number of positions.
-template <bool INLINE, int V, int NT, int MINB, int SLOG, unsigned KB>
+template <bool INLINE, int G, int V, int NT, int MINB, int SLOG, unsigned KB>
 __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
+  constexpr unsigned kWin = 32u * G;
   constexpr int NW = NT / 32;
   constexpr int kRound = NT >= 1024 ? 4 : 8;  // tiles per thread per reservation round
   __shared__ unsigned long long s_w[kRound * NW];
@@ -890,24 +891,24 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[0] = dev::global_ns();
   const unsigned lane = dev::lane_id(), wib = dev::warp_in_block();
   const unsigned lt_excl = (1u << lane) - 1u;
-  const unsigned G = gridDim.x, ntiles = (a.n + NT - 1) / NT;
+  const unsigned GB = gridDim.x, ntiles = (a.n + NT - 1) / NT;
   if (SLOG > 0)  // x at the planned hot columns, once per run
-    for (unsigned i = blockIdx.x * NT + threadIdx.x; i < (1u << SLOG); i += G * NT) {
+    for (unsigned i = blockIdx.x * NT + threadIdx.x; i < (1u << SLOG); i += GB * NT) {
       const int c = st.xhot_col[i];
       st.xhot_val[i] = c >= 0 ? __ldg(a.x + c) : 0.f;
     }
-  for (unsigned t0 = blockIdx.x; t0 < ntiles; t0 += G * kRound) {
+  for (unsigned t0 = blockIdx.x; t0 < ntiles; t0 += GB * kRound) {
     unsigned bb[kRound], ee[kRound], inc[kRound];
 #pragma unroll
     for (int k = 0; k < kRound; k++) {
-      const unsigned r = (t0 + k * G) * NT + threadIdx.x;
+      const unsigned r = (t0 + k * GB) * NT + threadIdx.x;
       bb[k] = ee[k] = 0;
-      if (t0 + k * G < ntiles && r < a.n) bb[k] = __ldg(a.rowptr + r), ee[k] = __ldg(a.rowptr + r + 1);
+      if (t0 + k * GB < ntiles && r < a.n) bb[k] = __ldg(a.rowptr + r), ee[k] = __ldg(a.rowptr + r + 1);
     }
 #pragma unroll
     for (int k = 0; k < kRound; k++) {
       const bool cons = ee[k] - bb[k] > a.threshold;
-      const unsigned len = cons ? stream_len(bb[k], ee[k]) : 0u;
+      const unsigned len = cons ? stream_len<G>(bb[k], ee[k]) : 0u;
       inc[k] = dev::warp_incl_scan(len);
       const unsigned cnt = __popc(__ballot_sync(kFull, cons));
       if (lane == 31) s_w[k * NW + wib] = (static_cast<unsigned long long>(cnt) << kPackShift) | inc[k];
@@ -928,8 +929,8 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
     const unsigned long long base = s_base;
 #pragma unroll
     for (int k = 0; k < kRound; k++) {
-      const unsigned r = (t0 + k * G) * NT + threadIdx.x;
-      const bool in = t0 + k * G < ntiles && r < a.n;
+      const unsigned r = (t0 + k * GB) * NT + threadIdx.x;
+      const bool in = t0 + k * GB < ntiles && r < a.n;
       const unsigned b = bb[k], e = ee[k];
       const bool cons = e - b > a.threshold;
       const unsigned ball = __ballot_sync(kFull, cons);
@@ -937,7 +938,7 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
       if (INLINE) sl = warp_light_rows(a, b, in && !cons ? e - b : 0u);
       if (in && !(a.xflags & 8u)) a.y[r] = cons ? 0.f : sl;
       if (cons) {
-        const unsigned len = stream_len(b, e);
+        const unsigned len = stream_len<G>(b, e);
         const unsigned long long at = base + s_w[k * NW + wib] +
                                       ((static_cast<unsigned long long>(__popc(ball & lt_excl)) << kPackShift) |
                                        (inc[k] - len));
@@ -962,38 +963,44 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
                                  kWin * kWin;
   const unsigned long long s0 = static_cast<unsigned long long>(gw) * per;
   if (ni > 0 && s0 < total && !(a.xflags & 1u))
-    stream_drain<V, KB, SLOG>(a, st, ni, static_cast<unsigned>(s0),
+    stream_drain<G, V, KB, SLOG>(a, st, ni, static_cast<unsigned>(s0),
                               static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
                               s_items + wib * KB, s_cache);
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&a.hdr->t[2], dev::global_ns());
 }
 
-// Stream kernel shapes (dpc_launch_cfg.flags bits 20-21), measured on config 2:
-//   0: 1024 threads x 1 block/SM, no cache                (default, best)
-//   1: 256 threads x 4 blocks/SM, no cache
-//   2: 1024 threads x 1 block/SM, hot-column cache of 2^14 slots
+// Stream kernel shapes (dpc_launch_cfg.flags bits 20-22), measured on config 2
+// (tools/prof_spmv.py --burst; the x gathers, not HBM, bound all of them):
+//   0: groups of 4 positions per lane, 4 windows per step, 1024 threads x 1
+//      block/SM (default, best)
+//   1: groups of 8, 2 windows per step, 1024 threads
+//   2: groups of 4, 256 threads x 4 blocks/SM
+//   3: groups of 4, 1024 threads, hot-column x cache of 2^14 slots
+//   4: groups of 8, 1024 threads, hot-column x cache
 struct StreamShape {
   const void* fn;
   int threads;
   int slog;
+  int group;
   size_t smem;  // dynamic shared memory bytes
 };
 constexpr int kHotLog = 14;
+template <int G, int V, int NT, int MINB, int SLOG, unsigned KB>
+static StreamShape shape_of(bool inl) {
+  const size_t cache = SLOG ? sizeof(uint2) << SLOG : 0;
+  return {inl ? reinterpret_cast<const void*>(grid_stream<true, G, V, NT, MINB, SLOG, KB>)
+              : reinterpret_cast<const void*>(grid_stream<false, G, V, NT, MINB, SLOG, KB>),
+          NT, SLOG, G, (NT / 32) * KB * sizeof(uint4) + cache};
+}
 static StreamShape stream_shape(bool inl, unsigned flags) {
-  const unsigned sh = (flags >> 20) & 3u;
-  const size_t c14 = sizeof(uint2) << kHotLog;
-  if (sh == 1)
-    return {inl ? reinterpret_cast<const void*>(grid_stream<true, 4, 256, 4, 0, 128>)
-                : reinterpret_cast<const void*>(grid_stream<false, 4, 256, 4, 0, 128>),
-            256, 0, 8 * 128 * sizeof(uint4)};
-  if (sh == 2)
-    return {inl ? reinterpret_cast<const void*>(grid_stream<true, 4, 1024, 1, kHotLog, 64>)
-                : reinterpret_cast<const void*>(grid_stream<false, 4, 1024, 1, kHotLog, 64>),
-            1024, kHotLog, 32 * 64 * sizeof(uint4) + c14};
-  return {inl ? reinterpret_cast<const void*>(grid_stream<true, 4, 1024, 1, 0, 128>)
-              : reinterpret_cast<const void*>(grid_stream<false, 4, 1024, 1, 0, 128>),
-          1024, 0, 32 * 128 * sizeof(uint4)};
+  switch ((flags >> 20) & 7u) {
+    case 1: return shape_of<8, 2, 1024, 1, 0, 128>(inl);
+    case 2: return shape_of<4, 4, 256, 4, 0, 128>(inl);
+    case 3: return shape_of<4, 4, 1024, 1, kHotLog, 64>(inl);
+    case 4: return shape_of<8, 2, 1024, 1, kHotLog, 64>(inl);
+    default: return shape_of<4, 4, 1024, 1, 0, 128>(inl);
+  }
 }
 
 using PersistentFn = void (*)(Args);
