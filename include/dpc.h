@@ -172,9 +172,11 @@ typedef struct dpc_launch_cfg {
 #define DPC_CFG_GRID_CDP 1 /* grid variant: last block launches the child via
                               CDP2 (else: one persistent cooperative kernel
                               with a device-wide barrier) */
-#define DPC_CFG_GRID_CHUNKED 2 /* SpMV persistent grid variant, comparison form:
-                                  drain fixed-size chunk items warp by warp
-                                  instead of the stream-balanced drain */
+#define DPC_CFG_GRID_CHUNKED 2 /* persistent grid variant, comparison forms: SpMV
+                                  drains fixed-size chunk items warp by warp
+                                  instead of the stream-balanced drain; SSSP
+                                  takes two device-wide barriers per level
+                                  (insert | drain) instead of one */
 #define DPC_CFG_GRID_ASYNC 8 /* GC / SSSP persistent grid variant: asynchronous
                                 worklist (device FIFO, no barrier between
                                 rounds) instead of round-synchronous grid

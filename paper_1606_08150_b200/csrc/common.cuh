@@ -50,6 +50,12 @@ struct Pool {
   unsigned cap;
 };
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned warp_in_block() { return threadIdx.x >> 5; }
 
@@ -149,6 +155,15 @@ struct BlockQueue {
       gdst[gs] = v;
     }
   }
+  // Appends v unless the queue is full (then the caller places it itself).
+  __device__ __forceinline__ bool try_push(unsigned v) {
+    cooperative_groups::coalesced_group g = cooperative_groups::coalesced_threads();
+    unsigned s = 0;
+    if (g.thread_rank() == 0) s = atomicAdd(&n, g.size());
+    s = g.shfl(s, 0) + g.thread_rank();
+    if (s < CAP) items[s] = v;
+    return s < CAP;
+  }
   // All threads of the block call (uniform control flow).
   __device__ __forceinline__ void flush(unsigned* gcount, unsigned* gdst) {
     __syncthreads();
@@ -214,10 +229,41 @@ __device__ __forceinline__ void soft_grid_barrier(unsigned* count) {
     __threadfence();
     atomicAdd(count, 1u);
     unsigned seen;
+    const unsigned long long t0 = global_ns();
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(count) : "memory");
       if (seen < gridDim.x) __nanosleep(20);
+      if (global_ns() - t0 > 2000000000ull) break;  // watchdog: never hang the device
     } while (seen < gridDim.x);
+  }
+  __syncthreads();
+}
+
+// Reusable device-wide barrier (generation counting): `count` and `gen` are
+// zero at kernel start; the last block to arrive resets the count and bumps
+// the generation the others wait on.
+__device__ __forceinline__ void soft_grid_sync(unsigned* count, unsigned* gen, unsigned* watchdog) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g0;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gen) : "memory");
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *reinterpret_cast<volatile unsigned*>(count) = 0;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      unsigned g;
+      const unsigned long long t0 = global_ns();
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+        if (g == g0) __nanosleep(20);
+        if (global_ns() - t0 > 2000000000ull) {  // watchdog: a block never arrived
+          atomicOr(watchdog, 4u);
+          break;
+        }
+      } while (g == g0);
+    }
   }
   __syncthreads();
 }
@@ -234,11 +280,6 @@ __device__ __forceinline__ void note_launch(RunHeader* hdr) {
   }
 }
 
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 __host__ __device__ __forceinline__ unsigned ceil_div(unsigned a, unsigned b) { return (a + b - 1) / b; }
 

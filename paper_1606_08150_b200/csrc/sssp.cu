@@ -77,7 +77,11 @@ struct Args {
   uint2* sendbuf;          // [world][sendcap] {global vertex, distance}
   unsigned* sendcnt;       // [world]
   unsigned sendcap;
+  unsigned coop;           // grid_persistent1: cooperative launch (grid.sync) vs soft barrier
+  unsigned classify;       // grid_persistent1: next-level vertices are classified at push time
 };
+
+__device__ void spill_classify(const Args& a, unsigned it, unsigned v);
 
 // Per-block state every relaxing kernel carries in shared memory.
 struct Block {
@@ -131,8 +135,25 @@ __device__ __forceinline__ void relax(const Args& a, unsigned it, Block& s, unsi
   }
   if (nd < __ldcg(a.dist + v)) {
     unsigned old = atomicMin(a.dist + v, nd);
-    if (nd < old && atomicExch(a.stamp + v, it + 1) != it + 1)
-      s.q.push(v, next_count(a, it), next_front(a, it));
+    if (nd < old && atomicExch(a.stamp + v, it + 1) != it + 1) {
+      if (!a.classify) s.q.push(v, next_count(a, it), next_front(a, it));
+      else if (!s.q.try_push(v)) spill_classify(a, it, v);
+    }
+  }
+}
+
+// One-barrier form, shared queue full: classify v for level it+1 right here
+// (heavy -> chunk items in pool half (it+1) % 2, light -> next list).
+__device__ __noinline__ void spill_classify(const Args& a, unsigned it, unsigned v) {
+  const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+  const unsigned nxt = (it + 1) % 3;
+  if (e - b > a.threshold) {
+    const unsigned nch = dev::nchunks(e - b, a.chunk);
+    const unsigned at = atomicAdd(&a.ctr->pool[nxt], nch);
+    const dev::Pool p{a.pool.items + ((it + 1) % 2) * a.pool.cap, a.pool.cap};
+    dev::write_chunks(p, a.hdr, at, v, b, e, a.chunk);
+  } else {
+    next_front(a, it)[atomicAdd(&a.ctr->fsize[nxt], 1u)] = v;
   }
 }
 
@@ -178,6 +199,16 @@ __global__ void __launch_bounds__(256) init_kernel(Args a, unsigned source) {
     a.ctr->fsize[1] = a.ctr->fsize[2] = 0;
     a.ctr->pool[0] = a.ctr->pool[1] = a.ctr->pool[2] = 0;
     a.ctr->iters = 0;
+    if (mine && a.classify) {  // one-barrier form: a heavy source starts as chunk items
+      const unsigned b = a.rowptr[ls], e = a.rowptr[ls + 1];
+      if (e - b > a.threshold) {
+        const dev::Pool p{a.pool.items, a.pool.cap};
+        const unsigned nch = dev::nchunks(e - b, a.chunk);
+        dev::write_chunks(p, a.hdr, 0, ls, b, e, a.chunk);
+        a.ctr->pool[0] = nch;
+        a.ctr->fsize[0] = 0;
+      }
+    }
   }
 }
 
@@ -413,6 +444,87 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iter
   if (gtid == 0) a.ctr->iters = it;
 }
 
+// Level-synchronous persistent form with ONE device-wide barrier per level:
+// the consolidation of level it+1 happens while level it is flushed.  A
+// block's queued next-frontier vertices are classified at flush time: heavy
+// ones become chunk items of the next level right away (pool half
+// (it+1) % 2), light ones go to the next frontier list.  So after the
+// barrier a level needs no insert phase: every warp relaxes its share of the
+// light list (warp-cooperative) and drains its share of the chunk items in
+// the same pass.  (Vertices spilled past the shared queue land in the list
+// and are relaxed warp-cooperatively whatever their degree.)
+__device__ __forceinline__ void flush_classify(const Args& a, unsigned it, Block& s, unsigned half) {
+  __syncthreads();
+  const unsigned n = min(s.q.n, kQueue);
+  const unsigned nxt = (it + 1) % 3;
+  for (unsigned base = 0; base < n; base += blockDim.x) {  // uniform trip count
+    const unsigned i = base + threadIdx.x;
+    unsigned v = 0, b = 0, e = 0, want = 0, light = 0;
+    if (i < n) {
+      v = s.q.items[i];
+      b = __ldg(a.rowptr + v);
+      e = __ldg(a.rowptr + v + 1);
+      if (e - b > a.threshold) want = dev::nchunks(e - b, a.chunk);
+      else light = 1;
+    }
+    dev::block_add_u64(&s.work, want ? e - b : 0u);  // heavy edges are relaxed next level (all lanes)
+    unsigned lbase, ltot;
+    const unsigned lat = dev::block_reserve(&a.ctr->fsize[nxt], light, &lbase, &ltot);
+    if (light) next_front(a, it)[lat] = v;
+    unsigned cbase, ctot;
+    const unsigned cat = dev::block_reserve(&a.ctr->pool[nxt], want, &cbase, &ctot);
+    if (want) {
+      const dev::Pool p{a.pool.items + half * a.pool.cap, a.pool.cap};
+      dev::write_chunks(p, a.hdr, cat, v, b, e, a.chunk);
+    }
+  }
+  if (threadIdx.x == 0) {
+    s.q.n = 0;
+    if (s.work) atomicAdd(&a.hdr->work, s.work);
+    s.work = 0;
+  }
+  __syncthreads();
+}
+
+// a.pool.cap = capacity of ONE half of the pool (the host allocates two).
+__global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_iters) {
+  __shared__ Block s;
+  const unsigned stride = gridDim.x * blockDim.x;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  block_begin(s);
+  unsigned it = 0;
+  for (; it < max_iters; it++) {
+    const unsigned fs = *reinterpret_cast<volatile unsigned*>(&a.ctr->fsize[it % 3]);
+    const unsigned pc = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[it % 3]), a.pool.cap);
+    if (fs == 0 && pc == 0) break;
+    if (gtid == 0) {  // the counters level it+1 produces into were last read at level it-1
+      atomicAdd(&a.hdr->aux1, pc);
+      atomicMax(&a.hdr->count, pc);
+      a.ctr->fsize[(it + 2) % 3] = 0;
+      a.ctr->pool[(it + 2) % 3] = 0;
+    }
+    // the level's light list, warp-cooperatively (any degree)
+    for (unsigned base = blockIdx.x * blockDim.x; base < fs; base += stride) {
+      const unsigned i = base + threadIdx.x;
+      unsigned b = 0, du = 0, deg = 0;
+      if (i < fs) {
+        const unsigned u = cur_front(a, it)[i];
+        b = __ldg(a.rowptr + u);
+        deg = __ldg(a.rowptr + u + 1) - b;
+        du = __ldcg(a.dist + u);
+      }
+      dev::block_add_u64(&s.work, deg);
+      warp_light_relax(a, it, s, b, du, deg);
+    }
+    // the level's chunk items (inserted while the previous level flushed)
+    drain_items(a, it, s, a.pool.items + (it % 2) * a.pool.cap, pc, gtid >> 5, stride >> 5);
+    flush_classify(a, it, s, (it + 1) % 2);
+    if (a.coop) cg::this_grid().sync();
+    else dev::soft_grid_sync(&a.hdr->ticket, &a.hdr->iter, &a.hdr->overflow);
+  }
+  if (gtid == 0) a.ctr->iters = it;
+}
+
 // ---------------------------------------------------------------------------
 // Asynchronous grid consolidation (DPC_CFG_GRID_ASYNC; single GPU).  Measured
 // slower than the level-synchronous persistent form on R-MAT SSSP (the
@@ -612,6 +724,8 @@ static dpc_status sssp_setup(dpc_ctx* ctx, dpc_dgraph* g, const dpc_launch_cfg* 
   a->fsize = 1;
   a->r0 = 0;
   a->rows_per_rank = 0xffffffffu;
+  a->classify = 0;
+  a->coop = 1;
   if (c->variant != DPC_FLAT && c->variant != DPC_BASIC) {
     st = ensure_pool(g, pool_need(g, c->threshold, c->chunk));
     if (st != DPC_OK) return st;
@@ -670,6 +784,17 @@ extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t sourc
   dpc_status st = sssp_setup(ctx, g, cfg, &a, &c);
   if (st != DPC_OK) return st;
   cudaStream_t s = ctx->stream;
+  const bool one_barrier = c.variant == DPC_GRID && c.grid_persistent &&
+                           !(c.flags & (DPC_CFG_GRID_ASYNC | DPC_CFG_GRID_CHUNKED));
+  if (one_barrier) {
+    // two pool halves: level it drains one while its flush fills the other
+    const uint64_t half = pool_need(g, c.threshold, c.chunk) + 1;
+    st = ensure_pool(g, 2 * half);
+    if (st != DPC_OK) return st;
+    a.pool = dev::Pool{g->items, static_cast<unsigned>(half)};
+    a.classify = 1;
+    a.coop = (c.flags & DPC_CFG_COOP_LAUNCH) ? 1u : 0u;
+  }
   const unsigned nb = std::max(1u, dev::ceil_div(a.n, 256u));
   sssp::init_kernel<<<nb, 256, 0, s>>>(a, static_cast<unsigned>(source));
   DPC_CUDA(cudaGetLastError());
@@ -698,6 +823,17 @@ extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t sourc
                                          dim3(blocks), dim3(256), args, 0, s));
     host_launches += 1;
     iters = 1;
+  } else if (one_barrier) {
+    const void* fn = reinterpret_cast<const void*>(sssp::grid_persistent1);
+    int blocks = coop_blocks_sssp(ctx, fn, 256);
+    unsigned max_iters = a.n + 1;
+    void* args[] = {&a, &max_iters};
+    if (a.coop) DPC_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(256), args, 0, s));
+    else DPC_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(256), args, 0, s));
+    host_launches += 1;
+    DPC_CUDA(cudaMemcpyAsync(ctr_host, a.ctr, sizeof(sssp::Ctr), cudaMemcpyDeviceToHost, s));
+    DPC_CUDA(cudaStreamSynchronize(s));
+    iters = ctr_host->iters;
   } else if (c.variant == DPC_GRID && c.grid_persistent) {
     int blocks = coop_blocks_sssp(ctx, reinterpret_cast<const void*>(sssp::grid_persistent), 256);
     unsigned max_iters = a.n + 1;

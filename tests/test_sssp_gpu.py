@@ -87,14 +87,16 @@ def test_sssp_invalid(ctx):
         dpc.run_sssp(g2, 0, "grid", ctx=ctx)
 
 
-@pytest.mark.parametrize("form", ["rounds", "async"])
+@pytest.mark.parametrize("form", ["one_barrier", "one_barrier_soft", "two_barrier", "async"])
 @pytest.mark.parametrize("scale", [10, 14])
 def test_sssp_grid_forms(ctx, orc, form, scale):
     """The persistent grid variant's two forms (level-synchronous default and
     the asynchronous worklist) are bit-exact against Dijkstra, including an
     isolated source and zero-weight edges."""
     g = dpc.gen_rmat(scale, 16, seed=scale + 1, wmin=0, wmax=3)
-    cfg = dpc.launch_cfg("sssp", "grid", grid_async=(form == "async"))
+    cfg = dpc.launch_cfg("sssp", "grid", grid_async=(form == "async"), grid_chunked=(form == "two_barrier"))
+    if form == "one_barrier_soft":
+        cfg.flags &= ~4                      # normal launch + software grid barrier
     for s in (int(np.argmax(g.degrees())), int(np.flatnonzero(g.degrees() == 0)[0])):
         d, met = dpc.run_sssp(g, s, "grid", cfg=cfg, ctx=ctx)
         assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, s))
