@@ -28,6 +28,10 @@
 #include <algorithm>
 #include <cstdlib>
 
+#ifndef BW_CFG
+#define BW_CFG 4
+#endif
+
 #include "common.cuh"
 #include "ctx.h"
 
@@ -562,21 +566,33 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iter
 //     writes the color, then enqueues phase B chunks that release the lower
 //     neighbours (releases must follow the color write)
 // Same coloring as sequential greedy in priority order (see top of file).
-constexpr int kAsyncW = 4;               // edges per lane per step (loads in flight)
-constexpr unsigned kAsyncHeavy = 128;    // edges a single warp takes (one step)
+// Widths measured on config 3: wider steps (16 edges per lane, 512-edge
+// warp tasks) cost registers (72 -> 3 blocks/SM) and ran 35 ms vs 22 ms.
+constexpr int kAsyncW = 4;               // edges per lane per step, light vertices
+constexpr int kAsyncWide = 4;            // edges per lane per step, medium / chunk tasks
+constexpr unsigned kAsyncLight = 128;    // light: one 128-edge step
+constexpr unsigned kAsyncHeavy = 128;    // medium (<= this): one warp
 constexpr unsigned kAsyncChunk = 128;    // edges per heavy chunk task
 constexpr unsigned long long kEmpty = ~0ull;
 
 // Queue counters, one per 128-byte line: thousands of warps poll / bump
 // them, and sharing a line would serialise all of them on one L2 slice.
-constexpr unsigned kTail = 32, kSlots = 64, kColored = 96, kDeadlock = 128, kDone = 160;
+constexpr unsigned kTail = 32, kSlots = 64, kColored = 96, kDeadlock = 128, kDone = 160, kBTail = 192,
+                   kBDone = 224;
+constexpr unsigned kBlockMax = 2048;  // medium vertices (kAsyncHeavy, kBlockMax] go to a block server
+constexpr int kBW = BW_CFG;           // edges per thread per block-server step
 
 struct Async {
-  unsigned long long* q;   // task slots
-  unsigned* qctr;          // [kTail], [kSlots] heavy states used, [kColored] vertices colored
+  unsigned long long* q;   // warp queue: light vertices and chunk tasks
+  unsigned* qctr;          // counters, one per 128-byte line (see k* offsets)
   unsigned qcap;
   unsigned* hstate;        // kStateWords per heavy vertex in flight
   unsigned hcap;
+  unsigned long long* bq;  // block queue: medium vertices, served by a whole block
+  unsigned bqcap;
+  unsigned char* vclass;   // per vertex: 0 light, 1 medium (block), 2 heavy (chunked)
+  unsigned nbs;            // block servers: blocks [0, nbs)
+  unsigned bmax;           // medium vertices have (kAsyncHeavy, bmax] edges
 };
 
 // Release / acquire primitives (PTX memory model, gpu scope): a color
@@ -604,20 +620,22 @@ __device__ __forceinline__ unsigned long long task(unsigned v, unsigned chunk, u
          (static_cast<unsigned long long>(slot) << (32 + kChunkBits)) | (static_cast<unsigned long long>(phase) << 63);
 }
 
-// Warp-aggregated enqueue of the lanes' tasks (want = true).  All lanes call.
-__device__ __forceinline__ void enqueue(const Args& a, const Async& q, bool want, unsigned long long t) {
+// Warp-aggregated append of the lanes' tasks (want = true) to one queue.
+// All lanes call.
+__device__ __forceinline__ void append(const Args& a, const Async& q, unsigned long long* qq, unsigned cap,
+                                       unsigned tail_off, bool want, unsigned long long t) {
   const unsigned ball = __ballot_sync(kFull, want);
   if (!ball) return;
   const unsigned lane = dev::lane_id();
   unsigned base = 0;
-  if (lane == __ffs(ball) - 1) base = atomicAdd(q.qctr + kTail, __popc(ball));
+  if (lane == __ffs(ball) - 1) base = atomicAdd(q.qctr + tail_off, __popc(ball));
   base = __shfl_sync(kFull, base, __ffs(ball) - 1);
   if (want) {
     const unsigned at = base + __popc(ball & ((1u << lane) - 1u));
-    if (at < q.qcap) {
+    if (at < cap) {
       // the slot store depends on the count-down's returned value, which
       // follows the (fenced) color stores of every higher neighbour
-      *reinterpret_cast<volatile unsigned long long*>(q.q + at) = t;
+      *reinterpret_cast<volatile unsigned long long*>(qq + at) = t;
       if (a.trace && (t >> 32) == 0) a.trace[a.n + static_cast<unsigned>(t)] = dev::global_ns();
     } else {
       atomicOr(&a.hdr->overflow, 1u);
@@ -626,38 +644,53 @@ __device__ __forceinline__ void enqueue(const Args& a, const Async& q, bool want
   }
 }
 
+// Enqueue of tasks: medium vertex tasks go to the block queue, everything
+// else (light vertices, heavy vertices, chunk tasks) to the warp queue.
+__device__ __forceinline__ void enqueue(const Args& a, const Async& q, bool want, unsigned long long t,
+                                        unsigned cls = 0) {
+  const bool blk = want && cls == 1 && (t >> 32) == 0;
+  append(a, q, q.q, q.qcap, kTail, want && !blk, t);
+  append(a, q, q.bq, q.bqcap, kBTail, blk, t);
+}
+
 // Lower neighbours of a colored vertex v among edges [b, e): release each
 // (relaxed count-down: the color store was fenced once before), and keep ONE
 // vertex that became ready as this warp's next task -- work-first: the
 // releaser serves it itself, without a queue round trip -- enqueueing the
 // rest.  Four edges per lane per step.  Returns the kept task or kEmpty.
 // All lanes call.
+// KEEPX: the class this server may not keep (1 for warps: medium vertices
+// belong to block servers; 0 for block servers: light ones to warps).
+template <int W, unsigned KEEPX = 1>
 __device__ __forceinline__ unsigned long long release_range(const Args& a, const Async& q, unsigned v,
                                                             unsigned long long pv, unsigned b, unsigned e,
                                                             unsigned long long keep) {
-  for (unsigned k0 = b; k0 < e; k0 += 32 * kAsyncW) {
-    unsigned u[kAsyncW];
-    bool low[kAsyncW], ready[kAsyncW];
+  for (unsigned k0 = b; k0 < e; k0 += 32 * W) {
+    unsigned u[W];
+    bool low[W], ready[W];
 #pragma unroll
-    for (int j = 0; j < kAsyncW; j++) {
+    for (int j = 0; j < W; j++) {
       const unsigned k = k0 + 32 * j + dev::lane_id();
       u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
     }
 #pragma unroll
-    for (int j = 0; j < kAsyncW; j++) low[j] = u[j] != v && !higher(u[j], prio(a, u[j]), v, pv);
+    for (int j = 0; j < W; j++) low[j] = u[j] != v && !higher(u[j], prio(a, u[j]), v, pv);
+    unsigned cls[W];
 #pragma unroll
-    for (int j = 0; j < kAsyncW; j++) ready[j] = low[j] && atomicSub(a.cnt + u[j], 1u) == 1u;
+    for (int j = 0; j < W; j++) cls[j] = low[j] ? q.vclass[u[j]] : 0u;  // issued beside the count-downs
 #pragma unroll
-    for (int j = 0; j < kAsyncW; j++) {
-      if (keep == kEmpty) {
-        const unsigned ball = __ballot_sync(kFull, ready[j]);
+    for (int j = 0; j < W; j++) ready[j] = low[j] && atomicSub(a.cnt + u[j], 1u) == 1u;
+#pragma unroll
+    for (int j = 0; j < W; j++) {
+      if (keep == kEmpty) {  // work-first: keep one this server can take
+        const unsigned ball = __ballot_sync(kFull, ready[j] && cls[j] != KEEPX);
         if (ball) {
           const unsigned l = __ffs(ball) - 1;
           keep = task(__shfl_sync(kFull, u[j], l), 0, 0, 0);
           if (dev::lane_id() == l) ready[j] = false;
         }
       }
-      enqueue(a, q, ready[j], task(u[j], 0, 0, 0));
+      enqueue(a, q, ready[j], task(u[j], 0, 0, 0), cls[j]);
     }
   }
   return keep;
@@ -665,21 +698,22 @@ __device__ __forceinline__ unsigned long long release_range(const Args& a, const
 
 // ORs the colors of v's higher neighbours among [b, e) into the warp bitmap
 // (colors < 32 * kVW); returns true (warp-uniform) if a larger color was seen.
+template <int W>
 __device__ __forceinline__ bool gather_colors(const Args& a, unsigned v, unsigned long long pv, unsigned b,
                                               unsigned e, unsigned* wbm) {
   bool over = false;
-  for (unsigned k0 = b; k0 < e; k0 += 32 * kAsyncW) {
-    unsigned u[kAsyncW];
-    int c[kAsyncW];
+  for (unsigned k0 = b; k0 < e; k0 += 32 * W) {
+    unsigned u[W];
+    int c[W];
 #pragma unroll
-    for (int j = 0; j < kAsyncW; j++) {
+    for (int j = 0; j < W; j++) {
       const unsigned k = k0 + 32 * j + dev::lane_id();
       u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
     }
 #pragma unroll
-    for (int j = 0; j < kAsyncW; j++) c[j] = (u[j] != v && higher(u[j], prio(a, u[j]), v, pv)) ? __ldcg(a.color + u[j]) : -1;
+    for (int j = 0; j < W; j++) c[j] = (u[j] != v && higher(u[j], prio(a, u[j]), v, pv)) ? __ldcg(a.color + u[j]) : -1;
 #pragma unroll
-    for (int j = 0; j < kAsyncW; j++) {
+    for (int j = 0; j < W; j++) {
       if (c[j] >= static_cast<int>(kVW * 32)) over = true;
       else if (c[j] >= 0) atomicOr(wbm + (c[j] >> 5), 1u << (c[j] & 31));
     }
@@ -737,7 +771,8 @@ __device__ unsigned long long serve(const Args& a, const Async& q, Block& s, uns
   if (e - b <= kAsyncHeavy && !phase_b && chunk == 0 && slot == 0) {
     wbm[lane] = 0;
     __syncwarp();
-    const bool over = gather_colors(a, v, pv, b, e, wbm);
+    const bool over = e - b <= kAsyncLight ? gather_colors<kAsyncW>(a, v, pv, b, e, wbm)
+                                           : gather_colors<kAsyncWide>(a, v, pv, b, e, wbm);
     __syncwarp();
     int c = bitmap_mex(wbm[lane]);
     if (c < 0 || over) {
@@ -746,7 +781,8 @@ __device__ unsigned long long serve(const Args& a, const Async& q, Block& s, uns
     }
     __syncwarp();
     set_color_async(a, q, s, v, c);
-    return release_range(a, q, v, pv, b, e, kEmpty);
+    return e - b <= kAsyncLight ? release_range<kAsyncW>(a, q, v, pv, b, e, kEmpty)
+                                : release_range<kAsyncWide>(a, q, v, pv, b, e, kEmpty);
   }
   const unsigned nch = (e - b + kAsyncChunk - 1) / kAsyncChunk;
   if (!phase_b && chunk == 0 && slot == 0) {
@@ -771,7 +807,7 @@ __device__ unsigned long long serve(const Args& a, const Async& q, Block& s, uns
   if (!phase_b) {
     wbm[lane] = 0;
     __syncwarp();
-    const bool over = gather_colors(a, v, pv, cb, ce, wbm);
+    const bool over = gather_colors<kAsyncWide>(a, v, pv, cb, ce, wbm);
     __syncwarp();
     const unsigned wv = wbm[lane];
     if (wv) atomicOr(st + lane, wv);
@@ -787,9 +823,85 @@ __device__ unsigned long long serve(const Args& a, const Async& q, Block& s, uns
     // phase B: chunk 0 released by this warp right away, the rest queued
     for (unsigned c0 = 0; c0 < nch; c0 += 32)
       enqueue(a, q, c0 + lane < nch && c0 + lane > 0, task(v, c0 + lane, slot, 1));
-    return release_range(a, q, v, pv, b, min(e, b + kAsyncChunk), kEmpty);
+    return release_range<kAsyncWide>(a, q, v, pv, b, min(e, b + kAsyncChunk), kEmpty);
   }
-  return release_range(a, q, v, pv, cb, ce, kEmpty);
+  return release_range<kAsyncWide>(a, q, v, pv, cb, ce, kEmpty);
+}
+
+// Whether the asynchronous drain is over (thread-level; call from one lane):
+// every vertex colored, a fault raised, or both queues drained with
+// vertices left uncolored (asymmetric input).  done counters are read
+// before the tails: equal pairs mean nothing was in flight in between.
+__device__ bool async_over(const Args& a, const Async& q, unsigned long long* since) {
+  volatile unsigned* vq = q.qctr;
+  if (vq[kColored] >= a.n || vq[kDeadlock]) return true;
+  const unsigned long long now = dev::global_ns();
+  if (!*since) *since = now;
+  if (now - *since > 2000000000ull) {  // watchdog: the reference's deadlock fault (sim.hpp:946-955)
+    atomicOr(&a.hdr->overflow, 4u);
+    atomicExch(q.qctr + kDeadlock, 1u);
+    return true;
+  }
+  const unsigned dl = vq[kDone], db = vq[kBDone];
+  if (dl == vq[kTail] && db == vq[kBTail] && vq[kColored] < a.n) {
+    atomicOr(&a.hdr->overflow, 8u);
+    atomicExch(q.qctr + kDeadlock, 1u);
+    return true;
+  }
+  return false;
+}
+
+// A medium vertex served by a whole block (block-level consolidation of its
+// edge loop): 256 threads gather the higher neighbours' colors into a
+// shared bitmap, warp 0 takes the mex and writes the color, then every warp
+// releases its share of the lower neighbours.  All threads call.
+__device__ void block_serve(const Args& a, const Async& q, Block& s, unsigned v, unsigned* sbm, unsigned* sflag) {
+  const unsigned tid = threadIdx.x;
+  const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+  const unsigned long long pv = prio(a, v);
+  if (tid < kVW) sbm[tid] = 0;
+  if (tid == 0) *sflag = 0;
+  __syncthreads();
+  bool over = false;
+  for (unsigned k0 = b; k0 < e; k0 += kBW * blockDim.x) {
+    unsigned u[kBW];
+    int c[kBW];
+#pragma unroll
+    for (int j = 0; j < kBW; j++) {
+      const unsigned k = k0 + j * blockDim.x + tid;
+      u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
+    }
+#pragma unroll
+    for (int j = 0; j < kBW; j++) c[j] = (u[j] != v && higher(u[j], prio(a, u[j]), v, pv)) ? __ldcg(a.color + u[j]) : -1;
+#pragma unroll
+    for (int j = 0; j < kBW; j++) {
+      if (c[j] >= static_cast<int>(kVW * 32)) over = true;
+      else if (c[j] >= 0) atomicOr(sbm + (c[j] >> 5), 1u << (c[j] & 31));
+    }
+  }
+  if (over) atomicOr(sflag, 1u);
+  __syncthreads();
+  if (tid < 32) {
+    int c = bitmap_mex(sbm[tid]);
+    if (c < 0) c = mex_windowed(a, v, pv);
+    set_color_async(a, q, s, v, c);
+  }
+  __syncthreads();
+  for (unsigned k0 = b; k0 < e; k0 += kBW * blockDim.x) {
+    unsigned u[kBW], cls[kBW];
+    bool low[kBW], ready[kBW];
+#pragma unroll
+    for (int j = 0; j < kBW; j++) {
+      const unsigned k = k0 + j * blockDim.x + tid;
+      u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
+      low[j] = u[j] != v && !higher(u[j], prio(a, u[j]), v, pv);
+      cls[j] = low[j] ? q.vclass[u[j]] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kBW; j++) ready[j] = low[j] && atomicSub(a.cnt + u[j], 1u) == 1u;
+#pragma unroll
+    for (int j = 0; j < kBW; j++) enqueue(a, q, ready[j], task(u[j], 0, 0, 0), cls[j]);
+  }
 }
 
 __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
@@ -807,6 +919,7 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
       e = __ldg(a.rowptr + v + 1);
       if (e - b <= a.threshold) a.cnt[v] = count_higher(a, v, b, e, 1, 0);
       else want = dev::nchunks(e - b, a.chunk);
+      q.vclass[v] = e - b <= kAsyncHeavy ? 0 : (e - b <= q.bmax && q.nbs ? 1 : 2);
     }
     unsigned bbase, bt;
     unsigned at = dev::block_reserve(&a.ctr->pool[0], want, &bbase, &bt);
@@ -820,16 +933,46 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
   for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
     const unsigned v = base + threadIdx.x;
     const bool ready = v < a.n && __ldcg(a.cnt + v) == 0;
-    enqueue(a, q, ready, task(v, 0, 0, 0));
+    enqueue(a, q, ready, task(v, 0, 0, 0), ready ? q.vclass[v] : 0u);
   }
   grid.sync();
+  if (blockIdx.x < q.nbs) {
+    // block servers: block-queue position p is served by block p mod nbs
+    __shared__ unsigned long long s_task;
+    __shared__ unsigned s_bm[kVW], s_flag;
+    for (unsigned p = blockIdx.x; p < q.bqcap; p += q.nbs) {
+      if (threadIdx.x == 0) {
+        unsigned long long t = kEmpty, since = 0;
+        unsigned spins = 0;
+        while (true) {
+          t = *reinterpret_cast<volatile unsigned long long*>(q.bq + p);
+          if (t != kEmpty) break;
+          if ((++spins & 15) == 0 && async_over(a, q, &since)) break;
+          if (spins > 32) __nanosleep(64);
+        }
+        s_task = t;
+      }
+      __syncthreads();
+      const unsigned long long t = s_task;
+      __syncthreads();
+      if (t == kEmpty) break;
+      if (a.trace && threadIdx.x == 0) a.trace[2ull * a.n + static_cast<unsigned>(t)] = dev::global_ns();
+      block_serve(a, q, s, static_cast<unsigned>(t), s_bm, &s_flag);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(q.qctr + kBDone, 1u);
+      }
+    }
+    block_end(a, 0, s);
+    return;
+  }
   // drain: queue position p is served by warp p mod W, in order (no claim
   // atomics; consecutive tasks land on different warps).  A position is
   // filled by the p-th enqueue, whose producer serves an earlier position,
   // so in-order waiting cannot deadlock.  Stop once every vertex is colored
   // (positions past the last task never fill).
-  const unsigned nwarps = stride >> 5, gw = gtid >> 5;
-  volatile unsigned* vq = q.qctr;
+  const unsigned nwarps = (stride - q.nbs * blockDim.x) >> 5, gw = (gtid - q.nbs * blockDim.x) >> 5;
   for (unsigned p = gw; p < q.qcap; p += nwarps) {
     unsigned long long t = kEmpty;
     unsigned spins = 0;
@@ -839,28 +982,7 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
       t = __shfl_sync(kFull, t, 0);
       if (t != kEmpty) break;
       unsigned fin = 0;
-      if (lane == 0 && (++spins & 15) == 0) {
-        fin = vq[kColored] >= a.n;
-        // watchdog: no progress for 2 s means a lost task -- report the
-        // reference's "deadlock" fault (sim.hpp:946-955) instead of hanging
-        const unsigned long long now = dev::global_ns();
-        if (!since) since = now;
-        if (now - since > 2000000000ull) {
-          atomicOr(&a.hdr->overflow, 4u);
-          atomicExch(q.qctr + kDeadlock, 1u);
-          fin = 1;
-        }
-        if (vq[kDeadlock]) fin = 1;
-        // drained: every queued task served (done read before tail) yet
-        // uncolored vertices remain -- their counts never reach 0, which
-        // only an asymmetric adjacency produces
-        const unsigned d = vq[kDone];
-        if (!fin && d == vq[kTail] && vq[kColored] < a.n) {
-          atomicOr(&a.hdr->overflow, 8u);
-          atomicExch(q.qctr + kDeadlock, 1u);
-          fin = 1;
-        }
-      }
+      if (lane == 0 && (++spins & 15) == 0) fin = async_over(a, q, &since);
       if (__shfl_sync(kFull, fin, 0)) break;
       if (spins > 32) __nanosleep(64);
     }
@@ -957,13 +1079,16 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
     if (heavy + 1 >= (1ull << gc::kSlotBits) || static_cast<uint64_t>(g->max_deg) >= (uint64_t{gc::kAsyncChunk} << gc::kChunkBits))
       return fail(DPC_E_OVERFLOW, "asynchronous GC task encoding exceeded (clear DPC_CFG_GRID_ASYNC)");
     const uint64_t qcap = static_cast<uint64_t>(g->n) + 2 * pool_need(g, gc::kAsyncHeavy, gc::kAsyncChunk) + 32;
-    if (g->gc_q_cap < qcap) {
+    const uint64_t bqcap = static_cast<uint64_t>(g->n) + 32;
+    // one buffer: [warp queue][1 KB counters][block queue][vertex classes]
+    const uint64_t words = qcap + 128 + bqcap + (static_cast<uint64_t>(g->n) + 7) / 8;
+    if (g->gc_q_cap < words) {
       DPC_CUDA(cudaStreamSynchronize(s));
       if (g->gc_q) cudaFree(g->gc_q);
       g->gc_q = nullptr;
       g->gc_q_cap = 0;
-      DPC_CUDA(cudaMalloc(&g->gc_q, sizeof(unsigned long long) * qcap + 1024));
-      g->gc_q_cap = qcap;
+      DPC_CUDA(cudaMalloc(&g->gc_q, sizeof(unsigned long long) * words));
+      g->gc_q_cap = words;
     }
     if (g->gc_hstate_cap < heavy + 1) {
       DPC_CUDA(cudaStreamSynchronize(s));
@@ -973,18 +1098,26 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
       DPC_CUDA(cudaMalloc(&g->gc_hstate, sizeof(unsigned) * gc::kStateWords * (heavy + 1)));
       g->gc_hstate_cap = heavy + 1;
     }
-    gc::Async q;
-    q.q = reinterpret_cast<unsigned long long*>(g->gc_q);
-    q.qctr = reinterpret_cast<unsigned*>(q.q + qcap);  // 128 words after the slots
-    q.qcap = static_cast<unsigned>(qcap);
-    q.hstate = g->gc_hstate;
-    q.hcap = static_cast<unsigned>(g->gc_hstate_cap);
-    DPC_CUDA(cudaMemsetAsync(q.q, 0xff, sizeof(unsigned long long) * qcap, s));
-    DPC_CUDA(cudaMemsetAsync(q.qctr, 0, 1024, s));
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(gc::async_persistent),
                                                   256, 0);
     int blocks = std::max(1, per_sm) * ctx->sms;
+    gc::Async q;
+    q.q = reinterpret_cast<unsigned long long*>(g->gc_q);
+    q.qctr = reinterpret_cast<unsigned*>(q.q + qcap);
+    q.qcap = static_cast<unsigned>(qcap);
+    q.bq = q.q + qcap + 128;
+    q.bqcap = static_cast<unsigned>(bqcap);
+    q.vclass = reinterpret_cast<unsigned char*>(q.bq + bqcap);
+    q.hstate = g->gc_hstate;
+    q.hcap = static_cast<unsigned>(g->gc_hstate_cap);
+    // one block server per SM when there are more blocks per SM to host the
+    // warp servers (flag bit 19 off); flag bit 19: warp servers only
+    q.nbs = (per_sm > 1 && !(c.flags & (1u << 19))) ? static_cast<unsigned>(ctx->sms) : 0u;
+    // experiment switch (flag bits 24-27): medium bound = 256 << k, default kBlockMax
+    q.bmax = (c.flags >> 24) & 15u ? (256u << ((c.flags >> 24) & 15u)) : gc::kBlockMax;
+    DPC_CUDA(cudaMemsetAsync(q.q, 0xff, sizeof(unsigned long long) * (qcap + 128 + bqcap), s));
+    DPC_CUDA(cudaMemsetAsync(q.qctr, 0, 1024, s));
     void* args[] = {&a, &q};
     DPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(gc::async_persistent), dim3(blocks),
                                          dim3(256), args, 0, s));
