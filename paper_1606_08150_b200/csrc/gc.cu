@@ -581,6 +581,14 @@ constexpr unsigned kTail = 32, kSlots = 64, kColored = 96, kDeadlock = 128, kDon
                    kBDone = 224;
 constexpr unsigned kBlockMax = 2048;  // medium vertices (kAsyncHeavy, kBlockMax] go to a block server
 constexpr int kBW = BW_CFG;           // edges per thread per block-server step
+// Idle servers sleep between polls.  ncu counts 9.4G instructions (50 % SM
+// throughput) for the 18 ms config-3 run, mostly polling, yet longer sleeps
+// measured slower (100 ns: 18.2 ms, 400: 18.6, 1500: 19.6): the detection
+// delay on the dependency chain costs more than the issue slots.
+#ifndef POLL_NS
+#define POLL_NS 64
+#endif
+constexpr unsigned kPollNs = POLL_NS;
 
 struct Async {
   unsigned long long* q;   // warp queue: light vertices and chunk tasks
@@ -948,7 +956,7 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
           t = *reinterpret_cast<volatile unsigned long long*>(q.bq + p);
           if (t != kEmpty) break;
           if ((++spins & 15) == 0 && async_over(a, q, &since)) break;
-          if (spins > 32) __nanosleep(64);
+          if (spins > 32) __nanosleep(kPollNs);
         }
         s_task = t;
       }
@@ -984,7 +992,7 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
       unsigned fin = 0;
       if (lane == 0 && (++spins & 15) == 0) fin = async_over(a, q, &since);
       if (__shfl_sync(kFull, fin, 0)) break;
-      if (spins > 32) __nanosleep(64);
+      if (spins > 32) __nanosleep(kPollNs);
     }
     if (t == kEmpty) break;
     // serve it, then the vertices it makes ready first (work-first chain)

@@ -29,6 +29,16 @@ for s in $STAGES; do
         -s 2 -c 1 -f -o gpurun_out/prof_spmv_grid python tools/prof_spmv.py grid --reps 3 \
         > gpurun_out/ncu_full.log 2>&1
       echo "ncu-full rc=$?"; tail -3 gpurun_out/ncu_full.log ;;
+    appsncu)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file gpurun_out/launches_apps.csv python tools/prof_grid_apps.py 2 > gpurun_out/ncu_apps.log 2>&1
+      for k in grid_persistent1 async_persistent; do
+        timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -f \
+          -o gpurun_out/prof_$k python tools/prof_grid_apps.py 2 >> gpurun_out/ncu_apps.log 2>&1
+      done
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tree.*grid_persistent" -s 1 -c 1 -f \
+          -o gpurun_out/prof_tree_grid python tools/prof_grid_apps.py 2 >> gpurun_out/ncu_apps.log 2>&1
+      echo "appsncu rc=$?"; tail -3 gpurun_out/ncu_apps.log ;;
     apps)
       timeout 1200 python tools/prof_apps.py --json gpurun_out/apps.json > gpurun_out/apps.log 2>&1
       echo "apps rc=$?"; tail -c 2000 gpurun_out/apps.log ;;
