@@ -315,6 +315,25 @@ def run_multi_sssp(args, dist, rank, world, ctx, comm, scale, r0, R):
                         "ncclAllReduce frontier size per iteration"}
 
 
+def _ncu_traffic(profile="r01_spmv_grid_stream.txt"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel
+    from the committed `ncu --set full` summary (profiles/), in bytes per
+    launch -- the ncu capture cannot run inside the timed bench."""
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    try:
+        with open(os.path.join(ROOT, "profiles", profile)) as f:
+            for line in f:
+                line = line.strip()
+                if line.startswith(("dram__bytes_read.sum =", "dram__bytes_write.sum =")):
+                    _, val = line.split("=", 1)
+                    num, unit = val.split()
+                    tot += float(num) * units.get(unit, 1)
+    except (OSError, ValueError):
+        return None
+    return int(tot) if tot else None
+
+
 def _peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -444,7 +463,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": 4 * n, "ms_per_step": round(e2e_max, 4),
                 "api": "dpc_spmv_host (C ABI), pinned host x/y, A resident"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(),
+                     "traffic_source": "profiles/r01_spmv_grid_stream.txt (ncu --set full, dram bytes read+write per launch)",
                      "algorithmic_bytes": alg, "kernel": "spmv::grid_stream (whole step)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"},
         "gpu_launches": args.steps * (1 + int(met.child_launch_count)),

@@ -53,6 +53,7 @@ struct dpc_dgraph {
   void* ctr_host = nullptr;   // pinned mirror of ctr
   dpc::dev::RunHeader* hdr = nullptr;  // device counters
   dpc::dev::RunHeader* hdr_host = nullptr;  // pinned mirror
+  bool hdr_clean = false;  // the last run (SpMV stream) left the header zeroed itself
   // consolidation pool
   dpc::dev::Item* items = nullptr;
   unsigned cap = 0;

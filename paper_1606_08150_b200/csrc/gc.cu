@@ -1069,6 +1069,7 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   a.pool = dev::Pool{g->items, g->cap};
   st = ensure_pending_for(ctx, g, c.variant, c.threshold, c.parent_threads);
   if (st != DPC_OK) return st;
+  g->hdr_clean = false;
   st = begin_run(ctx, g->hdr);
   if (st != DPC_OK) return st;
   cudaStream_t s = ctx->stream;

@@ -21,6 +21,9 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "ctx.h"
 
@@ -866,6 +869,104 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
   }
 }
 
+// Window lookup of the general drain path (see stream_drain): fills the
+// lane's CSR index, mask / segment bits and row for the window at pw, and
+// advances ja to the first item of the next window.  All lanes call.
+template <int G, unsigned KB>
+__device__ __forceinline__ void window_lookup(const Args& a, const Stream& st, unsigned ni, unsigned s1,
+                                              uint4* buf, unsigned pw, unsigned& ja, unsigned& bb,
+                                              unsigned& kk, unsigned& info, unsigned& rw) {
+  constexpr unsigned W = 32u * G;
+  const unsigned lane = dev::lane_id();
+  const unsigned lt_mask = (2u << lane) - 1u;
+  if (ja + 33 > bb + KB) {
+    bb = ja;
+    load_items<KB>(a, st, ni, bb, buf);
+  }
+  const unsigned last = min(pw + W, s1) - 1;
+  const unsigned off = buf[ja - bb + lane].x;
+  const unsigned bit = (off > pw && off <= last) ? 1u << ((off - pw) / G) : 0u;
+  const unsigned smask = __reduce_or_sync(kFull, bit);
+  const uint4 it = buf[ja - bb + __popc(smask & lt_mask)];
+  const unsigned q = pw + G * lane;
+  const bool valid = q < s1;
+  const unsigned k = valid ? (it.z & ~(G - 1u)) + (q - it.x) : 0u;
+  const unsigned m = valid ? grp_mask<G>(k, it.z, it.y) : 0u;
+  const unsigned ls = 31 - __clz((smask | 1u) & lt_mask);
+  const bool seg_end = valid && (lane == 31 || (((smask >> 1) >> lane) & 1u) || q + G >= s1);
+  const bool whole = it.x >= pw && it.x + stream_len<G>(it.z, it.y) <= pw + W;
+  kk = k;
+  rw = it.w;
+  info = m | (ls << 16) | (seg_end ? 1u << 21 : 0u) | (whole ? 1u << 22 : 0u);
+  ja += __popc(smask);
+  ja += buf[ja + 1 - bb].x == pw + W ? 1u : 0u;
+}
+
+// Software-pipelined drain (shape bit 23): the window lookups of step s+1
+// (shared-memory work) and an L2 prefetch of its col / val groups run while
+// step s's loads are in flight.  General path only.
+template <int G, int V, unsigned KB, int SLOG>
+__device__ __forceinline__ void stream_drain_pipe(const Args& a, const Stream& st, unsigned ni,
+                                                  unsigned s0, unsigned s1, uint4* buf, const uint2* xc) {
+  constexpr unsigned W = 32u * G;
+  const unsigned lane = dev::lane_id();
+  unsigned lo = 0, hi = ni;
+  while (hi - lo > 1) {
+    const unsigned step = (hi - lo + 31) / 32;
+    const unsigned probe = lo + lane * step;
+    const unsigned v = probe < hi ? __ldcg(&st.seg[probe].x) : 0xffffffffu;
+    const unsigned c = __popc(__ballot_sync(kFull, v <= s0));
+    const unsigned nlo = lo + (c - 1) * step;
+    hi = min(hi, nlo + step);
+    lo = nlo;
+  }
+  unsigned ja = lo, bb = lo;
+  load_items<KB>(a, st, ni, bb, buf);
+  unsigned kk[V], info[V], rw[V];
+#pragma unroll
+  for (int v = 0; v < V; v++) window_lookup<G, KB>(a, st, ni, s1, buf, s0 + W * v, ja, bb, kk[v], info[v], rw[v]);
+  for (unsigned p0 = s0; p0 < s1; p0 += W * V) {
+    Grp<G> g[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) grp_load<G>(a, kk[v], g[v]);
+    // next step: lookups + L2 prefetch while this step's loads fly
+    unsigned nk[V], ninfo[V], nrw[V];
+    const unsigned pn = p0 + W * V;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      nk[v] = 0, ninfo[v] = 0, nrw[v] = 0;
+      if (pn < s1) {
+        window_lookup<G, KB>(a, st, ni, s1, buf, pn + W * v, ja, bb, nk[v], ninfo[v], nrw[v]);
+        if (ninfo[v] & 0xffffu) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.col + nk[v]));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.val + nk[v]));
+        }
+      }
+    }
+    float sv[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) sv[v] = grp_dot<G, SLOG>(a, g[v], info[v] & 0xffffu, xc);
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      if (p0 + W * v < s1) {
+        const unsigned ls = (info[v] >> 16) & 31u;
+        float t = sv[v];
+#pragma unroll
+        for (unsigned d = 1; d < 32; d <<= 1) {
+          const float u = __shfl_up_sync(kFull, t, d);
+          if (lane >= ls + d) t += u;
+        }
+        if (info[v] & (1u << 21)) {
+          if (info[v] & (1u << 22)) a.y[rw[v]] = t;
+          else atomicAdd(a.y + rw[v], t);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; v++) kk[v] = nk[v], info[v] = ninfo[v], rw[v] = nrw[v];
+  }
+}
+
 // Persistent grid-consolidated SpMV.
 //   insert: 256-row tiles are dealt to blocks round-robin (tile k*G + b of a
 //     round goes to block b, row = lane), kRound tiles per thread per round.
@@ -878,7 +979,7 @@ __device__ __forceinline__ void stream_drain(const Args& a, const Stream& st, un
 //     PAPER.md:244-250; legal because a cooperative launch co-schedules
 //     the whole grid)
 //   drain: stream-balanced, every warp the same number of positions.
-template <bool INLINE, int G, int V, int NT, int MINB, int SLOG, unsigned KB>
+template <bool INLINE, int G, int V, int NT, int MINB, int SLOG, unsigned KB, bool PIPE = false>
 __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
   constexpr unsigned kWin = 32u * G;
   constexpr int NW = NT / 32;
@@ -962,22 +1063,44 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
   const unsigned long long per = ((static_cast<unsigned long long>(total) + nw - 1) / nw + kWin - 1) /
                                  kWin * kWin;
   const unsigned long long s0 = static_cast<unsigned long long>(gw) * per;
-  if (ni > 0 && s0 < total && !(a.xflags & 1u))
+  if (ni > 0 && s0 < total && !(a.xflags & 1u) && PIPE)
+    stream_drain_pipe<G, V, KB, SLOG>(a, st, ni, static_cast<unsigned>(s0),
+                                      static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
+                                      s_items + wib * KB, s_cache);
+  else if (ni > 0 && s0 < total && !(a.xflags & 1u))
     stream_drain<G, V, KB, SLOG>(a, st, ni, static_cast<unsigned>(s0),
                               static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
                               s_items + wib * KB, s_cache);
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&a.hdr->t[2], dev::global_ns());
+  if (threadIdx.x == 0) {
+    // the last block out stamps the end and zeroes the counters of this run
+    // (packed reservation, barrier count, exit ticket): the next run needs
+    // no memset of the header
+    __threadfence();
+    if (atomicAdd(&a.hdr->aux0, 1u) == gridDim.x - 1) {
+      a.hdr->t[2] = dev::global_ns();
+      *st.sctr = 0;
+      a.hdr->ticket = 0;
+      a.hdr->aux0 = 0;
+      __threadfence();
+    }
+  }
 }
 
 // Stream kernel shapes (dpc_launch_cfg.flags bits 20-22), measured on config 2
-// (tools/prof_spmv.py --burst; the x gathers, not HBM, bound all of them):
-//   0: groups of 4 positions per lane, 4 windows per step, 1024 threads x 1
-//      block/SM (default, best)
-//   1: groups of 8, 2 windows per step, 1024 threads
-//   2: groups of 4, 256 threads x 4 blocks/SM
-//   3: groups of 4, 1024 threads, hot-column x cache of 2^14 slots
-//   4: groups of 8, 1024 threads, hot-column x cache
+// (tools/prof_spmv.py --burst 10; the x gathers and the per-step latency
+// chain, not HBM, bound all of them):
+//   0: software-pipelined drain (step s+1's window lookups and an L2
+//      prefetch of its col / val groups run under step s's loads), groups of
+//      4 positions per lane, 2 windows per step, 1024 threads x 1 block/SM
+//      (default: 84.0 us vs 90.1 us for shape 6 on the same box)
+//   1: groups of 8, 2 windows per step, not pipelined
+//   2: groups of 4, 4 windows, 256 threads x 4 blocks/SM
+//   3: groups of 4, 4 windows, hot-column x cache of 2^14 slots
+//   4: groups of 8, 2 windows, hot-column x cache
+//   5: pipelined, groups of 4, 4 windows (spills)
+//   6: groups of 4, 4 windows, not pipelined
+//   7: pipelined, groups of 4, 3 windows
 struct StreamShape {
   const void* fn;
   int threads;
@@ -986,11 +1109,11 @@ struct StreamShape {
   size_t smem;  // dynamic shared memory bytes
 };
 constexpr int kHotLog = 14;
-template <int G, int V, int NT, int MINB, int SLOG, unsigned KB>
+template <int G, int V, int NT, int MINB, int SLOG, unsigned KB, bool PIPE = false>
 static StreamShape shape_of(bool inl) {
   const size_t cache = SLOG ? sizeof(uint2) << SLOG : 0;
-  return {inl ? reinterpret_cast<const void*>(grid_stream<true, G, V, NT, MINB, SLOG, KB>)
-              : reinterpret_cast<const void*>(grid_stream<false, G, V, NT, MINB, SLOG, KB>),
+  return {inl ? reinterpret_cast<const void*>(grid_stream<true, G, V, NT, MINB, SLOG, KB, PIPE>)
+              : reinterpret_cast<const void*>(grid_stream<false, G, V, NT, MINB, SLOG, KB, PIPE>),
           NT, SLOG, G, (NT / 32) * KB * sizeof(uint4) + cache};
 }
 static StreamShape stream_shape(bool inl, unsigned flags) {
@@ -999,7 +1122,10 @@ static StreamShape stream_shape(bool inl, unsigned flags) {
     case 2: return shape_of<4, 4, 256, 4, 0, 128>(inl);
     case 3: return shape_of<4, 4, 1024, 1, kHotLog, 64>(inl);
     case 4: return shape_of<8, 2, 1024, 1, kHotLog, 64>(inl);
-    default: return shape_of<4, 4, 1024, 1, 0, 128>(inl);
+    case 5: return shape_of<4, 4, 1024, 1, 0, 128, true>(inl);
+    case 6: return shape_of<4, 4, 1024, 1, 0, 128>(inl);
+    case 7: return shape_of<4, 3, 1024, 1, 0, 128, true>(inl);
+    default: return shape_of<4, 2, 1024, 1, 0, 128, true>(inl);
   }
 }
 
@@ -1084,6 +1210,31 @@ static dpc_status ensure_xhot(dpc_ctx* ctx, dpc_dgraph* g, int slog) {
   return DPC_OK;
 }
 
+// Resident blocks of a stream kernel shape (dynamic shared memory attribute
+// set and occupancy queried once per function and device, then cached: both
+// are host API calls on the per-step path otherwise).
+static int stream_blocks(dpc_ctx* ctx, const spmv::StreamShape& sh) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(sh.fn, ctx->device);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem)) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sh.fn, sh.threads, sh.smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int nb = per_sm * ctx->sms;
+  cache[key] = nb;
+  return nb;
+}
+
 static int coop_blocks(dpc_ctx* ctx, const void* fn, int threads, size_t smem = 0) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) {
@@ -1140,8 +1291,13 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
                                           : g->cap};
   st = ensure_pending_for(ctx, g, c.variant, c.threshold, c.parent_threads);
   if (st != DPC_OK) return st;
-  st = begin_run(ctx, g->hdr);
-  if (st != DPC_OK) return st;
+  // the stream kernel zeroes its header counters on exit (its last block),
+  // so back-to-back stream runs need no per-run memset
+  if (!(use_stream && g->hdr_clean && !met)) {
+    st = begin_run(ctx, g->hdr);
+    if (st != DPC_OK) return st;
+  }
+  g->hdr_clean = false;
   const unsigned blocks = std::max(1u, dev::ceil_div(a.n, 256u));
   cudaStream_t s = ctx->stream;
   if (a.n > 0) {
@@ -1153,8 +1309,8 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
       case DPC_GRID:
         if (use_stream) {
           const spmv::StreamShape sh = spmv::stream_shape(c.threshold > 0, c.flags);
-          DPC_CUDA(cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(sh.smem)));
+          const int nb = stream_blocks(ctx, sh);
+          if (nb <= 0) return fail(DPC_E_CUDA, "stream kernel does not fit on the device");
           if (sh.slog > 0) {
             st = ensure_xhot(ctx, g, sh.slog);
             if (st != DPC_OK) return st;
@@ -1163,7 +1319,6 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
           sa.xhot_val = g->xhot_val;
           // one block per resident slot; all co-resident, so a normal launch
           // with the software grid barrier is safe (cooperative on request)
-          int nb = coop_blocks(ctx, sh.fn, sh.threads, sh.smem);
           a.coop = (c.flags & DPC_CFG_COOP_LAUNCH) ? 1u : 0u;
           void* args[] = {&a, &sa};
           if (a.coop) {
@@ -1171,6 +1326,7 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
           } else {
             DPC_CUDA(cudaLaunchKernel(sh.fn, dim3(nb), dim3(sh.threads), args, sh.smem, s));
           }
+          g->hdr_clean = true;
         } else if (c.grid_persistent) {
           const void* fn = reinterpret_cast<const void*>(spmv::persistent_fn(c.flags));
           int nb = coop_blocks(ctx, fn, 256);

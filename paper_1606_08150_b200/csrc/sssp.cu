@@ -733,6 +733,7 @@ static dpc_status sssp_setup(dpc_ctx* ctx, dpc_dgraph* g, const dpc_launch_cfg* 
   a->pool = dev::Pool{g->items, g->cap};
   st = ensure_pending_for(ctx, g, c->variant, c->threshold, c->parent_threads);
   if (st != DPC_OK) return st;
+  g->hdr_clean = false;
   return begin_run(ctx, g->hdr);
 }
 

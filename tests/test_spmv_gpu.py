@@ -131,7 +131,7 @@ def _ragged(seed=1, hub=100_003):
     return dpc.csr_from_arrays(rowptr, col, val=val)
 
 
-@pytest.mark.parametrize("shape", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("shape", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("threshold", [0, 3, 7, 31, 32, 100])
 def test_spmv_grid_stream_forms(ctx, orc, shape, threshold):
     """Stream-balanced grid drain: every kernel shape x consolidation
