@@ -18,6 +18,9 @@ import paper_1606_08150_b200 as dpc  # noqa: E402
 VARIANTS = ["flat", "basic", "warp", "block", "grid"]
 TREE = dict(depth=24, lo=1, hi=4, fill=0.84, seed=1)      # ~3.35M nodes, depth 24
 TREE_PAPER = dict(depth=5, lo=32, hi=128, fill=0.4, seed=1)  # paper-shaped, ~2.7M nodes
+# depth 24 at the size basic-DP still fits in the device pending-launch pool
+# (599,186 on B200; 196,634 internal nodes -> ~394K outstanding launches)
+TREE_DEEP_FIT = dict(depth=24, lo=1, hi=4, fill=0.75, seed=1)  # 491,454 nodes
 
 
 def _time(ctx, fn, reps):
@@ -124,13 +127,17 @@ def run_apps(ctx, apps, reps=3):
         elif a in ("td_paper", "th_paper"):
             out[a] = app_tree(ctx, orc, reps, "tree_desc" if a == "td_paper" else "tree_height",
                               TREE_PAPER)
+        elif a in ("td_deep_fit", "th_deep_fit"):
+            out[a] = app_tree(ctx, orc, reps, "tree_desc" if a == "td_deep_fit" else "tree_height",
+                              TREE_DEEP_FIT)
         out[a]["wall_s"] = round(time.time() - t0, 1)
     return out
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--apps", nargs="*", default=["sssp", "gc", "td", "th", "td_paper", "th_paper"])
+    ap.add_argument("--apps", nargs="*", default=["sssp", "gc", "td", "th", "td_paper", "th_paper",
+                                                  "td_deep_fit", "th_deep_fit"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--json", default=None)
     a = ap.parse_args()
