@@ -236,7 +236,7 @@ class CsrGraph:
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and _lib is not None:  # interpreter shutdown clears module globals
             _lib.dpc_csr_free(h)
 
 
@@ -258,7 +258,7 @@ class Tree:
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and _lib is not None:  # interpreter shutdown clears module globals
             _lib.dpc_tree_free(h)
 
 
@@ -431,7 +431,7 @@ class Context:
 
     def close(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and _lib is not None:  # interpreter shutdown clears module globals
             _lib.dpc_ctx_destroy(h)
 
     __del__ = close
@@ -522,7 +522,7 @@ class DeviceGraph:
 
     def close(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and _lib is not None:  # interpreter shutdown clears module globals
             _lib.dpc_dgraph_free(h)
 
     __del__ = close
@@ -557,7 +557,7 @@ class Comm:
 
     def close(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and _lib is not None:  # interpreter shutdown clears module globals
             _lib.dpc_comm_destroy(h)
 
     __del__ = close
@@ -624,7 +624,7 @@ class DeviceTree:
 
     def close(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and _lib is not None:  # interpreter shutdown clears module globals
             _lib.dpc_dtree_free(h)
 
     __del__ = close

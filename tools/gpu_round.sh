@@ -39,6 +39,12 @@ for s in $STAGES; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tree.*grid_persistent" -s 1 -c 1 -f \
           -o gpurun_out/prof_tree_grid python tools/prof_grid_apps.py 2 >> gpurun_out/ncu_apps.log 2>&1
       echo "appsncu rc=$?"; tail -3 gpurun_out/ncu_apps.log ;;
+    compare)
+      timeout 900 ncu --replay-mode app-range --csv --log-file gpurun_out/compare_ncu.csv \
+        --metrics gpu__time_duration.sum,smsp__thread_inst_executed_per_inst_executed.ratio,sm__warps_active.avg.pct_of_peak_sustained_active,dram__sectors_read.sum,dram__sectors_write.sum \
+        python tools/compare_metrics.py collect > gpurun_out/compare.log 2>&1
+      timeout 600 python tools/compare_metrics.py report gpurun_out/compare_ncu.csv gpurun_out/compare.md >> gpurun_out/compare.log 2>&1
+      echo "compare rc=$?"; tail -20 gpurun_out/compare.log ;;
     apps)
       timeout 1200 python tools/prof_apps.py --json gpurun_out/apps.json > gpurun_out/apps.log 2>&1
       echo "apps rc=$?"; tail -c 2000 gpurun_out/apps.log ;;
