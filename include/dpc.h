@@ -236,6 +236,11 @@ dpc_status dpc_run_sssp(dpc_ctx* ctx, const dpc_csr* g, int32_t source, uint32_t
 /* Greedy first-fit coloring in descending priority order, priority(v) =
  * (hash64(v ^ seed), v); g must be symmetric without self loops.
  * *ncolors receives the number of colors. */
+/* BFS levels from `source` (the paper's BFS-Rec benchmark; SPEC.md:454 oracle
+ * "BFS levels"): the SSSP consolidation with unit edge weights, weights in
+ * G ignored.  level[v] = hops from source, UINT32_MAX if unreachable. */
+dpc_status dpc_run_bfs(dpc_ctx* ctx, const dpc_csr* G, int32_t source, uint32_t* level,
+                       const dpc_launch_cfg* cfg, dpc_metrics* met);
 dpc_status dpc_run_color(dpc_ctx* ctx, const dpc_csr* g, uint64_t seed, int32_t* color,
                          int32_t* ncolors, const dpc_launch_cfg* cfg, dpc_metrics* met);
 /* desc[v] = number of proper descendants of v (TD). */
@@ -268,6 +273,9 @@ dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* dg, const float* d_x, float
                            const dpc_launch_cfg* cfg, dpc_metrics* met);
 /* Synchronous at the end (termination is device-driven; the host reads the
  * iteration count once). */
+/* BFS levels on a device-resident graph (weights not needed). */
+dpc_status dpc_bfs_device(dpc_ctx* ctx, dpc_dgraph* dg, int32_t source, const dpc_launch_cfg* cfg,
+                          dpc_metrics* met);
 dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* dg, int32_t source,
                            const dpc_launch_cfg* cfg, dpc_metrics* met);
 dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* dg, uint64_t seed,

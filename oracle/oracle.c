@@ -342,3 +342,27 @@ int orc_tree_height(int64_t n, const int32_t* parent, int32_t* height) {
   free(q);
   return 0;
 }
+
+/* BFS levels ("BFS-Rec = BFS levels"): hops from source by a
+ * FIFO sweep; UINT32_MAX = unreachable. */
+int orc_bfs(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t source, uint32_t* level) {
+  for (int64_t i = 0; i < n; i++) level[i] = UINT32_MAX;
+  if (source < 0 || source >= n) return -1;
+  int32_t* q = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  if (!q) return -1;
+  int64_t head = 0, tail = 0;
+  level[source] = 0;
+  q[tail++] = source;
+  while (head < tail) {
+    int32_t u = q[head++];
+    for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++) {
+      int32_t v = col[e];
+      if (level[v] == UINT32_MAX) {
+        level[v] = level[u] + 1;
+        q[tail++] = v;
+      }
+    }
+  }
+  free(q);
+  return 0;
+}

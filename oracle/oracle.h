@@ -45,4 +45,6 @@ int orc_color_valid(int64_t n, const int64_t* rowptr, const int32_t* col, const 
 int orc_tree_desc(int64_t n, const int32_t* parent, int32_t* desc);
 int orc_tree_height(int64_t n, const int32_t* parent, int32_t* height);
 
+/* BFS levels from source (UINT32_MAX = unreachable). */
+int orc_bfs(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t source, uint32_t* level);
 #endif

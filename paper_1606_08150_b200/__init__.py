@@ -151,6 +151,8 @@ _SIGS = {
     "dpc_spmv_device": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_sssp_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_bfs_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_run_bfs": (C.c_int, [_P, _CsrP, _i32, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_color_device": (C.c_int, [_P, _P, _u64, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_dtree_upload": (C.c_int, [_P, _TreeP, C.POINTER(_P)]),
     "dpc_dtree_free": (None, [_P]),
@@ -513,6 +515,13 @@ class DeviceGraph:
                                     C.byref(met) if met is not None else None))
         return met
 
+    def bfs(self, source: int, variant="grid", cfg=None, metrics: bool = True):
+        """BFS levels into the handle's dist buffer (get_dist())."""
+        met = Metrics() if metrics else None
+        _check(_lib.dpc_bfs_device(self.ctx.handle, self._h, source, _cfg_arg("sssp", variant, cfg),
+                                   C.byref(met) if met is not None else None))
+        return met
+
     def color(self, seed: int, variant="grid", cfg=None, metrics: bool = True):
         met = Metrics() if metrics else None
         _check(_lib.dpc_color_device(self.ctx.handle, self._h, seed & (2**64 - 1),
@@ -660,6 +669,17 @@ def run_sssp(G: CsrGraph, source: int, variant="grid", cfg=None, ctx: Context | 
     _check(_lib.dpc_run_sssp(ctx.handle, G._h, source, _ptr(dist), _cfg_arg("sssp", variant, cfg),
                              C.byref(met)))
     return dist, met
+
+
+def run_bfs(G: CsrGraph, source: int, variant="grid", cfg=None, ctx: Context | None = None):
+    """BFS levels (uint32 hops, UINT32_MAX = unreachable) -- the paper's BFS-Rec
+    benchmark as the SSSP consolidation with unit weights.  Returns (level, Metrics)."""
+    ctx = ctx or default_context()
+    level = np.empty(G.n, dtype=np.uint32)
+    met = Metrics()
+    _check(_lib.dpc_run_bfs(ctx.handle, G._h, source, _ptr(level), _cfg_arg("sssp", variant, cfg),
+                            C.byref(met)))
+    return level, met
 
 
 def run_color(G: CsrGraph, seed: int = 1, variant="grid", cfg=None, ctx: Context | None = None):

@@ -433,6 +433,20 @@ dpc_status dpc_run_sssp(dpc_ctx* c, const dpc_csr* G, int32_t source, uint32_t* 
   return st;
 }
 
+dpc_status dpc_run_bfs(dpc_ctx* c, const dpc_csr* G, int32_t source, uint32_t* level,
+                       const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!c || !G || !level) return fail(DPC_E_INVALID, "NULL argument");
+  dpc_dgraph* g = nullptr;
+  dpc_status st = dpc_dgraph_upload(c, G, &g);
+  if (st != DPC_OK) return st;
+  if (met) std::memset(met, 0, sizeof(*met));
+  st = dpc_bfs_device(c, g, source, cfg, met);
+  if (st == DPC_OK) st = dpc_copy_d2h(c, level, g->dist, sizeof(unsigned) * static_cast<size_t>(G->n));
+  dpc_dgraph_free(g);
+  return st;
+}
+
 dpc_status dpc_run_color(dpc_ctx* c, const dpc_csr* G, uint64_t seed, int32_t* color,
                          int32_t* ncolors, const dpc_launch_cfg* cfg, dpc_metrics* met) {
   clear_error();

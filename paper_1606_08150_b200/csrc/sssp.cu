@@ -83,6 +83,12 @@ struct Args {
 
 __device__ void spill_classify(const Args& a, unsigned it, unsigned v);
 
+// Edge weight; BFS (a.w == nullptr) is SSSP with unit weights: its levels are
+// the unit-weight distances (the reference's BFS-Rec benchmark).
+__device__ __forceinline__ unsigned edge_w(const Args& a, unsigned k) {
+  return a.w ? static_cast<unsigned>(__ldg(a.w + k)) : 1u;
+}
+
 // Per-block state every relaxing kernel carries in shared memory.
 struct Block {
   Queue q;
@@ -159,7 +165,7 @@ __device__ __noinline__ void spill_classify(const Args& a, unsigned it, unsigned
 
 __device__ __forceinline__ void relax_edge(const Args& a, unsigned it, Block& s, unsigned du,
                                            unsigned k) {
-  unsigned long long nd = static_cast<unsigned long long>(du) + static_cast<unsigned>(__ldg(a.w + k));
+  unsigned long long nd = static_cast<unsigned long long>(du) + edge_w(a, k);
   if (nd < kInf) relax(a, it, s, static_cast<unsigned>(__ldg(a.col + k)), static_cast<unsigned>(nd));
 }
 
@@ -591,7 +597,7 @@ __device__ __forceinline__ unsigned long long a_relax(const Args& a, const Async
       v[j] = 0;
       if (k < e) {
         v[j] = static_cast<unsigned>(__ldg(a.col + k));
-        const unsigned long long d = static_cast<unsigned long long>(du) + static_cast<unsigned>(__ldg(a.w + k));
+        const unsigned long long d = static_cast<unsigned long long>(du) + edge_w(a, k);
         nd[j] = d < 0x7fffffffull ? static_cast<unsigned>(d) : kInf;  // task words hold 31-bit distances
       }
     }
@@ -695,8 +701,8 @@ using namespace dpc;
 // Builds the kernel arguments of one SSSP run on `g` (a square graph, or the
 // row block [r0, r0 + g->n) of an n_global-vertex graph).
 static dpc_status sssp_setup(dpc_ctx* ctx, dpc_dgraph* g, const dpc_launch_cfg* cfg, sssp::Args* a,
-                             Cfg* c) {
-  if (g->m > 0 && !g->w) return fail(DPC_E_INVALID, "graph was uploaded without weights (w)");
+                             Cfg* c, bool unit = false) {
+  if (!unit && g->m > 0 && !g->w) return fail(DPC_E_INVALID, "graph was uploaded without weights (w)");
   dpc_status st = resolve_cfg(ctx, DPC_APP_SSSP, cfg, c);
   if (st != DPC_OK) return st;
   if (c->parent_threads != 256 || c->child_threads > 256)
@@ -708,7 +714,7 @@ static dpc_status sssp_setup(dpc_ctx* ctx, dpc_dgraph* g, const dpc_launch_cfg* 
   *a = sssp::Args{};
   a->rowptr = g->rowptr;
   a->col = g->col;
-  a->w = g->w;
+  a->w = unit ? nullptr : g->w;
   a->dist = g->dist;
   a->stamp = g->stamp;
   a->front0 = g->front[0];
@@ -774,15 +780,15 @@ static dpc_status sssp_finish(dpc_ctx* ctx, dpc_dgraph* g, int64_t host_launches
   return check_header(g->hdr_host);
 }
 
-extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t source,
-                                      const dpc_launch_cfg* cfg, dpc_metrics* met) {
+static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dpc_launch_cfg* cfg,
+                           dpc_metrics* met, bool unit) {
   clear_error();
   if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
   if (g->ncols != g->n) return fail(DPC_E_INVALID, "SSSP needs a square graph (not a row slice)");
   if (source < 0 || source >= g->n) return fail(DPC_E_INVALID, "source out of range");
   Cfg c;
   sssp::Args a;
-  dpc_status st = sssp_setup(ctx, g, cfg, &a, &c);
+  dpc_status st = sssp_setup(ctx, g, cfg, &a, &c, unit);
   if (st != DPC_OK) return st;
   cudaStream_t s = ctx->stream;
   const bool one_barrier = c.variant == DPC_GRID && c.grid_persistent &&
@@ -861,6 +867,16 @@ extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t sourc
     }
   }
   return sssp_finish(ctx, g, host_launches, iters, met);
+}
+
+extern "C" dpc_status dpc_sssp_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t source,
+                                      const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  return sssp_run(ctx, g, source, cfg, met, false);
+}
+
+extern "C" dpc_status dpc_bfs_device(dpc_ctx* ctx, dpc_dgraph* g, int32_t source,
+                                     const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  return sssp_run(ctx, g, source, cfg, met, true);
 }
 
 // ---------------------------------------------------------------------------

@@ -133,3 +133,11 @@ def test_live_reference_cross_check(orc):
     assert np.allclose(orc.spmv_f64(g.rowptr, g.col, g.val, x), y, rtol=1e-12, atol=0)
     rc, text = ref.consolidate_text(ref.kdl("spmv.kdl"), "grid")
     assert rc == 0 and "dp_grid_last" in text and "spmv_child_cons" in text
+
+
+def test_bfs_oracle_matches_unit_weight_dijkstra(orc):
+    import paper_1606_08150_b200 as dpc
+    g = dpc.gen_rmat(10, 8, seed=4)
+    ones = np.ones(g.m, np.int32)
+    for s in (0, int(np.argmax(g.degrees()))):
+        assert np.array_equal(orc.bfs(g.rowptr, g.col, s), orc.sssp(g.rowptr, g.col, ones, s))

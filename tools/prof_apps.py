@@ -83,6 +83,24 @@ def app_sssp(ctx, orc, reps, scale=16):
     return out
 
 
+def app_bfs(ctx, orc, reps, scale=16):
+    """BFS-Rec (the paper's seventh benchmark): config-1 graph, unit weights."""
+    g = dpc.gen_rmat(scale, 16, seed=1, weights=False)
+    s = int(np.argmax(g.degrees()))
+    ref = orc.bfs(g.rowptr, g.col, s)
+    m_reached = int(g.degrees()[ref != np.uint32(0xFFFFFFFF)].sum())
+    dg = dpc.DeviceGraph(ctx, g)
+    res = _variants(ctx, reps, lambda v, m: dg.bfs(s, v, metrics=m),
+                    lambda: np.array_equal(dg.get_dist(), ref),
+                    lambda met: {"iterations": met.iterations})
+    dg.close()
+    out = _summ(res, m_reached, "teps")
+    out.update({"workload": f"BFS R-MAT scale {scale}, source = max-degree vertex",
+                "unit": "GTEPS (edges of the reached component / time, Graph500)",
+                "m_reached": m_reached, "levels": int(ref[ref != np.uint32(0xFFFFFFFF)].max())})
+    return out
+
+
 def app_gc(ctx, orc, reps, scale=20):
     g = dpc.gen_rmat(scale, 16, seed=1, weights=False, symmetric=True)
     ref, k = orc.color(g.rowptr, g.col, 1)
@@ -122,6 +140,8 @@ def run_apps(ctx, apps, reps=3):
             out[a] = app_sssp(ctx, orc, reps)
         elif a == "gc":
             out[a] = app_gc(ctx, orc, reps)
+        elif a == "bfs":
+            out[a] = app_bfs(ctx, orc, reps)
         elif a in ("td", "th"):
             out[a] = app_tree(ctx, orc, reps, "tree_desc" if a == "td" else "tree_height")
         elif a in ("td_paper", "th_paper"):
@@ -136,7 +156,7 @@ def run_apps(ctx, apps, reps=3):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--apps", nargs="*", default=["sssp", "gc", "td", "th", "td_paper", "th_paper",
+    ap.add_argument("--apps", nargs="*", default=["sssp", "bfs", "gc", "td", "th", "td_paper", "th_paper",
                                                   "td_deep_fit", "th_deep_fit"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--json", default=None)
