@@ -564,7 +564,7 @@ def main():
     ap.add_argument("--multi", action="store_true",
                     help="run the partitioned (config 5) path even on one rank (testing)")
     ap.add_argument("--apps", nargs="*",
-                    default=["sssp", "bfs", "gc", "td", "th", "td_paper", "th_paper", "td_deep_fit",
+                    default=["sssp", "bfs", "pr", "gc", "td", "th", "td_paper", "th_paper", "td_deep_fit",
                              "th_deep_fit"],
                     help="other BASELINE apps timed in the same run (empty list: none)")
     args = ap.parse_args()

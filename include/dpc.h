@@ -313,6 +313,22 @@ dpc_status dpc_copy_d2h(dpc_ctx* ctx, void* dst_host, const void* src_dev, size_
  * the first `n` words of that record from the handle's last run. */
 dpc_status dpc_dgraph_trace(dpc_dgraph* g, uint64_t* out, int64_t n);
 
+/* ---- PageRank (the paper's PR benchmark; SPEC.md:454 / :468) ------------
+ * `iters` power iterations with damping d from r = 1/n:
+ *   r'[v] = (1-d)/n + d (sum over edges u->v of r[u] / outdeg(u) + D / n),
+ * D = rank mass of the vertices without out-edges.  Each iteration is one
+ * SpMV over the transposed graph with the SpMV variant of `cfg`
+ * (dpc_launch_cfg_default(DPC_APP_SPMV, ...)), built once per handle. */
+typedef struct dpc_prgraph dpc_prgraph;
+dpc_status dpc_pr_upload(dpc_ctx* ctx, const dpc_csr* g, dpc_prgraph** out);
+void dpc_pr_free(dpc_prgraph* h);
+dpc_status dpc_pr_device(dpc_ctx* ctx, dpc_prgraph* h, int32_t iters, double damping,
+                         const dpc_launch_cfg* cfg, dpc_metrics* met);
+/* Device pointer to the n ranks of the last dpc_pr_device run. */
+float* dpc_pr_rank(dpc_prgraph* h);
+dpc_status dpc_run_pagerank(dpc_ctx* ctx, const dpc_csr* g, int32_t iters, double damping, float* rank,
+                            const dpc_launch_cfg* cfg, dpc_metrics* met);
+
 /* ---- multi-GPU (one process per GPU; NCCL over NVLink) ------------------
  * Row / vertex partition of a graph across `world` ranks (BASELINE config 5).
  */

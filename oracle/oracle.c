@@ -366,3 +366,28 @@ int orc_bfs(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t source
   free(q);
   return 0;
 }
+
+/* PageRank, SPEC.md:454 ("PR = one-or-more power iterations with damping
+ * 0.85") with the fixed iteration count of SPEC.md:468: r0 = 1/n,
+ * r'[v] = (1-d)/n + d (sum_{u->v} r[u]/outdeg(u) + D/n), D = dangling mass.
+ * fp64, push order over the CSR. */
+int orc_pagerank(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t iters, double d,
+                 double* rank) {
+  if (n <= 0) return 0;
+  double* nxt = (double*)malloc(sizeof(double) * (size_t)n);
+  if (!nxt) return -1;
+  for (int64_t v = 0; v < n; v++) rank[v] = 1.0 / (double)n;
+  for (int32_t it = 0; it < iters; it++) {
+    double dm = 0.0;
+    for (int64_t v = 0; v < n; v++) nxt[v] = 0.0;
+    for (int64_t u = 0; u < n; u++) {
+      const int64_t deg = rowptr[u + 1] - rowptr[u];
+      if (deg == 0) { dm += rank[u]; continue; }
+      const double c = rank[u] / (double)deg;
+      for (int64_t e = rowptr[u]; e < rowptr[u + 1]; e++) nxt[col[e]] += c;
+    }
+    for (int64_t v = 0; v < n; v++) rank[v] = (1.0 - d) / (double)n + d * (nxt[v] + dm / (double)n);
+  }
+  free(nxt);
+  return 0;
+}

@@ -47,4 +47,7 @@ int orc_tree_height(int64_t n, const int32_t* parent, int32_t* height);
 
 /* BFS levels from source (UINT32_MAX = unreachable). */
 int orc_bfs(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t source, uint32_t* level);
+/* PageRank: iters power iterations, damping d, fp64. */
+int orc_pagerank(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t iters, double d,
+                 double* rank);
 #endif

@@ -153,6 +153,11 @@ _SIGS = {
     "dpc_sssp_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_bfs_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_run_bfs": (C.c_int, [_P, _CsrP, _i32, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_pr_upload": (C.c_int, [_P, _CsrP, C.POINTER(_P)]),
+    "dpc_pr_free": (None, [_P]),
+    "dpc_pr_device": (C.c_int, [_P, _P, _i32, C.c_double, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_pr_rank": (_P, [_P]),
+    "dpc_run_pagerank": (C.c_int, [_P, _CsrP, _i32, C.c_double, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_color_device": (C.c_int, [_P, _P, _u64, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_dtree_upload": (C.c_int, [_P, _TreeP, C.POINTER(_P)]),
     "dpc_dtree_free": (None, [_P]),
@@ -680,6 +685,45 @@ def run_bfs(G: CsrGraph, source: int, variant="grid", cfg=None, ctx: Context | N
     _check(_lib.dpc_run_bfs(ctx.handle, G._h, source, _ptr(level), _cfg_arg("sssp", variant, cfg),
                             C.byref(met)))
     return level, met
+
+
+def run_pagerank(G: CsrGraph, iters: int = 20, damping: float = 0.85, variant="grid", cfg=None,
+                 ctx: Context | None = None):
+    """PageRank ranks (float32): `iters` power iterations, each one SpMV of the
+    transposed graph with the SpMV consolidation `variant`.  Returns (rank, Metrics)."""
+    ctx = ctx or default_context()
+    rank = np.empty(G.n, dtype=np.float32)
+    met = Metrics()
+    _check(_lib.dpc_run_pagerank(ctx.handle, G._h, iters, damping, _ptr(rank), _cfg_arg("spmv", variant, cfg),
+                                 C.byref(met)))
+    return rank, met
+
+
+class PageRankGraph:
+    """dpc_prgraph: the transposed graph resident in HBM for repeated PR runs."""
+
+    def __init__(self, ctx: Context, g: CsrGraph):
+        h = C.c_void_p()
+        _check(_lib.dpc_pr_upload(ctx.handle, g._h, C.byref(h)))
+        self._h, self.ctx, self.n = h, ctx, g.n
+
+    def run(self, iters=20, damping=0.85, variant="grid", cfg=None, metrics: bool = True):
+        met = Metrics() if metrics else None
+        _check(_lib.dpc_pr_device(self.ctx.handle, self._h, iters, damping, _cfg_arg("spmv", variant, cfg),
+                                  C.byref(met) if met is not None else None))
+        return met
+
+    def rank(self) -> np.ndarray:
+        r = np.empty(self.n, dtype=np.float32)
+        _check(_lib.dpc_copy_d2h(self.ctx.handle, _ptr(r), _lib.dpc_pr_rank(self._h), r.nbytes))
+        return r
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _lib is not None:  # interpreter shutdown clears module globals
+            _lib.dpc_pr_free(h)
+
+    __del__ = close
 
 
 def run_color(G: CsrGraph, seed: int = 1, variant="grid", cfg=None, ctx: Context | None = None):

@@ -37,6 +37,7 @@ class Oracle:
         L.orc_spmv_f32_mt.restype, L.orc_spmv_f32_mt.argtypes = None, [i64, P, P, P, P, P, C.c_int]
         L.orc_sssp_dijkstra.restype, L.orc_sssp_dijkstra.argtypes = C.c_int, [i64, P, P, P, i32, P]
         L.orc_bfs.restype, L.orc_bfs.argtypes = C.c_int, [i64, P, P, i32, P]
+        L.orc_pagerank.restype, L.orc_pagerank.argtypes = C.c_int, [i64, P, P, i32, C.c_double, P]
         L.orc_sssp_bf_mt.restype, L.orc_sssp_bf_mt.argtypes = i64, [i64, P, P, P, i32, P, C.c_int]
         L.orc_color_greedy.restype, L.orc_color_greedy.argtypes = i32, [i64, P, P, u64, P]
         L.orc_color_valid.restype, L.orc_color_valid.argtypes = C.c_int, [i64, P, P, P, i32]
@@ -59,6 +60,13 @@ class Oracle:
         y = np.empty(len(rowptr) - 1, np.float32)
         self.L.orc_spmv_f32_mt(len(y), _p(rowptr), _p(col), _p(val), _p(x), _p(y), threads)
         return y
+
+    def pagerank(self, rowptr, col, iters, damping=0.85):
+        rowptr = np.ascontiguousarray(rowptr, np.int64)
+        col = np.ascontiguousarray(col, np.int32)
+        r = np.empty(len(rowptr) - 1, np.float64)
+        assert self.L.orc_pagerank(len(r), _p(rowptr), _p(col), iters, damping, _p(r)) == 0
+        return r
 
     def bfs(self, rowptr, col, source):
         rowptr = np.ascontiguousarray(rowptr, np.int64)

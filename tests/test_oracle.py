@@ -141,3 +141,14 @@ def test_bfs_oracle_matches_unit_weight_dijkstra(orc):
     ones = np.ones(g.m, np.int32)
     for s in (0, int(np.argmax(g.degrees()))):
         assert np.array_equal(orc.bfs(g.rowptr, g.col, s), orc.sssp(g.rowptr, g.col, ones, s))
+
+
+def test_pagerank_oracle_known_answers(orc):
+    # PR with damping 0.85; a directed 3-cycle is uniform at 1/3,
+    # a star's hub collects the mass; total mass stays 1
+    import paper_1606_08150_b200 as dpc
+    g = dpc.csr_from_arrays([0, 1, 2, 3], [1, 2, 0])
+    assert np.allclose(orc.pagerank(g.rowptr, g.col, 30), 1 / 3)
+    g = dpc.csr_from_arrays([0, 0, 1, 2, 3], [0, 0, 0])        # leaves -> hub 0 (dangling)
+    r = orc.pagerank(g.rowptr, g.col, 50)
+    assert r[0] > r[1] and np.isclose(r.sum(), 1.0) and np.allclose(r[1:], r[1])

@@ -101,6 +101,25 @@ def app_bfs(ctx, orc, reps, scale=16):
     return out
 
 
+def app_pr(ctx, orc, reps, scale=20, iters=20):
+    """PageRank (the paper's PR benchmark): 20 power iterations on the config-2
+    graph pattern (directed R-MAT scale 20), each one SpMV of the transpose."""
+    g = dpc.gen_rmat(scale, 16, seed=1, weights=False)
+    ref = orc.pagerank(g.rowptr, g.col, iters, 0.85)
+    pg = dpc.PageRankGraph(ctx, g)
+    res = _variants(ctx, reps, lambda v, m: pg.run(iters, 0.85, v, metrics=m),
+                    lambda: bool(np.max(np.abs(pg.rank() - ref) / ref) <= 1e-4),
+                    lambda met: {"iterations": iters})
+    pg.close()
+    out = _summ(res, iters * g.m, "teps")
+    out.update({"workload": f"PageRank R-MAT scale {scale} directed ({g.m} arcs), {iters} iterations, d = 0.85",
+                "unit": "GTEPS (arcs x iterations / time)", "check": "max rel err vs fp64 oracle <= 1e-4"})
+    for r in out["variants"].values():
+        if "bit_exact" in r:
+            r["within_1e-4"] = r.pop("bit_exact")
+    return out
+
+
 def app_gc(ctx, orc, reps, scale=20):
     g = dpc.gen_rmat(scale, 16, seed=1, weights=False, symmetric=True)
     ref, k = orc.color(g.rowptr, g.col, 1)
@@ -142,6 +161,8 @@ def run_apps(ctx, apps, reps=3):
             out[a] = app_gc(ctx, orc, reps)
         elif a == "bfs":
             out[a] = app_bfs(ctx, orc, reps)
+        elif a == "pr":
+            out[a] = app_pr(ctx, orc, reps)
         elif a in ("td", "th"):
             out[a] = app_tree(ctx, orc, reps, "tree_desc" if a == "td" else "tree_height")
         elif a in ("td_paper", "th_paper"):
@@ -156,7 +177,7 @@ def run_apps(ctx, apps, reps=3):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--apps", nargs="*", default=["sssp", "bfs", "gc", "td", "th", "td_paper", "th_paper",
+    ap.add_argument("--apps", nargs="*", default=["sssp", "bfs", "pr", "gc", "td", "th", "td_paper", "th_paper",
                                                   "td_deep_fit", "th_deep_fit"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--json", default=None)
