@@ -181,6 +181,10 @@ typedef struct dpc_launch_cfg {
                                 worklist (device FIFO, no barrier between
                                 rounds) instead of round-synchronous grid
                                 barriers; GC default */
+#define DPC_CFG_ALLOC_MALLOC 16 /* SpMV warp / block variants: per-owner buffers from
+                                  the device heap (malloc / tail-launched free)
+                                  instead of the pre-allocated pool -- the
+                                  paper's allocator study, PAPER.md:296 */
 #define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */

@@ -199,6 +199,9 @@ dpc_status dpc_ctx_create(int32_t device, dpc_ctx** out) {
     e = cudaMalloc(&c->flush_buf, c->flush_bytes);
   }
   if (e == cudaSuccess) e = cudaDeviceSetLimit(cudaLimitDevRuntimePendingLaunchCount, 2048);
+  // device heap for the allocator-study variants (DPC_CFG_ALLOC_MALLOC): must
+  // be sized before any kernel calls malloc
+  if (e == cudaSuccess) e = cudaDeviceSetLimit(cudaLimitMallocHeapSize, size_t{512} << 20);
   if (e != cudaSuccess) {
     dpc_ctx_destroy(c);
     return cuda_fail(e, "dpc_ctx_create");

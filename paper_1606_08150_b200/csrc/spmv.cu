@@ -458,6 +458,60 @@ __global__ void __launch_bounds__(256) block_parent(Args a) {
   }
 }
 
+// Allocator study (Fig. 5; memplan.hpp:45-58): the warp / block
+// consolidation with each owner's buffer from the CUDA device heap (malloc in
+// the parent, free in a tail-launched grid once the child is done) instead of
+// a slice of the pre-allocated pool.  DPC_CFG_ALLOC_MALLOC.
+__global__ void free_tail(void* p) { free(p); }
+
+__global__ void __launch_bounds__(256) block_parent_malloc(Args a) {
+  __shared__ Item* s_buf;
+  unsigned row = blockIdx.x * blockDim.x + threadIdx.x, b = 0, e = 0;
+  unsigned want = parent_prework(a, row, &b, &e);
+  unsigned btotal;
+  unsigned off = dev::block_excl_scan(want, &btotal);
+  if (threadIdx.x == 0) {
+    s_buf = btotal ? static_cast<Item*>(malloc(sizeof(Item) * btotal)) : nullptr;
+    if (btotal && !s_buf) atomicOr(&a.hdr->overflow, 1u);
+  }
+  __syncthreads();
+  if (want && s_buf) {
+    dev::write_chunks(dev::Pool{s_buf, btotal}, a.hdr, off, row, b, e, a.chunk);
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_buf) {
+    cons_child<<<dev::child_blocks(btotal, a.child_threads, a.child_blocks), a.child_threads, 0,
+                 cudaStreamFireAndForget>>>(a, s_buf, btotal);
+    dev::note_launch(a.hdr);
+    free_tail<<<1, 1, 0, cudaStreamTailLaunch>>>(s_buf);
+  }
+}
+
+__global__ void __launch_bounds__(256) warp_parent_malloc(Args a) {
+  unsigned row = blockIdx.x * blockDim.x + threadIdx.x, b = 0, e = 0;
+  unsigned want = parent_prework(a, row, &b, &e);
+  const unsigned incl = dev::warp_incl_scan(want), wtotal = __shfl_sync(kFull, incl, 31);
+  if (!wtotal) return;
+  const unsigned leader = __ffs(__ballot_sync(kFull, want != 0)) - 1;
+  unsigned long long p = 0;
+  if (dev::lane_id() == leader) {
+    p = reinterpret_cast<unsigned long long>(malloc(sizeof(Item) * wtotal));
+    if (!p) atomicOr(&a.hdr->overflow, 1u);
+  }
+  Item* buf = reinterpret_cast<Item*>(__shfl_sync(kFull, p, leader));
+  if (!buf) return;
+  if (want) dev::write_chunks(dev::Pool{buf, wtotal}, a.hdr, incl - want, row, b, e, a.chunk);
+  __threadfence();
+  __syncwarp();
+  if (dev::lane_id() == leader) {
+    cons_child<<<dev::child_blocks(wtotal, a.child_threads, a.child_blocks), a.child_threads, 0,
+                 cudaStreamFireAndForget>>>(a, buf, wtotal);
+    dev::note_launch(a.hdr);
+    free_tail<<<1, 1, 0, cudaStreamTailLaunch>>>(buf);
+  }
+}
+
 __global__ void __launch_bounds__(256) grid_parent(Args a) {
   unsigned row = blockIdx.x * blockDim.x + threadIdx.x, b = 0, e = 0;
   unsigned want = parent_prework(a, row, &b, &e);
@@ -1395,6 +1449,13 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
                                           : g->cap};
   st = ensure_pending_for(ctx, g, c.variant, c.threshold, c.parent_threads);
   if (st != DPC_OK) return st;
+  if ((c.flags & DPC_CFG_ALLOC_MALLOC) && (c.variant == DPC_WARP || c.variant == DPC_BLOCK)) {
+    // device heap for the per-owner buffers (+ one tail launch per owner)
+    st = ensure_pending_limit(ctx, 2 * static_cast<size_t>(std::max<int64_t>(g->n / 32, 1)) + 1024);
+    if (st != DPC_OK) return st;
+    // the device heap is sized once at context creation (kDeviceHeap); a
+    // malloc that does not fit raises the overflow fault
+  }
   // the stream kernel zeroes its header counters on exit (its last block),
   // so back-to-back stream runs need no per-run memset
   if (!(use_stream && g->hdr_clean && !met)) {
@@ -1408,8 +1469,14 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
     switch (c.variant) {
       case DPC_FLAT: spmv::flat_kernel<<<blocks, 256, 0, s>>>(a); break;
       case DPC_BASIC: spmv::basic_parent<<<blocks, 256, 0, s>>>(a); break;
-      case DPC_WARP: spmv::warp_parent<<<blocks, 256, 0, s>>>(a); break;
-      case DPC_BLOCK: spmv::block_parent<<<blocks, 256, 0, s>>>(a); break;
+      case DPC_WARP:
+        if (c.flags & DPC_CFG_ALLOC_MALLOC) spmv::warp_parent_malloc<<<blocks, 256, 0, s>>>(a);
+        else spmv::warp_parent<<<blocks, 256, 0, s>>>(a);
+        break;
+      case DPC_BLOCK:
+        if (c.flags & DPC_CFG_ALLOC_MALLOC) spmv::block_parent_malloc<<<blocks, 256, 0, s>>>(a);
+        else spmv::block_parent<<<blocks, 256, 0, s>>>(a);
+        break;
       case DPC_GRID:
         if (use_stream) {
           const spmv::StreamShape sh = spmv::stream_shape(c.threshold > 0, c.flags);

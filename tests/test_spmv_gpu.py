@@ -153,3 +153,15 @@ def test_spmv_grid_chunked_form(ctx, orc, threshold):
     cfg = dpc.launch_cfg("spmv", "grid", grid_chunked=True, threshold=threshold)
     y, _ = dpc.run_spmv(g, x, "grid", cfg=cfg, ctx=ctx)
     _check(orc, g, x, y)
+
+
+@pytest.mark.parametrize("variant", ["warp", "block"])
+def test_spmv_device_heap_allocator(ctx, orc, variant):
+    """Allocator study form (DPC_CFG_ALLOC_MALLOC): same results as the pool."""
+    g = _ragged(seed=5)
+    x = _x(g.n)
+    cfg = dpc.launch_cfg("spmv", variant)
+    cfg.flags |= 16
+    y, met = dpc.run_spmv(g, x, variant, cfg=cfg, ctx=ctx)
+    _check(orc, g, x, y)
+    assert met.child_launch_count > 0
