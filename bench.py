@@ -535,7 +535,7 @@ def run_reference(args):
     sample = (f"seeded random 1/{args.ref_stride} of the rows ({rows} rows, {nnz} nnz) of the "
               f"config-2 matrix per "
               f"step, dpcons::simulate "
-              f"grid-consolidated (oracle/kdl/spmv.kdl), single-threaded simulator")
+              f"grid-consolidated (paper_1606_08150_b200/kdl/programs/spmv.kdl), single-threaded simulator")
     print(json.dumps({
         "impl": "reference",
         "metric": "SSSP/SpMV GTEPS per B200 (1-8 GPU) & speedup vs basic-DP and flat kernels",

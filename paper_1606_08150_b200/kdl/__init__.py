@@ -1,0 +1,308 @@
+"""B200 consolidation compiler for the reference's kernel DSL (.kdl):
+parse -> consolidate (warp / block / grid, the paper's directive compiler)
+-> sm_100a CUDA (kdl_rt.cuh runtime) -> nvcc -> a loadable module that runs
+the program on the GPU with CDP2 device launches.
+
+    import paper_1606_08150_b200.kdl as kdl
+    mod = kdl.compile(open("spmv.kdl").read(), mode="grid")
+    res = mod.run({"n": n, "m": m, "nx": n, "thr": 32},
+                  {"rowptr": rowptr, "col": col, "val": val, "x": x})
+    y = res.arrays["y"]
+
+`mode` is "basic" (the program as written: one device launch per annotated
+site execution, Fig. 1), "warp" / "block" / "grid" (consolidated at that
+granularity, the reference's granularityOverride) or "directive" (each
+site's own consltdt clause).  `consolidated=True` takes an already
+consolidated program (e.g. the reference's consolidate() text) as is.
+
+This mirrors the reference's compiler pipeline (parse_program,
+parser.hpp:783 -> consolidate, transform.hpp:971) with the simulator
+(simulate, sim.hpp:1746) replaced by real execution on a B200.  There is no
+CPU fallback: running a module needs the CUDA device.
+"""
+import ctypes as C
+import glob
+import hashlib
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+from . import ast
+from .transform import Config, consolidate, k20c_occupancy, lower_kc
+from .cuda import generate
+from .parse import KdlError, parse_program
+
+__all__ = ["compile", "compile_program", "Module", "KdlError", "KdlFault", "Config", "parse_program",
+           "consolidate", "lower_kc", "k20c_occupancy", "generate", "build_programs", "PROGRAMS"]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BUILD = os.path.join(HERE, "_build")
+PROGRAMS = os.path.join(HERE, "programs")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-rdc=true", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+NVCC_LIBS = ["-lcudadevrt", "-lcudart_static", "-lpthread", "-ldl", "-lrt"]
+MODES = ("basic", "warp", "block", "grid", "directive")
+
+FAULTS = {1: ("overflow", "consolidation buffer overflow"), 2: ("overflow", "pre-allocated pool exhausted"),
+          4: ("runtime", "array index out of bounds"), 8: ("runtime", "integer division or modulo by zero"),
+          16: ("config", "launch extents outside [1, 2^31) x [1, 1024]"),
+          32: ("oom", "device launch refused (pending-launch pool)"), 64: ("oom", "launch-record arena exhausted"),
+          128: ("runtime", "dp_buf_get / dp_buf_cfg index out of range")}
+
+
+class KdlFault(RuntimeError):
+    """A fault raised by the running program (the simulator's SimFault kinds,
+    sim.hpp:49-52)."""
+
+    def __init__(self, bits):
+        self.bits = bits
+        self.kinds = sorted({FAULTS[b][0] for b in FAULTS if bits & b})
+        super().__init__("; ".join(f"{FAULTS[b][0]}: {FAULTS[b][1]}" for b in FAULTS if bits & b))
+
+
+def read_program(name):
+    with open(os.path.join(PROGRAMS, name)) as f:
+        return f.read()
+
+
+def _nvcc():
+    return os.environ.get("NVCC") or ("/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc")
+                                      else "nvcc")
+
+
+_build_lock = threading.Lock()
+
+
+def build_so(cu_src, tag):
+    """Compile one generated unit into paper_1606_08150_b200/kdl/_build/
+    (cached by content hash; the .so travels with the repo snapshot)."""
+    with open(os.path.join(HERE, "kdl_rt.cuh")) as f:
+        rt = f.read()
+    h = hashlib.sha1((cu_src + rt + " ".join(NVCC_FLAGS)).encode()).hexdigest()[:16]
+    so = os.path.join(BUILD, f"{tag}_{h}.so")
+    if os.path.exists(so):
+        return so
+    os.makedirs(BUILD, exist_ok=True)
+    cu = so[:-3] + ".cu"
+    with open(cu, "w") as f:
+        f.write(cu_src)
+    tmp = so + f".tmp{os.getpid()}"
+    cmd = [_nvcc(), *NVCC_FLAGS, "-I", HERE, cu, "-o", tmp, *NVCC_LIBS]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise KdlError("cuda.nvcc", f"nvcc failed for {cu}:\n{r.stderr[-4000:]}")
+    os.replace(tmp, so)
+    # keep one build per (program, mode): drop units of older sources
+    for old in glob.glob(os.path.join(BUILD, f"{glob.escape(tag)}_" + "[0-9a-f]" * 16 + ".*")):
+        if not old.startswith(so[:-3]):
+            try:
+                os.remove(old)
+            except OSError:
+                pass
+    return so
+
+
+def eval_host(e, scalars):
+    """Evaluate a host-side expression (array lengths, entry launch) over the
+    workload scalars, with the DSL's int64 / float rules."""
+    k = e.kind
+    if k == "int":
+        return int(e.ival)
+    if k == "float":
+        return float(e.fval)
+    if k == "name":
+        if e.name not in scalars:
+            raise KdlError("run.scalar", f"workload scalar {e.name!r} is not given")
+        return scalars[e.name]
+    if k == "unary":
+        v = eval_host(e.args[0], scalars)
+        return int(v == 0) if e.name == "!" else -v
+    if k == "minmax":
+        a, b = (eval_host(x, scalars) for x in e.args)
+        return min(a, b) if e.name == "min" else max(a, b)
+    if k == "binary":
+        a, b = (eval_host(x, scalars) for x in e.args)
+        op = e.name
+        flt = isinstance(a, float) or isinstance(b, float)
+        if op == "/":
+            if flt:
+                return a / b
+            q = abs(a) // abs(b)
+            return q if (a >= 0) == (b >= 0) else -q
+        if op == "%":
+            return a - b * (abs(a) // abs(b) * (1 if (a >= 0) == (b >= 0) else -1))
+        return {"+": lambda: a + b, "-": lambda: a - b, "*": lambda: a * b,
+                "<": lambda: int(a < b), "<=": lambda: int(a <= b), ">": lambda: int(a > b),
+                ">=": lambda: int(a >= b), "==": lambda: int(a == b), "!=": lambda: int(a != b),
+                "&&": lambda: int(bool(a) and bool(b)), "||": lambda: int(bool(a) or bool(b))}[op]()
+    raise KdlError("run.expr", f"{k!r} is not allowed in a host-side expression")
+
+
+class _Rt(C.Structure):
+    _fields_ = [("arr", C.c_void_p * 64), ("len", C.c_int64 * 64), ("ctr", C.c_void_p),
+                ("arena", C.c_void_p), ("arena_words", C.c_uint64), ("inst", C.c_void_p),
+                ("inst_cap", C.c_uint64), ("region", C.c_void_p * 2), ("region_words", C.c_uint64),
+                ("narr", C.c_int64)]
+
+
+class Result:
+    def __init__(self, arrays, launches, runs, kc, ms):
+        self.arrays, self.launches, self.runs, self.kc, self.ms = arrays, launches, runs, kc, ms
+
+
+class Module:
+    """A compiled program.  run() owns device memory through torch (plumbing);
+    every kernel that executes is generated code from this module's .so."""
+
+    def __init__(self, prog, so, kc, mode):
+        self.prog, self.so, self.kc_rows, self.mode = prog, so, kc, mode
+        self.lib = None
+        self._dev = None
+        self.grid_total = max([s.total_bytes for k in prog.kernels for s in k.body
+                               if s.kind == "buf_decl" and s.gran == "grid"] or [0])
+
+    def _load(self, device, pending):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("kdl modules run on the CUDA device only (no CPU fallback)")
+        if self.lib is None:
+            L = C.CDLL(self.so)
+            L.dk_error.restype = C.c_char_p
+            L.dk_init.argtypes = [C.c_int, C.c_longlong]
+            L.dk_set_rt.argtypes = [C.c_void_p]
+            L.dk_kc_values.argtypes = [C.c_void_p]
+            L.dk_launch_entry.argtypes = [C.c_longlong, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]
+            if L.dk_sizeof_rt() != C.sizeof(_Rt):
+                raise RuntimeError("kdl runtime struct layout mismatch")
+            self.lib = L
+        if self._dev != device:
+            torch.cuda.set_device(device)
+            torch.cuda.synchronize()
+            if self.lib.dk_init(device, pending) != 0:
+                raise RuntimeError("dk_init: " + self.lib.dk_error().decode())
+            self._dev = device
+        kc = (C.c_longlong * max(1, len(self.kc_rows)))()
+        self.lib.dk_kc_values(kc)
+        return {f"{k}/KC_{x}/T{t}": int(kc[i]) for i, (k, x, t) in enumerate(self.kc_rows)}
+
+    def run(self, scalars, arrays=None, *, until_stable=None, max_runs=10000, device=0,
+            pool_bytes=1 << 30, inst_cap=1 << 20, pending=1 << 17, timed=False):
+        """Run the entry launch once, or — with `until_stable=<array>` —
+        repeat it until that array stops changing (the host sweep loop the
+        SSSP / TH formulations need).  Returns Result(arrays as numpy,
+        device launches, entry runs, KC block counts, device ms)."""
+        import torch
+        kc = self._load(device, pending)
+        arrays = arrays or {}
+        dev = torch.device("cuda", device)
+        for n in arrays:
+            if self.prog.global_(n) is None:
+                raise KdlError("run.array", f"{n!r} is not a global array of the program")
+        rt = _Rt()
+        keep = []
+        tens = {}
+        for i, g in enumerate(self.prog.globals):
+            ln = int(eval_host(g.length, scalars))
+            if ln < 0:
+                raise KdlError("run.array", f"array {g.name!r} has negative length {ln}")
+            dt = torch.float64 if g.type == ast.FLOAT else torch.int64
+            if g.name in arrays:
+                a = np.asarray(arrays[g.name], dtype=np.float64 if g.type == ast.FLOAT else np.int64)
+                if a.shape != (ln,):
+                    raise KdlError("run.array", f"array {g.name!r} must have {ln} elements, got {a.shape}")
+                t = torch.from_numpy(a.copy()).to(dev)
+            else:
+                t = torch.zeros(max(ln, 0), dtype=dt, device=dev)
+            tens[g.name] = t
+            rt.arr[i] = t.data_ptr() if ln > 0 else 0
+            rt.len[i] = ln
+        rt.narr = len(self.prog.globals)
+        ctr = torch.zeros(8, dtype=torch.int64, device=dev)
+        arena_words = max(1, pool_bytes // 8)
+        arena = torch.empty(arena_words, dtype=torch.int64, device=dev)
+        inst = torch.zeros(3 * inst_cap, dtype=torch.int64, device=dev)
+        region_words = max(1, self.grid_total // 8) if self.grid_total else 1
+        regions = [torch.empty(region_words, dtype=torch.int64, device=dev) for _ in range(2)]
+        keep += [ctr, arena, inst] + regions
+        rt.ctr, rt.arena, rt.arena_words = ctr.data_ptr(), arena.data_ptr(), arena_words
+        rt.inst, rt.inst_cap = inst.data_ptr(), inst_cap
+        rt.region[0], rt.region[1] = regions[0].data_ptr(), regions[1].data_ptr()
+        rt.region_words = region_words
+        if self.lib.dk_set_rt(C.byref(rt)) != 0:
+            raise RuntimeError("dk_set_rt: " + self.lib.dk_error().decode())
+
+        e = self.prog.entry
+        ek = self.prog.kernel(e.kernel)
+        g = int(eval_host(e.grid, scalars))
+        b = int(eval_host(e.block, scalars))
+        if len(e.args) != len(ek.params):
+            raise KdlError("run.entry", f"entry passes {len(e.args)} arguments, kernel takes {len(ek.params)}")
+        args = (C.c_longlong * max(1, len(e.args)))()
+        for j, (a, p) in enumerate(zip(e.args, ek.params)):
+            if p.is_array:
+                args[j] = [x.name for x in self.prog.globals].index(a.name)
+            elif p.type == ast.FLOAT:
+                args[j] = int(np.array([float(eval_host(a, scalars))], np.float64).view(np.int64)[0])
+            else:
+                v = eval_host(a, scalars)
+                if isinstance(v, float):
+                    raise KdlError("run.entry", f"float argument for int parameter {p.name!r}")
+                args[j] = int(v)
+        stream = torch.cuda.current_stream(dev)
+        launches, runs, ms = 0, 0, 0.0
+        watch = tens.get(until_stable) if until_stable else None
+        if until_stable and watch is None:
+            raise KdlError("run.array", f"until_stable names unknown array {until_stable!r}")
+        while True:
+            ctr.zero_()
+            ctr[3] = 1
+            inst[:3].zero_()
+            before = watch.clone() if watch is not None else None
+            if timed:
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record(stream)
+            rc = self.lib.dk_launch_entry(g, b, args, inst.data_ptr(), C.c_void_p(stream.cuda_stream))
+            if rc != 0:
+                raise RuntimeError("entry launch: " + self.lib.dk_error().decode())
+            if timed:
+                t1.record(stream)
+            stream.synchronize()
+            if timed:
+                ms += t0.elapsed_time(t1)
+            c = ctr.cpu().tolist()
+            runs += 1
+            launches += c[1]
+            if c[0]:
+                raise KdlFault(c[0])
+            if watch is None or torch.equal(before, watch) or runs >= max_runs:
+                break
+        out = {n: t.cpu().numpy() for n, t in tens.items()}
+        del keep
+        return Result(out, launches, runs, kc, ms)
+
+
+def compile_program(prog, mode="basic", config=None, name="kdl", consolidated=False):
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}")
+    if not consolidated and mode != "basic":
+        prog = consolidate(prog, granularity=None if mode == "directive" else mode, config=config)
+    src, kc = generate(prog, name)
+    so = build_so(src, f"{name}_{mode}")
+    return Module(prog, so, kc, mode)
+
+
+def compile(source, mode="basic", config=None, name="kdl", consolidated=False):  # noqa: A001
+    """.kdl text -> Module (compiled for sm_100a; cached under kdl/_build)."""
+    return compile_program(parse_program(source), mode, config, name, consolidated)
+
+
+def build_programs(jobs=8):
+    """Pre-compile the bundled programs in every mode (called by build())."""
+    from concurrent.futures import ThreadPoolExecutor
+    work = [(f, m) for f in sorted(os.listdir(PROGRAMS)) if f.endswith(".kdl")
+            for m in ("basic", "warp", "block", "grid")]
+    with ThreadPoolExecutor(jobs) as ex:
+        list(ex.map(lambda fm: compile(read_program(fm[0]), fm[1], name=fm[0][:-4]), work))
+    return len(work)

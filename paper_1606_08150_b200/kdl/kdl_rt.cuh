@@ -1,0 +1,275 @@
+// Device runtime of the .kdl -> sm_100a CUDA builder (paper_1606_08150_b200/kdl):
+// the consolidated-program builtins (dp_buffers / dp_insert / dp_buf_* /
+// dp_grid_last, ast.hpp:25-33 and 63-65) mapped onto B200 primitives.
+//
+//   * owner buffers (warp / block: shared-memory record; grid: per-launch
+//     Inst record in HBM) hold {base, count, cap}; storage is reserved lazily,
+//     once per owner, from a pre-allocated arena (the paper's "pre-alloc"
+//     allocator) — owners that never insert cost nothing;
+//   * dp_insert is warp-aggregated: one shared/global atomic per warp per
+//     insert instruction, whatever the divergence;
+//   * grid buffers alternate between two regions by launch level, so a
+//     recursive grid-level chain (level L reads what L-1 wrote while it fills
+//     the other region) never needs more than two;
+//   * dp_grid_last is the last-block ticket (__threadfence + atomicAdd on the
+//     launch's own Inst record), cached per block like sim.hpp:1708-1716;
+//   * device launches are CDP2 fire-and-forget; a launch that follows
+//     sync_device becomes a tail launch (runs after the whole parent grid and
+//     everything it launched, which is what the postwork needs);
+//   * every fault the simulator reports (sim.hpp:49-52: overflow, runtime,
+//     config) sets a bit in ctr[0] instead of trapping.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+namespace dk {
+
+enum : unsigned long long {
+  F_OVERFLOW = 1,   // consolidation buffer overflow / non-positive capacity
+  F_POOL = 2,       // pre-allocated pool exhausted
+  F_BOUNDS = 4,     // array index out of bounds
+  F_DIV = 8,        // integer division / modulo by zero
+  F_CONFIG = 16,    // launch extents outside [1, 2^31) x [1, 1024]
+  F_LAUNCH = 32,    // device launch refused (pending-launch pool, resources)
+  F_INST = 64,      // launch-record arena exhausted
+  F_BUFGET = 128,   // dp_buf_get / dp_buf_cfg index out of range
+};
+
+constexpr int kMaxArrays = 64;
+
+struct Inst {                 // one per device launch that needs it
+  unsigned long long count;   // grid buffer fill
+  unsigned int ticket;        // dp_grid_last counter
+  unsigned int level;         // launch depth: grid buffer region = level & 1
+  unsigned long long aux;     // sync_device split: phase state base (0 unset, 1 busy, else off + 2)
+};
+
+struct Inh {                  // the buffer a consolidated kernel drains
+  const long long* items;     // [n][stride] words: cfgGrid, cfgBlock, work...
+  long long n;
+  long long stride;
+};
+
+struct Own {                  // warp / block owner record (shared memory)
+  unsigned long long base;    // 0 unset, 1 being reserved, ~0 failed, else word offset + 2
+  unsigned long long count;
+  long long cap;
+};
+
+struct Rt {
+  void* arr[kMaxArrays];
+  long long len[kMaxArrays];
+  unsigned long long* ctr;    // [0] fault bits [1] launches [2] arena top (words) [3] inst top
+  long long* arena;
+  unsigned long long arena_words;
+  Inst* inst;
+  unsigned long long inst_cap;
+  long long* region[2];
+  unsigned long long region_words;
+  long long narr;
+};
+
+constexpr unsigned long long kNoBase = ~0ull;
+
+}  // namespace dk
+
+__constant__ dk::Rt dk_rt;
+__device__ long long dk_sink_i[2];
+__device__ double dk_sink_f[2];
+
+__device__ __forceinline__ void dk_fault(unsigned long long bit) { atomicOr(&dk_rt.ctr[0], bit); }
+
+// ---- checked array access (the simulator faults on out-of-bounds) ----
+__device__ __forceinline__ bool dk_ok(long long id, long long i) {
+  if (static_cast<unsigned long long>(id) >= static_cast<unsigned long long>(dk_rt.narr) ||
+      static_cast<unsigned long long>(i) >= static_cast<unsigned long long>(dk_rt.len[id])) {
+    dk_fault(dk::F_BOUNDS);
+    return false;
+  }
+  return true;
+}
+__device__ __forceinline__ long long* dk_ip(long long id, long long i) {
+  return dk_ok(id, i) ? static_cast<long long*>(dk_rt.arr[id]) + i : dk_sink_i;
+}
+__device__ __forceinline__ double* dk_fp(long long id, long long i) {
+  return dk_ok(id, i) ? static_cast<double*>(dk_rt.arr[id]) + i : dk_sink_f;
+}
+__device__ __forceinline__ long long dk_atomic_i(long long* p, long long v) {
+  return static_cast<long long>(atomicAdd(reinterpret_cast<unsigned long long*>(p),
+                                          static_cast<unsigned long long>(v)));
+}
+__device__ __forceinline__ double dk_atomic_f(double* p, double v) { return atomicAdd(p, v); }
+
+// ---- arithmetic with the simulator's fault rules (sim.hpp:1574-1590) ----
+__device__ __forceinline__ long long dk_idiv(long long a, long long b) {
+  if (b == 0) { dk_fault(dk::F_DIV); return 0; }
+  return a / b;
+}
+__device__ __forceinline__ long long dk_imod(long long a, long long b) {
+  if (b == 0) { dk_fault(dk::F_DIV); return 0; }
+  return a % b;
+}
+template <class T> __device__ __forceinline__ T dk_min(T a, T b) { return b < a ? b : a; }
+template <class T> __device__ __forceinline__ T dk_max(T a, T b) { return a < b ? b : a; }
+
+// ---- owner buffers ----
+__device__ __forceinline__ unsigned dk_lane() { return threadIdx.x & 31u; }
+
+// Reserve the owner's storage once (the first inserting warp wins the CAS).
+__device__ __noinline__ unsigned long long dk_own_base(dk::Own* o, long long stride) {
+  unsigned long long b = atomicCAS(&o->base, 0ull, 1ull);
+  if (b == 0) {
+    b = dk::kNoBase;
+    if (o->cap < 1) {
+      dk_fault(dk::F_OVERFLOW);
+    } else {
+      const unsigned long long words = static_cast<unsigned long long>(o->cap) * stride;
+      const unsigned long long off = atomicAdd(&dk_rt.ctr[2], words);
+      if (off + words > dk_rt.arena_words) dk_fault(dk::F_POOL);
+      else b = off + 2;
+    }
+    atomicExch(&o->base, b);
+    return b;
+  }
+  while (b == 1) {
+    __nanosleep(32);
+    b = atomicAdd(&o->base, 0ull);
+  }
+  return b;
+}
+
+// Warp-aggregated slot reservation in a shared-memory owner (warp or block).
+__device__ __forceinline__ long long* dk_reserve_own(dk::Own* o, long long stride) {
+  const unsigned m = __activemask();
+  const unsigned lane = dk_lane();
+  const int leader = __ffs(m) - 1;
+  unsigned long long pos = 0, base = 0;
+  if (lane == static_cast<unsigned>(leader)) {
+    pos = atomicAdd(&o->count, static_cast<unsigned long long>(__popc(m)));
+    base = dk_own_base(o, stride);
+  }
+  pos = __shfl_sync(m, pos, leader) + __popc(m & ((1u << lane) - 1u));
+  base = __shfl_sync(m, base, leader);
+  if (base == dk::kNoBase) return nullptr;
+  if (pos >= static_cast<unsigned long long>(o->cap)) {
+    dk_fault(dk::F_OVERFLOW);
+    return nullptr;
+  }
+  return dk_rt.arena + (base - 2) + pos * stride;
+}
+
+__device__ __forceinline__ long long dk_grid_cap(long long total_bytes, long long nv, long long stride) {
+  const long long c = total_bytes / (nv * 8);
+  const long long r = static_cast<long long>(dk_rt.region_words) / stride;
+  return c < r ? c : r;
+}
+
+// Grid owner: the launch's Inst record, storage = region[level & 1].
+__device__ __forceinline__ long long* dk_reserve_grid(dk::Inst* in, long long stride, long long cap) {
+  const unsigned m = __activemask();
+  const unsigned lane = dk_lane();
+  const int leader = __ffs(m) - 1;
+  unsigned long long pos = 0;
+  if (lane == static_cast<unsigned>(leader))
+    pos = atomicAdd(&in->count, static_cast<unsigned long long>(__popc(m)));
+  pos = __shfl_sync(m, pos, leader) + __popc(m & ((1u << lane) - 1u));
+  if (cap < 1 || pos >= static_cast<unsigned long long>(cap)) {
+    dk_fault(dk::F_OVERFLOW);
+    return nullptr;
+  }
+  return dk_rt.region[in->level & 1u] + pos * stride;
+}
+
+__device__ __forceinline__ long long dk_clamp_count(unsigned long long c, long long cap) {
+  return static_cast<long long>(c) < cap ? static_cast<long long>(c) : cap;
+}
+
+__device__ __forceinline__ long long dk_pending_own(dk::Own* o) {
+  __syncwarp(__activemask());
+  return dk_clamp_count(*reinterpret_cast<volatile unsigned long long*>(&o->count), o->cap);
+}
+__device__ __forceinline__ long long dk_pending_grid(dk::Inst* in, long long cap) {
+  return dk_clamp_count(*reinterpret_cast<volatile unsigned long long*>(&in->count), cap);
+}
+
+// The buffer a launch from this owner hands to its child (sim.hpp:1530-1541).
+__device__ __forceinline__ dk::Inh dk_inherit_own(dk::Own* o, long long stride) {
+  __threadfence();
+  const unsigned long long b = *reinterpret_cast<volatile unsigned long long*>(&o->base);
+  if (b < 2 || b == dk::kNoBase) return dk::Inh{nullptr, 0, stride};
+  return dk::Inh{dk_rt.arena + (b - 2), dk_pending_own(o), stride};
+}
+__device__ __forceinline__ dk::Inh dk_inherit_grid(dk::Inst* in, long long stride, long long cap) {
+  __threadfence();
+  return dk::Inh{dk_rt.region[in->level & 1u], dk_pending_grid(in, cap), stride};
+}
+
+__device__ __forceinline__ long long dk_buf_word(const dk::Inh& h, long long i, long long w) {
+  if (i < 0 || i >= h.n) {
+    dk_fault(dk::F_BUFGET);
+    return 0;
+  }
+  return h.items[i * h.stride + w];
+}
+
+// ---- launches ----
+__device__ __forceinline__ dk::Inst* dk_new_inst(const dk::Inst* parent) {
+  const unsigned long long i = atomicAdd(&dk_rt.ctr[3], 1ull);
+  if (i >= dk_rt.inst_cap) {
+    dk_fault(dk::F_INST);
+    return nullptr;
+  }
+  dk::Inst* r = dk_rt.inst + i;
+  r->count = 0;
+  r->ticket = 0;
+  r->level = parent ? parent->level + 1 : 1;
+  r->aux = 0;
+  return r;
+}
+
+// State area of one split phase (one reservation per launch, CAS on aux).
+__device__ __noinline__ long long* dk_state_base(dk::Inst* in, long long words) {
+  unsigned long long b = atomicCAS(&in->aux, 0ull, 1ull);
+  if (b == 0) {
+    b = dk::kNoBase;
+    const unsigned long long off = atomicAdd(&dk_rt.ctr[2], static_cast<unsigned long long>(words));
+    if (off + words > dk_rt.arena_words) dk_fault(dk::F_POOL);
+    else b = off + 2;
+    atomicExch(&in->aux, b);
+  }
+  while (b == 1) {
+    __nanosleep(32);
+    b = atomicAdd(&in->aux, 0ull);
+  }
+  return b == dk::kNoBase ? nullptr : dk_rt.arena + (b - 2);
+}
+
+__device__ __forceinline__ bool dk_launch_ok(long long g, long long b) {
+  if (g < 1 || g > 0x7fffffffLL || b < 1 || b > 1024) {
+    dk_fault(dk::F_CONFIG);
+    return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void dk_launched(cudaError_t e) {
+  if (e != cudaSuccess) dk_fault(dk::F_LAUNCH);
+  else atomicAdd(&dk_rt.ctr[1], 1ull);
+}
+
+// Last-block election of one launch (transform.hpp:620-633 counter/exit
+// protocol); block-convergent, evaluated once per block.
+__device__ __forceinline__ long long dk_grid_last(dk::Inst* in, int* cache) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && *cache < 0) {
+    const unsigned t = atomicAdd(&in->ticket, 1u);
+    *cache = (t == gridDim.x - 1) ? 1 : 0;
+    __threadfence();
+  }
+  __syncthreads();
+  return *cache;
+}

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_DIR = os.path.join(ROOT, "oracle")
 LIB = os.path.join(ORACLE_DIR, "liboracle.so")
 REF = os.path.join(ORACLE_DIR, "_ref", "libref_sim.so")
-KDL_DIR = os.path.join(ORACLE_DIR, "kdl")
+KDL_DIR = os.path.join(ROOT, "paper_1606_08150_b200", "kdl", "programs")
 
 
 def _p(a):

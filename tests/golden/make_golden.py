@@ -1,7 +1,7 @@
 """Generates the golden fixtures in this directory by running the REFERENCE
 itself: the unmodified dpcons simulator (oracle/_ref/libref_sim.so, compiled
 in place from /root/reference/proj/include) executing our .kdl formulations
-(oracle/kdl/) in basic / warp / block / grid mode.  Run here (the container
+(paper_1606_08150_b200/kdl/programs/) in basic / warp / block / grid mode.  Run here (the container
 with /root/reference); the JSON fixtures are committed so the CPU tests can
 pin oracle/oracle.c without the reference present.
 

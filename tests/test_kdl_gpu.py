@@ -1,0 +1,182 @@
+"""GPU parity of the .kdl -> sm_100a compiler: the
+generated CUDA, run on the B200 with CDP2 device launches, against the
+reference simulator's results on the same programs and inputs
+(tests/golden/reference_runs.json, tests/golden/kdl_reference.json), and
+against the oracle at larger sizes.  Integer programs are bit-exact; fp64
+SpMV within 1e-12 relative (atomicAdd order)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1606_08150_b200 as dpc
+import paper_1606_08150_b200.kdl as kdl
+from paper_1606_08150_b200.kdl import transform as T
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "reference_runs.json")))
+KG = json.load(open(os.path.join(HERE, "golden", "kdl_reference.json")))
+MODES = ["basic", "warp", "block", "grid"]
+INF = 2**40
+_cache = {}
+
+
+def src_of(name):
+    p = os.path.join(kdl.PROGRAMS, name)
+    if not os.path.exists(p):
+        p = os.path.join(HERE, "kdl", name)
+    return open(p).read()
+
+
+def module(name, mode, k20c=False):
+    key = (name, mode, k20c)
+    if key not in _cache:
+        if k20c and mode != "basic":
+            prog = T.lower_kc(kdl.consolidate(kdl.parse_program(src_of(name)), mode), T.k20c_occupancy)
+            _cache[key] = kdl.compile_program(prog, mode, name=name[:-4] + "_k20c", consolidated=True)
+        else:
+            _cache[key] = kdl.compile(src_of(name), mode, name=name[:-4])
+    return _cache[key]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_spmv_program_matches_reference(mode):
+    for case in GOLD["spmv"]:
+        n, m = len(case["rowptr"]) - 1, len(case["col"])
+        res = module("spmv.kdl", mode).run(
+            {"n": n, "m": m, "nx": n, "thr": 32},
+            {"rowptr": case["rowptr"], "col": case["col"], "val": case["val"], "x": case["x"]})
+        ref = np.array(case["ref"][mode]["y"])
+        np.testing.assert_allclose(res.arrays["y"], ref, rtol=1e-12, atol=1e-12)
+        # launches: one per heavy row (basic), per non-empty warp / block
+        # buffer, one per grid — the simulator's childLaunchCount
+        assert res.launches == case["ref"][mode]["childLaunchCount"]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sssp_program_matches_reference(mode):
+    for case in GOLD["sssp"]:
+        n, m = len(case["rowptr"]) - 1, len(case["col"])
+        dist = np.full(n, INF, np.int64)
+        dist[case["source"]] = 0
+        res = module("sssp.kdl", mode).run(
+            {"n": n, "m": m, "thr": 32},
+            {"rowptr": case["rowptr"], "col": case["col"], "w": case["w"], "dist": dist},
+            until_stable="dist")
+        d = np.where(res.arrays["dist"] >= INF, 2**32 - 1, res.arrays["dist"])
+        np.testing.assert_array_equal(d, np.array(case["ref"][mode]["dist"]))
+
+
+def tree_inputs(shape, out):
+    t = dpc.gen_tree(*shape)
+    scal = {"n": t.n, "root": t.root, "rootnc": len(t.children(t.root))}
+    arrs = {"cstart": t.cstart, "clist": t.clist, "parent": t.parent, out: np.zeros(t.n, np.int64)}
+    return t, scal, arrs
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_tree_programs_match_reference(mode):
+    for case in GOLD["tree"]:
+        for name, out, fix in [("td.kdl", "desc", False), ("th.kdl", "height", True)]:
+            t, scal, arrs = tree_inputs(case["shape"], out)
+            assert t.parent.tolist() == case["parent"]
+            res = module(name, mode).run(scal, arrs, until_stable=out if fix else None)
+            np.testing.assert_array_equal(res.arrays[out], np.array(case["ref"][mode][out]))
+
+
+@pytest.mark.parametrize("mode", ["warp", "block", "grid"])
+def test_recursive_launch_counts_match_simulator(mode):
+    """With the reference's K20c launch sizes the recursive consolidation
+    issues exactly the simulator's number of device launches."""
+    for case in GOLD["tree"]:
+        t, scal, arrs = tree_inputs(case["shape"], "desc")
+        res = module("td.kdl", mode, k20c=True).run(scal, arrs)
+        np.testing.assert_array_equal(res.arrays["desc"], np.array(case["ref"][mode]["desc"]))
+        assert res.launches == case["ref"][mode]["desc_childLaunchCount"]
+
+
+@pytest.mark.parametrize("name", ["solo.kdl", "mold.kdl", "post.kdl"])
+@pytest.mark.parametrize("mode", MODES)
+def test_shape_programs_match_reference(name, mode):
+    """Solo-thread, moldable multi-block and grid-postwork children, and a
+    top-level sync_device (split into tail-launched phases on CDP2)."""
+    r = KG["runs"]
+    scal = {"n": len(r["rowptr"]) - 1, "m": len(r["col"]), "t": r["t"]}
+    n, m = scal["n"], scal["m"]
+    arrays = {"solo.kdl": {"rowptr": r["rowptr"], "col": r["col"]},
+              "mold.kdl": {"rowptr": r["rowptr"], "val": r["val"]},
+              "post.kdl": {"rowptr": r["rowptr"], "col": r["col"]}}[name]
+    out = {"solo.kdl": "sum", "mold.kdl": "scaled", "post.kdl": "out"}[name]
+    res = module(name, mode).run(scal, arrays)
+    want = r[name][mode]
+    # post.kdl basic / warp / block: + the tail launch of the phase after sync_device
+    extra = 1 if name == "post.kdl" and mode != "grid" else 0
+    assert res.launches == want["childLaunchCount"] + extra
+    if (name, mode) == ("post.kdl", "grid"):
+        # the reference's own grid rewrite of this program is wrong (its
+        # postwork kernel reads an undefined `v`, see tests/test_kdl.py);
+        # ours must equal the other three modes' reference result
+        basic = np.array(r[name]["basic"]["out"])
+        assert not np.array_equal(np.array(want["out"]), basic)
+        want = r[name]["basic"]
+    if out == "scaled":
+        np.testing.assert_allclose(res.arrays[out], np.array(want["out"]), rtol=1e-15)
+    else:
+        np.testing.assert_array_equal(res.arrays[out], np.array(want["out"]))
+    assert res.arrays[out].shape == ((m,) if out == "scaled" else (n,))
+
+
+@pytest.mark.parametrize("mode", ["warp", "block", "grid"])
+def test_reference_consolidated_text_runs(mode):
+    """The backend runs the reference's own consolidate() output."""
+    case = GOLD["spmv"][1]
+    n, m = len(case["rowptr"]) - 1, len(case["col"])
+    mod = kdl.compile(KG["consolidated"]["spmv.kdl"][mode], mode, name="spmv_refcons", consolidated=True)
+    res = mod.run({"n": n, "m": m, "nx": n, "thr": 32},
+                  {"rowptr": case["rowptr"], "col": case["col"], "val": case["val"], "x": case["x"]})
+    np.testing.assert_allclose(res.arrays["y"], np.array(case["ref"][mode]["y"]), rtol=1e-12, atol=1e-12)
+
+
+FAULTY = """
+global int a[n];
+kernel child(int v) { atomicAdd(a, v % 8, 1); }
+kernel parent(int k) {
+    int v = blockIdx * blockDim + threadIdx;
+    #pragma dp consltdt(warp) buffer(custom, 2) work(v)
+    child<<<1, 1>>>(v);
+    a[k] = 1;
+}
+entry parent<<<1, 64>>>(0);
+"""
+
+
+def test_faults_are_reported():
+    with pytest.raises(kdl.KdlFault) as ei:
+        kdl.compile(FAULTY, "warp", name="faulty").run({"n": 8})
+    assert "overflow" in ei.value.kinds       # 32 inserts per warp, capacity 2
+    bad = FAULTY.replace("entry parent<<<1, 64>>>(0);", "entry parent<<<1, 64>>>(9);")
+    with pytest.raises(kdl.KdlFault) as ei:
+        kdl.compile(bad, "basic", name="faulty").run({"n": 8})
+    assert ei.value.kinds == ["runtime"]       # a[9] out of bounds
+
+
+def test_spmv_program_larger_vs_oracle(orc):
+    g = dpc.gen_rmat(14, 16, seed=5, weights=False, values=True)
+    x = (np.arange(g.n) % 13 + 1) / 16.0   # exact in fp32 (the oracle computes from fp32 inputs)
+    want = orc.spmv_f64(g.rowptr, g.col, g.val.astype(np.float64), x)
+    for mode in MODES:
+        res = module("spmv.kdl", mode).run({"n": g.n, "m": g.m, "nx": g.n, "thr": 32},
+                                          {"rowptr": g.rowptr, "col": g.col, "val": g.val, "x": x})
+        np.testing.assert_allclose(res.arrays["y"], want, rtol=1e-10, atol=1e-10)
+
+
+def test_tree_program_larger_vs_oracle(orc):
+    t = dpc.gen_tree(6, 4, 12, 0.6, 3)
+    want = orc.tree_desc(t.parent)
+    for mode in MODES:
+        _, scal, arrs = tree_inputs((6, 4, 12, 0.6, 3), "desc")
+        res = module("td.kdl", mode).run(scal, arrs)
+        np.testing.assert_array_equal(res.arrays["desc"], want)
