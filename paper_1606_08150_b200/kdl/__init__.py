@@ -283,26 +283,30 @@ class Module:
         return Result(out, launches, runs, kc, ms)
 
 
-def compile_program(prog, mode="basic", config=None, name="kdl", consolidated=False):
+def compile_program(prog, mode="basic", config=None, name="kdl", consolidated=False, schedule="block"):
     if mode not in MODES:
         raise ValueError(f"mode must be one of {MODES}")
     if not consolidated and mode != "basic":
-        prog = consolidate(prog, granularity=None if mode == "directive" else mode, config=config)
+        prog = consolidate(prog, granularity=None if mode == "directive" else mode, config=config,
+                           schedule=schedule)
     src, kc = generate(prog, name)
-    so = build_so(src, f"{name}_{mode}")
+    tag = f"{name}_{mode}" + ("" if schedule == "block" or consolidated or mode == "basic" else f"_{schedule}")
+    so = build_so(src, tag)
     return Module(prog, so, kc, mode)
 
 
-def compile(source, mode="basic", config=None, name="kdl", consolidated=False):  # noqa: A001
-    """.kdl text -> Module (compiled for sm_100a; cached under kdl/_build)."""
-    return compile_program(parse_program(source), mode, config, name, consolidated)
+def compile(source, mode="basic", config=None, name="kdl", consolidated=False, schedule="block"):  # noqa: A001
+    """.kdl text -> Module (compiled for sm_100a; cached under kdl/_build).
+    schedule="block" (default) drains multi-block children one item per
+    block; "reference" keeps the reference's drain loop."""
+    return compile_program(parse_program(source), mode, config, name, consolidated, schedule)
 
 
 def build_programs(jobs=8):
     """Pre-compile the bundled programs in every mode (called by build())."""
     from concurrent.futures import ThreadPoolExecutor
-    work = [(f, m) for f in sorted(os.listdir(PROGRAMS)) if f.endswith(".kdl")
+    work = [(f, m, "block") for f in sorted(os.listdir(PROGRAMS)) if f.endswith(".kdl")
             for m in ("basic", "warp", "block", "grid")]
     with ThreadPoolExecutor(jobs) as ex:
-        list(ex.map(lambda fm: compile(read_program(fm[0]), fm[1], name=fm[0][:-4]), work))
+        list(ex.map(lambda w: compile(read_program(w[0]), w[1], name=w[0][:-4], schedule=w[2]), work))
     return len(work)

@@ -167,7 +167,10 @@ class _Site:
 
 
 class _Consolidator:
-    def __init__(self, prog, gran_override, config, default_threads):
+    def __init__(self, prog, gran_override, config, default_threads, schedule="reference"):
+        if schedule not in ("reference", "block"):
+            raise ValueError("schedule must be 'reference' or 'block'")
+        self.schedule = schedule
         self.prog = prog
         self.gran_override = gran_override
         self.config = config or Config()
@@ -294,6 +297,20 @@ class _Consolidator:
             item.append(A.for_("__vt", A.intr("threadIdx"), A.ref("__ob"), A.intr("blockDim"),
                                subst(body, {"threadIdx": A.ref("__vt"), "blockIdx": A.lit(0),
                                             "blockDim": A.ref("__ob"), "gridDim": A.lit(1)})))
+            out.append(A.for_("__i", A.intr("blockIdx"), A.ref("__n"), A.intr("gridDim"), item))
+        elif self.schedule == "block":
+            # B200 schedule: one item per block, the item's virtual threads
+            # strided over the block.  Rebinding the four intrinsics to the
+            # item's own geometry is valid for every multi-block child
+            # (moldable or not); it removes the reference form's O(#items)
+            # loop that every thread of the grid runs.
+            item.append(A.let(A.INT, "__og", A.Expr("buf_cfg_grid", args=[A.ref("__i")])))
+            item.append(A.let(A.INT, "__ob", A.Expr("buf_cfg_block", args=[A.ref("__i")])))
+            tbl = {"threadIdx": A.binop("%", A.ref("__vt"), A.ref("__ob")),
+                   "blockIdx": A.binop("/", A.ref("__vt"), A.ref("__ob")),
+                   "blockDim": A.ref("__ob"), "gridDim": A.ref("__og")}
+            item.append(A.for_("__vt", A.intr("threadIdx"), A.binop("*", A.ref("__og"), A.ref("__ob")),
+                               A.intr("blockDim"), subst(body, tbl)))
             out.append(A.for_("__i", A.intr("blockIdx"), A.ref("__n"), A.intr("gridDim"), item))
         else:
             if p.moldable:
@@ -449,13 +466,16 @@ class _Consolidator:
         return body + self.tail(p, cons, args, grid, block, True)
 
 
-def consolidate(prog, granularity=None, config=None, default_threads=256):
+def consolidate(prog, granularity=None, config=None, default_threads=256, schedule="reference"):
     """Rewrite every annotated site of `prog` (ast.Program, not modified).
     `granularity` overrides the directives' consltdt clause (the reference's
-    TransformOptions.granularityOverride, transform.hpp:219-225)."""
+    TransformOptions.granularityOverride, transform.hpp:219-225).
+    `schedule` picks the multi-block drain: "reference" (transform.hpp:
+    538-566: the whole grid walks every item) or "block" (one item per
+    block; the B200 default of kdl.compile)."""
     if granularity not in (None, "warp", "block", "grid"):
         raise ValueError(f"granularity must be warp, block or grid, not {granularity!r}")
-    return _Consolidator(prog, granularity, config, default_threads).run()
+    return _Consolidator(prog, granularity, config, default_threads, schedule).run()
 
 
 def kc_blocks(occupancy_blocks, x):

@@ -31,22 +31,25 @@ def src_of(name):
     return open(p).read()
 
 
-def module(name, mode, k20c=False):
-    key = (name, mode, k20c)
+def module(name, mode, k20c=False, schedule="block"):
+    key = (name, mode, k20c, schedule)
     if key not in _cache:
         if k20c and mode != "basic":
             prog = T.lower_kc(kdl.consolidate(kdl.parse_program(src_of(name)), mode), T.k20c_occupancy)
             _cache[key] = kdl.compile_program(prog, mode, name=name[:-4] + "_k20c", consolidated=True)
         else:
-            _cache[key] = kdl.compile(src_of(name), mode, name=name[:-4])
+            _cache[key] = kdl.compile(src_of(name), mode, name=name[:-4], schedule=schedule)
     return _cache[key]
 
 
-@pytest.mark.parametrize("mode", MODES)
-def test_spmv_program_matches_reference(mode):
+SCHED = [(m, s) for m in MODES for s in ("block", "reference") if not (m == "basic" and s == "reference")]
+
+
+@pytest.mark.parametrize("mode,schedule", SCHED)
+def test_spmv_program_matches_reference(mode, schedule):
     for case in GOLD["spmv"]:
         n, m = len(case["rowptr"]) - 1, len(case["col"])
-        res = module("spmv.kdl", mode).run(
+        res = module("spmv.kdl", mode, schedule=schedule).run(
             {"n": n, "m": m, "nx": n, "thr": 32},
             {"rowptr": case["rowptr"], "col": case["col"], "val": case["val"], "x": case["x"]})
         ref = np.array(case["ref"][mode]["y"])
@@ -56,13 +59,13 @@ def test_spmv_program_matches_reference(mode):
         assert res.launches == case["ref"][mode]["childLaunchCount"]
 
 
-@pytest.mark.parametrize("mode", MODES)
-def test_sssp_program_matches_reference(mode):
+@pytest.mark.parametrize("mode,schedule", SCHED)
+def test_sssp_program_matches_reference(mode, schedule):
     for case in GOLD["sssp"]:
         n, m = len(case["rowptr"]) - 1, len(case["col"])
         dist = np.full(n, INF, np.int64)
         dist[case["source"]] = 0
-        res = module("sssp.kdl", mode).run(
+        res = module("sssp.kdl", mode, schedule=schedule).run(
             {"n": n, "m": m, "thr": 32},
             {"rowptr": case["rowptr"], "col": case["col"], "w": case["w"], "dist": dist},
             until_stable="dist")
@@ -99,8 +102,8 @@ def test_recursive_launch_counts_match_simulator(mode):
 
 
 @pytest.mark.parametrize("name", ["solo.kdl", "mold.kdl", "post.kdl"])
-@pytest.mark.parametrize("mode", MODES)
-def test_shape_programs_match_reference(name, mode):
+@pytest.mark.parametrize("mode,schedule", SCHED)
+def test_shape_programs_match_reference(name, mode, schedule):
     """Solo-thread, moldable multi-block and grid-postwork children, and a
     top-level sync_device (split into tail-launched phases on CDP2)."""
     r = KG["runs"]
@@ -110,7 +113,7 @@ def test_shape_programs_match_reference(name, mode):
               "mold.kdl": {"rowptr": r["rowptr"], "val": r["val"]},
               "post.kdl": {"rowptr": r["rowptr"], "col": r["col"]}}[name]
     out = {"solo.kdl": "sum", "mold.kdl": "scaled", "post.kdl": "out"}[name]
-    res = module(name, mode).run(scal, arrays)
+    res = module(name, mode, schedule=schedule).run(scal, arrays)
     want = r[name][mode]
     # post.kdl basic / warp / block: + the tail launch of the phase after sync_device
     extra = 1 if name == "post.kdl" and mode != "grid" else 0
@@ -167,8 +170,8 @@ def test_spmv_program_larger_vs_oracle(orc):
     g = dpc.gen_rmat(14, 16, seed=5, weights=False, values=True)
     x = (np.arange(g.n) % 13 + 1) / 16.0   # exact in fp32 (the oracle computes from fp32 inputs)
     want = orc.spmv_f64(g.rowptr, g.col, g.val.astype(np.float64), x)
-    for mode in MODES:
-        res = module("spmv.kdl", mode).run({"n": g.n, "m": g.m, "nx": g.n, "thr": 32},
+    for mode, schedule in SCHED:
+        res = module("spmv.kdl", mode, schedule=schedule).run({"n": g.n, "m": g.m, "nx": g.n, "thr": 32},
                                           {"rowptr": g.rowptr, "col": g.col, "val": g.val, "x": x})
         np.testing.assert_allclose(res.arrays["y"], want, rtol=1e-10, atol=1e-10)
 
