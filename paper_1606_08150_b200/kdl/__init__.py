@@ -40,6 +40,7 @@ __all__ = ["compile", "compile_program", "Module", "KdlError", "KdlFault", "Conf
 HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD = os.path.join(HERE, "_build")
 PROGRAMS = os.path.join(HERE, "programs")
+INCLUDE = os.path.join(os.path.dirname(os.path.dirname(HERE)), "include")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-rdc=true", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 NVCC_LIBS = ["-lcudadevrt", "-lcudart_static", "-lpthread", "-ldl", "-lrt"]
@@ -78,8 +79,10 @@ _build_lock = threading.Lock()
 def build_so(cu_src, tag):
     """Compile one generated unit into paper_1606_08150_b200/kdl/_build/
     (cached by content hash; the .so travels with the repo snapshot)."""
-    with open(os.path.join(HERE, "kdl_rt.cuh")) as f:
-        rt = f.read()
+    rt = ""
+    for hdr in (os.path.join(HERE, "kdl_rt.cuh"), os.path.join(INCLUDE, "dpc_kdl.h")):
+        with open(hdr) as f:
+            rt += f.read()
     h = hashlib.sha1((cu_src + rt + " ".join(NVCC_FLAGS)).encode()).hexdigest()[:16]
     so = os.path.join(BUILD, f"{tag}_{h}.so")
     if os.path.exists(so):
@@ -89,7 +92,7 @@ def build_so(cu_src, tag):
     with open(cu, "w") as f:
         f.write(cu_src)
     tmp = so + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", HERE, cu, "-o", tmp, *NVCC_LIBS]
+    cmd = [_nvcc(), *NVCC_FLAGS, "-I", HERE, "-I", INCLUDE, cu, "-o", tmp, *NVCC_LIBS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise KdlError("cuda.nvcc", f"nvcc failed for {cu}:\n{r.stderr[-4000:]}")

@@ -341,7 +341,8 @@ class Builder:
             return [f"{ind}*{p} = {self.ex(s.exprs[1])};"]
         if k == "atomic":
             aid, t = self.array_of(s.name)
-            return [f"{ind}{self.atomic(aid, t, s.exprs[0], s.exprs[1])};"]
+            code = self.atomic(aid, t, s.exprs[0], s.exprs[1])
+            return [f"{ind}{code.replace('dk_atomic_', 'dk_add_', 1)};"]
         if k == "if":
             out = [f"{ind}if (({self.ex(s.exprs[0])}) != 0) {{"]
             out += self.emit_body(s.body, ind + "  ")

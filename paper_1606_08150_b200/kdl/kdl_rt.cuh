@@ -25,6 +25,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include "dpc_kdl.h"
+
 namespace dk {
 
 enum : unsigned long long {
@@ -74,6 +76,9 @@ struct Rt {
 
 constexpr unsigned long long kNoBase = ~0ull;
 
+static_assert(sizeof(Rt) == sizeof(dk_rt_t), "dk::Rt must match include/dpc_kdl.h");
+static_assert(sizeof(Inst) == 24, "launch records are 24 bytes (include/dpc_kdl.h)");
+
 }  // namespace dk
 
 __constant__ dk::Rt dk_rt;
@@ -97,11 +102,70 @@ __device__ __forceinline__ long long* dk_ip(long long id, long long i) {
 __device__ __forceinline__ double* dk_fp(long long id, long long i) {
   return dk_ok(id, i) ? static_cast<double*>(dk_rt.arr[id]) + i : dk_sink_f;
 }
-__device__ __forceinline__ long long dk_atomic_i(long long* p, long long v) {
-  return static_cast<long long>(atomicAdd(reinterpret_cast<unsigned long long*>(p),
-                                          static_cast<unsigned long long>(v)));
+// atomicAdd, warp-aggregated per address: the lanes of a warp that hit the
+// same element (__match_any_sync) combine their values with shuffles and one
+// lane issues the atomic; each lane still gets a distinct "old" value (the
+// aggregate's old + its exclusive prefix), a valid order of the original
+// atomics.  Same-address atomics serialise in L2, so this turns a hot
+// ancestor / row update from 32 serial atomics into one.
+template <class T>
+__device__ __forceinline__ T dk_atomic_agg(T* p, T v) {
+  const unsigned m = __activemask();
+  const unsigned peers = __match_any_sync(m, reinterpret_cast<unsigned long long>(p));
+  const unsigned lane = threadIdx.x & 31u;
+  if (peers == (1u << lane)) return atomicAdd(p, v);
+  const int leader = __ffs(peers) - 1;
+  T total = T(0), pre = T(0);
+  for (unsigned r = peers; r; r &= r - 1) {
+    const int l = __ffs(r) - 1;
+    const T x = __shfl_sync(peers, v, l);
+    total += x;
+    if (static_cast<unsigned>(l) < lane) pre += x;
+  }
+  T old = T(0);
+  if (lane == static_cast<unsigned>(leader)) old = atomicAdd(p, total);
+  return __shfl_sync(peers, old, leader) + pre;
 }
-__device__ __forceinline__ double dk_atomic_f(double* p, double v) { return atomicAdd(p, v); }
+// Statement form (result unused): when every active lane of the warp hits
+// the same element, the lanes combine first and one lane issues the atomic
+// (ints: three redux.sync on 16/16/32-bit pieces, exact mod 2^64; doubles: a
+// butterfly for a full warp, a shuffle loop otherwise); mixed addresses go
+// out as plain fire-and-forget REDs.
+__device__ __forceinline__ void dk_add_i(long long* p, long long v) {
+  const unsigned m = __activemask();
+  unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
+  if (__match_any_sync(m, reinterpret_cast<unsigned long long>(p)) != m) {
+    atomicAdd(q, static_cast<unsigned long long>(v));
+    return;
+  }
+  const unsigned long long u = static_cast<unsigned long long>(v);
+  const unsigned lo16 = __reduce_add_sync(m, static_cast<unsigned>(u & 0xffffu));
+  const unsigned hi16 = __reduce_add_sync(m, static_cast<unsigned>((u >> 16) & 0xffffu));
+  const unsigned hi32 = __reduce_add_sync(m, static_cast<unsigned>(u >> 32));
+  if ((threadIdx.x & 31u) == static_cast<unsigned>(__ffs(m) - 1))
+    atomicAdd(q, (static_cast<unsigned long long>(hi32) << 32) + (static_cast<unsigned long long>(hi16) << 16) +
+                     lo16);
+}
+__device__ __forceinline__ void dk_add_f(double* p, double v) {
+  const unsigned m = __activemask();
+  if (__match_any_sync(m, reinterpret_cast<unsigned long long>(p)) != m) {
+    atomicAdd(p, v);
+    return;
+  }
+  if (m == 0xffffffffu) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
+  } else {
+    double t = 0.0;
+    for (unsigned r = m; r; r &= r - 1) t += __shfl_sync(m, v, __ffs(r) - 1);
+    v = t;
+  }
+  if ((threadIdx.x & 31u) == static_cast<unsigned>(__ffs(m) - 1)) atomicAdd(p, v);
+}
+__device__ __forceinline__ long long dk_atomic_i(long long* p, long long v) {
+  return static_cast<long long>(dk_atomic_agg(reinterpret_cast<unsigned long long*>(p),
+                                              static_cast<unsigned long long>(v)));
+}
+__device__ __forceinline__ double dk_atomic_f(double* p, double v) { return dk_atomic_agg(p, v); }
 
 // ---- arithmetic with the simulator's fault rules (sim.hpp:1574-1590) ----
 __device__ __forceinline__ long long dk_idiv(long long a, long long b) {
