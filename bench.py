@@ -479,6 +479,15 @@ def run_ours(args):
         from prof_apps import run_apps
         dg.close()
         out["apps"] = run_apps(ctx, args.apps, reps=2)
+    if rank == 0 and world == 1 and args.kdl:
+        # the DSL compiler's output: bundled .kdl programs
+        # compiled for sm_100a in basic / warp / block / grid mode
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from kdl_bench import run_compiled
+        try:
+            out["kdl"] = run_compiled(reps=2)
+        except Exception as e:  # noqa: BLE001 - the headline line must still print
+            out["kdl"] = {"error": str(e)[:300]}
     if rank == 0:
         print(json.dumps(out), flush=True)
     dg.close()
@@ -563,6 +572,8 @@ def main():
     ap.add_argument("--ref-stride", type=int, default=256)
     ap.add_argument("--multi", action="store_true",
                     help="run the partitioned (config 5) path even on one rank (testing)")
+    ap.add_argument("--no-kdl", dest="kdl", action="store_false",
+                    help="skip timing the DSL compiler's generated programs")
     ap.add_argument("--apps", nargs="*",
                     default=["sssp", "bfs", "pr", "gc", "td", "th", "td_paper", "th_paper", "td_deep_fit",
                              "th_deep_fit"],

@@ -175,5 +175,9 @@ def test_generated_unit_builds_for_sm100a(tmp_path, monkeypatch):
     assert os.path.exists(mod.so)
     import subprocess
     out = subprocess.run(["nm", "-D", mod.so], capture_output=True, text=True).stdout
-    for sym in ("dk_init", "dk_set_rt", "dk_launch_entry", "dk_kc_values", "dk_sizeof_rt", "dk_error"):
+    import re
+    hdr = open(os.path.join(os.path.dirname(HERE), "include", "dpc_kdl.h")).read()
+    syms = re.findall(r"^(?:int|const char\*) (dk_\w+)\(", hdr, re.M)
+    assert len(syms) == 7
+    for sym in syms:   # every entry point include/dpc_kdl.h declares
         assert f" T {sym}" in out, sym

@@ -22,7 +22,7 @@ for s in $STAGES; do
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
         --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --variants grid \
-        --no-cpu-baseline --apps > gpurun_out/ncu_launch_bench.log 2>&1
+        --no-cpu-baseline --no-kdl --apps > gpurun_out/ncu_launch_bench.log 2>&1
       echo "ncu-launches rc=$?" ;;
     full)
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:grid_stream \

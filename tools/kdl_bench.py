@@ -41,12 +41,12 @@ def best(fn, reps):
     return min(ms), out
 
 
-def spmv(scale, reps, orc):
+def spmv(scale, reps, orc, runs=None):
     g = dpc.gen_rmat(scale, 16, seed=7, weights=False, values=True)
     x = ((np.arange(g.n) % 97) + 1) / 128.0
     want = orc.spmv_f64(g.rowptr, g.col, g.val, x)
     rows = {}
-    for mode, sch in RUNS:
+    for mode, sch in runs or RUNS:
         mod = kdl.compile(kdl.read_program("spmv.kdl"), mode, name="spmv", schedule=sch)
         try:
             ms, res = best(lambda: mod.run({"n": g.n, "m": g.m, "nx": g.n, "thr": 32},
@@ -60,12 +60,12 @@ def spmv(scale, reps, orc):
     return {"workload": f"spmv.kdl, R-MAT scale {scale} ef 16 ({g.n} rows, {g.m} nnz), thr 32", "modes": rows}
 
 
-def sssp(scale, reps, orc):
+def sssp(scale, reps, orc, runs=None):
     g = dpc.gen_rmat(scale, 16, seed=3)
     s = int(np.argmax(g.degrees()))
     want = orc.sssp(g.rowptr, g.col, g.w, s)
     rows = {}
-    for mode, sch in RUNS:
+    for mode, sch in runs or RUNS:
         mod = kdl.compile(kdl.read_program("sssp.kdl"), mode, name="sssp", schedule=sch)
         dist = np.full(g.n, INF, np.int64)
         dist[s] = 0
@@ -138,6 +138,28 @@ def hand_written(scale_spmv, scale_sssp, shape):
         out[f"td/{v}"] = round((time.perf_counter() - t0) / 3 * 1e3, 4)
     ctx.close()
     return out
+
+
+def summarize(app):
+    ms = {k: v["ms"] for k, v in app["modes"].items() if "ms" in v}
+    if "basic" in ms:
+        best = min((v, k) for k, v in ms.items() if k in ("warp", "block", "grid"))
+        app["best_consolidated"] = best[1]
+        app["best_vs_basic"] = round(ms["basic"] / best[0], 2)
+    return app
+
+
+def run_compiled(reps=2, scale_spmv=18, scale_sssp=16, shape=(5, 32, 128, 0.4, 1)):
+    """bench.py's `kdl` object: the compiler's output for the bundled
+    programs (B200 drain schedule), each checked against the oracle."""
+    from tests._oracle import Oracle
+    orc = Oracle()
+    runs = [(m, "block") for m in MODES]
+    return {"spmv": summarize(spmv(scale_spmv, reps, orc, runs)),
+            "sssp": summarize(sssp(scale_sssp, reps, orc, runs)),
+            "td": summarize(tree(list(shape), reps, orc)),
+            "note": "generated by paper_1606_08150_b200.kdl from the .kdl programs (int64 / fp64 data, "
+                    "CDP2 device launches); device time of the entry launch tree, CUDA events"}
 
 
 def main():
