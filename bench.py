@@ -425,7 +425,32 @@ def run_ours(args):
         ctx.record(3)
         e2e_ms.append(ctx.elapsed_ms(2, 3))
     e2e_ok = bool(np.all(np.abs(ya.astype(np.float64) - y64) <= 1e-5 * np.abs(y64)))
-    e2e_max = _max_over_ranks(dist, float(np.mean(e2e_ms)))
+    e2e_sync_max = _max_over_ranks(dist, float(np.mean(e2e_ms)))
+    # serving form: dpc_spmv_host_batch over the K steps, copy-in of vector
+    # i+1 and copy-out of vector i-1 overlapping SpMV i (every vector still
+    # crosses PCIe both ways inside the timed region); 4 rotating pinned
+    # host vector pairs; no L2 flush inside the pipeline (A + x + y > L2)
+    nbuf = 4
+    xhs = [dpc._lib.dpc_host_alloc(4 * n) for _ in range(nbuf)]
+    yhs = [dpc._lib.dpc_host_alloc(4 * n) for _ in range(nbuf)]
+    xbs = [np.frombuffer((C.c_float * n).from_address(p), np.float32) for p in xhs]
+    ybs = [np.frombuffer((C.c_float * n).from_address(p), np.float32) for p in yhs]
+    for xb in xbs:
+        xb[:] = x
+    dg.spmv_host_batch([xbs[i % nbuf] for i in range(max(2, args.warmup))],
+                       [ybs[i % nbuf] for i in range(max(2, args.warmup))], "grid")
+    for yb in ybs:
+        yb[:] = 0
+    _barrier(dist)
+    ctx.flush_l2()
+    ctx.record(2)
+    dg.spmv_host_batch([xbs[i % nbuf] for i in range(args.steps)], [ybs[i % nbuf] for i in range(args.steps)],
+                       "grid")
+    ctx.record(3)
+    batch_ms = ctx.elapsed_ms(2, 3) / max(1, args.steps)
+    e2e_ok = e2e_ok and all(bool(np.all(np.abs(ybs[i].astype(np.float64) - y64) <= 1e-5 * np.abs(y64)))
+                            for i in range(min(nbuf, args.steps)))
+    e2e_max = _max_over_ranks(dist, batch_ms)
     e2e_value = total_nnz / (e2e_max * 1e-3) / 1e9
 
     peaks = {}
@@ -461,7 +486,12 @@ def run_ours(args):
                    "max_rel_err": float(err.max())},
         "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS", "h2d_bytes_per_step": 4 * n,
                 "d2h_bytes_per_step": 4 * n, "ms_per_step": round(e2e_max, 4),
-                "api": "dpc_spmv_host (C ABI), pinned host x/y, A resident"},
+                "api": "dpc_spmv_host_batch (C ABI): K host vectors, copy-in / SpMV / copy-out pipelined "
+                       "over two copy streams; pinned host x/y, A resident; no L2 flush inside the batch "
+                       "(A + x + y = 147 MB > 126 MB L2)",
+                "sync_per_call": {"value": round(total_nnz / (e2e_sync_max * 1e-3) / 1e9, 3),
+                                  "ms_per_step": round(e2e_sync_max, 4),
+                                  "api": "dpc_spmv_host (C ABI), one synchronous call per step, L2 flushed"}},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(),
                      "traffic_source": "profiles/r01_spmv_grid_stream.txt (ncu --set full, dram bytes read+write per launch)",

@@ -297,6 +297,15 @@ int32_t* dpc_dtree_result(dpc_dtree* dt);
 dpc_status dpc_spmv_host(dpc_ctx* ctx, dpc_dgraph* dg, const float* x_host, float* y_host,
                          const dpc_launch_cfg* cfg, dpc_metrics* met);
 
+/* The same over `count` independent host vectors, pipelined: vector i+1's
+ * host->device copy and vector i-1's device->host copy overlap vector i's
+ * SpMV (two copy streams + the context stream, two device slots).  Returns
+ * when every y is in host memory.  Host vectors should be pinned
+ * (dpc_host_alloc) for the copies to overlap.  Serving form of the
+ * reference's per-call simulate() (sim.hpp:1746). */
+dpc_status dpc_spmv_host_batch(dpc_ctx* ctx, dpc_dgraph* dg, const float* const* x_host, float* const* y_host,
+                               int64_t count, const dpc_launch_cfg* cfg, dpc_metrics* met);
+
 /* Device memory on the context's GPU (caller-owned vectors for the
  * device-pointer entry points). */
 void* dpc_dev_alloc(dpc_ctx* ctx, size_t bytes);

@@ -150,6 +150,7 @@ _SIGS = {
     "dpc_dgraph_trace": (C.c_int, [_P, _P, _i64]),
     "dpc_spmv_device": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_spmv_host_batch": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_sssp_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_bfs_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_run_bfs": (C.c_int, [_P, _CsrP, _i32, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
@@ -512,6 +513,17 @@ class DeviceGraph:
         _check(_lib.dpc_spmv_host(self.ctx.handle, self._h, x.ctypes.data_as(C.c_void_p),
                                   y.ctypes.data_as(C.c_void_p), _cfg_arg("spmv", variant, cfg),
                                   None))
+
+    def spmv_host_batch(self, xs, ys, variant="grid", cfg=None):
+        """Pipelined end-to-end SpMV over len(xs) host vectors (pinned for
+        overlap): copy-in / kernel / copy-out of consecutive vectors overlap."""
+        if len(xs) != len(ys):
+            raise ValueError("xs and ys must have the same length")
+        k = len(xs)
+        xp = (C.c_void_p * max(1, k))(*[x.ctypes.data for x in xs])
+        yp = (C.c_void_p * max(1, k))(*[y.ctypes.data for y in ys])
+        _check(_lib.dpc_spmv_host_batch(self.ctx.handle, self._h, xp, yp, k, _cfg_arg("spmv", variant, cfg),
+                                        None))
 
     def sssp(self, source: int, variant="grid", cfg=None, metrics: bool = True):
         met = Metrics() if metrics else None

@@ -218,6 +218,10 @@ void dpc_ctx_destroy(dpc_ctx* c) {
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->flush_buf) cudaFree(c->flush_buf);
+  for (auto& ev : c->pev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -306,7 +310,8 @@ void dpc_dgraph_free(dpc_dgraph* g) {
   void* bufs[] = {g->rowptr, g->col,      g->w,        g->val,   g->x,    g->y,
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
                   g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val,
-                  g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt, g->gc_q, g->gc_hstate, g->trace};
+                  g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt, g->gc_q, g->gc_hstate, g->trace,
+                  g->x2, g->y2};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->ms_state) dpc::sssp_state_free(g->ms_state);
@@ -402,6 +407,58 @@ dpc_status dpc_spmv_host(dpc_ctx* c, dpc_dgraph* g, const float* x, float* y,
   if (st != DPC_OK) return st;
   DPC_CUDA(cudaMemcpyAsync(y, g->y, ybytes, cudaMemcpyDeviceToHost, c->stream));
   DPC_CUDA(cudaStreamSynchronize(c->stream));
+  return DPC_OK;
+}
+
+// Pipelined host-vector SpMV over `count` independent vectors (serving
+// form of dpc_spmv_host): two device x / y slots; copy-in on one stream,
+// the SpMV on the context stream, copy-out on a third, so vector i+1's
+// host->device copy and vector i-1's device->host copy overlap vector i's
+// kernel on the two copy engines.  Every vector still crosses PCIe both ways.
+dpc_status dpc_spmv_host_batch(dpc_ctx* c, dpc_dgraph* g, const float* const* xs, float* const* ys,
+                               int64_t count, const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!c || !g || !xs || !ys || count < 0) return fail(DPC_E_INVALID, "bad arguments");
+  for (int64_t i = 0; i < count; i++)
+    if (!xs[i] || !ys[i]) return fail(DPC_E_INVALID, "NULL vector in batch");
+  DPC_CUDA(cudaSetDevice(c->device));
+  if (!c->h2d) {
+    DPC_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    DPC_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (auto& ev : c->pev) DPC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  const size_t xbytes = sizeof(float) * static_cast<size_t>(g->ncols);
+  const size_t ybytes = sizeof(float) * static_cast<size_t>(g->n);
+  if (!g->x2) {
+    DPC_CUDA(cudaMalloc(&g->x2, xbytes + 16));
+    DPC_CUDA(cudaMalloc(&g->y2, ybytes + 16));
+  }
+  float* dx[2] = {g->x, g->x2};
+  float* dy[2] = {g->y, g->y2};
+  // pev: [0,1] x ready  [2,3] x free  [4,5] y ready  [6,7] y free  [8] start
+  cudaEvent_t* e = c->pev;
+  DPC_CUDA(cudaEventRecord(e[8], c->stream));
+  DPC_CUDA(cudaStreamWaitEvent(c->h2d, e[8], 0));
+  DPC_CUDA(cudaStreamWaitEvent(c->d2h, e[8], 0));
+  for (int64_t i = 0; i < count; i++) {
+    const int s = static_cast<int>(i & 1);
+    if (i >= 2) DPC_CUDA(cudaStreamWaitEvent(c->h2d, e[2 + s], 0));
+    DPC_CUDA(cudaMemcpyAsync(dx[s], xs[i], xbytes, cudaMemcpyHostToDevice, c->h2d));
+    DPC_CUDA(cudaEventRecord(e[s], c->h2d));
+    DPC_CUDA(cudaStreamWaitEvent(c->stream, e[s], 0));
+    if (i >= 2) DPC_CUDA(cudaStreamWaitEvent(c->stream, e[6 + s], 0));
+    dpc_status st = dpc_spmv_device(c, g, dx[s], dy[s], cfg, i + 1 == count ? met : nullptr);
+    if (st != DPC_OK) return st;
+    DPC_CUDA(cudaEventRecord(e[2 + s], c->stream));
+    DPC_CUDA(cudaEventRecord(e[4 + s], c->stream));
+    DPC_CUDA(cudaStreamWaitEvent(c->d2h, e[4 + s], 0));
+    DPC_CUDA(cudaMemcpyAsync(ys[i], dy[s], ybytes, cudaMemcpyDeviceToHost, c->d2h));
+    DPC_CUDA(cudaEventRecord(e[6 + s], c->d2h));
+  }
+  // the context stream (and its timing events) is ordered after the last copy-out
+  DPC_CUDA(cudaEventRecord(e[8], c->d2h));
+  DPC_CUDA(cudaStreamWaitEvent(c->stream, e[8], 0));
+  DPC_CUDA(cudaStreamSynchronize(c->d2h));
   return DPC_OK;
 }
 

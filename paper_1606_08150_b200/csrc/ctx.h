@@ -24,6 +24,10 @@ struct dpc_ctx {
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
   int coop = 0;  // cooperative launch supported
+  // pipelined host-vector runs (dpc_spmv_host_batch): copy-in / copy-out
+  // streams and per-slot events, created on first use
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t pev[9] = {};
 };
 
 // Device-resident graph plus every buffer its apps need.
@@ -54,6 +58,8 @@ struct dpc_dgraph {
   dpc::dev::RunHeader* hdr = nullptr;  // device counters
   dpc::dev::RunHeader* hdr_host = nullptr;  // pinned mirror
   bool hdr_clean = false;  // the last run (SpMV stream) left the header zeroed itself
+  float* x2 = nullptr;     // second x / y slot of the pipelined host-vector path
+  float* y2 = nullptr;
   // consolidation pool
   dpc::dev::Item* items = nullptr;
   unsigned cap = 0;

@@ -165,3 +165,19 @@ def test_spmv_device_heap_allocator(ctx, orc, variant):
     y, met = dpc.run_spmv(g, x, variant, cfg=cfg, ctx=ctx)
     _check(orc, g, x, y)
     assert met.child_launch_count > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("count", [1, 2, 5])
+def test_spmv_host_batch_pipelined(ctx, orc, count):
+    """dpc_spmv_host_batch: distinct host vectors through the pipelined
+    copy-in / SpMV / copy-out path, each y checked against the oracle."""
+    g = dpc.gen_rmat(14, 16, seed=9, weights=False, values=True)
+    dg = dpc.DeviceGraph(ctx, g)
+    xs = [((np.arange(g.n) * (i + 3)) % 101 + 1).astype(np.float32) / 101.0 for i in range(count)]
+    ys = [np.zeros(g.n, np.float32) for _ in range(count)]
+    dg.spmv_host_batch(xs, ys, "grid")
+    for x, y in zip(xs, ys):
+        y64 = orc.spmv_f64(g.rowptr, g.col, g.val, x)
+        assert np.all(np.abs(y - y64) <= 1e-5 * np.abs(y64) + 1e-30)
+    dg.close()
