@@ -70,6 +70,28 @@ def main():
                                         out_float=is_float)
             runs.setdefault(name, {})[mode] = ({"out": res.tolist(), "childLaunchCount": met["childLaunchCount"]}
                                                if rc == 0 else {"error": err})
+    # BFS-Rec (bundled bfs.kdl): sweeps to a fixpoint; first-run launches
+    gb = dpc.gen_rmat(8, 8, seed=4)
+    s = int(np.argmax(gb.degrees()))
+    bfs = {"rowptr": gb.rowptr.tolist(), "col": gb.col.tolist(), "src": s}
+    for mode in MODES:
+        lev = np.full(gb.n, 2**40, np.int64)
+        lev[s] = 0
+        first = None
+        while True:
+            rc, res, met, err = ref.run(srcs["bfs.kdl"], mode,
+                                        {"n": gb.n, "m": gb.m, "src": s, "srcs": int(gb.rowptr[s]),
+                                         "srce": int(gb.rowptr[s + 1])},
+                                        {"rowptr": gb.rowptr, "col": gb.col, "level": lev}, {},
+                                        out="level", out_len=gb.n)
+            if rc != 0:
+                raise RuntimeError(err)
+            first = met["childLaunchCount"] if first is None else first
+            if np.array_equal(res, lev):
+                break
+            lev = res
+        bfs[mode] = {"level": lev.tolist(), "childLaunchCount_first_run": first}
+    runs["bfs.kdl"] = bfs
     data = {"generator": "tests/golden/make_kdl_golden.py (reference consolidate() + simulator via oracle/_ref)",
             "consolidated": cons, "runs": runs}
     path = os.path.join(HERE, "kdl_reference.json")

@@ -183,3 +183,31 @@ def test_tree_program_larger_vs_oracle(orc):
         _, scal, arrs = tree_inputs((6, 4, 12, 0.6, 3), "desc")
         res = module("td.kdl", mode).run(scal, arrs)
         np.testing.assert_array_equal(res.arrays["desc"], want)
+
+
+def run_bfs(mod, rowptr, col, src):
+    n = len(rowptr) - 1
+    lev = np.full(n, INF, np.int64)
+    lev[src] = 0
+    res = mod.run({"n": n, "m": len(col), "src": src, "srcs": int(rowptr[src]), "srce": int(rowptr[src + 1])},
+                  {"rowptr": rowptr, "col": col, "level": lev}, until_stable="level")
+    return res
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_bfs_rec_program_matches_reference(mode):
+    """BFS-Rec: recursive consolidation on a graph (compare-and-store levels,
+    sweeps to a fixpoint) against the simulator's levels."""
+    r = KG["runs"]["bfs.kdl"]
+    res = run_bfs(module("bfs.kdl", mode), np.array(r["rowptr"]), np.array(r["col"]), r["src"])
+    np.testing.assert_array_equal(res.arrays["level"], np.array(r[mode]["level"]))
+
+
+def test_bfs_rec_program_larger_vs_oracle(orc):
+    g = dpc.gen_rmat(13, 16, seed=8)
+    s = int(np.argmax(g.degrees()))
+    want = orc.bfs(g.rowptr, g.col, s).astype(np.int64)
+    for mode in MODES:
+        res = run_bfs(module("bfs.kdl", mode), g.rowptr, g.col, s)
+        got = np.where(res.arrays["level"] >= INF, 2**32 - 1, res.arrays["level"])
+        np.testing.assert_array_equal(got, want)

@@ -99,6 +99,29 @@ def tree(shape, reps, orc, name="td.kdl", out="desc"):
     return {"workload": f"{name}, gen_tree{tuple(shape)} = {t.n} nodes", "modes": rows}
 
 
+def bfs(scale, reps, orc):
+    g = dpc.gen_rmat(scale, 16, seed=3)
+    s = int(np.argmax(g.degrees()))
+    want = orc.bfs(g.rowptr, g.col, s).astype(np.int64)
+    rows = {}
+    for mode in MODES:
+        mod = kdl.compile(kdl.read_program("bfs.kdl"), mode, name="bfs")
+        lev = np.full(g.n, INF, np.int64)
+        lev[s] = 0
+        try:
+            ms, res = best(lambda: mod.run({"n": g.n, "m": g.m, "src": s, "srcs": int(g.rowptr[s]),
+                                            "srce": int(g.rowptr[s + 1])},
+                                           {"rowptr": g.rowptr, "col": g.col, "level": lev},
+                                           until_stable="level", timed=True), reps)
+            got = np.where(res.arrays["level"] >= INF, 2**32 - 1, res.arrays["level"])
+            rows[mode] = {"ms": round(ms, 4), "runs": res.runs, "launches": res.launches,
+                          "bit_exact": bool(np.array_equal(got, want))}
+        except Exception as e:  # noqa: BLE001
+            rows[mode] = {"error": str(e)[:200]}
+    return {"workload": f"bfs.kdl (BFS-Rec, recursive, runs to a fixpoint), R-MAT scale {scale} ef 16 "
+                        f"({g.n} V, {g.m} E)", "modes": rows}
+
+
 def hand_written(scale_spmv, scale_sssp, shape):
     """libdpc's hand-written kernels on the same inputs (grid variant)."""
     ctx = dpc.Context(0)
@@ -158,6 +181,7 @@ def run_compiled(reps=2, scale_spmv=18, scale_sssp=16, shape=(5, 32, 128, 0.4, 1
     return {"spmv": summarize(spmv(scale_spmv, reps, orc, runs)),
             "sssp": summarize(sssp(scale_sssp, reps, orc, runs)),
             "td": summarize(tree(list(shape), reps, orc)),
+            "bfs": summarize(bfs(scale_sssp, reps, orc)),
             "note": "generated by paper_1606_08150_b200.kdl from the .kdl programs (int64 / fp64 data, "
                     "CDP2 device launches); device time of the entry launch tree, CUDA events"}
 
@@ -174,7 +198,7 @@ def main():
     orc = Oracle()
     shape = [float(v) if "." in v else int(v) for v in a.tree.split(",")]
     res = {"spmv": spmv(a.scale_spmv, a.reps, orc), "sssp": sssp(a.scale_sssp, a.reps, orc),
-           "td": tree(shape, a.reps, orc)}
+           "td": tree(shape, a.reps, orc), "bfs": bfs(a.scale_sssp, a.reps, orc)}
     try:
         res["hand_written_wall_ms"] = hand_written(a.scale_spmv, a.scale_sssp, shape)
     except Exception as e:  # noqa: BLE001
