@@ -388,15 +388,12 @@ class Builder:
         if s.gran == "warp":
             return [f"{ind}{{",
                     f"{ind}  const long long dk_cap = {cap};",
-                    f"{ind}  if ((threadIdx.x & 31u) == 0) {{",
-                    f"{ind}    dk_wown[threadIdx.x >> 5].base = 0; dk_wown[threadIdx.x >> 5].count = 0;",
-                    f"{ind}    dk_wown[threadIdx.x >> 5].cap = dk_cap;",
-                    f"{ind}  }}",
+                    f"{ind}  if ((threadIdx.x & 31u) == 0) dk_own_init(&dk_wown[threadIdx.x >> 5], dk_cap);",
                     f"{ind}  __syncwarp(__activemask());",
                     f"{ind}}}"]
         return [f"{ind}{{",
                 f"{ind}  const long long dk_cap = {cap};",
-                f"{ind}  if (threadIdx.x == 0) {{ dk_bown.base = 0; dk_bown.count = 0; dk_bown.cap = dk_cap; }}",
+                f"{ind}  if (threadIdx.x == 0) dk_own_init(&dk_bown, dk_cap);",
                 f"{ind}  __syncthreads();",
                 f"{ind}}}"]
 
@@ -648,7 +645,7 @@ class Builder:
             "  (void)a;",
             "  if (g < 1 || g > 0x7fffffffLL || b < 1 || b > 1024) { snprintf(dk_msg, sizeof dk_msg, \"entry launch extents\"); return 2; }",
             f"  k_{ek.name}<<<(unsigned)g, (unsigned)b, 0, (cudaStream_t)stream>>>("
-            + ", ".join(unpack + ["dk::Inh{nullptr, 0, 0}", "(dk::Inst*)inst0"]) + ");",
+            + ", ".join(unpack + ["dk::Inh{nullptr, nullptr, 0, 0, 0}", "(dk::Inst*)inst0"]) + ");",
             "  cudaError_t e = cudaGetLastError();",
             "  return e == cudaSuccess ? 0 : dk_fail(e);",
             "}",

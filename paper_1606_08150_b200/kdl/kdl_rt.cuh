@@ -50,15 +50,24 @@ struct Inst {                 // one per device launch that needs it
 };
 
 struct Inh {                  // the buffer a consolidated kernel drains
-  const long long* items;     // [n][stride] words: cfgGrid, cfgBlock, work...
+  const long long* items;     // contiguous [n][stride] words (grid regions), or nullptr
+  const unsigned long long* segs;  // warp / block owners: segment table (word offset + 2)
   long long n;
   long long stride;
+  long long shift;            // items per segment = 1 << shift
 };
 
-struct Own {                  // warp / block owner record (shared memory)
-  unsigned long long base;    // 0 unset, 1 being reserved, ~0 failed, else word offset + 2
+// Warp / block owner record (shared memory).  The buffer is a chain of up to
+// kSegs segments of `cap` items (cap = the directive's capacity rounded up to
+// a power of two), each reserved from the arena when the first item lands in
+// it: the reference faults when one buffer fills (sim.hpp:1513), this runtime
+// grows it by up to kSegs x before raising the same overflow fault.
+constexpr int kSegs = 32;
+struct Own {
   unsigned long long count;
-  long long cap;
+  long long cap;              // items per segment (power of two), < 1 = invalid
+  long long shift;
+  unsigned long long seg[kSegs];  // 0 unset, 1 being reserved, ~0 failed, else word offset + 2
 };
 
 struct Rt {
@@ -182,25 +191,32 @@ template <class T> __device__ __forceinline__ T dk_max(T a, T b) { return a < b 
 // ---- owner buffers ----
 __device__ __forceinline__ unsigned dk_lane() { return threadIdx.x & 31u; }
 
-// Reserve the owner's storage once (the first inserting warp wins the CAS).
-__device__ __noinline__ unsigned long long dk_own_base(dk::Own* o, long long stride) {
-  unsigned long long b = atomicCAS(&o->base, 0ull, 1ull);
+// Owner init (dp_buffers, block- or warp-convergent, one thread per owner).
+__device__ __forceinline__ void dk_own_init(dk::Own* o, long long cap) {
+  long long sh = 0;
+  while (sh < 40 && (1LL << sh) < cap) sh++;
+  o->count = 0;
+  o->cap = cap < 1 ? 0 : (1LL << sh);
+  o->shift = sh;
+  for (int j = 0; j < dk::kSegs; j++) o->seg[j] = 0;
+}
+
+// Segment j of an owner: reserved once from the arena (the first lane to need
+// it wins the CAS; the others wait for the pointer).
+__device__ __noinline__ unsigned long long dk_seg_base(dk::Own* o, long long j, long long stride) {
+  unsigned long long b = atomicCAS(&o->seg[j], 0ull, 1ull);
   if (b == 0) {
     b = dk::kNoBase;
-    if (o->cap < 1) {
-      dk_fault(dk::F_OVERFLOW);
-    } else {
-      const unsigned long long words = static_cast<unsigned long long>(o->cap) * stride;
-      const unsigned long long off = atomicAdd(&dk_rt.ctr[2], words);
-      if (off + words > dk_rt.arena_words) dk_fault(dk::F_POOL);
-      else b = off + 2;
-    }
-    atomicExch(&o->base, b);
+    const unsigned long long words = static_cast<unsigned long long>(o->cap) * stride;
+    const unsigned long long off = atomicAdd(&dk_rt.ctr[2], words);
+    if (off + words > dk_rt.arena_words) dk_fault(dk::F_POOL);
+    else b = off + 2;
+    atomicExch(&o->seg[j], b);
     return b;
   }
   while (b == 1) {
     __nanosleep(32);
-    b = atomicAdd(&o->base, 0ull);
+    b = atomicAdd(&o->seg[j], 0ull);
   }
   return b;
 }
@@ -210,19 +226,19 @@ __device__ __forceinline__ long long* dk_reserve_own(dk::Own* o, long long strid
   const unsigned m = __activemask();
   const unsigned lane = dk_lane();
   const int leader = __ffs(m) - 1;
-  unsigned long long pos = 0, base = 0;
-  if (lane == static_cast<unsigned>(leader)) {
+  unsigned long long pos = 0;
+  if (lane == static_cast<unsigned>(leader))
     pos = atomicAdd(&o->count, static_cast<unsigned long long>(__popc(m)));
-    base = dk_own_base(o, stride);
-  }
   pos = __shfl_sync(m, pos, leader) + __popc(m & ((1u << lane) - 1u));
-  base = __shfl_sync(m, base, leader);
-  if (base == dk::kNoBase) return nullptr;
-  if (pos >= static_cast<unsigned long long>(o->cap)) {
+  if (o->cap < 1 || pos >= static_cast<unsigned long long>(o->cap) * dk::kSegs) {
     dk_fault(dk::F_OVERFLOW);
     return nullptr;
   }
-  return dk_rt.arena + (base - 2) + pos * stride;
+  const long long j = static_cast<long long>(pos >> o->shift);
+  unsigned long long b = *reinterpret_cast<volatile unsigned long long*>(&o->seg[j]);
+  if (b < 2) b = dk_seg_base(o, j, stride);
+  if (b == dk::kNoBase) return nullptr;
+  return dk_rt.arena + (b - 2) + (pos & static_cast<unsigned long long>(o->cap - 1)) * stride;
 }
 
 __device__ __forceinline__ long long dk_grid_cap(long long total_bytes, long long nv, long long stride) {
@@ -253,22 +269,33 @@ __device__ __forceinline__ long long dk_clamp_count(unsigned long long c, long l
 
 __device__ __forceinline__ long long dk_pending_own(dk::Own* o) {
   __syncwarp(__activemask());
-  return dk_clamp_count(*reinterpret_cast<volatile unsigned long long*>(&o->count), o->cap);
+  return dk_clamp_count(*reinterpret_cast<volatile unsigned long long*>(&o->count), o->cap * dk::kSegs);
 }
 __device__ __forceinline__ long long dk_pending_grid(dk::Inst* in, long long cap) {
   return dk_clamp_count(*reinterpret_cast<volatile unsigned long long*>(&in->count), cap);
 }
 
-// The buffer a launch from this owner hands to its child (sim.hpp:1530-1541).
+// The buffer a launch from this owner hands to its child (sim.hpp:1530-1541):
+// the launching thread copies the owner's segment table (shared memory) into
+// the arena so the child can index item i as segs[i >> shift].
 __device__ __forceinline__ dk::Inh dk_inherit_own(dk::Own* o, long long stride) {
   __threadfence();
-  const unsigned long long b = *reinterpret_cast<volatile unsigned long long*>(&o->base);
-  if (b < 2 || b == dk::kNoBase) return dk::Inh{nullptr, 0, stride};
-  return dk::Inh{dk_rt.arena + (b - 2), dk_pending_own(o), stride};
+  const long long n = dk_pending_own(o);
+  if (n <= 0 || o->cap < 1) return dk::Inh{nullptr, nullptr, 0, stride, 0};
+  const long long nseg = (n + o->cap - 1) >> o->shift;
+  const unsigned long long off = atomicAdd(&dk_rt.ctr[2], static_cast<unsigned long long>(nseg));
+  if (off + nseg > dk_rt.arena_words) {
+    dk_fault(dk::F_POOL);
+    return dk::Inh{nullptr, nullptr, 0, stride, 0};
+  }
+  unsigned long long* t = reinterpret_cast<unsigned long long*>(dk_rt.arena + off);
+  for (long long j = 0; j < nseg; j++) t[j] = *reinterpret_cast<volatile unsigned long long*>(&o->seg[j]);
+  __threadfence();
+  return dk::Inh{nullptr, t, n, stride, o->shift};
 }
 __device__ __forceinline__ dk::Inh dk_inherit_grid(dk::Inst* in, long long stride, long long cap) {
   __threadfence();
-  return dk::Inh{dk_rt.region[in->level & 1u], dk_pending_grid(in, cap), stride};
+  return dk::Inh{dk_rt.region[in->level & 1u], nullptr, dk_pending_grid(in, cap), stride, 0};
 }
 
 __device__ __forceinline__ long long dk_buf_word(const dk::Inh& h, long long i, long long w) {
@@ -276,7 +303,13 @@ __device__ __forceinline__ long long dk_buf_word(const dk::Inh& h, long long i, 
     dk_fault(dk::F_BUFGET);
     return 0;
   }
-  return h.items[i * h.stride + w];
+  if (h.items) return h.items[i * h.stride + w];
+  const unsigned long long b = h.segs[i >> h.shift];
+  if (b < 2 || b == dk::kNoBase) {
+    dk_fault(dk::F_BUFGET);
+    return 0;
+  }
+  return dk_rt.arena[(b - 2) + (i & ((1LL << h.shift) - 1)) * h.stride + w];
 }
 
 // ---- launches ----

@@ -148,8 +148,10 @@ global int a[n];
 kernel child(int v) { atomicAdd(a, v % 8, 1); }
 kernel parent(int k) {
     int v = blockIdx * blockDim + threadIdx;
-    #pragma dp consltdt(warp) buffer(custom, 2) work(v)
-    child<<<1, 1>>>(v);
+    for (int r = 0; r < 3; r += 1) {
+        #pragma dp consltdt(warp) buffer(custom, 2) work(v)
+        child<<<1, 1>>>(v);
+    }
     a[k] = 1;
 }
 entry parent<<<1, 64>>>(0);
@@ -159,7 +161,8 @@ entry parent<<<1, 64>>>(0);
 def test_faults_are_reported():
     with pytest.raises(kdl.KdlFault) as ei:
         kdl.compile(FAULTY, "warp", name="faulty").run({"n": 8})
-    assert "overflow" in ei.value.kinds       # 32 inserts per warp, capacity 2
+    # 96 inserts per warp; capacity 2 per segment x 32 segments = 64
+    assert "overflow" in ei.value.kinds
     bad = FAULTY.replace("entry parent<<<1, 64>>>(0);", "entry parent<<<1, 64>>>(9);")
     with pytest.raises(kdl.KdlFault) as ei:
         kdl.compile(bad, "basic", name="faulty").run({"n": 8})
