@@ -24,6 +24,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -79,6 +82,7 @@ struct Args {
   unsigned sendcap;
   unsigned coop;           // grid_persistent1: cooperative launch (grid.sync) vs soft barrier
   unsigned classify;       // grid_persistent1: next-level vertices are classified at push time
+  unsigned long long* ptrace;  // optional phase timeline (DPC_SSSP_PHASES=1): per level, max over blocks
 };
 
 __device__ void spill_classify(const Args& a, unsigned it, unsigned v);
@@ -509,6 +513,17 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
       a.ctr->fsize[(it + 2) % 3] = 0;
       a.ctr->pool[(it + 2) % 3] = 0;
     }
+    auto mark = [&](int k) {
+      if (a.ptrace && threadIdx.x == 0 && it < 64) {
+        if (k == 0) atomicMin(a.ptrace + it * 8, dev::global_ns());
+        else atomicMax(a.ptrace + it * 8 + k, dev::global_ns());
+        if (k == 0 && blockIdx.x == 0) {
+          a.ptrace[it * 8 + 5] = fs;
+          a.ptrace[it * 8 + 6] = pc;
+        }
+      }
+    };
+    mark(0);
     // the level's light list, warp-cooperatively (any degree)
     for (unsigned base = blockIdx.x * blockDim.x; base < fs; base += stride) {
       const unsigned i = base + threadIdx.x;
@@ -523,10 +538,14 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
       warp_light_relax(a, it, s, b, du, deg);
     }
     // the level's chunk items (inserted while the previous level flushed)
+    mark(1);
     drain_items(a, it, s, a.pool.items + (it % 2) * a.pool.cap, pc, gtid >> 5, stride >> 5);
+    mark(2);
     flush_classify(a, it, s, (it + 1) % 2);
+    mark(3);
     if (a.coop) cg::this_grid().sync();
     else dev::soft_grid_sync(&a.hdr->ticket, &a.hdr->iter, &a.hdr->overflow);
+    mark(4);
   }
   if (gtid == 0) a.ctr->iters = it;
 }
@@ -834,6 +853,15 @@ static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dp
     const void* fn = reinterpret_cast<const void*>(sssp::grid_persistent1);
     int blocks = coop_blocks_sssp(ctx, fn, 256);
     unsigned max_iters = a.n + 1;
+    // DPC_SSSP_PHASES=1: per-level phase timeline to stderr (diagnostics)
+    static const bool phases = std::getenv("DPC_SSSP_PHASES") != nullptr;
+    std::vector<unsigned long long> ph(64 * 8, 0);
+    if (phases) {
+      for (int i = 0; i < 64; i++) ph[i * 8] = ~0ull;
+      DPC_CUDA(cudaMalloc(&a.ptrace, sizeof(unsigned long long) * ph.size()));
+      DPC_CUDA(cudaMemcpyAsync(a.ptrace, ph.data(), sizeof(unsigned long long) * ph.size(),
+                               cudaMemcpyHostToDevice, s));
+    }
     void* args[] = {&a, &max_iters};
     if (a.coop) DPC_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(256), args, 0, s));
     else DPC_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(256), args, 0, s));
@@ -841,6 +869,18 @@ static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dp
     DPC_CUDA(cudaMemcpyAsync(ctr_host, a.ctr, sizeof(sssp::Ctr), cudaMemcpyDeviceToHost, s));
     DPC_CUDA(cudaStreamSynchronize(s));
     iters = ctr_host->iters;
+    if (phases) {
+      DPC_CUDA(cudaMemcpy(ph.data(), a.ptrace, sizeof(unsigned long long) * ph.size(), cudaMemcpyDeviceToHost));
+      cudaFree(a.ptrace);
+      a.ptrace = nullptr;
+      const unsigned long long t0 = ph[0];
+      for (int64_t i = 0; i < std::min<int64_t>(iters, 64); i++) {
+        const unsigned long long* r = &ph[i * 8];
+        std::fprintf(stderr, "sssp level %2lld fs %7llu pc %6llu | start %7.2f light %6.2f drain %6.2f flush %6.2f "
+                     "barrier %6.2f us\n", static_cast<long long>(i), r[5], r[6], (r[0] - t0) / 1e3,
+                     (r[1] - r[0]) / 1e3, (r[2] - r[1]) / 1e3, (r[3] - r[2]) / 1e3, (r[4] - r[3]) / 1e3);
+      }
+    }
   } else if (c.variant == DPC_GRID && c.grid_persistent) {
     int blocks = coop_blocks_sssp(ctx, reinterpret_cast<const void*>(sssp::grid_persistent), 256);
     unsigned max_iters = a.n + 1;
