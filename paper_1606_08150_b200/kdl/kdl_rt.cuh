@@ -177,12 +177,16 @@ __device__ __forceinline__ long long dk_atomic_i(long long* p, long long v) {
 __device__ __forceinline__ double dk_atomic_f(double* p, double v) { return dk_atomic_agg(p, v); }
 
 // ---- arithmetic with the simulator's fault rules (sim.hpp:1574-1590) ----
+// (64-bit division is a long software sequence on the GPU; operands that fit
+// in 31 bits take the 32-bit unsigned path, same result)
 __device__ __forceinline__ long long dk_idiv(long long a, long long b) {
   if (b == 0) { dk_fault(dk::F_DIV); return 0; }
+  if (((a | b) >> 31) == 0) return static_cast<long long>(static_cast<unsigned>(a) / static_cast<unsigned>(b));
   return a / b;
 }
 __device__ __forceinline__ long long dk_imod(long long a, long long b) {
   if (b == 0) { dk_fault(dk::F_DIV); return 0; }
+  if (((a | b) >> 31) == 0) return static_cast<long long>(static_cast<unsigned>(a) % static_cast<unsigned>(b));
   return a % b;
 }
 template <class T> __device__ __forceinline__ T dk_min(T a, T b) { return b < a ? b : a; }

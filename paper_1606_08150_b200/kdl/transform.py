@@ -299,18 +299,18 @@ class _Consolidator:
                                             "blockDim": A.ref("__ob"), "gridDim": A.lit(1)})))
             out.append(A.for_("__i", A.intr("blockIdx"), A.ref("__n"), A.intr("gridDim"), item))
         elif self.schedule == "block":
-            # B200 schedule: one item per block, the item's virtual threads
-            # strided over the block.  Rebinding the four intrinsics to the
-            # item's own geometry is valid for every multi-block child
-            # (moldable or not); it removes the reference form's O(#items)
-            # loop that every thread of the grid runs.
+            # B200 schedule: one item per block; the block walks the item's
+            # virtual blocks in turn and strides each one's virtual threads.
+            # Rebinding the four intrinsics to the item's own geometry is
+            # valid for every multi-block child (moldable or not); it removes
+            # the reference form's O(#items) loop that every thread of the
+            # grid runs, and the 2-D loop needs no per-thread division.
             item.append(A.let(A.INT, "__og", A.Expr("buf_cfg_grid", args=[A.ref("__i")])))
             item.append(A.let(A.INT, "__ob", A.Expr("buf_cfg_block", args=[A.ref("__i")])))
-            tbl = {"threadIdx": A.binop("%", A.ref("__vt"), A.ref("__ob")),
-                   "blockIdx": A.binop("/", A.ref("__vt"), A.ref("__ob")),
+            tbl = {"threadIdx": A.ref("__vt"), "blockIdx": A.ref("__vb"),
                    "blockDim": A.ref("__ob"), "gridDim": A.ref("__og")}
-            item.append(A.for_("__vt", A.intr("threadIdx"), A.binop("*", A.ref("__og"), A.ref("__ob")),
-                               A.intr("blockDim"), subst(body, tbl)))
+            inner = A.for_("__vt", A.intr("threadIdx"), A.ref("__ob"), A.intr("blockDim"), subst(body, tbl))
+            item.append(A.for_("__vb", A.lit(0), A.ref("__og"), A.lit(1), [inner]))
             out.append(A.for_("__i", A.intr("blockIdx"), A.ref("__n"), A.intr("gridDim"), item))
         else:
             if p.moldable:
