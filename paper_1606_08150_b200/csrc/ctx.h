@@ -53,6 +53,8 @@ struct dpc_dgraph {
   size_t gc_q_cap = 0;
   unsigned* gc_hstate = nullptr;  // GC async heavy-vertex states
   size_t gc_hstate_cap = 0;
+  int* gc_hcol = nullptr;         // GC async: adjacency split per vertex, higher-priority neighbours first
+  unsigned* gc_hsplit = nullptr;  // GC async: number of higher-priority neighbours per vertex
   unsigned* ctr = nullptr;    // per-iteration counters (app-specific layout, 64 B)
   void* ctr_host = nullptr;   // pinned mirror of ctr
   dpc::dev::RunHeader* hdr = nullptr;  // device counters

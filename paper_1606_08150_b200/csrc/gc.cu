@@ -591,6 +591,8 @@ constexpr int kBW = BW_CFG;           // edges per thread per block-server step
 constexpr unsigned kPollNs = POLL_NS;
 
 struct Async {
+  const int* hcol;         // adjacency split per vertex: [b, b + h) higher-priority neighbours, [b + h, e) the rest
+  const unsigned* hsplit;  // h per vertex (= the initial pending count)
   unsigned long long* q;   // warp queue: light vertices and chunk tasks
   unsigned* qctr;          // counters, one per 128-byte line (see k* offsets)
   unsigned qcap;
@@ -671,18 +673,17 @@ __device__ __forceinline__ void enqueue(const Args& a, const Async& q, bool want
 // belong to block servers; 0 for block servers: light ones to warps).
 template <int W, unsigned KEEPX = 1>
 __device__ __forceinline__ unsigned long long release_range(const Args& a, const Async& q, unsigned v,
-                                                            unsigned long long pv, unsigned b, unsigned e,
-                                                            unsigned long long keep) {
+                                                            unsigned b, unsigned e, unsigned long long keep) {
+  // [b, e) lies in v's lower part of the split adjacency: no priority tests
   for (unsigned k0 = b; k0 < e; k0 += 32 * W) {
     unsigned u[W];
     bool low[W], ready[W];
 #pragma unroll
     for (int j = 0; j < W; j++) {
       const unsigned k = k0 + 32 * j + dev::lane_id();
-      u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
+      u[j] = k < e ? static_cast<unsigned>(__ldg(q.hcol + k)) : v;
+      low[j] = u[j] != v;
     }
-#pragma unroll
-    for (int j = 0; j < W; j++) low[j] = u[j] != v && !higher(u[j], prio(a, u[j]), v, pv);
     unsigned cls[W];
 #pragma unroll
     for (int j = 0; j < W; j++) cls[j] = low[j] ? q.vclass[u[j]] : 0u;  // issued beside the count-downs
@@ -704,22 +705,22 @@ __device__ __forceinline__ unsigned long long release_range(const Args& a, const
   return keep;
 }
 
-// ORs the colors of v's higher neighbours among [b, e) into the warp bitmap
-// (colors < 32 * kVW); returns true (warp-uniform) if a larger color was seen.
+// ORs the colors of the higher neighbours in [b, e) (a slice of the split
+// adjacency's higher part) into the warp bitmap (colors < 32 * kVW); returns
+// true (warp-uniform) if a larger color was seen.
 template <int W>
-__device__ __forceinline__ bool gather_colors(const Args& a, unsigned v, unsigned long long pv, unsigned b,
-                                              unsigned e, unsigned* wbm) {
+__device__ __forceinline__ bool gather_colors(const Args& a, const Async& q, unsigned b, unsigned e,
+                                              unsigned* wbm) {
   bool over = false;
   for (unsigned k0 = b; k0 < e; k0 += 32 * W) {
-    unsigned u[W];
     int c[W];
 #pragma unroll
     for (int j = 0; j < W; j++) {
       const unsigned k = k0 + 32 * j + dev::lane_id();
-      u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
+      c[j] = k < e ? static_cast<int>(__ldg(q.hcol + k)) : -1;
     }
 #pragma unroll
-    for (int j = 0; j < W; j++) c[j] = (u[j] != v && higher(u[j], prio(a, u[j]), v, pv)) ? __ldcg(a.color + u[j]) : -1;
+    for (int j = 0; j < W; j++) c[j] = c[j] >= 0 ? __ldcg(a.color + c[j]) : -1;
 #pragma unroll
     for (int j = 0; j < W; j++) {
       if (c[j] >= static_cast<int>(kVW * 32)) over = true;
@@ -739,16 +740,13 @@ __device__ __forceinline__ int bitmap_mex(unsigned word) {
 }
 
 // Colors >= 32 * kVW: windowed warp scan over all of v's higher neighbours.
-__device__ int mex_windowed(const Args& a, unsigned v, unsigned long long pv) {
-  const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+__device__ int mex_windowed(const Args& a, const Async& q, unsigned v) {
+  const unsigned b = __ldg(a.rowptr + v), e = b + __ldg(q.hsplit + v);
   for (int base = kVW * 32;; base += 32) {
     unsigned w = 0;
     for (unsigned k = b + dev::lane_id(); k < e; k += 32) {
-      const unsigned u = static_cast<unsigned>(__ldg(a.col + k));
-      if (u != v && higher(u, prio(a, u), v, pv)) {
-        const int c = __ldcg(a.color + u) - base;
-        if (c >= 0 && c < 32) w |= 1u << c;
-      }
+      const int c = __ldcg(a.color + __ldg(q.hcol + k)) - base;
+      if (c >= 0 && c < 32) w |= 1u << c;
     }
     for (int o = 16; o > 0; o >>= 1) w |= __shfl_xor_sync(kFull, w, o);
     if (~w) return base + __ffs(~w) - 1;
@@ -766,7 +764,8 @@ __device__ __forceinline__ void set_color_async(const Args& a, const Async& q, B
   __syncwarp();
 }
 
-// Serves one task with the whole warp.
+// Serves one task with the whole warp.  Gathers read v's higher part
+// [b, b + h) of the split adjacency, releases its lower part [b + h, e).
 __device__ unsigned long long serve(const Args& a, const Async& q, Block& s, unsigned long long t) {
   const unsigned lane = dev::lane_id();
   unsigned* wbm = s.wbm[dev::warp_in_block() & 7];
@@ -775,25 +774,29 @@ __device__ unsigned long long serve(const Args& a, const Async& q, Block& s, uns
   const unsigned slot = static_cast<unsigned>(t >> (32 + kChunkBits)) & ((1u << kSlotBits) - 1u);
   const bool phase_b = t >> 63;
   const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
-  const unsigned long long pv = prio(a, v);
+  const unsigned m = b + __ldg(q.hsplit + v);  // end of the higher part
   if (e - b <= kAsyncHeavy && !phase_b && chunk == 0 && slot == 0) {
     wbm[lane] = 0;
     __syncwarp();
-    const bool over = e - b <= kAsyncLight ? gather_colors<kAsyncW>(a, v, pv, b, e, wbm)
-                                           : gather_colors<kAsyncWide>(a, v, pv, b, e, wbm);
+    const bool over = e - b <= kAsyncLight ? gather_colors<kAsyncW>(a, q, b, m, wbm)
+                                           : gather_colors<kAsyncWide>(a, q, b, m, wbm);
     __syncwarp();
     int c = bitmap_mex(wbm[lane]);
-    if (c < 0 || over) {
-      const int cw = c < 0 ? mex_windowed(a, v, pv) : c;
-      c = cw;
-    }
+    if (c < 0 || over) c = c < 0 ? mex_windowed(a, q, v) : c;
     __syncwarp();
     set_color_async(a, q, s, v, c);
-    return e - b <= kAsyncLight ? release_range<kAsyncW>(a, q, v, pv, b, e, kEmpty)
-                                : release_range<kAsyncWide>(a, q, v, pv, b, e, kEmpty);
+    return e - b <= kAsyncLight ? release_range<kAsyncW>(a, q, v, m, e, kEmpty)
+                                : release_range<kAsyncWide>(a, q, v, m, e, kEmpty);
   }
-  const unsigned nch = (e - b + kAsyncChunk - 1) / kAsyncChunk;
+  const unsigned ncha = (m - b + kAsyncChunk - 1) / kAsyncChunk;   // gather chunks
+  const unsigned nchb = (e - m + kAsyncChunk - 1) / kAsyncChunk;   // release chunks
   if (!phase_b && chunk == 0 && slot == 0) {
+    if (ncha == 0) {  // no higher neighbour: color 0, then the release chunks
+      set_color_async(a, q, s, v, 0);
+      for (unsigned c0 = 0; c0 < nchb; c0 += 32)
+        enqueue(a, q, c0 + lane < nchb && c0 + lane > 0, task(v, c0 + lane, 1, 1));
+      return release_range<kAsyncWide>(a, q, v, m, min(e, m + kAsyncChunk), kEmpty);
+    }
     // heavy vertex: take a state slot, fan out phase A chunks
     unsigned sl = 0;
     if (lane == 0) sl = atomicAdd(q.qctr + kSlots, 1u);
@@ -804,18 +807,18 @@ __device__ unsigned long long serve(const Args& a, const Async& q, Block& s, uns
     }
     unsigned* st = q.hstate + static_cast<size_t>(sl) * kStateWords;
     if (lane < kVW) st[lane] = 0;
-    if (lane == 0) st[kVW] = nch, st[kVW + 1] = 0;
+    if (lane == 0) st[kVW] = ncha, st[kVW + 1] = 0;
     __threadfence();
-    for (unsigned c0 = 0; c0 < nch; c0 += 32)
-      enqueue(a, q, c0 + lane < nch, task(v, c0 + lane, sl + 1, 0));
+    for (unsigned c0 = 0; c0 < ncha; c0 += 32)
+      enqueue(a, q, c0 + lane < ncha, task(v, c0 + lane, sl + 1, 0));
     return kEmpty;
   }
-  const unsigned cb = b + chunk * kAsyncChunk, ce = min(e, cb + kAsyncChunk);
-  unsigned* st = q.hstate + static_cast<size_t>(slot - 1) * kStateWords;
   if (!phase_b) {
+    const unsigned cb = b + chunk * kAsyncChunk, ce = min(m, cb + kAsyncChunk);
+    unsigned* st = q.hstate + static_cast<size_t>(slot - 1) * kStateWords;
     wbm[lane] = 0;
     __syncwarp();
-    const bool over = gather_colors<kAsyncWide>(a, v, pv, cb, ce, wbm);
+    const bool over = gather_colors<kAsyncWide>(a, q, cb, ce, wbm);
     __syncwarp();
     const unsigned wv = wbm[lane];
     if (wv) atomicOr(st + lane, wv);
@@ -826,14 +829,15 @@ __device__ unsigned long long serve(const Args& a, const Async& q, Block& s, uns
     if (!__shfl_sync(kFull, last, 0)) return kEmpty;
     __threadfence();
     int c = bitmap_mex(__ldcg(st + lane));
-    if (c < 0 || __ldcg(st + kVW + 1)) c = c < 0 ? mex_windowed(a, v, pv) : c;
+    if (c < 0 || __ldcg(st + kVW + 1)) c = c < 0 ? mex_windowed(a, q, v) : c;
     set_color_async(a, q, s, v, c);
-    // phase B: chunk 0 released by this warp right away, the rest queued
-    for (unsigned c0 = 0; c0 < nch; c0 += 32)
-      enqueue(a, q, c0 + lane < nch && c0 + lane > 0, task(v, c0 + lane, slot, 1));
-    return release_range<kAsyncWide>(a, q, v, pv, b, min(e, b + kAsyncChunk), kEmpty);
+    // phase B: release chunk 0 by this warp right away, the rest queued
+    for (unsigned c0 = 0; c0 < nchb; c0 += 32)
+      enqueue(a, q, c0 + lane < nchb && c0 + lane > 0, task(v, c0 + lane, slot, 1));
+    return release_range<kAsyncWide>(a, q, v, m, min(e, m + kAsyncChunk), kEmpty);
   }
-  return release_range<kAsyncWide>(a, q, v, pv, cb, ce, kEmpty);
+  const unsigned rb = m + chunk * kAsyncChunk;
+  return release_range<kAsyncWide>(a, q, v, rb, min(e, rb + kAsyncChunk), kEmpty);
 }
 
 // Whether the asynchronous drain is over (thread-level; call from one lane):
@@ -860,27 +864,28 @@ __device__ bool async_over(const Args& a, const Async& q, unsigned long long* si
 }
 
 // A medium vertex served by a whole block (block-level consolidation of its
-// edge loop): 256 threads gather the higher neighbours' colors into a
-// shared bitmap, warp 0 takes the mex and writes the color, then every warp
-// releases its share of the lower neighbours.  All threads call.
-__device__ void block_serve(const Args& a, const Async& q, Block& s, unsigned v, unsigned* sbm, unsigned* sflag) {
+// edge loop): 256 threads gather the higher neighbours' colors (the split
+// adjacency's higher part) into a shared bitmap, warp 0 takes the mex and
+// writes the color, then every warp releases its share of the lower part.
+// All threads call.
+__device__ void block_serve(const Args& a, const Async& q, Block& s, unsigned v, unsigned* sbm, unsigned* sflag,
+                            unsigned long long* skeep) {
   const unsigned tid = threadIdx.x;
   const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
-  const unsigned long long pv = prio(a, v);
+  const unsigned m = b + __ldg(q.hsplit + v);
   if (tid < kVW) sbm[tid] = 0;
   if (tid == 0) *sflag = 0;
   __syncthreads();
   bool over = false;
-  for (unsigned k0 = b; k0 < e; k0 += kBW * blockDim.x) {
-    unsigned u[kBW];
+  for (unsigned k0 = b; k0 < m; k0 += kBW * blockDim.x) {
     int c[kBW];
 #pragma unroll
     for (int j = 0; j < kBW; j++) {
       const unsigned k = k0 + j * blockDim.x + tid;
-      u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
+      c[j] = k < m ? static_cast<int>(__ldg(q.hcol + k)) : -1;
     }
 #pragma unroll
-    for (int j = 0; j < kBW; j++) c[j] = (u[j] != v && higher(u[j], prio(a, u[j]), v, pv)) ? __ldcg(a.color + u[j]) : -1;
+    for (int j = 0; j < kBW; j++) c[j] = c[j] >= 0 ? __ldcg(a.color + c[j]) : -1;
 #pragma unroll
     for (int j = 0; j < kBW; j++) {
       if (c[j] >= static_cast<int>(kVW * 32)) over = true;
@@ -889,26 +894,90 @@ __device__ void block_serve(const Args& a, const Async& q, Block& s, unsigned v,
   }
   if (over) atomicOr(sflag, 1u);
   __syncthreads();
+  // the first release batch's neighbours and classes do not depend on the
+  // color: load them before warp 0's mex / color store / fence, off the
+  // dependency chain
+  unsigned u[kBW], cls[kBW];
+#pragma unroll
+  for (int j = 0; j < kBW; j++) {
+    const unsigned k = m + j * blockDim.x + tid;
+    u[j] = k < e ? static_cast<unsigned>(__ldg(q.hcol + k)) : v;
+    cls[j] = u[j] != v ? q.vclass[u[j]] : 0u;
+  }
   if (tid < 32) {
     int c = bitmap_mex(sbm[tid]);
-    if (c < 0) c = mex_windowed(a, v, pv);
+    if (c < 0) c = mex_windowed(a, q, v);
     set_color_async(a, q, s, v, c);
   }
   __syncthreads();
-  for (unsigned k0 = b; k0 < e; k0 += kBW * blockDim.x) {
-    unsigned u[kBW], cls[kBW];
+  for (unsigned k0 = m; k0 < e; k0 += kBW * blockDim.x) {
     bool low[kBW], ready[kBW];
+    if (k0 != m) {
 #pragma unroll
-    for (int j = 0; j < kBW; j++) {
-      const unsigned k = k0 + j * blockDim.x + tid;
-      u[j] = k < e ? static_cast<unsigned>(__ldg(a.col + k)) : v;
-      low[j] = u[j] != v && !higher(u[j], prio(a, u[j]), v, pv);
-      cls[j] = low[j] ? q.vclass[u[j]] : 0u;
+      for (int j = 0; j < kBW; j++) {
+        const unsigned k = k0 + j * blockDim.x + tid;
+        u[j] = k < e ? static_cast<unsigned>(__ldg(q.hcol + k)) : v;
+        cls[j] = u[j] != v ? q.vclass[u[j]] : 0u;
+      }
     }
+#pragma unroll
+    for (int j = 0; j < kBW; j++) low[j] = u[j] != v;
 #pragma unroll
     for (int j = 0; j < kBW; j++) ready[j] = low[j] && atomicSub(a.cnt + u[j], 1u) == 1u;
 #pragma unroll
-    for (int j = 0; j < kBW; j++) enqueue(a, q, ready[j], task(u[j], 0, 0, 0), cls[j]);
+    for (int j = 0; j < kBW; j++) {
+      // work-first: the block keeps one medium vertex it made ready and
+      // serves it next, without the block-queue round trip
+      if (ready[j] && cls[j] == 1 && *skeep == kEmpty &&
+          atomicCAS(skeep, kEmpty, task(u[j], 0, 0, 0)) == kEmpty)
+        ready[j] = false;
+      enqueue(a, q, ready[j], task(u[j], 0, 0, 0), cls[j]);
+    }
+  }
+}
+
+// Adjacency split by JP priority (init of the asynchronous form): v's
+// higher-priority neighbours go to the front of its slice of hcol, the rest
+// (lower, self loops) to the back; positions inside each part are free.
+// Light vertices: one thread, serial (independent loads, no atomics).
+__device__ __forceinline__ unsigned split_serial(const Args& a, const Async& q, unsigned v, unsigned b,
+                                                 unsigned e) {
+  const unsigned long long pv = prio(a, v);
+  int* hcol = const_cast<int*>(q.hcol);
+  unsigned h = 0, l = 0;
+  for (unsigned k = b; k < e; k++) {
+    const unsigned u = static_cast<unsigned>(__ldg(a.col + k));
+    if (u != v && higher(u, prio(a, u), v, pv)) hcol[b + h++] = static_cast<int>(u);
+    else hcol[e - 1 - l++] = static_cast<int>(u);
+  }
+  return h;
+}
+
+// Heavy vertices: one warp per chunk item of a.chunk edges; the parts'
+// fill counters (hpos = hsplit, lpos) are claimed once per chunk.
+__device__ __forceinline__ void split_chunk(const Args& a, const Async& q, unsigned* lpos, const Item& t) {
+  const unsigned lane = dev::lane_id();
+  const unsigned v = t.v, b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
+  const unsigned ce = min(t.begin + a.chunk, e);
+  const unsigned long long pv = prio(a, v);
+  int* hcol = const_cast<int*>(q.hcol);
+  unsigned* hpos = const_cast<unsigned*>(q.hsplit);
+  for (unsigned k0 = t.begin; k0 < ce; k0 += 32) {
+    const unsigned k = k0 + lane;
+    const unsigned u = k < ce ? static_cast<unsigned>(__ldg(a.col + k)) : v;
+    const bool hi = k < ce && u != v && higher(u, prio(a, u), v, pv);
+    const bool lo = k < ce && !hi;
+    const unsigned hb = __ballot_sync(kFull, hi), lb = __ballot_sync(kFull, lo);
+    unsigned hbase = 0, lbase = 0;
+    if (lane == 0) {
+      if (hb) hbase = atomicAdd(hpos + v, __popc(hb));
+      if (lb) lbase = atomicAdd(lpos + v, __popc(lb));
+    }
+    hbase = __shfl_sync(kFull, hbase, 0);
+    lbase = __shfl_sync(kFull, lbase, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (hi) hcol[b + hbase + __popc(hb & lt)] = static_cast<int>(u);
+    if (lo) hcol[e - 1 - (lbase + __popc(lb & lt))] = static_cast<int>(u);
   }
 }
 
@@ -919,14 +988,22 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
   const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned lane = dev::lane_id();
   block_begin(s);
-  // init pass: cnt[v] = higher neighbours (light inline, heavy as chunk items)
+  // init pass: split every adjacency by priority and count the higher
+  // neighbours (= pending count): light vertices inline, heavy ones as chunk
+  // items drained by warps; vertex classes
+  unsigned* lpos = const_cast<unsigned*>(q.hsplit) + a.n;
   for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
     unsigned v = base + threadIdx.x, b = 0, e = 0, want = 0;
     if (v < a.n) {
       b = __ldg(a.rowptr + v);
       e = __ldg(a.rowptr + v + 1);
-      if (e - b <= a.threshold) a.cnt[v] = count_higher(a, v, b, e, 1, 0);
-      else want = dev::nchunks(e - b, a.chunk);
+      if (e - b <= a.threshold) {
+        const unsigned h = split_serial(a, q, v, b, e);
+        const_cast<unsigned*>(q.hsplit)[v] = h;
+        a.cnt[v] = h;
+      } else {
+        want = dev::nchunks(e - b, a.chunk);
+      }
       q.vclass[v] = e - b <= kAsyncHeavy ? 0 : (e - b <= q.bmax && q.nbs ? 1 : 2);
     }
     unsigned bbase, bt;
@@ -934,8 +1011,15 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
     if (want) dev::write_chunks(a.pool, a.hdr, at, v, b, e, a.chunk);
   }
   grid.sync();
-  init_drain(a, a.pool.items, min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[0]), a.pool.cap),
-             gtid >> 5, stride >> 5);
+  {
+    const unsigned cnt = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[0]), a.pool.cap);
+    for (unsigned i = gtid >> 5; i < cnt; i += stride >> 5) split_chunk(a, q, lpos, a.pool.items[i]);
+  }
+  grid.sync();
+  for (unsigned v = gtid; v < a.n; v += stride) {
+    const unsigned deg = __ldg(a.rowptr + v + 1) - __ldg(a.rowptr + v);
+    if (deg > a.threshold) a.cnt[v] = __ldcg(q.hsplit + v);
+  }
   grid.sync();
   // seed: every vertex without a higher neighbour is ready
   for (unsigned base = blockIdx.x * blockDim.x; base < a.n; base += stride) {
@@ -946,8 +1030,9 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
   grid.sync();
   if (blockIdx.x < q.nbs) {
     // block servers: block-queue position p is served by block p mod nbs
-    __shared__ unsigned long long s_task;
+    __shared__ unsigned long long s_task, s_keep;
     __shared__ unsigned s_bm[kVW], s_flag;
+    if (threadIdx.x == 0) s_keep = kEmpty;
     for (unsigned p = blockIdx.x; p < q.bqcap; p += q.nbs) {
       if (threadIdx.x == 0) {
         unsigned long long t = kEmpty, since = 0;
@@ -965,8 +1050,18 @@ __global__ void __launch_bounds__(256) async_persistent(Args a, Async q) {
       __syncthreads();
       if (t == kEmpty) break;
       if (a.trace && threadIdx.x == 0) a.trace[2ull * a.n + static_cast<unsigned>(t)] = dev::global_ns();
-      block_serve(a, q, s, static_cast<unsigned>(t), s_bm, &s_flag);
+      block_serve(a, q, s, static_cast<unsigned>(t), s_bm, &s_flag, &s_keep);
       __syncthreads();
+      while (true) {  // the work-first chain of kept medium vertices
+        const unsigned long long k = s_keep;
+        __syncthreads();
+        if (k == kEmpty) break;
+        if (threadIdx.x == 0) s_keep = kEmpty;
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[2ull * a.n + static_cast<unsigned>(k)] = dev::global_ns();
+        block_serve(a, q, s, static_cast<unsigned>(k), s_bm, &s_flag, &s_keep);
+        __syncthreads();
+      }
       if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(q.qctr + kBDone, 1u);
@@ -1127,6 +1222,16 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
     q.bmax = (c.flags >> 24) & 15u ? (256u << ((c.flags >> 24) & 15u)) : gc::kBlockMax;
     DPC_CUDA(cudaMemsetAsync(q.q, 0xff, sizeof(unsigned long long) * (qcap + 128 + bqcap), s));
     DPC_CUDA(cudaMemsetAsync(q.qctr, 0, 1024, s));
+    // the adjacency split by this run's priorities (built by the kernel's
+    // init pass): hcol (m), hsplit + lpos fill counters (2n, zeroed)
+    if (!g->gc_hcol) {
+      DPC_CUDA(cudaStreamSynchronize(s));
+      DPC_CUDA(cudaMalloc(&g->gc_hcol, sizeof(int) * static_cast<size_t>(std::max<int64_t>(g->m, 1))));
+      DPC_CUDA(cudaMalloc(&g->gc_hsplit, sizeof(unsigned) * 2 * nv));
+    }
+    DPC_CUDA(cudaMemsetAsync(g->gc_hsplit, 0, sizeof(unsigned) * 2 * nv, s));
+    q.hcol = g->gc_hcol;
+    q.hsplit = g->gc_hsplit;
     void* args[] = {&a, &q};
     DPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(gc::async_persistent), dim3(blocks),
                                          dim3(256), args, 0, s));
