@@ -579,7 +579,7 @@ constexpr unsigned long long kEmpty = ~0ull;
 // them, and sharing a line would serialise all of them on one L2 slice.
 constexpr unsigned kTail = 32, kSlots = 64, kColored = 96, kDeadlock = 128, kDone = 160, kBTail = 192,
                    kBDone = 224;
-constexpr unsigned kBlockMax = 2048;  // medium vertices (kAsyncHeavy, kBlockMax] go to a block server
+constexpr unsigned kBlockMax = 4096;  // medium vertices (kAsyncHeavy, kBlockMax] go to a block server
 constexpr int kBW = BW_CFG;           // edges per thread per block-server step
 // Idle servers sleep between polls.  ncu counts 9.4G instructions (50 % SM
 // throughput) for the 18 ms config-3 run, mostly polling, yet longer sleeps

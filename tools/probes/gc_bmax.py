@@ -14,3 +14,4 @@ for k in [0, 1, 2, 3, 4, 5, 6, 8]:
     for _ in range(3):
         ctx.flush_l2(); ctx.record(0); dg.color(1, 'grid', cfg=cfg, metrics=False); ctx.record(1); ts.append(ctx.elapsed_ms(0, 1))
     print('bmax', (256 << k) if k else 2048, 'exact', ok, 'ms', round(min(ts), 3), flush=True)
+dg.close(); ctx.close()
