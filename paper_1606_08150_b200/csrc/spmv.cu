@@ -1247,8 +1247,11 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
 // chain, not HBM, bound all of them):
 //   0: software-pipelined drain (step s+1's window lookups and an L2
 //      prefetch of its col / val groups run under step s's loads), groups of
-//      4 positions per lane, 2 windows per step, 1024 threads x 1 block/SM
-//      (default: 84.0 us vs 90.1 us for shape 6 on the same box)
+//      4 positions per lane, 2 windows per step, 1024 threads x 1 block/SM,
+//      64-item batches per warp (32 KB shared: the rest of the 256 KB
+//      unified L1 caches x; 128-item batches 82.0 us, 64 79.9, 32 84.0; a
+//      max-shared carve-out doubles the drain time)
+//      (default: 84.0 us vs 90.1 us for shape 6 on the same box, 128 items)
 //   1: groups of 8, 2 windows per step, not pipelined
 //   2: groups of 4, 4 windows, 256 threads x 4 blocks/SM
 //   3: groups of 4, 4 windows, hot-column x cache of 2^14 slots
@@ -1283,7 +1286,7 @@ static StreamShape stream_shape(bool inl, unsigned flags) {
     case 5: return shape_of<4, 2, 1024, 1, 0, 64, 2>(inl);
     case 6: return shape_of<4, 4, 1024, 1, 0, 128>(inl);
     case 7: return shape_of<4, 3, 1024, 1, 0, 128, 1>(inl);
-    default: return shape_of<4, 2, 1024, 1, 0, 128, 1>(inl);
+    default: return shape_of<4, 2, 1024, 1, 0, 64, 1>(inl);  // KB 64: 32 KB batch, more L1 for x (-2.6 %)
   }
 }
 
@@ -1383,6 +1386,12 @@ static int stream_blocks(dpc_ctx* ctx, const spmv::StreamShape& sh) {
     cudaGetLastError();
     return 0;
   }
+  // unified L1 / shared memory: as little carve-out as the batch needs, the
+  // rest stays L1 for the x gathers (DPC_SPMV_CARVEOUT overrides, percent)
+  static const int carve = std::getenv("DPC_SPMV_CARVEOUT") ? std::atoi(std::getenv("DPC_SPMV_CARVEOUT")) : -2;
+  if (carve != -2 &&
+      cudaFuncSetAttribute(sh.fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve) != cudaSuccess)
+    cudaGetLastError();
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sh.fn, sh.threads, sh.smem) != cudaSuccess) {
     cudaGetLastError();
