@@ -524,18 +524,26 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
       }
     };
     mark(0);
-    // the level's light list, warp-cooperatively (any degree)
-    for (unsigned base = blockIdx.x * blockDim.x; base < fs; base += stride) {
-      const unsigned i = base + threadIdx.x;
-      unsigned b = 0, du = 0, deg = 0;
-      if (i < fs) {
-        const unsigned u = cur_front(a, it)[i];
-        b = __ldg(a.rowptr + u);
-        deg = __ldg(a.rowptr + u + 1) - b;
-        du = __ldcg(a.dist + u);
+    // the level's light list, warp-cooperatively (any degree), spread over
+    // ALL warps: each takes a contiguous slice of ceil(fs / warps) vertices
+    // (a level's relax rounds per warp, not the first fs / 256 blocks, set
+    // its latency)
+    {
+      const unsigned nw = stride >> 5, gw = gtid >> 5;
+      const unsigned per = max(1u, (fs + nw - 1) / nw);
+      const unsigned v0 = min(fs, gw * per), v1 = min(fs, v0 + per);
+      for (unsigned base = v0; base < v1; base += 32) {  // warp-uniform
+        const unsigned i = base + dev::lane_id();
+        unsigned b = 0, du = 0, deg = 0;
+        if (i < v1) {
+          const unsigned u = cur_front(a, it)[i];
+          b = __ldg(a.rowptr + u);
+          deg = __ldg(a.rowptr + u + 1) - b;
+          du = __ldcg(a.dist + u);
+        }
+        dev::block_add_u64(&s.work, deg);
+        warp_light_relax(a, it, s, b, du, deg);
       }
-      dev::block_add_u64(&s.work, deg);
-      warp_light_relax(a, it, s, b, du, deg);
     }
     // the level's chunk items (inserted while the previous level flushed)
     mark(1);
