@@ -107,6 +107,7 @@ struct dpc_dtree {
   int64_t root_children = 0;
   int64_t internal = 0;              // nodes with >= 1 child
   unsigned group = 1;                // lanes per work item (mean fan-out)
+  unsigned* pend = nullptr;          // persistent grid: pending internal children per node
 };
 
 namespace dpc {

@@ -55,6 +55,8 @@ struct Args {
   unsigned child_threads;
   unsigned child_blocks;
   int is_max;      // TH (max) vs TD (sum)
+  const int* parent;  // persistent grid: parent[v] (-1 at the root)
+  unsigned* pend;     // persistent grid: internal children not yet folded
 };
 
 __device__ __forceinline__ unsigned nkids(const Args& a, unsigned v) {
@@ -252,11 +254,21 @@ __global__ void __launch_bounds__(256) cons_kernel(Args a, const unsigned* items
 }
 
 // ---------------------------------------------------------------- persistent
+// Top-down: the recursion's levels, consolidated per level with a
+// device-wide barrier; each internal node also records
+// its leaf children's share of the postwork (TD: one per leaf child, TH: 1
+// if it has one) in res[v] and its internal-children count in pend[v].
+// Bottom-up: the postwork of a node runs once all its children's postwork
+// has (the tail-launch semantics) by count-down instead of a barrier per
+// level: a finished node pushes res + 1 into its parent and the child that
+// brings the parent's count to zero carries on with the parent, so the
+// chains climb the tree concurrently (<= depth dependent steps, no barrier).
+constexpr unsigned kNoInternal = 0x80000000u;  // pend mark: no internal child
+
 __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_levels) {
   cg::grid_group grid = cg::this_grid();
   const unsigned g = a.group, lane = threadIdx.x & 31u, sub = threadIdx.x & (g - 1);
   const unsigned gpw = 32 / g;
-  const unsigned warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
   // cnt[0..2]: per-level append counters, triple-buffered so that the
   // counter read after a level's barrier is never reset or appended to by a
@@ -275,10 +287,56 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
       unsigned i = base + dev::warp_in_block() * gpw + lane / g;
       bool active = i < hi;
       unsigned v = active ? a.nodes[i] : 0;
-      unsigned want = count_kids(a, v, sub, g, active);
+      // the lane's first kKeep internal children stay in registers for the
+      // write below (no second dependent clist / cstart round trip)
+      constexpr unsigned kKeep = 4;
+      unsigned want = 0, leaves = 0, kid[kKeep];
+      if (active) {
+        const unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
+        for (unsigned k = b + sub; k < e; k += g) {
+          const unsigned c = static_cast<unsigned>(__ldg(a.clist + k));
+          if (nkids(a, c) > 0) {
+#pragma unroll
+            for (unsigned j = 0; j < kKeep; j++)
+              if (j == want) kid[j] = c;
+            want++;
+          } else {
+            leaves++;
+          }
+        }
+      }
+      unsigned wi = want, wl = leaves;
+      for (unsigned o = g >> 1; o > 0; o >>= 1) {
+        wi += __shfl_xor_sync(dev::kFull, wi, o);
+        wl += __shfl_xor_sync(dev::kFull, wl, o);
+      }
+      if (active && sub == 0) {
+        a.res[v] = a.is_max ? (wl ? 1 : 0) : static_cast<int>(wl);
+        a.pend[v] = wi ? wi : kNoInternal;
+      }
       unsigned bb, bt;
       unsigned at = hi + dev::block_reserve(app, want, &bb, &bt);
-      write_kids(a, v, sub, g, active && want, at);
+      if (active && want) {
+#pragma unroll
+        for (unsigned j = 0; j < kKeep; j++) {
+          if (j < want) {
+            if (at + j < a.cap) a.nodes[at + j] = kid[j];
+            else atomicOr(&a.hdr->overflow, 1u);
+          }
+        }
+        if (want > kKeep) {  // rare: more internal children than kept
+          const unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
+          unsigned seen = 0, pos = at + kKeep;
+          for (unsigned k = b + sub; k < e; k += g) {
+            const unsigned c = static_cast<unsigned>(__ldg(a.clist + k));
+            if (nkids(a, c) > 0 && seen++ >= kKeep) {
+              if (pos < a.cap) a.nodes[pos] = c;
+              else atomicOr(&a.hdr->overflow, 1u);
+              pos++;
+            }
+          }
+        }
+      }
     }
     grid.sync();
     levels++;
@@ -286,16 +344,25 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
     hi = min(hi + *reinterpret_cast<volatile unsigned*>(app), a.cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) off[levels + 1] = hi;
   }
-  // bottom-up in reverse level order
-  for (int L = static_cast<int>(levels) - 1; L >= 0; L--) {
-    unsigned l0 = off[L], l1 = off[L + 1];
-    if (L == static_cast<int>(levels) - 1) l1 = lo;
-    for (unsigned base = l0 + warp_g * gpw; base < l1; base += nwarps * gpw) {
-      unsigned i = base + lane / g;
-      bool active = i < l1;
-      fold_node(a, active ? a.nodes[i] : 0, sub, g, active);
+  // bottom-up: count-down chains from the nodes with only leaf children
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < lo; i += stride) {
+    unsigned u = a.nodes[i];
+    if (__ldcg(a.pend + u) != kNoInternal) continue;
+    while (true) {
+      const int r = atomicAdd(a.res + u, 0);  // every child's share is in
+      const int p = __ldg(a.parent + u);
+      if (p < 0) break;
+      if (a.is_max) atomicMax(a.res + p, r + 1);
+      else atomicAdd(a.res + p, r + 1);
+      // acq_rel count-down: releases this share, and the child that takes
+      // the count to zero acquires every sibling's (no full fences)
+      unsigned old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"
+                   : "=r"(old) : "l"(a.pend + p), "r"(0xffffffffu) : "memory");
+      if (old != 1u) break;
+      u = static_cast<unsigned>(p);
     }
-    grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->iter = levels;
 }
@@ -365,7 +432,7 @@ dpc_status dpc_dtree_upload(dpc_ctx* c, const dpc_tree* t, dpc_dtree** out) {
 void dpc_dtree_free(dpc_dtree* d) {
   if (!d) return;
   if (d->ctx) cudaStreamSynchronize(d->ctx->stream);
-  void* bufs[] = {d->parent, d->cstart, d->clist, d->result, d->level_nodes, d->level_off, d->hdr};
+  void* bufs[] = {d->parent, d->cstart, d->clist, d->result, d->level_nodes, d->level_off, d->hdr, d->pend};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (d->hdr_host) cudaFreeHost(d->hdr_host);
@@ -399,6 +466,8 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
   a.child_threads = k.child_threads;
   a.child_blocks = k.child_blocks;
   a.is_max = which == DPC_APP_TREE_HEIGHT;
+  a.parent = d->parent;
+  a.pend = nullptr;
   cudaStream_t s = c->stream;
   size_t need = 2048;
   if (k.variant == DPC_BASIC) need = 2 * static_cast<size_t>(d->internal) + 1024;
@@ -465,6 +534,8 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
         break;
       case DPC_GRID:
         if (k.grid_persistent) {
+          if (!d->pend) DPC_CUDA(cudaMalloc(&d->pend, sizeof(unsigned) * static_cast<size_t>(d->n)));
+          a.pend = d->pend;
           int per_sm = 0;
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(
               &per_sm, reinterpret_cast<const void*>(tree::grid_persistent), 256, 0);
