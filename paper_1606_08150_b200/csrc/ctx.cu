@@ -448,7 +448,11 @@ dpc_status dpc_spmv_host_batch(dpc_ctx* c, dpc_dgraph* g, const float* const* xs
     DPC_CUDA(cudaStreamWaitEvent(c->stream, e[s], 0));
     if (i >= 2) DPC_CUDA(cudaStreamWaitEvent(c->stream, e[6 + s], 0));
     dpc_status st = dpc_spmv_device(c, g, dx[s], dy[s], cfg, i + 1 == count ? met : nullptr);
-    if (st != DPC_OK) return st;
+    if (st != DPC_OK) {  // no copy may still touch the caller's host vectors
+      cudaStreamSynchronize(c->h2d);
+      cudaStreamSynchronize(c->d2h);
+      return st;
+    }
     DPC_CUDA(cudaEventRecord(e[2 + s], c->stream));
     DPC_CUDA(cudaEventRecord(e[4 + s], c->stream));
     DPC_CUDA(cudaStreamWaitEvent(c->d2h, e[4 + s], 0));
