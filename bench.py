@@ -14,7 +14,7 @@ basic-DP, warp and block are timed in the same run and reported beside it
               host x / y (H2D of x and D2H of y inside the timed region; A is
               the resident operator, uploaded once)
   roofline  : algorithmic bytes nnz*8 + (n+1)*4 + n*4 + n*4 per step over the
-              step time (one persistent cooperative kernel = the whole step)
+              step time (one persistent kernel = the whole step)
   cpu_baseline : oracle port (multi-threaded fp32 CSR SpMV, all host cores)
 
 --impl reference runs the reference's own CPU path: the unmodified dpcons
@@ -470,7 +470,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "BASELINE config 2: SpMV CSR, synthetic R-MAT scale-20 matrix "
                                "(1,048,576 rows, 16,777,216 nnz, fp32 values/x in (0,1], seed 1)",
-                   "variant": "grid-consolidated: one persistent cooperative kernel, insert phase + "
+                   "variant": "grid-consolidated: one persistent kernel (one 1024-thread block per SM, all co-resident), insert phase + "
                               "device-wide barrier + stream-balanced drain (threshold 0, measured)",
                    "n": n, "nnz": nnz, "l2": "flushed (512 MB memset) before every timed step",
                    "parallelism": f"replicas{world}" if world > 1 else "single GPU",
