@@ -25,7 +25,6 @@ import glob
 import hashlib
 import os
 import subprocess
-import threading
 
 import numpy as np
 
@@ -71,9 +70,6 @@ def read_program(name):
 def _nvcc():
     return os.environ.get("NVCC") or ("/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc")
                                       else "nvcc")
-
-
-_build_lock = threading.Lock()
 
 
 def build_so(cu_src, tag):
