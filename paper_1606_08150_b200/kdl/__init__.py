@@ -34,7 +34,7 @@ from .cuda import generate
 from .parse import KdlError, parse_program
 
 __all__ = ["compile", "compile_program", "Module", "KdlError", "KdlFault", "Config", "parse_program",
-           "consolidate", "lower_kc", "k20c_occupancy", "generate", "build_programs", "PROGRAMS"]
+           "consolidate", "lower_kc", "k20c_occupancy", "generate", "build_programs", "autotune", "PROGRAMS"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD = os.path.join(HERE, "_build")
@@ -299,6 +299,35 @@ def compile(source, mode="basic", config=None, name="kdl", consolidated=False, s
     schedule="block" (default) drains multi-block children one item per
     block; "reference" keeps the reference's drain loop."""
     return compile_program(parse_program(source), mode, config, name, consolidated, schedule)
+
+
+def autotune(source, scalars, arrays=None, *, until_stable=None, modes=("warp", "block", "grid"),
+             kc=(None, 4, 16, 64), reps=3, name="kdl", device=0):
+    """Pick the consolidation granularity and the KC_X concurrency of a
+    program by measurement on the device (the reference picks them from its
+    cost model: directive + KC_X defaults, config.hpp:77-86).  Every
+    candidate runs `reps` times on the same inputs (device time of the entry
+    launch tree); candidates whose output differs from the first one's are
+    rejected.  Returns (best, table) with rows {mode, kc_x, ms, launches}."""
+    from .transform import default_concurrency
+    table, ref_out = [], None
+    for mode in modes:
+        for x in kc:
+            if mode == "grid" and x not in (None, 1):
+                continue  # KC_1: the grid form's single consolidated launch fills the device
+            cfg = Config("kc", x=x) if x else None
+            mod = compile(source, mode, config=cfg, name=f"{name}_x{x or 0}")
+            runs = [mod.run(scalars, arrays, until_stable=until_stable, device=device, timed=True)
+                    for _ in range(reps)]
+            outs = runs[-1].arrays
+            if ref_out is None:
+                ref_out = outs
+            same = all(np.array_equal(outs[k], ref_out[k]) if outs[k].dtype.kind != "f"
+                       else np.allclose(outs[k], ref_out[k], rtol=1e-9, atol=1e-12) for k in outs)
+            table.append({"mode": mode, "kc_x": x or default_concurrency(mode), "ms": min(r.ms for r in runs),
+                          "launches": runs[-1].launches, "same_result": bool(same)})
+    ok = [r for r in table if r["same_result"]]
+    return min(ok, key=lambda r: r["ms"]), table
 
 
 def build_programs(jobs=8):

@@ -214,3 +214,18 @@ def test_bfs_rec_program_larger_vs_oracle(orc):
         res = run_bfs(module("bfs.kdl", mode), g.rowptr, g.col, s)
         got = np.where(res.arrays["level"] >= INF, 2**32 - 1, res.arrays["level"])
         np.testing.assert_array_equal(got, want)
+
+
+def test_autotune_picks_a_measured_form(orc):
+    t = dpc.gen_tree(6, 2, 8, 0.6, 5)
+    want = orc.tree_desc(t.parent)
+    best, table = kdl.autotune(src_of("td.kdl"), {"n": t.n, "root": t.root, "rootnc": len(t.children(t.root))},
+                               {"cstart": t.cstart, "clist": t.clist, "parent": t.parent},
+                               kc=(None, 8), reps=2, name="td_tune")
+    assert best in table and all(r["same_result"] for r in table)
+    assert {r["mode"] for r in table} == {"warp", "block", "grid"}
+    mod = kdl.compile(src_of("td.kdl"), best["mode"], config=kdl.Config("kc", x=best["kc_x"]),
+                      name=f"td_tune_x{best['kc_x']}")
+    res = mod.run({"n": t.n, "root": t.root, "rootnc": len(t.children(t.root))},
+                  {"cstart": t.cstart, "clist": t.clist, "parent": t.parent})
+    np.testing.assert_array_equal(res.arrays["desc"], want)
