@@ -179,6 +179,77 @@ def _x_global(n):
     return (rng.integers(1, 1 << 24, n) / float(1 << 24)).astype(np.float32)
 
 
+def _run_fused(args, dist, ctx, dg, dx, R, rank, world, y64):
+    """dpc_multi_spmv_fused over IPC-mapped peer x slices: per step a device
+    peer barrier (x written), the SpMV gathering x from the owners, a peer
+    barrier (x reads done); max over ranks.  Any failure falls back to the
+    NCCL numbers (reported)."""
+    import paper_1606_08150_b200 as dpc
+    res, opened, bufs = {"ok": False}, [], []
+    try:
+        flags = ctx.alloc(8 * world)
+        bufs.append(flags)
+        ctx.h2d(flags, np.zeros(world, np.uint64))
+        ctx.synchronize()
+        hs = [None] * world
+        dist.all_gather_object(hs, (dpc.ipc_handle(dx), dpc.ipc_handle(flags)))
+        xs, fs = [], []
+        for q in range(world):
+            if q == rank:
+                xs.append(dx)
+                fs.append(flags)
+            else:
+                xp, fp = dpc.ipc_open(ctx, hs[q][0]), dpc.ipc_open(ctx, hs[q][1])
+                opened += [xp, fp]
+                xs.append(xp)
+                fs.append(fp)
+        xtab, ftab = ctx.alloc(8 * world), ctx.alloc(8 * world)
+        bufs += [xtab, ftab]
+        ctx.h2d(xtab, np.array(xs, np.uint64))
+        ctx.h2d(ftab, np.array(fs, np.uint64))
+        yd = ctx.alloc(4 * R)
+        bufs.append(yd)
+        epoch = 0
+
+        def step():
+            nonlocal epoch
+            dpc.p2p_barrier(ctx, ftab, world, rank, epoch + 1)
+            dg.spmv_fused(xtab, world, R, yd)
+            dpc.p2p_barrier(ctx, ftab, world, rank, epoch + 2)
+            epoch += 2
+
+        step()
+        dpc.p2p_check(ctx)
+        y = ctx.d2h(yd, R).astype(np.float64)
+        ok = bool(np.all(np.abs(y - y64) <= 1e-5 * np.abs(y64)))
+        for _ in range(args.warmup):
+            step()
+        ctx.synchronize()
+        _barrier(dist)
+        ts = []
+        for _ in range(args.steps):
+            ctx.flush_l2()
+            ctx.record(4)
+            step()
+            ctx.record(5)
+            ts.append(ctx.elapsed_ms(4, 5))
+        dpc.p2p_check(ctx)
+        ms = float(np.mean(ts))
+        ok_all = _sum_over_ranks(dist, float(ok)) == world
+        res = {"ok": ok_all, "ms": ms, "ms_max": _max_over_ranks(dist, ms),
+               "api": "dpc_p2p_barrier + dpc_multi_spmv_fused + dpc_p2p_barrier (C ABI), per rank"}
+    except Exception as e:  # noqa: BLE001 - fall back to the NCCL path
+        res = {"ok": False, "error": str(e)[:300]}
+    for p in opened:
+        try:
+            dpc.ipc_close(p)
+        except Exception:  # noqa: BLE001
+            pass
+    for b in bufs:
+        ctx.free(b)
+    return res
+
+
 def run_multi(args, dist, rank, world, local):
     """BASELINE config 5 shape, weak scaling: a vertex-permuted R-MAT of scale
     20 + log2(N) split into N equal row blocks (2^20 rows, ~16.8M nnz per
@@ -244,6 +315,7 @@ def run_multi(args, dist, rank, world, local):
     e2e_max = _max_over_ranks(dist, float(np.mean(e2e)))
     e2e_ok = bool(np.all(np.abs(yl.astype(np.float64) - y64) <= 1e-5 * np.abs(y64)))
     ok_all = _sum_over_ranks(dist, float(parity_ok and e2e_ok)) == world
+    fused = _run_fused(args, dist, ctx, dg, dx, R, rank, world, y64)
     peak = _peak_hbm()
     alg = spmv_bytes(R, A.m) + 4 * (A.ncols - R)  # + the gathered remote x slices
     out = {
@@ -268,6 +340,20 @@ def run_multi(args, dist, rank, world, local):
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
+    if fused.get("ok"):
+        # headline: the fused path (x gathered from the owners inside the SpMV)
+        out["nccl_allgather"] = {"value": out["value"], "ms_per_step": out["ms_per_step"],
+                                 "kernel": "ncclAllGather + spmv::grid_stream"}
+        out["value"] = round(total_nnz / (fused["ms_max"] * 1e-3) / 1e9, 3)
+        out["ms_per_step"] = round(fused["ms_max"], 4)
+        out["config"]["parallelism"] = (f"row-partition x{world}; x read from the owners' memory inside the SpMV "
+                                        "(CUDA IPC peer pointers over NVLink / NVSwitch, device-side peer "
+                                        "barrier, no NCCL on the data path)")
+        out["roofline"]["kernel"] = "spmv::grid_stream with peer x (dpc_multi_spmv_fused, rank 0)"
+        out["roofline"]["achieved"] = round(alg / (fused["ms"] * 1e-3) / 1e9, 1)
+        out["roofline"]["frac"] = round(alg / (fused["ms"] * 1e-3) / 1e9 / peak, 4)
+        out["gpu_launches"] = 3 * args.steps
+    out["fused"] = {k: v for k, v in fused.items() if k != "ms_max"}
     out["sssp"] = run_multi_sssp(args, dist, rank, world, ctx, comm, scale, r0, R)
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -306,6 +306,26 @@ dpc_status dpc_spmv_host(dpc_ctx* ctx, dpc_dgraph* dg, const float* x_host, floa
 dpc_status dpc_spmv_host_batch(dpc_ctx* ctx, dpc_dgraph* dg, const float* const* x_host, float* const* y_host,
                                int64_t count, const dpc_launch_cfg* cfg, dpc_metrics* met);
 
+/* ---- fused multi-GPU path over peer memory (BASELINE config 5) ----
+ * CUDA IPC export / import of a device buffer; the caller moves the 64-byte
+ * handles between ranks (NCCL, MPI, torch.distributed). */
+dpc_status dpc_ipc_handle(const void* d_ptr, uint8_t out[64]);
+dpc_status dpc_ipc_open(dpc_ctx* ctx, const uint8_t handle[64], void** d_out);
+dpc_status dpc_ipc_close(void* d_ptr);
+/* Device-side barrier over peer memory: d_flag_tab is a DEVICE array of
+ * `world` pointers to the ranks' flag arrays (world x u64 each, zeroed once);
+ * epochs must increase (1, 2, ...).  Enqueued on the context stream. */
+dpc_status dpc_p2p_barrier(dpc_ctx* ctx, uint64_t* const* d_flag_tab, int32_t world, int32_t me, uint64_t epoch);
+/* Reports DPC_E_DEADLOCK if a barrier timed out (synchronises the stream). */
+dpc_status dpc_p2p_check(dpc_ctx* ctx);
+/* Grid stream SpMV of this rank's row block with x read from the owners:
+ * d_xpeer is a DEVICE array of `world` pointers, x entry i at
+ * d_xpeer[i / rows_per_rank][i % rows_per_rank] (replaces ncclAllGather +
+ * dpc_spmv_device, multi.cu).  Needs the grid variant with threshold 0. */
+dpc_status dpc_multi_spmv_fused(dpc_ctx* ctx, dpc_dgraph* local, const float* const* d_xpeer, int32_t world,
+                                int64_t rows_per_rank, float* d_y_local, const dpc_launch_cfg* cfg,
+                                dpc_metrics* met);
+
 /* Device memory on the context's GPU (caller-owned vectors for the
  * device-pointer entry points). */
 void* dpc_dev_alloc(dpc_ctx* ctx, size_t bytes);

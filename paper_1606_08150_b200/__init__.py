@@ -151,6 +151,13 @@ _SIGS = {
     "dpc_spmv_device": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host_batch": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_ipc_handle": (C.c_int, [_P, _P]),
+    "dpc_ipc_open": (C.c_int, [_P, _P, C.POINTER(_P)]),
+    "dpc_ipc_close": (C.c_int, [_P]),
+    "dpc_p2p_barrier": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_uint64]),
+    "dpc_p2p_check": (C.c_int, [_P]),
+    "dpc_multi_spmv_fused": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int64, _P, C.POINTER(LaunchCfg),
+                                       C.POINTER(Metrics)]),
     "dpc_sssp_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_bfs_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_run_bfs": (C.c_int, [_P, _CsrP, _i32, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
@@ -366,6 +373,33 @@ def save_tree(t: Tree, path: str):
     _check(_lib.dpc_save_tree(t._h, os.fsencode(path)))
 
 
+def ipc_handle(d_ptr: int) -> bytes:
+    """CUDA IPC handle (64 bytes) of a device buffer from dpc_dev_alloc."""
+    buf = (C.c_uint8 * 64)()
+    _check(_lib.dpc_ipc_handle(C.c_void_p(d_ptr), buf))
+    return bytes(buf)
+
+
+def ipc_open(ctx, handle: bytes) -> int:
+    """Maps a peer's buffer (its 64-byte IPC handle) into this process."""
+    out = C.c_void_p()
+    _check(_lib.dpc_ipc_open(ctx.handle, (C.c_uint8 * 64).from_buffer_copy(handle), C.byref(out)))
+    return int(out.value)
+
+
+def ipc_close(d_ptr: int):
+    _check(_lib.dpc_ipc_close(C.c_void_p(d_ptr)))
+
+
+def p2p_barrier(ctx, d_flag_table: int, world: int, me: int, epoch: int):
+    """Device-side barrier over peer memory (enqueued on ctx's stream)."""
+    _check(_lib.dpc_p2p_barrier(ctx.handle, C.c_void_p(d_flag_table), world, me, epoch))
+
+
+def p2p_check(ctx):
+    _check(_lib.dpc_p2p_check(ctx.handle))
+
+
 def launch_cfg(app: str, variant: str, **overrides) -> LaunchCfg:
     """Measured default dpc_launch_cfg for (app, variant), with overrides."""
     cfg = LaunchCfg()
@@ -524,6 +558,12 @@ class DeviceGraph:
         yp = (C.c_void_p * max(1, k))(*[y.ctypes.data for y in ys])
         _check(_lib.dpc_spmv_host_batch(self.ctx.handle, self._h, xp, yp, k, _cfg_arg("spmv", variant, cfg),
                                         None))
+
+    def spmv_fused(self, d_xpeer_table: int, world: int, rows_per_rank: int, d_y: int, variant="grid", cfg=None):
+        """Fused multi-GPU SpMV of this row block: x gathered from the owners
+        through a DEVICE table of `world` peer pointers (dpc_multi_spmv_fused)."""
+        _check(_lib.dpc_multi_spmv_fused(self.ctx.handle, self._h, C.c_void_p(d_xpeer_table), world, rows_per_rank,
+                                         C.c_void_p(d_y), _cfg_arg("spmv", variant, cfg), None))
 
     def sssp(self, source: int, variant="grid", cfg=None, metrics: bool = True):
         met = Metrics() if metrics else None

@@ -220,6 +220,7 @@ void dpc_ctx_destroy(dpc_ctx* c) {
   if (c->flush_buf) cudaFree(c->flush_buf);
   for (auto& ev : c->pev)
     if (ev) cudaEventDestroy(ev);
+  if (c->p2p_fault) cudaFree(c->p2p_fault);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->stream) cudaStreamDestroy(c->stream);

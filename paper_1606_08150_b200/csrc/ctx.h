@@ -28,6 +28,7 @@ struct dpc_ctx {
   // streams and per-slot events, created on first use
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t pev[9] = {};
+  unsigned* p2p_fault = nullptr;  // dpc_p2p_barrier timeout flag
 };
 
 // Device-resident graph plus every buffer its apps need.

@@ -59,7 +59,19 @@ struct Args {
   unsigned child_blocks;  // cap, 0 = none
   unsigned xflags;        // experiment switches (dpc_launch_cfg.flags >> 24), 0 in production
   unsigned coop;          // launched cooperatively (grid.sync) vs normal launch + soft barrier
+  // fused multi-GPU SpMV (dpc_multi_spmv_fused): x is distributed, entry i
+  // lives on rank i / rows at offset i % rows and is read straight from the
+  // owner's memory (NVLink peer loads); nullptr = local x
+  const float* const* xpeer;
+  unsigned rshift;        // log2(rows) when rows is a power of two, else ~0u
+  unsigned rows;
 };
+
+__device__ __forceinline__ float peer_x(const Args& a, unsigned idx) {
+  const unsigned o = a.rshift != ~0u ? idx >> a.rshift : idx / a.rows;
+  const unsigned l = a.rshift != ~0u ? idx & (a.rows - 1u) : idx - o * a.rows;
+  return __ldg(a.xpeer[o] + l);
+}
 
 __device__ __forceinline__ int4 ldg_stream(const int4* p) {
   int4 r;
@@ -742,7 +754,9 @@ __device__ __forceinline__ float grp_dot(const Args& a, const Grp<G>& g, unsigne
       if (a.xflags & 128u) idx &= 0xffff;   // probe: gathers confined to 256 KB of x
       const float wt = on ? wp[e] : 0.f;
       float xv;
-      if (a.xflags & 16u) {
+      if (a.xpeer) {
+        xv = peer_x(a, static_cast<unsigned>(idx));
+      } else if (a.xflags & 16u) {
         xv = 1.f;
       } else if (SLOG > 0) {
         const uint2 t = xc[xslot(static_cast<unsigned>(idx), SLOG)];
@@ -1415,9 +1429,19 @@ static int coop_blocks(dpc_ctx* ctx, const void* fn, int threads, size_t smem = 
 
 using namespace dpc;
 
+namespace dpc {
+dpc_status spmv_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, const dpc_launch_cfg* cfg,
+                    dpc_metrics* met, const float* const* xpeer, uint64_t rows);
+}
+
 extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y,
                                       const dpc_launch_cfg* cfg, dpc_metrics* met) {
   clear_error();
+  return dpc::spmv_run(ctx, g, d_x, d_y, cfg, met, nullptr, 0);
+}
+
+dpc_status dpc::spmv_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, const dpc_launch_cfg* cfg,
+                         dpc_metrics* met, const float* const* xpeer, uint64_t rows) {
   if (!ctx || !g || !d_x || !d_y) return fail(DPC_E_INVALID, "NULL argument");
   if (g->m > 0 && !g->val) return fail(DPC_E_INVALID, "graph was uploaded without values (val)");
   Cfg c;
@@ -1438,9 +1462,15 @@ extern "C" dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* g, const float* 
   a.child_threads = c.child_threads;
   a.child_blocks = c.child_blocks;
   a.xflags = c.flags >> 24;
+  a.xpeer = xpeer;
+  a.rows = static_cast<unsigned>(rows);
+  a.rshift = ~0u;
+  if (rows && (rows & (rows - 1)) == 0) a.rshift = static_cast<unsigned>(__builtin_ctzll(rows));
   a.coop = 1;
   // stream-balanced grid drain (grid_stream)
   const bool use_stream = c.variant == DPC_GRID && c.grid_persistent && !(c.flags & DPC_CFG_GRID_CHUNKED);
+  if (xpeer && !(use_stream && c.threshold == 0 && ((c.flags >> 20) & 7u) != 3u && ((c.flags >> 20) & 7u) != 4u))
+    return fail(DPC_E_INVALID, "fused multi-GPU SpMV runs on the grid stream kernel (threshold 0, no x cache)");
   spmv::Stream sa{};
   if (use_stream) {
     const uint64_t heavy = pool_need(g, c.threshold, 1u << 30);

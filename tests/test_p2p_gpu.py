@@ -1,0 +1,181 @@
+"""Fused multi-GPU SpMV over peer memory (BASELINE config 5):
+x gathered from the owners inside the SpMV (dpc_multi_spmv_fused), the
+device-side peer barrier (dpc_p2p_barrier) and CUDA IPC mapping
+(dpc_ipc_*).  One GPU in this pool, so the tests run the ranks' partitions
+(a) in one process with direct pointers and one context (stream) per rank,
+(b) in two processes on the same GPU with IPC-mapped buffers — the same
+code path as across GPUs, minus NVLink.  Results against the oracle
+(fp32 SpMV within 1e-5 of the fp64 reference)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_1606_08150_b200 as dpc
+
+pytestmark = pytest.mark.gpu
+
+SCALE, SEED = 12, 3
+
+
+def full_matrix():
+    return dpc.gen_rmat(SCALE, 16, seed=SEED, weights=False, values=True, permute=True)
+
+
+def x_vector(n, step=1):
+    return (((np.arange(n) * (7 + step)) % 89 + 1) / 89.0).astype(np.float32)
+
+
+def close(y, y64):
+    return np.all(np.abs(y.astype(np.float64) - y64) <= 1e-5 * np.abs(y64) + 1e-30)
+
+
+@pytest.mark.parametrize("world", [1, 3, 4])
+def test_fused_spmv_partitions_one_process(orc, world):
+    """world row blocks; x entry i lives on block i // R (R a power of two
+    for world 1 / 4, not for 3: the shift and the division paths)."""
+    g = full_matrix()
+    n = g.n
+    R = (n + world - 1) // world
+    x = x_vector(n)
+    y64 = orc.spmv_f64(g.rowptr, g.col, g.val, x)
+    ctx = dpc.Context(0)
+    bufs = []
+    try:
+        xs = []
+        for p in range(world):
+            d = ctx.alloc(4 * R)
+            bufs.append(d)
+            sl = np.zeros(R, np.float32)
+            part = x[p * R:min(n, (p + 1) * R)]
+            sl[:len(part)] = part
+            ctx.h2d(d, sl)
+            xs.append(d)
+        tab = ctx.alloc(8 * world)
+        bufs.append(tab)
+        ctx.h2d(tab, np.array(xs, np.uint64))
+        for p in range(world):
+            r0, r1 = p * R, min(n, (p + 1) * R)
+            A = dpc.gen_rmat_rows(SCALE, r0, r1, 16, seed=SEED, weights=False, values=True, permute=True)
+            dg = dpc.DeviceGraph(ctx, A)
+            yd = ctx.alloc(4 * max(1, r1 - r0))
+            bufs.append(yd)
+            dg.spmv_fused(tab, world, R, yd)
+            y = ctx.d2h(yd, r1 - r0)
+            assert close(y, y64[r0:r1]), f"rank {p}"
+            dg.close()
+    finally:
+        for b in bufs:
+            ctx.free(b)
+        ctx.close()
+
+
+def test_fused_spmv_rejects_non_stream_config():
+    g = full_matrix()
+    ctx = dpc.Context(0)
+    dg = dpc.DeviceGraph(ctx, g)
+    xd, yd, tab = ctx.alloc(4 * g.n), ctx.alloc(4 * g.n), ctx.alloc(8)
+    ctx.h2d(tab, np.array([xd], np.uint64))
+    with pytest.raises(dpc.DpcError):
+        dg.spmv_fused(tab, 1, g.n, yd, variant="block")
+    with pytest.raises(dpc.DpcError):
+        dg.spmv_fused(tab, 1, g.n, yd, cfg=dpc.launch_cfg("spmv", "grid", threshold=8))
+    for b in (xd, yd, tab):
+        ctx.free(b)
+    dg.close()
+    ctx.close()
+
+
+def test_p2p_barrier_contexts_one_process():
+    """Three ranks as three contexts (streams) on one device: every epoch
+    completes once all three signalled."""
+    world = 3
+    ctxs = [dpc.Context(0) for _ in range(world)]
+    flags = [ctxs[0].alloc(8 * world) for _ in range(world)]
+    for f in flags:
+        ctxs[0].h2d(f, np.zeros(world, np.uint64))
+    tab = ctxs[0].alloc(8 * world)
+    ctxs[0].h2d(tab, np.array(flags, np.uint64))
+    ctxs[0].synchronize()
+    for epoch in (1, 2, 3):
+        for q in range(world):
+            dpc.p2p_barrier(ctxs[q], tab, world, q, epoch)
+        for q in range(world):
+            dpc.p2p_check(ctxs[q])
+            got = ctxs[q].d2h(flags[q], world, np.uint64)
+            assert np.all(got == epoch)
+    for b in flags + [tab]:
+        ctxs[0].free(b)
+    for c in ctxs:
+        c.close()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, steps):
+    import torch.distributed as dist
+
+    from tests._oracle import Oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle()
+    g = full_matrix()
+    n = g.n
+    R = n // world
+    r0, r1 = rank * R, (rank + 1) * R
+    ctx = dpc.Context(0)
+    A = dpc.gen_rmat_rows(SCALE, r0, r1, 16, seed=SEED, weights=False, values=True, permute=True)
+    dg = dpc.DeviceGraph(ctx, A)
+    x_local = ctx.alloc(4 * R)
+    flags = ctx.alloc(8 * world)
+    ctx.h2d(flags, np.zeros(world, np.uint64))
+    ctx.synchronize()
+    hs = [None] * world
+    dist.all_gather_object(hs, (dpc.ipc_handle(x_local), dpc.ipc_handle(flags)))
+    xs, fs, opened = [], [], []
+    for q in range(world):
+        if q == rank:
+            xs.append(x_local)
+            fs.append(flags)
+        else:
+            xp, fp = dpc.ipc_open(ctx, hs[q][0]), dpc.ipc_open(ctx, hs[q][1])
+            opened += [xp, fp]
+            xs.append(xp)
+            fs.append(fp)
+    xtab, ftab, yd = ctx.alloc(8 * world), ctx.alloc(8 * world), ctx.alloc(4 * R)
+    ctx.h2d(xtab, np.array(xs, np.uint64))
+    ctx.h2d(ftab, np.array(fs, np.uint64))
+    ok = True
+    for s in range(1, steps + 1):
+        x = x_vector(n, s)
+        ctx.h2d(x_local, x[r0:r1])
+        dpc.p2p_barrier(ctx, ftab, world, rank, 2 * s - 1)   # every x slice written
+        dg.spmv_fused(xtab, world, R, yd)
+        dpc.p2p_barrier(ctx, ftab, world, rank, 2 * s)       # every peer done reading x
+        dpc.p2p_check(ctx)
+        y = ctx.d2h(yd, R)
+        ok = ok and bool(close(y, orc.spmv_f64(g.rowptr, g.col, g.val, x)[r0:r1]))
+    flag = [None] * world
+    dist.all_gather_object(flag, ok)
+    for p in opened:
+        dpc.ipc_close(p)
+    for b in (x_local, flags, xtab, ftab, yd):
+        ctx.free(b)
+    dg.close()
+    ctx.close()
+    dist.destroy_process_group()
+    assert all(flag), flag
+
+
+def test_fused_spmv_two_processes_ipc():
+    """Two processes, one GPU: IPC-mapped x slices and barrier flags, the
+    handles exchanged over gloo; three SpMV steps with changing x."""
+    import torch.multiprocessing as mp
+    mp.spawn(_rank, args=(2, _free_port(), 3), nprocs=2, join=True)
