@@ -187,9 +187,9 @@ def _run_fused(args, dist, ctx, dg, dx, R, rank, world, y64):
     import paper_1606_08150_b200 as dpc
     res, opened, bufs = {"ok": False}, [], []
     try:
-        flags = ctx.alloc(8 * world)
+        flags = ctx.alloc(16 * world)
         bufs.append(flags)
-        ctx.h2d(flags, np.zeros(world, np.uint64))
+        ctx.h2d(flags, np.zeros(2 * world, np.uint64))
         ctx.synchronize()
         hs = [None] * world
         dist.all_gather_object(hs, (dpc.ipc_handle(dx), dpc.ipc_handle(flags)))
@@ -393,12 +393,92 @@ def run_multi_sssp(args, dist, rank, world, ctx, comm, scale, r0, R):
         ts.append(ctx.elapsed_ms(4, 5))
     ms = _max_over_ranks(dist, float(np.median(ts)))
     edges = _sum_over_ranks(dist, te)
+    fused = _sssp_fused(args, dist, ctx, dg, rank, world, n, source, d)
     dg.close()
-    return {"metric": "SSSP GTEPS (edges of reached vertices / time)", "value": round(edges / (ms * 1e-3) / 1e9, 3),
-            "unit": "GTEPS", "ms": round(ms, 3), "iterations": int(met.iterations), "source": source,
-            "workload": f"R-MAT scale {scale}, vertex-permuted, {world} row blocks, int weights [1,255]",
-            "exchange": "grouped ncclSend/ncclRecv of {vertex, distance} pairs + ncclAllGather counts + "
-                        "ncclAllReduce frontier size per iteration"}
+    out = {"metric": "SSSP GTEPS (edges of reached vertices / time)", "value": round(edges / (ms * 1e-3) / 1e9, 3),
+           "unit": "GTEPS", "ms": round(ms, 3), "iterations": int(met.iterations), "source": source,
+           "workload": f"R-MAT scale {scale}, vertex-permuted, {world} row blocks, int weights [1,255]",
+           "exchange": "grouped ncclSend/ncclRecv of {vertex, distance} pairs + ncclAllGather counts + "
+                       "ncclAllReduce frontier size per iteration"}
+    if fused.get("ok"):
+        out["fused"] = {"value": round(edges / (fused["ms"] * 1e-3) / 1e9, 3), "ms": round(fused["ms"], 3),
+                        "exchange": "remote relaxations straight into the owners' dist / stamp / frontier "
+                                    "(CUDA IPC peer pointers, NVLink atomics) + device peer barriers"}
+    else:
+        out["fused"] = fused
+    return out
+
+
+def _sssp_fused(args, dist, ctx, dg, rank, world, n, source, d_ref):
+    """The fused partitioned SSSP (dpc_msssp_* with peer tables): per
+    iteration relax (remote vertices written in their owner's buffers), peer
+    barrier, apply, peer barrier carrying the next-frontier sizes."""
+    import paper_1606_08150_b200 as dpc
+    opened, bufs = [], []
+    try:
+        flags = ctx.alloc(16 * world)
+        bufs.append(flags)
+
+        def run():  # every rank re-initialised (flags, dist, frontier) before anyone relaxes
+            ctx.h2d(flags, np.zeros(2 * world, np.uint64))
+            ps = dpc.PartitionedSSSP(dg, rank, world, n, source)
+            ctx.synchronize()
+            _barrier(dist)
+            return ps
+
+        ps = run()
+        mine = ps.buffers()
+        hs = [None] * world
+        dist.all_gather_object(hs, ([dpc.ipc_handle(b) for b in mine], dpc.ipc_handle(flags)))
+        table, fl = [], []
+        for q in range(world):
+            if q == rank:
+                table += mine
+                fl.append(flags)
+            else:
+                ptrs = [dpc.ipc_open(ctx, h) for h in hs[q][0]]
+                fp = dpc.ipc_open(ctx, hs[q][1])
+                opened += ptrs + [fp]
+                table += ptrs
+                fl.append(fp)
+        tab, ftab = ctx.alloc(8 * 5 * world), ctx.alloc(8 * world)
+        bufs += [tab, ftab]
+        ctx.h2d(tab, np.array(table, np.uint64))
+        ctx.h2d(ftab, np.array(fl, np.uint64))
+
+        def solve(ps):
+            ps.set_peers(tab)
+            epoch = 0
+            for _ in range(n + 1):
+                ps.relax()
+                epoch += 1
+                dpc.p2p_barrier(ctx, ftab, world, rank, epoch)
+                nxt = ps.apply(np.zeros((0, 2), np.uint32))
+                epoch += 1
+                if dpc.p2p_barrier_sum(ctx, ftab, world, rank, epoch, nxt) == 0:
+                    break
+            ps.end()
+
+        solve(ps)
+        ok = _sum_over_ranks(dist, float(np.array_equal(dg.get_dist(), d_ref))) == world
+        ts = []
+        for _ in range(max(1, min(args.steps, 5))):
+            ps = run()
+            ctx.record(6)
+            solve(ps)
+            ctx.record(7)
+            ts.append(ctx.elapsed_ms(6, 7))
+        res = {"ok": ok, "ms": _max_over_ranks(dist, float(np.median(ts)))}
+    except Exception as e:  # noqa: BLE001 - the NCCL numbers stand
+        res = {"ok": False, "error": str(e)[:300]}
+    for p in opened:
+        try:
+            dpc.ipc_close(p)
+        except Exception:  # noqa: BLE001
+            pass
+    for b in bufs:
+        ctx.free(b)
+    return res
 
 
 def _ncu_traffic(profile="r01_spmv_grid_stream.txt"):

@@ -313,11 +313,25 @@ dpc_status dpc_ipc_handle(const void* d_ptr, uint8_t out[64]);
 dpc_status dpc_ipc_open(dpc_ctx* ctx, const uint8_t handle[64], void** d_out);
 dpc_status dpc_ipc_close(void* d_ptr);
 /* Device-side barrier over peer memory: d_flag_tab is a DEVICE array of
- * `world` pointers to the ranks' flag arrays (world x u64 each, zeroed once);
- * epochs must increase (1, 2, ...).  Enqueued on the context stream. */
+ * `world` pointers to the ranks' flag arrays (2 x world u64 each, zeroed
+ * once); epochs must increase by one per barrier (1, 2, ...) and stay below
+ * 2^32.  Enqueued on the context stream. */
 dpc_status dpc_p2p_barrier(dpc_ctx* ctx, uint64_t* const* d_flag_tab, int32_t world, int32_t me, uint64_t epoch);
+/* The same barrier carrying one u32 per rank: *sum = the sum over ranks
+ * (synchronous; an all-reduce riding on the flags, e.g. frontier sizes). */
+dpc_status dpc_p2p_barrier_sum(dpc_ctx* ctx, uint64_t* const* d_flag_tab, int32_t world, int32_t me,
+                               uint64_t epoch, uint32_t value, uint64_t* sum);
 /* Reports DPC_E_DEADLOCK if a barrier timed out (synchronises the stream). */
 dpc_status dpc_p2p_check(dpc_ctx* ctx);
+/* Fused partitioned SSSP (dpc_msssp_* with no send buffers): relaxations of
+ * remote vertices go straight into their owner's distance / stamp / next
+ * frontier through peer pointers.  dpc_msssp_buffers gives the 5 device
+ * buffers this rank exports (dist, stamp, front0, front1, counters; IPC-able
+ * cudaMalloc bases); d_peer_table is a DEVICE array of `world` such 5-pointer
+ * records, own and IPC-mapped.  Per iteration: relax, peer barrier, apply
+ * (0 pairs), dpc_p2p_barrier_sum of the next-frontier sizes. */
+dpc_status dpc_msssp_buffers(dpc_dgraph* dg, void* out[5]);
+dpc_status dpc_msssp_set_peers(dpc_dgraph* dg, const void* d_peer_table);
 /* Grid stream SpMV of this rank's row block with x read from the owners:
  * d_xpeer is a DEVICE array of `world` pointers, x entry i at
  * d_xpeer[i / rows_per_rank][i % rows_per_rank] (replaces ncclAllGather +

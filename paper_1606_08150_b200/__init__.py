@@ -156,6 +156,10 @@ _SIGS = {
     "dpc_ipc_close": (C.c_int, [_P]),
     "dpc_p2p_barrier": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_uint64]),
     "dpc_p2p_check": (C.c_int, [_P]),
+    "dpc_p2p_barrier_sum": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_uint64, C.c_uint32,
+                                      C.POINTER(C.c_uint64)]),
+    "dpc_msssp_buffers": (C.c_int, [_P, _P]),
+    "dpc_msssp_set_peers": (C.c_int, [_P, _P]),
     "dpc_multi_spmv_fused": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int64, _P, C.POINTER(LaunchCfg),
                                        C.POINTER(Metrics)]),
     "dpc_sssp_device": (C.c_int, [_P, _P, _i32, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
@@ -398,6 +402,13 @@ def p2p_barrier(ctx, d_flag_table: int, world: int, me: int, epoch: int):
 
 def p2p_check(ctx):
     _check(_lib.dpc_p2p_check(ctx.handle))
+
+
+def p2p_barrier_sum(ctx, d_flag_table: int, world: int, me: int, epoch: int, value: int) -> int:
+    """Peer barrier carrying one u32 per rank; returns the sum over ranks."""
+    out = C.c_uint64()
+    _check(_lib.dpc_p2p_barrier_sum(ctx.handle, C.c_void_p(d_flag_table), world, me, epoch, value, C.byref(out)))
+    return int(out.value)
 
 
 def launch_cfg(app: str, variant: str, **overrides) -> LaunchCfg:
@@ -666,6 +677,18 @@ class PartitionedSSSP:
         met = Metrics()
         _check(_lib.dpc_msssp_end(self.ctx.handle, self.g._h, C.byref(met)))
         return met
+
+    # ---- fused form: remote relaxations straight into the owners' buffers
+    def buffers(self):
+        """The 5 device buffers this rank exports (dist, stamp, front0,
+        front1, counters) for the fused form."""
+        out = (C.c_void_p * 5)()
+        _check(_lib.dpc_msssp_buffers(self.g._h, out))
+        return [int(p) for p in out]
+
+    def set_peers(self, d_peer_table: int):
+        """DEVICE array of world x 5 pointers (every rank's buffers()), own and mapped."""
+        _check(_lib.dpc_msssp_set_peers(self.g._h, C.c_void_p(d_peer_table)))
 
 
 class DeviceTree:

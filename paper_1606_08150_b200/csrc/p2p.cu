@@ -38,23 +38,34 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
-// One warp; lane q < P signals rank q, then waits for rank q's signal here.
+// One warp.  Flag arrays hold 2P words: epoch e uses half e & 1 (a peer can
+// be at most one barrier ahead, so it never overwrites the half being read),
+// each word = epoch << 32 | payload.  Lane q signals rank q, then waits for
+// rank q's word here and adds its payload into *sum (an all-reduce of one
+// u32 per rank riding on the barrier).
 __global__ void __launch_bounds__(32) barrier_kernel(unsigned long long* const* flags, int P, int me,
-                                                     unsigned long long epoch, unsigned* fault) {
+                                                     unsigned epoch, unsigned payload, unsigned* fault,
+                                                     unsigned long long* sum) {
   const int q = static_cast<int>(threadIdx.x);
-  __threadfence_system();  // this rank's earlier writes (x_local) before the signal
-  for (int p = q; p < P; p += 32) st_release_sys(flags[p] + me, epoch);
+  const unsigned half = (epoch & 1u) * static_cast<unsigned>(P);
+  const unsigned long long word = (static_cast<unsigned long long>(epoch) << 32) | payload;
+  __threadfence_system();  // this rank's earlier writes (x slice, peer relaxations) before the signal
+  for (int p = q; p < P; p += 32) st_release_sys(flags[p] + half + me, word);
   const unsigned long long t0 = dev::global_ns();
+  unsigned long long acc = 0;
   for (int p = q; p < P; p += 32) {
-    while (ld_acquire_sys(flags[me] + p) < epoch) {
+    unsigned long long w;
+    while (((w = ld_acquire_sys(flags[me] + half + p)) >> 32) < epoch) {
       __nanosleep(256);
       if (dev::global_ns() - t0 > 5000000000ull) {  // 5 s: a peer is gone
         atomicOr(fault, 1u);
         break;
       }
     }
+    acc += w & 0xffffffffull;
   }
-  __syncwarp();
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (q == 0 && sum) *sum = acc;
 }
 
 }  // namespace p2p
@@ -91,17 +102,44 @@ dpc_status dpc_ipc_close(void* d_ptr) {
   return DPC_OK;
 }
 
+static dpc_status p2p_fault_flag(dpc_ctx* ctx) {
+  if (!ctx->p2p_fault) {
+    DPC_CUDA(cudaMalloc(&ctx->p2p_fault, 16));  // [0] fault flag, [8] barrier sum
+    DPC_CUDA(cudaMemsetAsync(ctx->p2p_fault, 0, 16, ctx->stream));
+  }
+  return DPC_OK;
+}
+
 dpc_status dpc_p2p_barrier(dpc_ctx* ctx, uint64_t* const* d_flag_tab, int32_t world, int32_t me, uint64_t epoch) {
   clear_error();
-  if (!ctx || !d_flag_tab || world < 1 || world > 1024 || me < 0 || me >= world || epoch == 0)
+  if (!ctx || !d_flag_tab || world < 1 || world > 1024 || me < 0 || me >= world || epoch == 0 ||
+      epoch >= (uint64_t{1} << 32))
     return fail(DPC_E_INVALID, "bad arguments");
-  if (!ctx->p2p_fault) {
-    DPC_CUDA(cudaMalloc(&ctx->p2p_fault, sizeof(unsigned)));
-    DPC_CUDA(cudaMemsetAsync(ctx->p2p_fault, 0, sizeof(unsigned), ctx->stream));
-  }
+  dpc_status st = p2p_fault_flag(ctx);
+  if (st != DPC_OK) return st;
   p2p::barrier_kernel<<<1, 32, 0, ctx->stream>>>(reinterpret_cast<unsigned long long* const*>(d_flag_tab), world,
-                                                  me, static_cast<unsigned long long>(epoch), ctx->p2p_fault);
+                                                  me, static_cast<unsigned>(epoch), 0u, ctx->p2p_fault, nullptr);
   DPC_CUDA(cudaGetLastError());
+  return DPC_OK;
+}
+
+dpc_status dpc_p2p_barrier_sum(dpc_ctx* ctx, uint64_t* const* d_flag_tab, int32_t world, int32_t me,
+                               uint64_t epoch, uint32_t value, uint64_t* sum) {
+  clear_error();
+  if (!ctx || !d_flag_tab || !sum || world < 1 || world > 1024 || me < 0 || me >= world || epoch == 0 ||
+      epoch >= (uint64_t{1} << 32))
+    return fail(DPC_E_INVALID, "bad arguments");
+  dpc_status st = p2p_fault_flag(ctx);
+  if (st != DPC_OK) return st;
+  auto* dsum = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->p2p_fault) + 8);
+  p2p::barrier_kernel<<<1, 32, 0, ctx->stream>>>(reinterpret_cast<unsigned long long* const*>(d_flag_tab), world,
+                                                  me, static_cast<unsigned>(epoch), value, ctx->p2p_fault, dsum);
+  DPC_CUDA(cudaGetLastError());
+  unsigned long long h[2] = {0, 0};
+  DPC_CUDA(cudaMemcpyAsync(h, ctx->p2p_fault, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  DPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h[0] & 0xffffffffull) return fail(DPC_E_DEADLOCK, "peer barrier timed out (a peer stopped signalling)");
+  *sum = h[1];
   return DPC_OK;
 }
 

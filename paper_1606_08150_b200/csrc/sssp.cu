@@ -83,6 +83,18 @@ struct Args {
   unsigned coop;           // grid_persistent1: cooperative launch (grid.sync) vs soft barrier
   unsigned classify;       // grid_persistent1: next-level vertices are classified at push time
   unsigned long long* ptrace;  // optional phase timeline (DPC_SSSP_PHASES=1): per level, max over blocks
+  const struct Peer* peers;    // fused multi-GPU relaxation: every rank's buffers (nullptr = send buffers)
+};
+
+// One rank's SSSP buffers as seen from this process (own or IPC-mapped):
+// the fused form relaxes remote vertices straight into their owner's
+// distance / stamp / next-frontier arrays (NVLink peer atomics).
+struct Peer {
+  unsigned* dist;
+  unsigned* stamp;
+  unsigned* front0;
+  unsigned* front1;
+  Ctr* ctr;
 };
 
 __device__ void spill_classify(const Args& a, unsigned it, unsigned v);
@@ -136,11 +148,26 @@ __device__ __noinline__ void relax_remote(const Args& a, unsigned v, unsigned nd
   else atomicOr(&a.hdr->overflow, 1u);
 }
 
+// Fused remote relaxation: atomicMin on the owner's distance, the owner's
+// stamp for dedup, and an append to the owner's next frontier (system-scope
+// atomics on peer memory; the level's peer barrier publishes them).
+__device__ __noinline__ void relax_peer(const Args& a, unsigned it, unsigned gv, unsigned nd) {
+  const unsigned o = gv / a.rows_per_rank, l = gv - o * a.rows_per_rank;
+  const Peer& p = a.peers[o];
+  if (nd >= __ldcv(p.dist + l)) return;
+  const unsigned old = atomicMin_system(p.dist + l, nd);
+  if (nd < old && atomicExch_system(p.stamp + l, it + 1) != it + 1) {
+    const unsigned slot = atomicAdd_system(&p.ctr->fsize[(it + 1) % 3], 1u);
+    ((it & 1) ? p.front0 : p.front1)[slot] = l;
+  }
+}
+
 __device__ __forceinline__ void relax(const Args& a, unsigned it, Block& s, unsigned gv,
                                       unsigned nd) {
   const unsigned v = gv - a.r0;  // local index (wraps for vertices below r0)
   if (v >= a.n) {
-    relax_remote(a, gv, nd);
+    if (a.peers) relax_peer(a, it, gv, nd);
+    else relax_remote(a, gv, nd);
     return;
   }
   if (nd < __ldcg(a.dist + v)) {
@@ -998,6 +1025,7 @@ extern "C" dpc_status dpc_msssp_begin(dpc_ctx* ctx, dpc_dgraph* g, int64_t r0, i
   m->a.sendbuf = reinterpret_cast<uint2*>(g->ms_send);
   m->a.sendcnt = g->ms_cnt;
   m->a.sendcap = static_cast<unsigned>(cap);
+  m->a.peers = nullptr;
   m->it = 0;
   m->host_launches = 0;
   m->remote_sent = 0;
@@ -1030,6 +1058,28 @@ extern "C" dpc_status dpc_msssp_relax(dpc_ctx* ctx, dpc_dgraph* g, uint32_t* sen
     if (send_counts[p] > m->a.sendcap) return fail(DPC_E_OVERFLOW, "send buffer overflow");
     m->remote_sent += send_counts[p];
   }
+  return DPC_OK;
+}
+
+// Fused form: the device pointers this rank exports (dist, stamp, front0,
+// front1, counters) and the table of every rank's (own + IPC-mapped).
+extern "C" dpc_status dpc_msssp_buffers(dpc_dgraph* g, void* out[5]) {
+  clear_error();
+  if (!g || !out) return fail(DPC_E_INVALID, "NULL argument");
+  if (!g->ctr) return fail(DPC_E_INVALID, "dpc_msssp_begin was not called");
+  out[0] = g->dist;
+  out[1] = g->stamp;
+  out[2] = g->front[0];
+  out[3] = g->front[1];
+  out[4] = g->ctr;
+  return DPC_OK;
+}
+
+extern "C" dpc_status dpc_msssp_set_peers(dpc_dgraph* g, const void* d_peer_table) {
+  clear_error();
+  MsState* m = g ? ms_state(g) : nullptr;
+  if (!m) return fail(DPC_E_INVALID, "dpc_msssp_begin was not called");
+  m->a.peers = static_cast<const sssp::Peer*>(d_peer_table);
   return DPC_OK;
 }
 

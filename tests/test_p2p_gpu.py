@@ -92,9 +92,9 @@ def test_p2p_barrier_contexts_one_process():
     completes once all three signalled."""
     world = 3
     ctxs = [dpc.Context(0) for _ in range(world)]
-    flags = [ctxs[0].alloc(8 * world) for _ in range(world)]
+    flags = [ctxs[0].alloc(16 * world) for _ in range(world)]
     for f in flags:
-        ctxs[0].h2d(f, np.zeros(world, np.uint64))
+        ctxs[0].h2d(f, np.zeros(2 * world, np.uint64))
     tab = ctxs[0].alloc(8 * world)
     ctxs[0].h2d(tab, np.array(flags, np.uint64))
     ctxs[0].synchronize()
@@ -103,8 +103,8 @@ def test_p2p_barrier_contexts_one_process():
             dpc.p2p_barrier(ctxs[q], tab, world, q, epoch)
         for q in range(world):
             dpc.p2p_check(ctxs[q])
-            got = ctxs[q].d2h(flags[q], world, np.uint64)
-            assert np.all(got == epoch)
+            got = ctxs[q].d2h(flags[q], 2 * world, np.uint64).reshape(2, world)[epoch & 1]
+            assert np.all((got >> 32) == epoch)
     for b in flags + [tab]:
         ctxs[0].free(b)
     for c in ctxs:
@@ -134,8 +134,8 @@ def _rank(rank, world, port, steps):
     A = dpc.gen_rmat_rows(SCALE, r0, r1, 16, seed=SEED, weights=False, values=True, permute=True)
     dg = dpc.DeviceGraph(ctx, A)
     x_local = ctx.alloc(4 * R)
-    flags = ctx.alloc(8 * world)
-    ctx.h2d(flags, np.zeros(world, np.uint64))
+    flags = ctx.alloc(16 * world)
+    ctx.h2d(flags, np.zeros(2 * world, np.uint64))
     ctx.synchronize()
     hs = [None] * world
     dist.all_gather_object(hs, (dpc.ipc_handle(x_local), dpc.ipc_handle(flags)))
@@ -179,3 +179,104 @@ def test_fused_spmv_two_processes_ipc():
     handles exchanged over gloo; three SpMV steps with changing x."""
     import torch.multiprocessing as mp
     mp.spawn(_rank, args=(2, _free_port(), 3), nprocs=2, join=True)
+
+
+def _sssp_parts(world, scale=11):
+    n = 1 << scale
+    R = n // world
+    return n, R, [dpc.gen_rmat_rows(scale, p * R, (p + 1) * R, 16, seed=SEED, weights=True, permute=True)
+                  for p in range(world)]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_sssp_partitions_one_process(orc, world):
+    """The fused partitioned SSSP with the ranks' steps run in turn in one
+    process (peer buffers = the other partitions' device buffers)."""
+    n, R, parts = _sssp_parts(world)
+    full = dpc.gen_rmat(11, 16, seed=SEED, weights=True, permute=True)
+    src = int(np.argmax(full.degrees()))
+    want = orc.sssp(full.rowptr, full.col, full.w, src)
+    ctx = dpc.Context(0)
+    dgs = [dpc.DeviceGraph(ctx, A) for A in parts]
+    ps = [dpc.PartitionedSSSP(dg, p, world, n, src) for p, dg in enumerate(dgs)]
+    tab = ctx.alloc(8 * 5 * world)
+    ctx.h2d(tab, np.array([b for p in ps for b in p.buffers()], np.uint64))
+    for p in ps:
+        p.set_peers(tab)
+    for it in range(n + 1):
+        for p in ps:
+            cnt = p.relax()
+            assert not cnt.any()          # nothing goes through send buffers
+        total = sum(p.apply(np.zeros((0, 2), np.uint32)) for p in ps)
+        if total == 0:
+            break
+    got = np.concatenate([dg.get_dist() for dg in dgs])
+    np.testing.assert_array_equal(got, want)
+    for p in ps:
+        p.end()
+    ctx.free(tab)
+    for dg in dgs:
+        dg.close()
+    ctx.close()
+
+
+def _sssp_rank(rank, world, port):
+    import torch.distributed as dist
+
+    from tests._oracle import Oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, R, parts = _sssp_parts(world)
+    full = dpc.gen_rmat(11, 16, seed=SEED, weights=True, permute=True)
+    src = int(np.argmax(full.degrees()))
+    want = Oracle().sssp(full.rowptr, full.col, full.w, src)[rank * R:(rank + 1) * R]
+    ctx = dpc.Context(0)
+    dg = dpc.DeviceGraph(ctx, parts[rank])
+    ps = dpc.PartitionedSSSP(dg, rank, world, n, src)
+    flags = ctx.alloc(16 * world)
+    ctx.h2d(flags, np.zeros(2 * world, np.uint64))
+    ctx.synchronize()
+    mine = ps.buffers()
+    hs = [None] * world
+    dist.all_gather_object(hs, ([dpc.ipc_handle(b) for b in mine], dpc.ipc_handle(flags)))
+    table, ftab_l, opened = [], [], []
+    for q in range(world):
+        if q == rank:
+            table += mine
+            ftab_l.append(flags)
+        else:
+            ptrs = [dpc.ipc_open(ctx, h) for h in hs[q][0]]
+            fp = dpc.ipc_open(ctx, hs[q][1])
+            opened += ptrs + [fp]
+            table += ptrs
+            ftab_l.append(fp)
+    tab, ftab = ctx.alloc(8 * 5 * world), ctx.alloc(8 * world)
+    ctx.h2d(tab, np.array(table, np.uint64))
+    ctx.h2d(ftab, np.array(ftab_l, np.uint64))
+    ps.set_peers(tab)
+    epoch = 0
+    for it in range(n + 1):
+        ps.relax()
+        epoch += 1
+        dpc.p2p_barrier(ctx, ftab, world, rank, epoch)      # every relaxation of the level landed
+        nxt = ps.apply(np.zeros((0, 2), np.uint32))
+        epoch += 1
+        if dpc.p2p_barrier_sum(ctx, ftab, world, rank, epoch, nxt) == 0:
+            break
+    ps.end()
+    ok = bool(np.array_equal(dg.get_dist(), want))
+    flag = [None] * world
+    dist.all_gather_object(flag, ok)
+    for p in opened:
+        dpc.ipc_close(p)
+    for b in (flags, tab, ftab):
+        ctx.free(b)
+    dg.close()
+    ctx.close()
+    dist.destroy_process_group()
+    assert all(flag), flag
+
+
+def test_fused_sssp_two_processes_ipc():
+    import torch.multiprocessing as mp
+    mp.spawn(_sssp_rank, args=(2, _free_port()), nprocs=2, join=True)
