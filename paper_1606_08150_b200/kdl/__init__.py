@@ -155,8 +155,8 @@ class Module:
     """A compiled program.  run() owns device memory through torch (plumbing);
     every kernel that executes is generated code from this module's .so."""
 
-    def __init__(self, prog, so, kc, mode):
-        self.prog, self.so, self.kc_rows, self.mode = prog, so, kc, mode
+    def __init__(self, prog, so, kc, mode, width=64):
+        self.prog, self.so, self.kc_rows, self.mode, self.width = prog, so, kc, mode, width
         self.lib = None
         self._dev = None
         self.grid_total = max([s.total_bytes for k in prog.kernels for s in k.body
@@ -206,9 +206,15 @@ class Module:
             ln = int(eval_host(g.length, scalars))
             if ln < 0:
                 raise KdlError("run.array", f"array {g.name!r} has negative length {ln}")
-            dt = torch.float64 if g.type == ast.FLOAT else torch.int64
+            w32 = self.width == 32
+            dt = (torch.float32 if w32 else torch.float64) if g.type == ast.FLOAT else \
+                (torch.int32 if w32 else torch.int64)
             if g.name in arrays:
-                a = np.asarray(arrays[g.name], dtype=np.float64 if g.type == ast.FLOAT else np.int64)
+                npt = (np.float32 if w32 else np.float64) if g.type == ast.FLOAT else (np.int32 if w32 else np.int64)
+                src = np.asarray(arrays[g.name])
+                if w32 and g.type != ast.FLOAT and src.size and (src.min() < -2**31 or src.max() >= 2**31):
+                    raise KdlError("run.array", f"array {g.name!r} does not fit the 32-bit width")
+                a = src.astype(npt)
                 if a.shape != (ln,):
                     raise KdlError("run.array", f"array {g.name!r} must have {ln} elements, got {a.shape}")
                 t = torch.from_numpy(a.copy()).to(dev)
@@ -282,23 +288,28 @@ class Module:
         return Result(out, launches, runs, kc, ms)
 
 
-def compile_program(prog, mode="basic", config=None, name="kdl", consolidated=False, schedule="block"):
+def compile_program(prog, mode="basic", config=None, name="kdl", consolidated=False, schedule="block",
+                    width=64):
     if mode not in MODES:
         raise ValueError(f"mode must be one of {MODES}")
     if not consolidated and mode != "basic":
         prog = consolidate(prog, granularity=None if mode == "directive" else mode, config=config,
                            schedule=schedule)
-    src, kc = generate(prog, name)
+    src, kc = generate(prog, name, width)
     tag = f"{name}_{mode}" + ("" if schedule == "block" or consolidated or mode == "basic" else f"_{schedule}")
+    tag += "" if width == 64 else "_w32"
     so = build_so(src, tag)
-    return Module(prog, so, kc, mode)
+    return Module(prog, so, kc, mode, width)
 
 
-def compile(source, mode="basic", config=None, name="kdl", consolidated=False, schedule="block"):  # noqa: A001
+def compile(source, mode="basic", config=None, name="kdl", consolidated=False, schedule="block",  # noqa: A001
+            width=64):
     """.kdl text -> Module (compiled for sm_100a; cached under kdl/_build).
     schedule="block" (default) drains multi-block children one item per
-    block; "reference" keeps the reference's drain loop."""
-    return compile_program(parse_program(source), mode, config, name, consolidated, schedule)
+    block; "reference" keeps the reference's drain loop.  width=64 keeps the
+    simulator's int64 / fp64 values; width=32 runs the program on int32 /
+    fp32 arrays and scalars (integer literals must fit)."""
+    return compile_program(parse_program(source), mode, config, name, consolidated, schedule, width)
 
 
 def autotune(source, scalars, arrays=None, *, until_stable=None, modes=("warp", "block", "grid"),

@@ -32,14 +32,15 @@ _CMP = {"<", "<=", ">", ">=", "==", "!="}
 
 
 def _ctype(t):
-    return "double" if t == A.FLOAT else "long long"
+    return "dk_flt" if t == A.FLOAT else "dk_int"
 
 
-def _float_lit(v):
+def _float_lit(v, width=64):
     s = repr(float(v))
     if "inf" in s or "nan" in s:
         raise KdlError("cuda.literal", f"non-finite float literal {s}")
-    return s if ("." in s or "e" in s) else s + ".0"
+    s = s if ("." in s or "e" in s) else s + ".0"
+    return s + "f" if width == 32 else s
 
 
 class _KInfo:
@@ -80,9 +81,12 @@ class _KInfo:
 
 
 class Builder:
-    def __init__(self, prog, name="kdl"):
+    def __init__(self, prog, name="kdl", width=64):
+        if width not in (32, 64):
+            raise KdlError("cuda.width", "width must be 32 or 64")
         self.prog = prog
         self.name = name
+        self.width = width
         if len(prog.globals) > 64:
             raise KdlError("cuda.arrays", "at most 64 global arrays")
         self.arr = {g.name: (i, g.type) for i, g in enumerate(prog.globals)}
@@ -207,17 +211,21 @@ class Builder:
     def ex(self, e):
         k = e.kind
         if k == "int":
+            if self.width == 32:
+                if not -2**31 <= e.ival < 2**31:
+                    raise KdlError("cuda.literal", f"integer literal {e.ival} does not fit the 32-bit width")
+                return f"({e.ival})"
             return f"{e.ival}LL"
         if k == "float":
-            return _float_lit(e.fval)
+            return _float_lit(e.fval, self.width)
         if k == "name":
             t = self.etype(e)
             if t == "array":
                 raise KdlError("cuda.name", f"array {e.name!r} used as a scalar")
             return f"v_{e.name}"
         if k == "intrinsic":
-            return {"threadIdx": "((long long)threadIdx.x)", "blockIdx": "((long long)blockIdx.x)",
-                    "blockDim": "((long long)blockDim.x)", "gridDim": "((long long)gridDim.x)"}[e.name]
+            return {"threadIdx": "((dk_int)threadIdx.x)", "blockIdx": "((dk_int)blockIdx.x)",
+                    "blockDim": "((dk_int)blockDim.x)", "gridDim": "((dk_int)gridDim.x)"}[e.name]
         if k == "index":
             aid, t = self.array_of(e.name)
             return f"(*dk_{'f' if t == A.FLOAT else 'i'}p({aid}, {self.int_ex(e.args[0])}))"
@@ -226,18 +234,18 @@ class Builder:
             return self.atomic(aid, t, e.args[0], e.args[1])
         if k == "unary":
             a = self.ex(e.args[0])
-            return f"((long long)(({a}) == 0))" if e.name == "!" else f"(-({a}))"
+            return f"((dk_int)(({a}) == 0))" if e.name == "!" else f"(-({a}))"
         if k == "binary":
             op = e.name
             l, r = e.args
             if op in ("&&", "||"):
-                return f"((long long)((({self.ex(l)}) != 0) {'&' if op == '&&' else '|'} (({self.ex(r)}) != 0)))"
+                return f"((dk_int)((({self.ex(l)}) != 0) {'&' if op == '&&' else '|'} (({self.ex(r)}) != 0)))"
             if op in _CMP:
-                return f"((long long)(({self.ex(l)}) {op} ({self.ex(r)})))"
+                return f"((dk_int)(({self.ex(l)}) {op} ({self.ex(r)})))"
             if self.etype(e) == A.FLOAT:
                 if op == "%":
                     raise KdlError("cuda.type", "modulo requires integer operands")
-                return f"((double)({self.ex(l)}) {op} (double)({self.ex(r)}))"
+                return f"((dk_flt)({self.ex(l)}) {op} (dk_flt)({self.ex(r)}))"
             if op == "/":
                 return f"dk_idiv({self.ex(l)}, {self.ex(r)})"
             if op == "%":
@@ -252,18 +260,18 @@ class Builder:
             return self.pending()
         if k == "buf_get":
             w = f"dk_buf_word(dk_inh, {self.int_ex(e.args[0])}, {2 + e.args[1].ival}LL)"
-            return f"__longlong_as_double({w})" if self.etype(e) == A.FLOAT else w
+            return f"dk_word_flt({w})" if self.etype(e) == A.FLOAT else f"((dk_int)({w}))"
         if k in ("buf_cfg_grid", "buf_cfg_block"):
-            return f"dk_buf_word(dk_inh, {self.int_ex(e.args[0])}, {0 if k == 'buf_cfg_grid' else 1}LL)"
+            return f"((dk_int)dk_buf_word(dk_inh, {self.int_ex(e.args[0])}, {0 if k == 'buf_cfg_grid' else 1}LL))"
         if k == "grid_last":
-            return "dk_grid_last(dk_inst, &dk_gl)"
+            return "((dk_int)dk_grid_last(dk_inst, &dk_gl))"
         if k == "kc_blocks":
             key = (e.name, e.ival, e.args[0].ival)
             if e.name not in self.info:
                 raise KdlError("cuda.kc", f"kc_blocks names unknown kernel {e.name!r}")
             if key not in self.kc:
                 self.kc.append(key)
-            return f"dk_kc[{self.kc.index(key)}]"
+            return f"((dk_int)dk_kc[{self.kc.index(key)}])"
         raise KdlError("cuda.expr", f"unknown expression kind {k!r}")
 
     def int_ex(self, e):
@@ -275,8 +283,8 @@ class Builder:
         if t == A.INT and self.etype(v) == A.FLOAT:
             raise KdlError("cuda.type", "atomicAdd of a float value on an int array")
         if t == A.FLOAT:
-            return f"dk_atomic_f(dk_fp({aid}, {self.int_ex(i)}), (double)({self.ex(v)}))"
-        return f"dk_atomic_i(dk_ip({aid}, {self.int_ex(i)}), {self.ex(v)})"
+            return f"dk_atomic_f(dk_fp({aid}, {self.int_ex(i)}), (dk_flt)({self.ex(v)}))"
+        return f"dk_atomic_i(dk_ip({aid}, {self.int_ex(i)}), (dk_int)({self.ex(v)}))"
 
     # ---------------- owner helpers ----------------
     def _own(self):
@@ -293,10 +301,10 @@ class Builder:
     def pending(self):
         d = self.cur.decl
         if d is None:
-            return "0LL"
+            return "((dk_int)0)"
         if d.gran == "grid":
-            return f"dk_pending_grid(dk_inst, {self._grid_cap()})"
-        return f"dk_pending_own({self._own()})"
+            return f"((dk_int)dk_pending_grid(dk_inst, {self._grid_cap()}))"
+        return f"((dk_int)dk_pending_own({self._own()}))"
 
     # ---------------- statements ----------------
     def emit_body(self, body, ind):
@@ -356,7 +364,7 @@ class Builder:
             if self.etype(a) != A.INT or self.etype(c) != A.INT:
                 raise KdlError("cuda.type", "for loop start and step must be integers")
             self.env.append({s.name: (A.INT, False)})
-            hdr = f"{ind}for (long long v_{s.name} = {self.ex(a)}; v_{s.name} < {self.ex(b)}; v_{s.name} += {self.ex(c)}) {{"
+            hdr = f"{ind}for (dk_int v_{s.name} = {self.ex(a)}; v_{s.name} < {self.ex(b)}; v_{s.name} += {self.ex(c)}) {{"
             out = [hdr] + self.emit_body(s.body, ind + "  ") + [f"{ind}}}"]
             self.env.pop()
             return out
@@ -410,7 +418,7 @@ class Builder:
         for j, v in enumerate(vals):
             c = self.ex(v)
             if self.etype(v) == A.FLOAT:
-                c = f"__double_as_longlong({c})"
+                c = f"dk_flt_word({c})"
             out.append(f"{ind}  const long long dk_w{j + 2} = {c};")
         st = self._stride()
         if d.gran == "grid":
@@ -527,7 +535,7 @@ class Builder:
                 for i, (n, t, arr) in enumerate(live):
                     w = f"dk_sl[{1 + i}]"
                     out.append(f"  {_ctype(t) if t != 'array' else 'long long'} v_{n} = "
-                               f"{'__longlong_as_double(' + w + ')' if t == A.FLOAT else w};")
+                               f"{'dk_word_flt(' + w + ')' if t == A.FLOAT else '(' + (_ctype(t) if t != 'array' else 'long long') + ')' + w};")
                     scope[n] = (t, arr)
             self.env = [scope, {}]
             new = []
@@ -547,7 +555,7 @@ class Builder:
             if not last:
                 live = live + new
                 W = 1 + len(live)
-                saves = " ".join(f"dk_so[{1 + i}] = {'__double_as_longlong(v_' + n + ')' if t == A.FLOAT else 'v_' + n};"
+                saves = " ".join(f"dk_so[{1 + i}] = {'dk_flt_word(v_' + n + ')' if t == A.FLOAT else '(long long)v_' + n};"
                                  for i, (n, t, _) in enumerate(live))
                 nxt = self.phase_name(k, j + 1)
                 out += [f"dk_split{j}:",
@@ -571,7 +579,7 @@ class Builder:
 
     def generate(self):
         lines = [f"// Generated by paper_1606_08150_b200.kdl from program {self.name!r}; do not edit.",
-                 '#include "kdl_rt.cuh"', ""]
+                 f"#define DK_WIDTH {self.width}", '#include "kdl_rt.cuh"', ""]
         for g in self.prog.globals:
             i, t = self.arr[g.name]
             lines.append(f"// array {i}: {t} {g.name}")
@@ -595,9 +603,11 @@ class Builder:
         unpack = []
         for j, p in enumerate(ek.params):
             if p.type == A.FLOAT and not p.is_array:
-                unpack.append(f"dk_bits(a[{j}])")
-            else:
+                unpack.append(f"(dk_flt)dk_bits(a[{j}])")
+            elif p.is_array:
                 unpack.append(f"a[{j}]")
+            else:
+                unpack.append(f"(dk_int)a[{j}]")
         kc_rows = ", ".join(f"{{(const void*)k_{k}, {x}, {t}}}" for (k, x, t) in self.kc) or "{nullptr, 1, 1}"
         nkc = len(self.kc)
         return [
@@ -652,8 +662,8 @@ class Builder:
         ]
 
 
-def generate(prog, name="kdl"):
+def generate(prog, name="kdl", width=64):
     """-> (CUDA source, list of (kernel, X, T) KC launch rows)."""
-    b = Builder(prog, name)
+    b = Builder(prog, name, width)
     src = b.generate()
     return src, list(b.kc)

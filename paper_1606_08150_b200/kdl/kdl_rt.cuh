@@ -91,8 +91,29 @@ static_assert(sizeof(Inst) == 24, "launch records are 24 bytes (include/dpc_kdl.
 }  // namespace dk
 
 __constant__ dk::Rt dk_rt;
-__device__ long long dk_sink_i[2];
-__device__ double dk_sink_f[2];
+
+// DSL value widths (compile option): 64 = the simulator's Value (int64 /
+// fp64, sim.hpp:72-80), 32 = int32 / fp32 arrays and scalars.  Buffer items,
+// counters and launch state stay 64-bit words either way.
+#ifndef DK_WIDTH
+#define DK_WIDTH 64
+#endif
+#if DK_WIDTH == 32
+typedef int dk_int;
+typedef float dk_flt;
+__device__ __forceinline__ dk_flt dk_word_flt(long long w) { return __int_as_float(static_cast<int>(w)); }
+__device__ __forceinline__ long long dk_flt_word(dk_flt v) {
+  return static_cast<long long>(static_cast<unsigned>(__float_as_int(v)));
+}
+#else
+typedef long long dk_int;
+typedef double dk_flt;
+__device__ __forceinline__ dk_flt dk_word_flt(long long w) { return __longlong_as_double(w); }
+__device__ __forceinline__ long long dk_flt_word(dk_flt v) { return __double_as_longlong(v); }
+#endif
+
+__device__ dk_int dk_sink_i[2];
+__device__ dk_flt dk_sink_f[2];
 
 __device__ __forceinline__ void dk_fault(unsigned long long bit) { atomicOr(&dk_rt.ctr[0], bit); }
 
@@ -105,11 +126,11 @@ __device__ __forceinline__ bool dk_ok(long long id, long long i) {
   }
   return true;
 }
-__device__ __forceinline__ long long* dk_ip(long long id, long long i) {
-  return dk_ok(id, i) ? static_cast<long long*>(dk_rt.arr[id]) + i : dk_sink_i;
+__device__ __forceinline__ dk_int* dk_ip(long long id, long long i) {
+  return dk_ok(id, i) ? static_cast<dk_int*>(dk_rt.arr[id]) + i : dk_sink_i;
 }
-__device__ __forceinline__ double* dk_fp(long long id, long long i) {
-  return dk_ok(id, i) ? static_cast<double*>(dk_rt.arr[id]) + i : dk_sink_f;
+__device__ __forceinline__ dk_flt* dk_fp(long long id, long long i) {
+  return dk_ok(id, i) ? static_cast<dk_flt*>(dk_rt.arr[id]) + i : dk_sink_f;
 }
 // atomicAdd, warp-aggregated per address: the lanes of a warp that hit the
 // same element (__match_any_sync) combine their values with shuffles and one
@@ -137,9 +158,9 @@ __device__ __forceinline__ T dk_atomic_agg(T* p, T v) {
 }
 // Statement form (result unused): when every active lane of the warp hits
 // the same element, the lanes combine first and one lane issues the atomic
-// (ints: three redux.sync on 16/16/32-bit pieces, exact mod 2^64; doubles: a
-// butterfly for a full warp, a shuffle loop otherwise); mixed addresses go
-// out as plain fire-and-forget REDs.
+// (ints: redux.sync — for int64 on 16/16/32-bit pieces, exact mod 2^64;
+// floats: a butterfly for a full warp, a shuffle loop otherwise); mixed
+// addresses go out as plain fire-and-forget REDs.
 __device__ __forceinline__ void dk_add_i(long long* p, long long v) {
   const unsigned m = __activemask();
   unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
@@ -155,7 +176,17 @@ __device__ __forceinline__ void dk_add_i(long long* p, long long v) {
     atomicAdd(q, (static_cast<unsigned long long>(hi32) << 32) + (static_cast<unsigned long long>(hi16) << 16) +
                      lo16);
 }
-__device__ __forceinline__ void dk_add_f(double* p, double v) {
+__device__ __forceinline__ void dk_add_i(int* p, int v) {
+  const unsigned m = __activemask();
+  if (__match_any_sync(m, reinterpret_cast<unsigned long long>(p)) != m) {
+    atomicAdd(p, v);
+    return;
+  }
+  const unsigned t = __reduce_add_sync(m, static_cast<unsigned>(v));
+  if ((threadIdx.x & 31u) == static_cast<unsigned>(__ffs(m) - 1)) atomicAdd(p, static_cast<int>(t));
+}
+template <class F>
+__device__ __forceinline__ void dk_add_f(F* p, F v) {
   const unsigned m = __activemask();
   if (__match_any_sync(m, reinterpret_cast<unsigned long long>(p)) != m) {
     atomicAdd(p, v);
@@ -164,7 +195,7 @@ __device__ __forceinline__ void dk_add_f(double* p, double v) {
   if (m == 0xffffffffu) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
   } else {
-    double t = 0.0;
+    F t = F(0);
     for (unsigned r = m; r; r &= r - 1) t += __shfl_sync(m, v, __ffs(r) - 1);
     v = t;
   }
@@ -174,7 +205,9 @@ __device__ __forceinline__ long long dk_atomic_i(long long* p, long long v) {
   return static_cast<long long>(dk_atomic_agg(reinterpret_cast<unsigned long long*>(p),
                                               static_cast<unsigned long long>(v)));
 }
-__device__ __forceinline__ double dk_atomic_f(double* p, double v) { return dk_atomic_agg(p, v); }
+__device__ __forceinline__ int dk_atomic_i(int* p, int v) { return dk_atomic_agg(p, v); }
+template <class F>
+__device__ __forceinline__ F dk_atomic_f(F* p, F v) { return dk_atomic_agg(p, v); }
 
 // ---- arithmetic with the simulator's fault rules (sim.hpp:1574-1590) ----
 // (64-bit division is a long software sequence on the GPU; operands that fit
@@ -187,6 +220,14 @@ __device__ __forceinline__ long long dk_idiv(long long a, long long b) {
 __device__ __forceinline__ long long dk_imod(long long a, long long b) {
   if (b == 0) { dk_fault(dk::F_DIV); return 0; }
   if (((a | b) >> 31) == 0) return static_cast<long long>(static_cast<unsigned>(a) % static_cast<unsigned>(b));
+  return a % b;
+}
+__device__ __forceinline__ int dk_idiv(int a, int b) {
+  if (b == 0) { dk_fault(dk::F_DIV); return 0; }
+  return a / b;
+}
+__device__ __forceinline__ int dk_imod(int a, int b) {
+  if (b == 0) { dk_fault(dk::F_DIV); return 0; }
   return a % b;
 }
 template <class T> __device__ __forceinline__ T dk_min(T a, T b) { return b < a ? b : a; }

@@ -248,3 +248,24 @@ def test_autotune_picks_a_measured_form(orc):
     res = mod.run({"n": t.n, "root": t.root, "rootnc": len(t.children(t.root))},
                   {"cstart": t.cstart, "clist": t.clist, "parent": t.parent})
     np.testing.assert_array_equal(res.arrays["desc"], want)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_width32_programs_vs_oracle(orc, mode):
+    """width=32: int32 / fp32 arrays and scalars (the hand-written kernels'
+    widths); SpMV within 1e-5 of fp64, tree descendants exact, and a literal
+    that does not fit is a compile error."""
+    g = dpc.gen_rmat(14, 16, seed=5, weights=False, values=True)
+    x = ((np.arange(g.n) % 13 + 1) / 16.0).astype(np.float32)
+    want = orc.spmv_f64(g.rowptr, g.col, g.val, x)
+    mod = kdl.compile(src_of("spmv.kdl"), mode, name="spmv", width=32)
+    res = mod.run({"n": g.n, "m": g.m, "nx": g.n, "thr": 32},
+                  {"rowptr": g.rowptr, "col": g.col, "val": g.val, "x": x})
+    assert res.arrays["y"].dtype == np.float32
+    assert np.all(np.abs(res.arrays["y"] - want) <= 1e-5 * np.abs(want) + 1e-30)
+    t = dpc.gen_tree(6, 4, 12, 0.6, 3)
+    _, scal, arrs = tree_inputs((6, 4, 12, 0.6, 3), "desc")
+    res = kdl.compile(src_of("td.kdl"), mode, name="td", width=32).run(scal, arrs)
+    np.testing.assert_array_equal(res.arrays["desc"], orc.tree_desc(t.parent))
+    with pytest.raises(kdl.KdlError):
+        kdl.compile(src_of("sssp.kdl"), mode, name="sssp", width=32)

@@ -41,13 +41,13 @@ def best(fn, reps):
     return min(ms), out
 
 
-def spmv(scale, reps, orc, runs=None):
+def spmv(scale, reps, orc, runs=None, width=64):
     g = dpc.gen_rmat(scale, 16, seed=7, weights=False, values=True)
     x = ((np.arange(g.n) % 97) + 1) / 128.0
     want = orc.spmv_f64(g.rowptr, g.col, g.val, x)
     rows = {}
     for mode, sch in runs or RUNS:
-        mod = kdl.compile(kdl.read_program("spmv.kdl"), mode, name="spmv", schedule=sch)
+        mod = kdl.compile(kdl.read_program("spmv.kdl"), mode, name="spmv", schedule=sch, width=width)
         try:
             ms, res = best(lambda: mod.run({"n": g.n, "m": g.m, "nx": g.n, "thr": 32},
                                            {"rowptr": g.rowptr, "col": g.col, "val": g.val, "x": x},
@@ -57,7 +57,8 @@ def spmv(scale, reps, orc, runs=None):
                                     "kc": res.kc}
         except Exception as e:  # noqa: BLE001 - report the fault per mode
             rows[key(mode, sch)] = {"error": str(e)[:200]}
-    return {"workload": f"spmv.kdl, R-MAT scale {scale} ef 16 ({g.n} rows, {g.m} nnz), thr 32", "modes": rows}
+    return {"workload": f"spmv.kdl, R-MAT scale {scale} ef 16 ({g.n} rows, {g.m} nnz), thr 32, "
+                        f"{'int64 / fp64' if width == 64 else 'int32 / fp32'}", "modes": rows}
 
 
 def sssp(scale, reps, orc, runs=None):
@@ -82,12 +83,12 @@ def sssp(scale, reps, orc, runs=None):
                         f"({g.n} V, {g.m} E)", "modes": rows}
 
 
-def tree(shape, reps, orc, name="td.kdl", out="desc"):
+def tree(shape, reps, orc, name="td.kdl", out="desc", width=64):
     t = dpc.gen_tree(*shape)
     want = orc.tree_desc(t.parent) if out == "desc" else orc.tree_height(t.parent)
     rows = {}
     for mode in MODES:
-        mod = kdl.compile(kdl.read_program(name), mode, name=name[:-4])
+        mod = kdl.compile(kdl.read_program(name), mode, name=name[:-4], width=width)
         arrs = {"cstart": t.cstart, "clist": t.clist, "parent": t.parent, out: np.zeros(t.n, np.int64)}
         try:
             ms, res = best(lambda: mod.run({"n": t.n, "root": t.root, "rootnc": len(t.children(t.root))}, arrs,
@@ -96,7 +97,8 @@ def tree(shape, reps, orc, name="td.kdl", out="desc"):
                           "bit_exact": bool(np.array_equal(res.arrays[out], want))}
         except Exception as e:  # noqa: BLE001
             rows[mode] = {"error": str(e)[:200]}
-    return {"workload": f"{name}, gen_tree{tuple(shape)} = {t.n} nodes", "modes": rows}
+    return {"workload": f"{name}, gen_tree{tuple(shape)} = {t.n} nodes, {'int64' if width == 64 else 'int32'}",
+            "modes": rows}
 
 
 def bfs(scale, reps, orc):
@@ -182,6 +184,8 @@ def run_compiled(reps=2, scale_spmv=18, scale_sssp=16, shape=(5, 32, 128, 0.4, 1
             "sssp": summarize(sssp(scale_sssp, reps, orc, runs)),
             "td": summarize(tree(list(shape), reps, orc)),
             "bfs": summarize(bfs(scale_sssp, reps, orc)),
+            "spmv_w32": summarize(spmv(scale_spmv, reps, orc, runs, width=32)),
+            "td_w32": summarize(tree(list(shape), reps, orc, width=32)),
             "note": "generated by paper_1606_08150_b200.kdl from the .kdl programs (int64 / fp64 data, "
                     "CDP2 device launches); device time of the entry launch tree, CUDA events"}
 
@@ -198,7 +202,9 @@ def main():
     orc = Oracle()
     shape = [float(v) if "." in v else int(v) for v in a.tree.split(",")]
     res = {"spmv": spmv(a.scale_spmv, a.reps, orc), "sssp": sssp(a.scale_sssp, a.reps, orc),
-           "td": tree(shape, a.reps, orc), "bfs": bfs(a.scale_sssp, a.reps, orc)}
+           "td": tree(shape, a.reps, orc), "bfs": bfs(a.scale_sssp, a.reps, orc),
+           "spmv_w32": spmv(a.scale_spmv, a.reps, orc, [(m, "block") for m in MODES], width=32),
+           "td_w32": tree(shape, a.reps, orc, width=32)}
     try:
         res["hand_written_wall_ms"] = hand_written(a.scale_spmv, a.scale_sssp, shape)
     except Exception as e:  # noqa: BLE001
