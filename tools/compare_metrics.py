@@ -69,6 +69,30 @@ def collect():
         torch.cuda.profiler.stop()
         order.append([app, v])
         launches[f"{app}/{v}"] = int(met.child_launch_count)
+    # the compiler's output for the same programs the simulator runs
+    import paper_1606_08150_b200.kdl as kdl
+    x64 = (np.arange(g.n) % 97 + 1) / 97.0
+    kruns = []
+    for v in ["basic", "warp", "block", "grid"]:
+        mod = kdl.compile(kdl.read_program("spmv.kdl"), v, name="spmv")
+        kruns.append(("kdl-spmv", v, lambda mod=mod: mod.run({"n": g.n, "m": g.m, "nx": g.n, "thr": 32},
+                                                             {"rowptr": g.rowptr, "col": g.col, "val": g.val,
+                                                              "x": x64})))
+    kids = np.diff(t.cstart)
+    for v in ["basic", "warp", "block", "grid"]:
+        mod = kdl.compile(kdl.read_program("td.kdl"), v, name="td")
+        kruns.append(("kdl-td", v, lambda mod=mod: mod.run({"n": t.n, "root": t.root, "rootnc": int(kids[t.root])},
+                                                           {"cstart": t.cstart, "clist": t.clist,
+                                                            "parent": t.parent})))
+    for app, v, fn in kruns:
+        fn()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        res = fn()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        order.append([app, v])
+        launches[f"{app}/{v}"] = int(res.launches)
     os.makedirs(OUT, exist_ok=True)
     with open(os.path.join(OUT, "compare_launches.json"), "w") as f:
         json.dump({"order": order, "launches": launches, "spmv_rows": g.n, "spmv_nnz": g.m, "td_nodes": t.n}, f)
@@ -129,10 +153,13 @@ def report(ncu_csv, out_md):
              "| B200 range time us (x faster; includes host API time) | sim launches | sim warp eff % | sim occupancy % "
              "| sim DRAM tx (x basic) | sim cycles (x faster) |",
              "|---|---|---|---|---|---|---|---|---|---|---|"]
-    for app in ["spmv", "td"]:
-        bb, sb = b200.get(f"{app}/basic", {}), sim.get(f"{app}/basic", {})
+    for app in ["spmv", "td", "kdl-spmv", "kdl-td"]:
+        simapp = app.replace("kdl-", "")
+        bb, sb = b200.get(f"{app}/basic", {}), sim.get(f"{simapp}/basic", {})
         for v in VARIANTS:
-            b, sm = b200.get(f"{app}/{v}", {}), sim.get(f"{app}/{v}", {})
+            if f"{app}/{v}" not in b200:
+                continue
+            b, sm = b200.get(f"{app}/{v}", {}), sim.get(f"{simapp}/{v}", {})
             dr = f"{b['dram_sectors']} ({b['dram_sectors'] / max(1, bb.get('dram_sectors', 1)):.2f})" if b else "-"
             tm = f"{b['time_us']} ({bb.get('time_us', 0) / max(1e-9, b['time_us']):.1f})" if b else "-"
             if "childLaunchCount" in sm:
@@ -147,7 +174,10 @@ def report(ncu_csv, out_md):
                 sl = sw = so = sd = sc = "-"
             lines.append(f"| {app} / {v} | {b.get('launches', '-')} | {b.get('warp_eff_pct', '-')} | "
                          f"{b.get('occupancy_pct', '-')} | {dr} | {tm} | {sl} | {sw} | {so} | {sd} | {sc} |")
-    lines += ["", "Paper (K20c, mean over its benchmarks): launches after consolidation "
+    lines += ["", "kdl-* rows: the same .kdl programs the simulator runs, compiled for sm_100a by "
+              "paper_1606_08150_b200.kdl (int64 / fp64 values, CDP2 launches); the other B200 rows are the "
+              "hand-written kernels (fp32 / int32).",
+              "", "Paper (K20c, mean over its benchmarks): launches after consolidation "
               f"{PAPER['launches_pct_of_basic']} of basic; warp efficiency {PAPER['warp_eff']}; "
               f"occupancy {PAPER['occupancy']}; DRAM % of basic {PAPER['dram_pct_of_basic']}; "
               f"mean speed-up vs basic {PAPER['speedup_vs_basic_mean']}."]
