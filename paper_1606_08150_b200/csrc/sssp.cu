@@ -206,9 +206,42 @@ __device__ __forceinline__ void relax_serial(const Args& a, unsigned it, Block& 
 }
 
 // Warp-cooperative relaxation of edges [b, e) of a vertex at distance du.
+// The part of relax() after the distance load (cur = dist[v] already read).
+__device__ __forceinline__ void relax_loaded(const Args& a, unsigned it, Block& s, unsigned gv, unsigned nd,
+                                             unsigned cur) {
+  const unsigned v = gv - a.r0;
+  if (v >= a.n) {
+    if (a.peers) relax_peer(a, it, gv, nd);
+    else relax_remote(a, gv, nd);
+    return;
+  }
+  if (nd < cur) {
+    const unsigned old = atomicMin(a.dist + v, nd);
+    if (nd < old && atomicExch(a.stamp + v, it + 1) != it + 1) {
+      if (!a.classify) s.q.push(v, next_count(a, it), next_front(a, it));
+      else if (!s.q.try_push(v)) spill_classify(a, it, v);
+    }
+  }
+}
+
+// Two edges per lane per step: both edges' col / w loads, then both dist
+// loads, are in flight before either compare (a level's drain is a few such
+// dependent rounds per warp).
 __device__ __forceinline__ void relax_warp(const Args& a, unsigned it, Block& s, unsigned du,
                                            unsigned b, unsigned e) {
-  for (unsigned k = b + dev::lane_id(); k < e; k += 32) relax_edge(a, it, s, du, k);
+  for (unsigned k = b + dev::lane_id(); k < e; k += 64) {
+    const unsigned k2 = k + 32;
+    const bool ok2 = k2 < e;
+    const unsigned g1 = static_cast<unsigned>(__ldg(a.col + k));
+    const unsigned g2 = ok2 ? static_cast<unsigned>(__ldg(a.col + k2)) : a.r0;
+    const unsigned long long t1 = static_cast<unsigned long long>(du) + edge_w(a, k);
+    const unsigned long long t2 = ok2 ? static_cast<unsigned long long>(du) + edge_w(a, k2) : kInf;
+    const unsigned v1 = g1 - a.r0, v2 = g2 - a.r0;
+    const unsigned c1 = (t1 < kInf && v1 < a.n) ? __ldcg(a.dist + v1) : 0u;
+    const unsigned c2 = (t2 < kInf && v2 < a.n) ? __ldcg(a.dist + v2) : 0u;
+    if (t1 < kInf) relax_loaded(a, it, s, g1, static_cast<unsigned>(t1), c1);
+    if (t2 < kInf) relax_loaded(a, it, s, g2, static_cast<unsigned>(t2), c2);
+  }
 }
 
 __device__ __forceinline__ void drain_items(const Args& a, unsigned it, Block& s, const Item* items,
