@@ -271,6 +271,15 @@ int32_t* dpc_dgraph_color(dpc_dgraph* dg);
 /* %globaltimer stamps (ns) of the last persistent-kernel run whose metrics
  * were read: kernel start, device-wide barrier, end (phase split). */
 dpc_status dpc_dgraph_phase_ns(dpc_dgraph* dg, uint64_t out[3]);
+/* Runs called without metrics return once their work is enqueued; a fault
+ * they raise is reported by the next call on the graph or by this check
+ * (synchronises the context stream). */
+dpc_status dpc_dgraph_check(dpc_ctx* ctx, dpc_dgraph* dg);
+/* Tree persistent grid: kernel start, end of the top-down levels, end of the
+ * count-down postwork (%globaltimer ns) of the last run. */
+dpc_status dpc_dtree_phase_ns(dpc_dtree* dt, uint64_t out[3]);
+/* Fault check of the last dpc_tree_device run made without metrics. */
+dpc_status dpc_dtree_check(dpc_ctx* ctx, dpc_dtree* dt);
 
 /* Asynchronous on the context stream (no host sync, no copies). */
 dpc_status dpc_spmv_device(dpc_ctx* ctx, dpc_dgraph* dg, const float* d_x, float* d_y,

@@ -151,6 +151,9 @@ _SIGS = {
     "dpc_spmv_device": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host_batch": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_dtree_phase_ns": (C.c_int, [_P, _P]),
+    "dpc_dgraph_check": (C.c_int, [_P, _P]),
+    "dpc_dtree_check": (C.c_int, [_P, _P]),
     "dpc_ipc_handle": (C.c_int, [_P, _P]),
     "dpc_ipc_open": (C.c_int, [_P, _P, C.POINTER(_P)]),
     "dpc_ipc_close": (C.c_int, [_P]),
@@ -523,7 +526,12 @@ class DeviceGraph:
         _check(_lib.dpc_copy_d2h(self.ctx.handle, _ptr(y), self.y_ptr, y.nbytes))
         return y
 
+    def check(self):
+        """Fault check of the last run made without metrics (dpc_dgraph_check)."""
+        _check(_lib.dpc_dgraph_check(self.ctx.handle, self._h))
+
     def get_dist(self) -> np.ndarray:
+        self.check()
         d = np.empty(self.n, dtype=np.uint32)
         _check(_lib.dpc_copy_d2h(self.ctx.handle, _ptr(d), _lib.dpc_dgraph_dist(self._h), d.nbytes))
         return d
@@ -706,7 +714,13 @@ class DeviceTree:
                                     C.byref(met) if met is not None else None))
         return met
 
+    def phase_ns(self):
+        out = (C.c_uint64 * 3)()
+        _check(_lib.dpc_dtree_phase_ns(self._h, out))
+        return [int(v) for v in out]
+
     def result(self) -> np.ndarray:
+        _check(_lib.dpc_dtree_check(self.ctx.handle, self._h))
         r = np.empty(self.n, dtype=np.int32)
         _check(_lib.dpc_copy_d2h(self.ctx.handle, _ptr(r), _lib.dpc_dtree_result(self._h), r.nbytes))
         return r

@@ -61,6 +61,7 @@ struct dpc_dgraph {
   dpc::dev::RunHeader* hdr = nullptr;  // device counters
   dpc::dev::RunHeader* hdr_host = nullptr;  // pinned mirror
   bool hdr_clean = false;  // the last run (SpMV stream) left the header zeroed itself
+  bool check_pending = false;  // an asynchronous run's header copy awaits its fault check
   float* x2 = nullptr;     // second x / y slot of the pipelined host-vector path
   float* y2 = nullptr;
   // consolidation pool
@@ -109,6 +110,7 @@ struct dpc_dtree {
   int64_t internal = 0;              // nodes with >= 1 child
   unsigned group = 1;                // lanes per work item (mean fan-out)
   unsigned* pend = nullptr;          // persistent grid: pending internal children per node
+  bool check_pending = false;        // an asynchronous run's header copy awaits its fault check
 };
 
 namespace dpc {

@@ -850,6 +850,22 @@ static dpc_status sssp_iterate(dpc_ctx* ctx, const Cfg& c, sssp::Args& a, unsign
   return DPC_OK;
 }
 
+// A run without metrics returns as soon as its work is enqueued (like the
+// SpMV path): its header is copied back asynchronously and checked for
+// faults at the next call on this graph (or dpc_dgraph_check).
+static dpc_status flush_check(dpc_ctx* ctx, dpc_dgraph* g) {
+  if (!g->check_pending) return DPC_OK;
+  g->check_pending = false;
+  DPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return check_header(g->hdr_host);
+}
+
+extern "C" dpc_status dpc_dgraph_check(dpc_ctx* ctx, dpc_dgraph* g) {
+  clear_error();
+  if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
+  return flush_check(ctx, g);
+}
+
 static dpc_status sssp_finish(dpc_ctx* ctx, dpc_dgraph* g, int64_t host_launches, int64_t iters,
                               dpc_metrics* met) {
   cudaStream_t s = ctx->stream;
@@ -863,8 +879,8 @@ static dpc_status sssp_finish(dpc_ctx* ctx, dpc_dgraph* g, int64_t host_launches
     return DPC_OK;
   }
   DPC_CUDA(cudaMemcpyAsync(g->hdr_host, g->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
-  DPC_CUDA(cudaStreamSynchronize(s));
-  return check_header(g->hdr_host);
+  g->check_pending = true;
+  return DPC_OK;
 }
 
 static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dpc_launch_cfg* cfg,
@@ -875,7 +891,9 @@ static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dp
   if (source < 0 || source >= g->n) return fail(DPC_E_INVALID, "source out of range");
   Cfg c;
   sssp::Args a;
-  dpc_status st = sssp_setup(ctx, g, cfg, &a, &c, unit);
+  dpc_status st = flush_check(ctx, g);
+  if (st != DPC_OK) return st;
+  st = sssp_setup(ctx, g, cfg, &a, &c, unit);
   if (st != DPC_OK) return st;
   cudaStream_t s = ctx->stream;
   const bool one_barrier = c.variant == DPC_GRID && c.grid_persistent &&
@@ -934,9 +952,11 @@ static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dp
     if (a.coop) DPC_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(256), args, 0, s));
     else DPC_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(256), args, 0, s));
     host_launches += 1;
-    DPC_CUDA(cudaMemcpyAsync(ctr_host, a.ctr, sizeof(sssp::Ctr), cudaMemcpyDeviceToHost, s));
-    DPC_CUDA(cudaStreamSynchronize(s));
-    iters = ctr_host->iters;
+    if (met || phases) {  // the level count is a metric; no host round trip without it
+      DPC_CUDA(cudaMemcpyAsync(ctr_host, a.ctr, sizeof(sssp::Ctr), cudaMemcpyDeviceToHost, s));
+      DPC_CUDA(cudaStreamSynchronize(s));
+      iters = ctr_host->iters;
+    }
     if (phases) {
       DPC_CUDA(cudaMemcpy(ph.data(), a.ptrace, sizeof(unsigned long long) * ph.size(), cudaMemcpyDeviceToHost));
       cudaFree(a.ptrace);

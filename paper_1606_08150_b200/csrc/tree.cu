@@ -253,6 +253,17 @@ __global__ void __launch_bounds__(256) cons_kernel(Args a, const unsigned* items
   }
 }
 
+// Run init: level counters / offsets and the root item.
+__global__ void __launch_bounds__(32) init_run(unsigned* off, unsigned* nodes, unsigned c0, unsigned r,
+                                               unsigned root, bool root_internal) {
+  if (threadIdx.x == 0) {
+    off[0] = c0;
+    off[1] = off[2] = off[3] = 0;
+    off[4] = r;
+    if (root_internal) nodes[0] = root;
+  }
+}
+
 // ---------------------------------------------------------------- persistent
 // Top-down: the recursion's levels, consolidated per level with a
 // device-wide barrier; each internal node also records
@@ -277,6 +288,7 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
   unsigned* ctr = a.cnt;
   unsigned* off = a.cnt + 3;
   unsigned lo = 0, hi = off[1], levels = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[0] = dev::global_ns();
   // top-down
   while (hi > lo && levels < max_levels) {
     unsigned* app = ctr + levels % 3;
@@ -344,6 +356,7 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
     hi = min(hi + *reinterpret_cast<volatile unsigned*>(app), a.cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) off[levels + 1] = hi;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[1] = dev::global_ns();
   // bottom-up: count-down chains from the nodes with only leaf children
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < lo; i += stride) {
@@ -365,6 +378,8 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->iter = levels;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&a.hdr->t[2], dev::global_ns());  // phase timeline: end
 }
 
 }  // namespace tree
@@ -373,6 +388,14 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
 using namespace dpc;
 
 extern "C" {
+
+// Phase timeline of the last persistent-grid tree run (ns): kernel start,
+// end of the top-down levels, end of the bottom-up postwork.
+dpc_status dpc_dtree_phase_ns(dpc_dtree* d, uint64_t out[3]) {
+  if (!d || !out || !d->hdr_host) return fail(DPC_E_INVALID, "bad arguments");
+  for (int i = 0; i < 3; i++) out[i] = d->hdr_host->t[i];
+  return DPC_OK;
+}
 
 dpc_status dpc_dtree_upload(dpc_ctx* c, const dpc_tree* t, dpc_dtree** out) {
   clear_error();
@@ -442,10 +465,23 @@ void dpc_dtree_free(dpc_dtree* d) {
 
 int32_t* dpc_dtree_result(dpc_dtree* d) { return d ? d->result : nullptr; }
 
+dpc_status dpc_dtree_check(dpc_ctx* c, dpc_dtree* d) {
+  clear_error();
+  if (!c || !d) return fail(DPC_E_INVALID, "NULL argument");
+  if (!d->check_pending) return DPC_OK;
+  d->check_pending = false;
+  DPC_CUDA(cudaStreamSynchronize(c->stream));
+  return check_header(d->hdr_host);
+}
+
 dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_launch_cfg* cfg,
                            dpc_metrics* met) {
   clear_error();
   if (!c || !d) return fail(DPC_E_INVALID, "NULL argument");
+  {
+    dpc_status pst = dpc_dtree_check(c, d);
+    if (pst != DPC_OK) return pst;
+  }
   if (which != DPC_APP_TREE_DESC && which != DPC_APP_TREE_HEIGHT)
     return fail(DPC_E_INVALID, "which must be DPC_APP_TREE_DESC or DPC_APP_TREE_HEIGHT");
   Cfg k;
@@ -485,10 +521,9 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
   // start of level L.
   const unsigned r = root_internal ? 1u : 0u;
   const bool persistent = k.variant == DPC_GRID && k.grid_persistent;
-  unsigned init[5] = {persistent ? 0u : r, 0u, 0u, 0u, r};
-  DPC_CUDA(cudaMemcpyAsync(d->level_off, init, sizeof(init), cudaMemcpyHostToDevice, s));
-  if (root_internal)
-    DPC_CUDA(cudaMemcpyAsync(d->level_nodes, &root, sizeof(unsigned), cudaMemcpyHostToDevice, s));
+  // (a kernel, not pageable host copies: those cost a host round trip each)
+  tree::init_run<<<1, 32, 0, s>>>(d->level_off, d->level_nodes, persistent ? 0u : r, r, root, root_internal);
+  DPC_CUDA(cudaGetLastError());
   int64_t host_launches = 0, levels = 0;
   if (root_internal) {
     switch (k.variant) {
@@ -536,9 +571,11 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
         if (k.grid_persistent) {
           if (!d->pend) DPC_CUDA(cudaMalloc(&d->pend, sizeof(unsigned) * static_cast<size_t>(d->n)));
           a.pend = d->pend;
-          int per_sm = 0;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-              &per_sm, reinterpret_cast<const void*>(tree::grid_persistent), 256, 0);
+          static int per_sm_cached[64] = {};
+          int& per_sm = per_sm_cached[c->device & 63];
+          if (!per_sm)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, reinterpret_cast<const void*>(tree::grid_persistent), 256, 0);
           int blocks = std::max(1, per_sm) * c->sms;
           unsigned max_levels = static_cast<unsigned>(d->depth) + 1;
           void* args[] = {&a, &max_levels};
@@ -553,6 +590,10 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
     DPC_CUDA(cudaGetLastError());
   }
   DPC_CUDA(cudaMemcpyAsync(d->hdr_host, d->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
+  if (!met) {  // asynchronous: the fault check happens at the next call (dpc_dtree_check)
+    d->check_pending = true;
+    return DPC_OK;
+  }
   DPC_CUDA(cudaStreamSynchronize(s));
   st = check_header(d->hdr_host);
   if (st != DPC_OK) return st;
