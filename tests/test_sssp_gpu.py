@@ -101,3 +101,23 @@ def test_sssp_grid_forms(ctx, orc, form, scale):
         d, met = dpc.run_sssp(g, s, "grid", cfg=cfg, ctx=ctx)
         assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, s))
         assert met.child_launch_count == 0
+
+
+@pytest.mark.gpu
+def test_async_runs_without_metrics(ctx, orc):
+    """Runs without metrics return once enqueued; results and the deferred
+    fault check (dpc_dgraph_check / dpc_dtree_check) are read afterwards."""
+    g = dpc.gen_rmat(12, 16, seed=4)
+    s = int(np.argmax(g.degrees()))
+    dg = dpc.DeviceGraph(ctx, g)
+    for _ in range(3):
+        assert dg.sssp(s, "grid", metrics=False) is None
+    dg.check()
+    assert np.array_equal(dg.get_dist(), orc.sssp(g.rowptr, g.col, g.w, s))
+    dg.close()
+    t = dpc.gen_tree(8, 1, 4, 0.8, 2)
+    dt = dpc.DeviceTree(ctx, t)
+    dt.run("tree_desc", "grid", metrics=False)
+    dt.run("tree_desc", "grid", metrics=False)
+    assert np.array_equal(dt.result(), orc.tree_desc(t.parent))
+    dt.close()
