@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(32) init_run(unsigned* off, unsigned* nodes, u
 // brings the parent's count to zero carries on with the parent, so the
 // chains climb the tree concurrently (<= depth dependent steps, no barrier).
 constexpr unsigned kNoInternal = 0x80000000u;  // pend mark: no internal child
+constexpr unsigned kSmallLevel = 3;            // levels of <= 3 block passes run in block 0 alone
 
 __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_levels) {
   cg::grid_group grid = cg::this_grid();
@@ -289,13 +290,11 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
   unsigned* off = a.cnt + 3;
   unsigned lo = 0, hi = off[1], levels = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[0] = dev::global_ns();
-  // top-down
-  while (hi > lo && levels < max_levels) {
-    unsigned* app = ctr + levels % 3;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(levels + 1) % 3] = 0;
-    // block-uniform trip count (block_reserve synchronises the block)
-    const unsigned per_block = (blockDim.x >> 5) * gpw;
-    for (unsigned base = lo + blockIdx.x * per_block; base < hi; base += nwarps * gpw) {
+  // one pass over the level's items [lo, hi): every block-uniform loop
+  // iteration takes per_block items (block_reserve synchronises the block)
+  const unsigned per_block = (blockDim.x >> 5) * gpw;
+  auto expand = [&](unsigned base0, unsigned stride, unsigned* app) {
+    for (unsigned base = base0; base < hi; base += stride) {
       unsigned i = base + dev::warp_in_block() * gpw + lane / g;
       bool active = i < hi;
       unsigned v = active ? a.nodes[i] : 0;
@@ -350,6 +349,46 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
         }
       }
     }
+  };
+  // top-down, small levels: block 0 alone with block barriers (a device-wide
+  // barrier costs more than the few passes such a level needs)
+  __shared__ unsigned s_state[3];
+  if (blockIdx.x == 0) {
+    while (hi > lo && levels < max_levels && hi - lo <= kSmallLevel * per_block) {
+      unsigned* app = ctr + levels % 3;
+      if (threadIdx.x == 0) ctr[(levels + 1) % 3] = 0;
+      __syncthreads();
+      expand(lo, per_block, app);
+      __syncthreads();
+      levels++;
+      lo = hi;
+      hi = min(hi + *reinterpret_cast<volatile unsigned*>(app), a.cap);
+      if (threadIdx.x == 0) off[levels + 1] = hi;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      unsigned* st = off + max_levels + 2;  // scratch past the level offsets: hand the state to every block
+      st[0] = lo;
+      st[1] = hi;
+      st[2] = levels;
+    }
+  }
+  grid.sync();
+  if (threadIdx.x == 0) {
+    const volatile unsigned* st = off + max_levels + 2;
+    s_state[0] = st[0];
+    s_state[1] = st[1];
+    s_state[2] = st[2];
+  }
+  __syncthreads();
+  lo = s_state[0];
+  hi = s_state[1];
+  levels = s_state[2];
+  // top-down, the rest: every block, one device-wide barrier per level
+  while (hi > lo && levels < max_levels) {
+    unsigned* app = ctr + levels % 3;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(levels + 1) % 3] = 0;
+    expand(lo + blockIdx.x * per_block, nwarps * gpw, app);
     grid.sync();
     levels++;
     lo = hi;
@@ -432,7 +471,7 @@ dpc_status dpc_dtree_upload(dpc_ctx* c, const dpc_tree* t, dpc_dtree** out) {
   chk(cudaMalloc(&d->clist, sizeof(int) * n));
   chk(cudaMalloc(&d->result, sizeof(int) * n));
   chk(cudaMalloc(&d->level_nodes, sizeof(unsigned) * std::max<size_t>(1, static_cast<size_t>(internal))));
-  chk(cudaMalloc(&d->level_off, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 8)));
+  chk(cudaMalloc(&d->level_off, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 16)));
   chk(cudaMalloc(&d->hdr, sizeof(dev::RunHeader)));
   chk(cudaMallocHost(&d->hdr_host, sizeof(dev::RunHeader)));
   chk(cudaMallocHost(&d->off_host, sizeof(unsigned) * (static_cast<size_t>(t->depth) + 8)));
