@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(32) init_run(unsigned* off, unsigned* nodes, u
 // chains climb the tree concurrently (<= depth dependent steps, no barrier).
 constexpr unsigned kNoInternal = 0x80000000u;  // pend mark: no internal child
 constexpr unsigned kSmallLevel = 3;            // levels of <= 3 block passes run in block 0 alone
+constexpr unsigned kPullMin = 65536;           // bottom-up levels this wide fold by gathering
 
 __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_levels) {
   cg::grid_group grid = cg::this_grid();
@@ -396,11 +397,32 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
     if (blockIdx.x == 0 && threadIdx.x == 0) off[levels + 1] = hi;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[1] = dev::global_ns();
-  // bottom-up: count-down chains from the nodes with only leaf children
+  // bottom-up.  The deep, wide levels (>= kPullMin internal nodes, a suffix
+  // of the levels) and the one above them fold by gathering their
+  // children's results, one device-wide barrier per level (no atomics);
+  // everything above by count-down chains started from that level and from
+  // the leaf-only nodes higher up.
   const unsigned stride = gridDim.x * blockDim.x;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < lo; i += stride) {
+  const unsigned gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  unsigned P = levels;
+  while (P > 0 && off[P] - off[P - 1] >= kPullMin) P--;
+  const unsigned pull_top = P > 0 ? P - 1 : 0;  // levels [pull_top, levels) gather
+  if (P < levels) {
+    for (int L = static_cast<int>(levels) - 1; L >= static_cast<int>(pull_top); L--) {
+      const unsigned l0 = off[L], l1 = off[L + 1];
+      for (unsigned base = l0 + gwarp * gpw; base < l1; base += nwarps * gpw) {
+        const unsigned i = base + lane / g;
+        const bool active = i < l1;
+        fold_node(a, active ? a.nodes[i] : 0, sub, g, active);
+      }
+      grid.sync();
+    }
+  }
+  const unsigned chain_end = P < levels ? off[pull_top + 1] : lo;   // nodes of the chain levels
+  const unsigned folded0 = P < levels ? off[pull_top] : lo;         // [folded0, chain_end): folded, start
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < chain_end; i += stride) {
     unsigned u = a.nodes[i];
-    if (__ldcg(a.pend + u) != kNoInternal) continue;
+    if (i < folded0 && __ldcg(a.pend + u) != kNoInternal) continue;
     while (true) {
       const int r = atomicAdd(a.res + u, 0);  // every child's share is in
       const int p = __ldg(a.parent + u);
