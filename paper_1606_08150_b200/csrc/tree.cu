@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
   while (P > 0 && off[P] - off[P - 1] >= kPullMin) P--;
   const unsigned pull_top = P > 0 ? P - 1 : 0;  // levels [pull_top, levels) gather
   if (P < levels) {
-    for (int L = static_cast<int>(levels) - 1; L >= static_cast<int>(pull_top); L--) {
+    // the deepest level's nodes have only leaf children: the top-down
+    // already left their final result (the leaf share) in res
+    for (int L = static_cast<int>(levels) - 2; L >= static_cast<int>(pull_top); L--) {
       const unsigned l0 = off[L], l1 = off[L + 1];
       for (unsigned base = l0 + gwarp * gpw; base < l1; base += nwarps * gpw) {
         const unsigned i = base + lane / g;
