@@ -57,6 +57,8 @@ struct Args {
   int is_max;      // TH (max) vs TD (sum)
   const int* parent;  // persistent grid: parent[v] (-1 at the root)
   unsigned* pend;     // persistent grid: internal children not yet folded
+  unsigned root;
+  unsigned root_internal;
 };
 
 __device__ __forceinline__ unsigned nkids(const Args& a, unsigned v) {
@@ -289,8 +291,19 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_leve
   // off[L] (= cnt + 3) = start of level L in nodes[].
   unsigned* ctr = a.cnt;
   unsigned* off = a.cnt + 3;
-  unsigned lo = 0, hi = off[1], levels = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[0] = dev::global_ns();
+  // run init inside the kernel (no memset / init launches before it): zero
+  // the results, set the level counters and the root item
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += gridDim.x * blockDim.x) a.res[v] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned r = a.root_internal ? 1u : 0u;
+    ctr[0] = ctr[1] = ctr[2] = 0;
+    off[0] = 0;
+    off[1] = r;
+    if (r) a.nodes[0] = a.root;
+  }
+  grid.sync();
+  unsigned lo = 0, hi = *reinterpret_cast<volatile unsigned*>(off + 1), levels = 0;
   // one pass over the level's items [lo, hi): every block-uniform loop
   // iteration takes per_block items (block_reserve synchronises the block)
   const unsigned per_block = (blockDim.x >> 5) * gpw;
@@ -574,8 +587,10 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
   else if (k.variant == DPC_GRID) need = 4 * static_cast<size_t>(d->depth) + 1024;
   st = ensure_pending_limit(c, need);
   if (st != DPC_OK) return st;
+  const bool persistent_grid = k.variant == DPC_GRID && k.grid_persistent;
   DPC_CUDA(cudaMemsetAsync(d->hdr, 0, sizeof(dev::RunHeader), s));
-  DPC_CUDA(cudaMemsetAsync(d->result, 0, sizeof(int) * static_cast<size_t>(d->n), s));
+  if (!persistent_grid)  // the persistent kernel zeroes the results itself
+    DPC_CUDA(cudaMemsetAsync(d->result, 0, sizeof(int) * static_cast<size_t>(d->n), s));
   const unsigned root = static_cast<unsigned>(d->root);
   const bool root_internal = d->internal > 0;
   // level_off[0] = bump pointer, level_off[1 + L] = start of level L
@@ -585,8 +600,12 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
   const unsigned r = root_internal ? 1u : 0u;
   const bool persistent = k.variant == DPC_GRID && k.grid_persistent;
   // (a kernel, not pageable host copies: those cost a host round trip each)
-  tree::init_run<<<1, 32, 0, s>>>(d->level_off, d->level_nodes, persistent ? 0u : r, r, root, root_internal);
-  DPC_CUDA(cudaGetLastError());
+  a.root = root;
+  a.root_internal = root_internal ? 1u : 0u;
+  if (!persistent) {
+    tree::init_run<<<1, 32, 0, s>>>(d->level_off, d->level_nodes, 0u + r, r, root, root_internal);
+    DPC_CUDA(cudaGetLastError());
+  }
   int64_t host_launches = 0, levels = 0;
   if (root_internal) {
     switch (k.variant) {
