@@ -272,12 +272,16 @@ __global__ void __launch_bounds__(256) init_kernel(Args a, unsigned source) {
     if (mine && a.classify) {  // one-barrier form: a heavy source starts as chunk items
       const unsigned b = a.rowptr[ls], e = a.rowptr[ls + 1];
       if (e - b > a.threshold) {
-        const dev::Pool p{a.pool.items, a.pool.cap};
-        const unsigned nch = dev::nchunks(e - b, a.chunk);
-        dev::write_chunks(p, a.hdr, 0, ls, b, e, a.chunk);
-        a.ctr->pool[0] = nch;
+        a.ctr->pool[0] = dev::nchunks(e - b, a.chunk);
         a.ctr->fsize[0] = 0;
       }
+    }
+  }
+  if (mine && a.classify) {  // the source's chunk items, one per thread (not a serial loop)
+    const unsigned b = __ldg(a.rowptr + ls), e = __ldg(a.rowptr + ls + 1);
+    if (e - b > a.threshold && i < dev::nchunks(e - b, a.chunk)) {
+      if (i < a.pool.cap) a.pool.items[i] = Item{ls, b + i * a.chunk};
+      else atomicOr(&a.hdr->overflow, 1u);
     }
   }
 }
