@@ -611,7 +611,11 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
     }
     // the level's chunk items (inserted while the previous level flushed)
     mark(1);
-    drain_items(a, it, s, a.pool.items + (it % 2) * a.pool.cap, pc, gtid >> 5, stride >> 5);
+    // warp rank block-interleaved: consecutive items land in different
+    // blocks, so a short item list (e.g. the source's chunks) spreads its
+    // pushes over every block's queue instead of a few
+    drain_items(a, it, s, a.pool.items + (it % 2) * a.pool.cap, pc,
+                dev::warp_in_block() * gridDim.x + blockIdx.x, stride >> 5);
     mark(2);
     flush_classify(a, it, s, (it + 1) % 2);
     mark(3);
