@@ -32,9 +32,10 @@ from . import ast
 from .transform import Config, consolidate, k20c_occupancy, lower_kc
 from .cuda import generate
 from .parse import KdlError, parse_program
+from .unparse import unparse
 
 __all__ = ["compile", "compile_program", "Module", "KdlError", "KdlFault", "Config", "parse_program",
-           "consolidate", "lower_kc", "k20c_occupancy", "generate", "build_programs", "autotune", "PROGRAMS"]
+           "consolidate", "lower_kc", "k20c_occupancy", "generate", "build_programs", "autotune", "unparse", "PROGRAMS"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD = os.path.join(HERE, "_build")

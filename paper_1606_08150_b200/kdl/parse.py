@@ -346,6 +346,15 @@ class _Parser:
             slot = self.take(kind="int")
             self.take(")")
             return A.Expr("buf_get", args=[i, A.lit(slot)])
+        if n == "dp_kc_blocks":  # B200 extension (unparse.py): KC_X launch size resolved at load
+            self.take("(")
+            k = self.ident()
+            self.take(",")
+            x = self.take(kind="int")
+            self.take(",")
+            t = self.expr()
+            self.take(")")
+            return A.Expr("kc_blocks", name=k, ival=x, args=[t])
         if n in ("dp_buf_cfg_grid", "dp_buf_cfg_block"):
             self.take("(")
             i = self.expr()

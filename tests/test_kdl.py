@@ -181,3 +181,51 @@ def test_generated_unit_builds_for_sm100a(tmp_path, monkeypatch):
     assert len(syms) == 7
     for sym in syms:   # every entry point include/dpc_kdl.h declares
         assert f" T {sym}" in out, sym
+
+
+@pytest.mark.parametrize("name,mode", CASES)
+def test_rewrite_prints_like_reference(name, mode):
+    """Character for character: our rewrite, printed in the reference's
+    layout, equals the reference's consolidate() text."""
+    if (name, mode) == ("post.kdl", "grid"):
+        pytest.skip("reference bug, see test_rewrite_matches_reference_consolidate")
+    ours = T.lower_kc(kdl.consolidate(kdl.parse_program(src_of(name)), mode), T.k20c_occupancy)
+    assert kdl.unparse(ours) == GOLD["consolidated"][name][mode]
+
+
+@pytest.mark.parametrize("name", sorted(GOLD["consolidated"]))
+def test_unparse_parse_round_trip(name):
+    p = kdl.parse_program(src_of(name))
+    assert kdl.parse_program(kdl.unparse(p)) == p
+    for mode in ("warp", "block", "grid"):
+        c = kdl.consolidate(p, mode)   # kc_blocks nodes print as dp_kc_blocks(...)
+        assert kdl.parse_program(kdl.unparse(c)) == c
+
+
+def test_expression_round_trip_random():
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    from paper_1606_08150_b200.kdl.unparse import expr as print_expr
+
+    leaves = st.one_of(st.integers(0, 10**12).map(A.lit), st.sampled_from(["a", "b"]).map(A.ref),
+                       st.sampled_from(A.INTRINSICS).map(A.intr),
+                       st.floats(0, 1e6, allow_nan=False).map(lambda v: A.Expr("float", fval=v)))
+    ops = ["+", "-", "*", "/", "%", "<", "<=", ">", ">=", "==", "!=", "&&", "||"]
+
+    def extend(children):
+        return st.one_of(
+            st.tuples(st.sampled_from(ops), children, children).map(lambda t: A.binop(*t)),
+            st.tuples(st.sampled_from(["-", "!"]), children).map(lambda t: A.Expr("unary", name=t[0], args=[t[1]])),
+            st.tuples(st.sampled_from(["min", "max"]), children, children).map(
+                lambda t: A.Expr("minmax", name=t[0], args=[t[1], t[2]])),
+            children.map(lambda c: A.Expr("index", name="arr", args=[c])))
+
+    @settings(max_examples=300, deadline=None)
+    @given(st.recursive(leaves, extend, max_leaves=12))
+    def check(e):
+        src = ("global int arr[n];\nkernel k(int a, int b) { int z = " + print_expr(e) +
+               "; }\nentry k<<<1, 1>>>(0, 0);")
+        assert kdl.parse_program(src).kernels[0].body[0].exprs[0] == e
+
+    check()
