@@ -23,7 +23,8 @@ struct dpc_prgraph {
   int64_t n = 0;
   unsigned* dangling = nullptr;  // ids of vertices without out-edges
   int64_t ndangling = 0;
-  double* dmass = nullptr;       // [2] dangling mass, ping-pong by iteration
+  double* dmass = nullptr;       // [3] dangling mass, rotated by iteration (read / accumulate / clear)
+  unsigned char* dflag = nullptr; // 1 for a dangling vertex (no out-edge)
 };
 
 namespace dpc {
@@ -32,27 +33,30 @@ namespace pr {
 __global__ void __launch_bounds__(256) init_kernel(float* r, unsigned n, double* dmass, double d0) {
   const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) r[i] = 1.0f / static_cast<float>(n);
-  if (i == 0) dmass[0] = d0, dmass[1] = 0.0;
+  if (i == 0) dmass[0] = d0, dmass[1] = 0.0, dmass[2] = 0.0;
 }
 
-// r[v] = (1-d)/n + d (y[v] + D/n); dmass[next] += r over the dangling list.
+// One kernel per iteration after the SpMV (y = P r):
+//   r[v] = (1-d)/n + d (y[v] + D/n),  D = dmass[it % 3]
+// and, for the next iteration, the dangling mass of the new ranks into
+// dmass[(it + 1) % 3]; dmass[(it + 2) % 3] (last read one iteration ago) is
+// cleared for the one after.  Replaces a clear launch and a pass over the
+// dangling list per iteration.
 __global__ void __launch_bounds__(256) update_kernel(float* __restrict__ r, const float* __restrict__ y, unsigned n,
-                                                      double damping, double* dmass, int cur) {
-  const double dn = dmass[cur] / n;
+                                                      double damping, double* dmass,
+                                                      const unsigned char* __restrict__ dflag, int it) {
+  const double dn = dmass[it % 3] / n;
   const double base = (1.0 - damping) / n;
-  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    r[v] = static_cast<float>(base + damping * (static_cast<double>(y[v]) + dn));
-}
-
-__global__ void __launch_bounds__(256) dangling_kernel(const float* __restrict__ r, const unsigned* __restrict__ ids,
-                                                        unsigned cnt, double* dmass, int next) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) dmass[(it + 2) % 3] = 0.0;
   double s = 0.0;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) s += r[ids[i]];
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const float nr = static_cast<float>(base + damping * (static_cast<double>(y[v]) + dn));
+    r[v] = nr;
+    if (dflag[v]) s += nr;
+  }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(dmass + next, s);
+  if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(dmass + (it + 1) % 3, s);
 }
-
-__global__ void clear_kernel(double* dmass, int which) { dmass[which] = 0.0; }
 
 }  // namespace pr
 }  // namespace dpc
@@ -104,9 +108,15 @@ dpc_status dpc_pr_upload(dpc_ctx* ctx, const dpc_csr* G, dpc_prgraph** out) {
   }
   h->ndangling = static_cast<int64_t>(dang.size());
   cudaError_t e = cudaMalloc(&h->dangling, sizeof(unsigned) * std::max<size_t>(dang.size(), 1));
-  if (e == cudaSuccess) e = cudaMalloc(&h->dmass, sizeof(double) * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&h->dmass, sizeof(double) * 3);
+  if (e == cudaSuccess) e = cudaMalloc(&h->dflag, static_cast<size_t>(std::max<int64_t>(n, 1)));
   if (e == cudaSuccess && !dang.empty())
     e = cudaMemcpy(h->dangling, dang.data(), sizeof(unsigned) * dang.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    std::vector<unsigned char> fl(static_cast<size_t>(std::max<int64_t>(n, 1)), 0);
+    for (unsigned v : dang) fl[v] = 1;
+    e = cudaMemcpy(h->dflag, fl.data(), fl.size(), cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     dpc_pr_free(h);
     return cuda_fail(e, "dpc_pr_upload");
@@ -120,6 +130,7 @@ void dpc_pr_free(dpc_prgraph* h) {
   if (h->pt) dpc_dgraph_free(h->pt);
   if (h->dangling) cudaFree(h->dangling);
   if (h->dmass) cudaFree(h->dmass);
+  if (h->dflag) cudaFree(h->dflag);
   delete h;
 }
 
@@ -138,17 +149,12 @@ dpc_status dpc_pr_device(dpc_ctx* ctx, dpc_prgraph* h, int32_t iters, double dam
   pr::init_kernel<<<nb, 256, 0, s>>>(pt->x, n, h->dmass, static_cast<double>(h->ndangling) / n);
   DPC_CUDA(cudaGetLastError());
   for (int32_t it = 0; it < iters; it++) {
-    const int cur = it & 1, next = cur ^ 1;
     dpc_status st = dpc_spmv_device(ctx, pt, pt->x, pt->y, cfg, met);  // y = P r
     if (st != DPC_OK) return st;
-    pr::clear_kernel<<<1, 1, 0, s>>>(h->dmass, next);
-    pr::update_kernel<<<gb, 256, 0, s>>>(pt->x, pt->y, n, damping, h->dmass, cur);
-    if (h->ndangling)
-      pr::dangling_kernel<<<std::min(gb, static_cast<unsigned>((h->ndangling + 255) / 256)), 256, 0, s>>>(
-          pt->x, h->dangling, static_cast<unsigned>(h->ndangling), h->dmass, next);
+    pr::update_kernel<<<gb, 256, 0, s>>>(pt->x, pt->y, n, damping, h->dmass, h->dflag, it);
     DPC_CUDA(cudaGetLastError());
   }
-  if (met) met->host_launches += 1 + 3 * static_cast<int64_t>(iters);
+  if (met) met->host_launches += 1 + 2 * static_cast<int64_t>(iters);
   return DPC_OK;
 }
 
