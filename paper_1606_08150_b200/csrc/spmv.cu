@@ -1275,6 +1275,10 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
 //      slower than shape 0 (196 vs 68 us drain)
 //   6: groups of 4, 4 windows, not pipelined
 //   7: pipelined, groups of 4, 3 windows
+// Higher occupancy loses: shape 0 at 512 threads x 3 blocks/SM (40 regs,
+// 216 B spills) 106.6 us, at 1024 x 2 (32 regs, 208 B spills, 32-item
+// batches) 114.4 us, vs 78.1 us: spills and the smaller x share of L1 cost
+// more than the extra warps hide.
 struct StreamShape {
   const void* fn;
   int threads;
