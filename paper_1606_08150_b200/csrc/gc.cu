@@ -1203,8 +1203,8 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
       g->gc_hstate_cap = heavy + 1;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(gc::async_persistent),
-                                                  256, 0);
+    DPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(gc::async_persistent),
+                                                  256, 0));
     int blocks = std::max(1, per_sm) * ctx->sms;
     gc::Async q;
     q.q = reinterpret_cast<unsigned long long*>(g->gc_q);
@@ -1241,8 +1241,8 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
     iters = 1;
   } else if (c.variant == DPC_GRID && c.grid_persistent) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(gc::grid_persistent),
-                                                  256, 0);
+    DPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(gc::grid_persistent),
+                                                  256, 0));
     int blocks = std::max(1, per_sm) * ctx->sms;
     unsigned max_iters = a.n + 1;
     void* args[] = {&a, &max_iters};

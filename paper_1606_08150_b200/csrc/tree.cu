@@ -656,8 +656,8 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
           static int per_sm_cached[64] = {};
           int& per_sm = per_sm_cached[c->device & 63];
           if (!per_sm)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, reinterpret_cast<const void*>(tree::grid_persistent), 256, 0);
+            DPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, reinterpret_cast<const void*>(tree::grid_persistent), 256, 0));
           int blocks = std::max(1, per_sm) * c->sms;
           unsigned max_levels = static_cast<unsigned>(d->depth) + 1;
           void* args[] = {&a, &max_levels};
