@@ -1279,6 +1279,11 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
 // 216 B spills) 106.6 us, at 1024 x 2 (32 regs, 208 B spills, 32-item
 // batches) 114.4 us, vs 78.1 us: spills and the smaller x share of L1 cost
 // more than the extra warps hide.
+// Register double-buffering (step s+1's col / val loaded into registers
+// under step s's gathers, lookups two steps ahead) also loses: 768 threads
+// x 80 regs 91.0 us, 512 x 96 regs 119.1 us, 1 window x 1024 threads 81.0 us
+// (all parity-equal): with the L2 prefetch already in place, warps x
+// gathers in flight is what the drain needs.
 struct StreamShape {
   const void* fn;
   int threads;
