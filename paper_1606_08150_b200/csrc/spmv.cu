@@ -1284,6 +1284,10 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
 // x 80 regs 91.0 us, 512 x 96 regs 119.1 us, 1 window x 1024 threads 81.0 us
 // (all parity-equal): with the L2 prefetch already in place, warps x
 // gathers in flight is what the drain needs.
+// On the vertex-permuted matrix (config 5 rows, tools/prof_spmv.py
+// --permute --burst 10): shape 0 87.4 us, 3 90.0, 4 81.8, 6 93.5, 7 91.3 —
+// the hot-column cache pays 6 % once permutation spreads the hubs; the
+// fused peer-x path does not use it.
 struct StreamShape {
   const void* fn;
   int threads;

@@ -18,9 +18,10 @@ ap.add_argument("--chunk", type=int, default=0)
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--threshold", type=int, default=-1)
 ap.add_argument("--burst", type=int, default=0)
+ap.add_argument("--permute", action="store_true", help="vertex-permuted R-MAT (config 5 shape)")
 a = ap.parse_args()
 ctx = dpc.Context(0)
-g = dpc.gen_rmat(a.scale, 16, seed=1, weights=False, values=True)
+g = dpc.gen_rmat(a.scale, 16, seed=1, weights=False, values=True, permute=a.permute)
 dg = dpc.DeviceGraph(ctx, g)
 dg.set_x((np.arange(g.n) % 1000 + 1).astype(np.float32) / 1000)
 for v in a.variants:
