@@ -211,32 +211,43 @@ def _run_fused(args, dist, ctx, dg, dx, R, rank, world, y64):
         bufs.append(yd)
         epoch = 0
 
-        def step():
+        def step(cfg):
             nonlocal epoch
             dpc.p2p_barrier(ctx, ftab, world, rank, epoch + 1)
-            dg.spmv_fused(xtab, world, R, yd)
+            dg.spmv_fused(xtab, world, R, yd, cfg=cfg)
             dpc.p2p_barrier(ctx, ftab, world, rank, epoch + 2)
             epoch += 2
 
-        step()
-        dpc.p2p_check(ctx)
-        y = ctx.d2h(yd, R).astype(np.float64)
-        ok = bool(np.all(np.abs(y - y64) <= 1e-5 * np.abs(y64)))
-        for _ in range(args.warmup):
-            step()
-        ctx.synchronize()
-        _barrier(dist)
-        ts = []
-        for _ in range(args.steps):
-            ctx.flush_l2()
-            ctx.record(4)
-            step()
-            ctx.record(5)
-            ts.append(ctx.elapsed_ms(4, 5))
-        dpc.p2p_check(ctx)
-        ms = float(np.mean(ts))
-        ok_all = _sum_over_ranks(dist, float(ok)) == world
-        res = {"ok": ok_all, "ms": ms, "ms_max": _max_over_ranks(dist, ms),
+        # two stream shapes: the default drain, and shape 4 (groups of 8 +
+        # a shared-memory cache of the block's hottest x columns, which pays
+        # once vertex permutation spreads the R-MAT hubs)
+        hot = dpc.launch_cfg("spmv", "grid")
+        hot.flags |= 4 << 20
+        shapes = {}
+        for name, cfg in (("default", None), ("hot_cache", hot)):
+            ctx.h2d(yd, np.zeros(R, np.float32))
+            step(cfg)
+            dpc.p2p_check(ctx)
+            y = ctx.d2h(yd, R).astype(np.float64)
+            ok = bool(np.all(np.abs(y - y64) <= 1e-5 * np.abs(y64)))
+            for _ in range(args.warmup):
+                step(cfg)
+            ctx.synchronize()
+            _barrier(dist)
+            ts = []
+            for _ in range(args.steps):
+                ctx.flush_l2()
+                ctx.record(4)
+                step(cfg)
+                ctx.record(5)
+                ts.append(ctx.elapsed_ms(4, 5))
+            dpc.p2p_check(ctx)
+            ms = float(np.mean(ts))
+            shapes[name] = {"ok": _sum_over_ranks(dist, float(ok)) == world, "ms_max": _max_over_ranks(dist, ms)}
+        good = {k: v for k, v in shapes.items() if v["ok"]}
+        best = min(good, key=lambda k: good[k]["ms_max"]) if good else "default"
+        res = {"ok": bool(good), "ms": shapes[best]["ms_max"], "ms_max": shapes[best]["ms_max"], "shape": best,
+               "shapes": shapes,
                "api": "dpc_p2p_barrier + dpc_multi_spmv_fused + dpc_p2p_barrier (C ABI), per rank"}
     except Exception as e:  # noqa: BLE001 - fall back to the NCCL path
         res = {"ok": False, "error": str(e)[:300]}

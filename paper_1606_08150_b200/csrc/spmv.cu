@@ -754,13 +754,15 @@ __device__ __forceinline__ float grp_dot(const Args& a, const Grp<G>& g, unsigne
       if (a.xflags & 128u) idx &= 0xffff;   // probe: gathers confined to 256 KB of x
       const float wt = on ? wp[e] : 0.f;
       float xv;
-      if (a.xpeer) {
+      if (SLOG > 0) {  // hot-column cache, misses to x (or the owner's x slice)
+        const uint2 t = xc[xslot(static_cast<unsigned>(idx), SLOG)];
+        xv = t.x == static_cast<unsigned>(idx) ? __uint_as_float(t.y)
+             : a.xpeer                         ? peer_x(a, static_cast<unsigned>(idx))
+                                               : __ldg(a.x + idx);
+      } else if (a.xpeer) {
         xv = peer_x(a, static_cast<unsigned>(idx));
       } else if (a.xflags & 16u) {
         xv = 1.f;
-      } else if (SLOG > 0) {
-        const uint2 t = xc[xslot(static_cast<unsigned>(idx), SLOG)];
-        xv = t.x == static_cast<unsigned>(idx) ? __uint_as_float(t.y) : __ldg(a.x + idx);
       } else if (a.xflags & 256u) {
         xv = __ldcg(a.x + idx);  // probe: x gathers through L2 only
       } else if (a.xflags & 512u) {
@@ -1159,7 +1161,7 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
   if (SLOG > 0)  // x at the planned hot columns, once per run
     for (unsigned i = blockIdx.x * NT + threadIdx.x; i < (1u << SLOG); i += GB * NT) {
       const int c = st.xhot_col[i];
-      st.xhot_val[i] = c >= 0 ? __ldg(a.x + c) : 0.f;
+      st.xhot_val[i] = c >= 0 ? (a.xpeer ? peer_x(a, static_cast<unsigned>(c)) : __ldg(a.x + c)) : 0.f;
     }
   for (unsigned t0 = blockIdx.x; t0 < ntiles; t0 += GB * kRound) {
     unsigned bb[kRound], ee[kRound], inc[kRound];
@@ -1482,8 +1484,8 @@ dpc_status dpc::spmv_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d
   a.coop = 1;
   // stream-balanced grid drain (grid_stream)
   const bool use_stream = c.variant == DPC_GRID && c.grid_persistent && !(c.flags & DPC_CFG_GRID_CHUNKED);
-  if (xpeer && !(use_stream && c.threshold == 0 && ((c.flags >> 20) & 7u) != 3u && ((c.flags >> 20) & 7u) != 4u))
-    return fail(DPC_E_INVALID, "fused multi-GPU SpMV runs on the grid stream kernel (threshold 0, no x cache)");
+  if (xpeer && !(use_stream && c.threshold == 0))
+    return fail(DPC_E_INVALID, "fused multi-GPU SpMV runs on the grid stream kernel (threshold 0)");
   spmv::Stream sa{};
   if (use_stream) {
     const uint64_t heavy = pool_need(g, c.threshold, 1u << 30);

@@ -31,10 +31,12 @@ def close(y, y64):
     return np.all(np.abs(y.astype(np.float64) - y64) <= 1e-5 * np.abs(y64) + 1e-30)
 
 
+@pytest.mark.parametrize("shape", [0, 4])
 @pytest.mark.parametrize("world", [1, 3, 4])
-def test_fused_spmv_partitions_one_process(orc, world):
+def test_fused_spmv_partitions_one_process(orc, world, shape):
     """world row blocks; x entry i lives on block i // R (R a power of two
-    for world 1 / 4, not for 3: the shift and the division paths)."""
+    for world 1 / 4, not for 3: the shift and the division paths); stream
+    shape 0 (default) and 4 (hot-column x cache filled from the owners)."""
     g = full_matrix()
     n = g.n
     R = (n + world - 1) // world
@@ -61,7 +63,9 @@ def test_fused_spmv_partitions_one_process(orc, world):
             dg = dpc.DeviceGraph(ctx, A)
             yd = ctx.alloc(4 * max(1, r1 - r0))
             bufs.append(yd)
-            dg.spmv_fused(tab, world, R, yd)
+            cfg = dpc.launch_cfg("spmv", "grid")
+            cfg.flags |= shape << 20
+            dg.spmv_fused(tab, world, R, yd, cfg=cfg)
             y = ctx.d2h(yd, r1 - r0)
             assert close(y, y64[r0:r1]), f"rank {p}"
             dg.close()
