@@ -185,6 +185,11 @@ typedef struct dpc_launch_cfg {
                                   the device heap (malloc / tail-launched free)
                                   instead of the pre-allocated pool -- the
                                   paper's allocator study, PAPER.md:296 */
+#define DPC_CFG_X_PEER_GATHER 32 /* fused multi-GPU SpMV: every x gather goes to its
+                                    owner's memory (default: the kernel first pulls the
+                                    owners' x slices into the local x with coalesced
+                                    peer reads, before the device-wide barrier it
+                                    already has, then gathers locally) */
 #define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */
@@ -344,7 +349,9 @@ dpc_status dpc_msssp_set_peers(dpc_dgraph* dg, const void* d_peer_table);
 /* Grid stream SpMV of this rank's row block with x read from the owners:
  * d_xpeer is a DEVICE array of `world` pointers, x entry i at
  * d_xpeer[i / rows_per_rank][i % rows_per_rank] (replaces ncclAllGather +
- * dpc_spmv_device, multi.cu).  Needs the grid variant with threshold 0. */
+ * dpc_spmv_device, multi.cu).  Needs the grid variant with threshold 0.
+ * Uses the local graph's x buffer (ncols entries) as the pulled copy of x
+ * unless DPC_CFG_X_PEER_GATHER. */
 dpc_status dpc_multi_spmv_fused(dpc_ctx* ctx, dpc_dgraph* local, const float* const* d_xpeer, int32_t world,
                                 int64_t rows_per_rank, float* d_y_local, const dpc_launch_cfg* cfg,
                                 dpc_metrics* met);

@@ -57,6 +57,7 @@ GEN_WEIGHTS, GEN_VALUES, GEN_PERMUTE, GEN_SYMMETRIC = 1, 2, 4, 8
 CFG_GRID_CDP = 1
 CFG_GRID_CHUNKED = 2
 CFG_GRID_ASYNC = 8
+CFG_X_PEER_GATHER = 32
 
 
 class DpcError(RuntimeError):

@@ -63,8 +63,10 @@ struct Args {
   // lives on rank i / rows at offset i % rows and is read straight from the
   // owner's memory (NVLink peer loads); nullptr = local x
   const float* const* xpeer;
+  float* xpull;           // pull mode: the owners' slices are copied here (= x) before the barrier
   unsigned rshift;        // log2(rows) when rows is a power of two, else ~0u
   unsigned rows;
+  unsigned ncols;         // x entries (pull mode)
 };
 
 __device__ __forceinline__ float peer_x(const Args& a, unsigned idx) {
@@ -757,9 +759,9 @@ __device__ __forceinline__ float grp_dot(const Args& a, const Grp<G>& g, unsigne
       if (SLOG > 0) {  // hot-column cache, misses to x (or the owner's x slice)
         const uint2 t = xc[xslot(static_cast<unsigned>(idx), SLOG)];
         xv = t.x == static_cast<unsigned>(idx) ? __uint_as_float(t.y)
-             : a.xpeer                         ? peer_x(a, static_cast<unsigned>(idx))
+             : a.xpeer && !a.xpull             ? peer_x(a, static_cast<unsigned>(idx))
                                                : __ldg(a.x + idx);
-      } else if (a.xpeer) {
+      } else if (a.xpeer && !a.xpull) {
         xv = peer_x(a, static_cast<unsigned>(idx));
       } else if (a.xflags & 16u) {
         xv = 1.f;
@@ -1213,6 +1215,30 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
     }
     __syncthreads();  // s_w / s_base are reused by the next round
   }
+  if (a.xpull) {
+    // fused multi-GPU pull: every owner's x slice into the local x with
+    // coalesced 16-byte peer reads (NVLink), overlapping the insert phase's
+    // tail; the barrier below orders it before the drain's gathers
+    const unsigned nx = a.ncols, stride = GB * NT;
+    if ((a.rows & 3u) == 0) {
+      for (unsigned i = blockIdx.x * NT + threadIdx.x; 4 * i < nx; i += stride) {
+        const unsigned c = 4 * i;
+        const unsigned o = a.rshift != ~0u ? c >> a.rshift : c / a.rows;
+        const unsigned l = c - o * a.rows;
+        const float* src = a.xpeer[o] + l;
+        if (c + 4 <= nx && !(reinterpret_cast<uintptr_t>(src) & 15u)) {
+          reinterpret_cast<float4*>(a.xpull)[i] = __ldcg(reinterpret_cast<const float4*>(src));
+        } else {
+          for (unsigned j = c; j < min(c + 4, nx); j++) a.xpull[j] = __ldcg(src + (j - c));
+        }
+      }
+    } else {
+      for (unsigned c = blockIdx.x * NT + threadIdx.x; c < nx; c += stride) {
+        const unsigned o = a.rshift != ~0u ? c >> a.rshift : c / a.rows;
+        a.xpull[c] = __ldcg(a.xpeer[o] + (c - o * a.rows));
+      }
+    }
+  }
   if (a.coop) cg::this_grid().sync();
   else dev::soft_grid_barrier(&a.hdr->ticket);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[1] = dev::global_ns();
@@ -1478,6 +1504,13 @@ dpc_status dpc::spmv_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d
   a.child_blocks = c.child_blocks;
   a.xflags = c.flags >> 24;
   a.xpeer = xpeer;
+  a.xpull = nullptr;
+  a.ncols = static_cast<unsigned>(g->ncols);
+  if (xpeer && !(c.flags & DPC_CFG_X_PEER_GATHER)) {
+    if (!g->x) return fail(DPC_E_INVALID, "fused SpMV pull mode needs the graph's x buffer");
+    a.xpull = g->x;
+    a.x = g->x;
+  }
   a.rows = static_cast<unsigned>(rows);
   a.rshift = ~0u;
   if (rows && (rows & (rows - 1)) == 0) a.rshift = static_cast<unsigned>(__builtin_ctzll(rows));

@@ -31,12 +31,14 @@ def close(y, y64):
     return np.all(np.abs(y.astype(np.float64) - y64) <= 1e-5 * np.abs(y64) + 1e-30)
 
 
-@pytest.mark.parametrize("shape", [0, 4])
+@pytest.mark.parametrize("mode", ["pull", "gather", "gather_hot"])
 @pytest.mark.parametrize("world", [1, 3, 4])
-def test_fused_spmv_partitions_one_process(orc, world, shape):
+def test_fused_spmv_partitions_one_process(orc, world, mode):
     """world row blocks; x entry i lives on block i // R (R a power of two
-    for world 1 / 4, not for 3: the shift and the division paths); stream
-    shape 0 (default) and 4 (hot-column x cache filled from the owners)."""
+    for world 1 / 4, not for 3: the shift and the division paths; R % 4 != 0
+    for world 3: the pull's scalar path).  Modes: the in-kernel pull of the
+    owners' slices (default), per-gather peer reads, and per-gather reads
+    behind shape 4's hot-column cache (filled from the owners)."""
     g = full_matrix()
     n = g.n
     R = (n + world - 1) // world
@@ -64,7 +66,8 @@ def test_fused_spmv_partitions_one_process(orc, world, shape):
             yd = ctx.alloc(4 * max(1, r1 - r0))
             bufs.append(yd)
             cfg = dpc.launch_cfg("spmv", "grid")
-            cfg.flags |= shape << 20
+            if mode != "pull":
+                cfg.flags |= dpc.CFG_X_PEER_GATHER | ((4 << 20) if mode == "gather_hot" else 0)
             dg.spmv_fused(tab, world, R, yd, cfg=cfg)
             y = ctx.d2h(yd, r1 - r0)
             assert close(y, y64[r0:r1]), f"rank {p}"
