@@ -1218,7 +1218,10 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
   if (a.xpull) {
     // fused multi-GPU pull: every owner's x slice into the local x with
     // coalesced 16-byte peer reads (NVLink), overlapping the insert phase's
-    // tail; the barrier below orders it before the drain's gathers
+    // tail; the barrier below orders it before the drain's gathers.  Nothing
+    // reads the local x before that barrier in fused mode (threshold 0: no
+    // inline rows; the hot-column fill reads the owners), so no SM holds a
+    // stale line of it when the drain's read-only (__ldg) gathers start.
     const unsigned nx = a.ncols, stride = GB * NT;
     if ((a.rows & 3u) == 0) {
       for (unsigned i = blockIdx.x * NT + threadIdx.x; 4 * i < nx; i += stride) {
