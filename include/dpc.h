@@ -194,8 +194,14 @@ typedef struct dpc_launch_cfg {
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */
 
-/* Fills the measured default for (app, variant) (configs/launch_cfg.json,
- * compiled in).  Replaces resolve_config, transform.hpp:417-475. */
+/* Bits 8-31 of dpc_launch_cfg.flags select measured alternative kernel
+ * shapes of the same computation (stream drain shapes, GC server bounds,
+ * ...): every value gives the same results.  Timing probes
+ * that skip work are compiled out of the library. */
+
+/* Fills the measured default for (app, variant) (profiles/r02_launch_cfg.json,
+ * compiled in as paper_1606_08150_b200/csrc/launch_table.inc).  Replaces
+ * resolve_config, transform.hpp:417-475. */
 dpc_status dpc_launch_cfg_default(int32_t app, int32_t variant, dpc_launch_cfg* cfg);
 
 /* ---- metrics (Metrics, sim.hpp:34-47) ---------------------------------- */
@@ -436,8 +442,12 @@ dpc_status dpc_multi_sssp(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, int64
  *                     queued for owner q (host array of `world` entries)
  *   dpc_msssp_send_buffer(q) : device pointer to those pairs
  *                     ({uint32 global vertex, uint32 distance} each)
- *   dpc_msssp_recv_buffer : device scratch large enough for every pair
- *                     this rank can receive in one iteration
+ *   dpc_msssp_recv_buffer : device receive area; it holds
+ *                     dpc_msssp_recv_capacity pairs (world x local edges
+ *                     at begin).  A rank can receive more than that (its
+ *                     peers' edge counts bound what they send), so callers
+ *                     that know the incoming count call
+ *                     dpc_msssp_recv_reserve, which grows the area
  *   dpc_msssp_send_counts : device copy of send_counts (for collectives)
  *   dpc_msssp_apply : apply `count` received pairs (device pointer), close
  *                     the iteration; *next_fsize = local |F_it+1|
@@ -447,6 +457,8 @@ dpc_status dpc_msssp_begin(dpc_ctx* ctx, dpc_dgraph* local, int64_t r0, int64_t 
 dpc_status dpc_msssp_relax(dpc_ctx* ctx, dpc_dgraph* local, uint32_t* send_counts);
 const void* dpc_msssp_send_buffer(dpc_dgraph* local, int32_t owner);
 void* dpc_msssp_recv_buffer(dpc_dgraph* local);
+uint64_t dpc_msssp_recv_capacity(dpc_dgraph* local);
+dpc_status dpc_msssp_recv_reserve(dpc_ctx* ctx, dpc_dgraph* local, uint64_t pairs, void** d_out);
 const uint32_t* dpc_msssp_send_counts(dpc_dgraph* local);
 dpc_status dpc_msssp_apply(dpc_ctx* ctx, dpc_dgraph* local, const void* d_pairs, uint64_t count,
                            uint32_t* next_fsize);

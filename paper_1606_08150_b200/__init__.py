@@ -197,6 +197,8 @@ _SIGS = {
     "dpc_msssp_relax": (C.c_int, [_P, _P, _P]),
     "dpc_msssp_send_buffer": (_P, [_P, _i32]),
     "dpc_msssp_recv_buffer": (_P, [_P]),
+    "dpc_msssp_recv_capacity": (C.c_uint64, [_P]),
+    "dpc_msssp_recv_reserve": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_void_p)]),
     "dpc_msssp_send_counts": (_P, [_P]),
     "dpc_msssp_apply": (C.c_int, [_P, _P, _P, _u64, C.POINTER(_u32)]),
     "dpc_msssp_end": (C.c_int, [_P, _P, C.POINTER(Metrics)]),
@@ -675,7 +677,9 @@ class PartitionedSSSP:
 
     def apply(self, pairs: np.ndarray) -> int:
         pairs = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
-        buf = _lib.dpc_msssp_recv_buffer(self.g._h)
+        pbuf = C.c_void_p()
+        _check(_lib.dpc_msssp_recv_reserve(self.ctx.handle, self.g._h, len(pairs), C.byref(pbuf)))
+        buf = pbuf.value
         if len(pairs):
             _check(_lib.dpc_copy_h2d(self.ctx.handle, buf, _ptr(pairs), pairs.nbytes))
         nxt = _u32()

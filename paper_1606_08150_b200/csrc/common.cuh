@@ -219,11 +219,19 @@ __device__ __forceinline__ bool grid_last_block(unsigned* ticket) {
   return s_last;
 }
 
+// Fault bit of a device-wide barrier that timed out (RunHeader.overflow):
+// reported as DPC_E_DEADLOCK, the reference's deadlock fault (sim.hpp:946-955).
+constexpr unsigned kFaultBarrier = 16u;
+
 // Device-wide barrier for a grid whose blocks are all co-resident (checked
 // by the host with the occupancy calculator before a normal launch): the
 // paper's custom global barrier without the cooperative
 // launch's extra setup cost.  `count` is zero at kernel start and used once.
-__device__ __forceinline__ void soft_grid_barrier(unsigned* count) {
+// If the grid is not co-resident after all (another context on the GPU, MPS)
+// the watchdog fires after 2 s: the block proceeds so the device never hangs,
+// and the run is marked failed (kFaultBarrier in *fault) -- its result is
+// never reported as valid.
+__device__ __forceinline__ void soft_grid_barrier(unsigned* count, unsigned* fault) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -233,7 +241,10 @@ __device__ __forceinline__ void soft_grid_barrier(unsigned* count) {
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(count) : "memory");
       if (seen < gridDim.x) __nanosleep(20);
-      if (global_ns() - t0 > 2000000000ull) break;  // watchdog: never hang the device
+      if (global_ns() - t0 > 2000000000ull) {  // watchdog: never hang the device
+        atomicOr(fault, kFaultBarrier);
+        break;
+      }
     } while (seen < gridDim.x);
   }
   __syncthreads();

@@ -125,9 +125,24 @@ dpc_status check_header(const RunHeader* h) {
                                 cudaGetErrorString(static_cast<cudaError_t>(h->aux0)));
   if (h->overflow & 8u)
     return fail(DPC_E_INVALID, "coloring needs a symmetric graph (the worklist drained with uncolored vertices)");
+  if (h->overflow & dpc::dev::kFaultBarrier)
+    return fail(DPC_E_DEADLOCK, "device-wide barrier timed out after 2 s (the grid was not co-resident: "
+                                "another context or MPS client on the GPU?)");
   if (h->overflow & 4u) return fail(DPC_E_DEADLOCK, "worklist made no progress for 2 s (lost task)");
   if (h->overflow & 1u) return fail(DPC_E_OVERFLOW, "consolidation pool overflow");
   return DPC_OK;
+}
+
+dpc_status flush_check(dpc_ctx* ctx, dpc_dgraph* g) {
+  if (!g->check_pending) return DPC_OK;
+  g->check_pending = false;
+  if (!g->hdr_copied)
+    DPC_CUDA(cudaMemcpyAsync(g->hdr_host, g->hdr, sizeof(RunHeader), cudaMemcpyDeviceToHost, ctx->stream));
+  g->hdr_copied = false;
+  DPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  const dpc_status st = check_header(g->hdr_host);
+  if (st != DPC_OK) g->hdr_clean = false;  // the next run re-zeroes the header
+  return st;
 }
 
 dpc_status begin_run(dpc_ctx* ctx, RunHeader* hdr) {
@@ -408,7 +423,7 @@ dpc_status dpc_spmv_host(dpc_ctx* c, dpc_dgraph* g, const float* x, float* y,
   if (st != DPC_OK) return st;
   DPC_CUDA(cudaMemcpyAsync(y, g->y, ybytes, cudaMemcpyDeviceToHost, c->stream));
   DPC_CUDA(cudaStreamSynchronize(c->stream));
-  return DPC_OK;
+  return flush_check(c, g);  // a device-side fault voids y
 }
 
 // Pipelined host-vector SpMV over `count` independent vectors (serving
@@ -464,7 +479,7 @@ dpc_status dpc_spmv_host_batch(dpc_ctx* c, dpc_dgraph* g, const float* const* xs
   DPC_CUDA(cudaEventRecord(e[8], c->d2h));
   DPC_CUDA(cudaStreamWaitEvent(c->stream, e[8], 0));
   DPC_CUDA(cudaStreamSynchronize(c->d2h));
-  return DPC_OK;
+  return flush_check(c, g);  // a device-side fault of any vector voids the batch
 }
 
 dpc_status dpc_run_spmv(dpc_ctx* c, const dpc_csr* A, const float* x, float* y,
@@ -493,6 +508,7 @@ dpc_status dpc_run_sssp(dpc_ctx* c, const dpc_csr* G, int32_t source, uint32_t* 
   if (st != DPC_OK) return st;
   if (met) std::memset(met, 0, sizeof(*met));
   st = dpc_sssp_device(c, g, source, cfg, met);
+  if (st == DPC_OK) st = flush_check(c, g);  // asynchronous run: its fault check
   if (st == DPC_OK) st = dpc_copy_d2h(c, dist, g->dist, sizeof(unsigned) * static_cast<size_t>(G->n));
   dpc_dgraph_free(g);
   return st;
@@ -507,6 +523,7 @@ dpc_status dpc_run_bfs(dpc_ctx* c, const dpc_csr* G, int32_t source, uint32_t* l
   if (st != DPC_OK) return st;
   if (met) std::memset(met, 0, sizeof(*met));
   st = dpc_bfs_device(c, g, source, cfg, met);
+  if (st == DPC_OK) st = flush_check(c, g);
   if (st == DPC_OK) st = dpc_copy_d2h(c, level, g->dist, sizeof(unsigned) * static_cast<size_t>(G->n));
   dpc_dgraph_free(g);
   return st;
@@ -523,6 +540,7 @@ dpc_status dpc_run_color(dpc_ctx* c, const dpc_csr* G, uint64_t seed, int32_t* c
   dpc_metrics* mp = met ? met : &local;
   std::memset(mp, 0, sizeof(*mp));
   st = dpc_color_device(c, g, seed, cfg, mp);
+  if (st == DPC_OK) st = flush_check(c, g);
   if (st == DPC_OK) st = dpc_copy_d2h(c, color, g->color, sizeof(int) * static_cast<size_t>(G->n));
   if (st == DPC_OK) {
     // Jones-Plassmann counts down higher-priority neighbours through the
@@ -548,6 +566,7 @@ static dpc_status run_tree(dpc_ctx* c, const dpc_tree* t, int which, int32_t* ou
   if (st != DPC_OK) return st;
   if (met) std::memset(met, 0, sizeof(*met));
   st = dpc_tree_device(c, d, which, cfg, met);
+  if (st == DPC_OK) st = dpc_dtree_check(c, d);  // asynchronous run: its fault check
   if (st == DPC_OK) st = dpc_copy_d2h(c, out, d->result, sizeof(int) * static_cast<size_t>(t->n));
   dpc_dtree_free(d);
   return st;

@@ -61,7 +61,8 @@ struct dpc_dgraph {
   dpc::dev::RunHeader* hdr = nullptr;  // device counters
   dpc::dev::RunHeader* hdr_host = nullptr;  // pinned mirror
   bool hdr_clean = false;  // the last run (SpMV stream) left the header zeroed itself
-  bool check_pending = false;  // an asynchronous run's header copy awaits its fault check
+  bool check_pending = false;  // an asynchronous run awaits its fault check
+  bool hdr_copied = false;     // ... and its header copy is already enqueued
   float* x2 = nullptr;     // second x / y slot of the pipelined host-vector path
   float* y2 = nullptr;
   // consolidation pool
@@ -79,6 +80,7 @@ struct dpc_dgraph {
   void* ms_recv = nullptr;
   unsigned* ms_cnt = nullptr;
   size_t ms_n = 0, ms_cap = 0;
+  size_t ms_rcap = 0;  // pairs the receive area holds (grown by dpc_msssp_recv_reserve)
   void* ms_state = nullptr;
   int* xhot_col = nullptr;
   float* xhot_val = nullptr;
@@ -151,6 +153,17 @@ dpc_status ensure_pending_for(dpc_ctx* ctx, dpc_dgraph* g, int variant, unsigned
 dpc_status ensure_pool(dpc_dgraph* g, uint64_t need);
 
 dpc_status begin_run(dpc_ctx* ctx, dpc::dev::RunHeader* hdr);
+// Reports the fault of the graph's last asynchronous run (one launched
+// without metrics), if any: synchronises, reads its header (copied by the
+// run or here) and maps the fault bits.  Every graph entry point calls it
+// first, so a fault is never lost behind a later run (dpc.h: dpc_dgraph_check).
+dpc_status flush_check(dpc_ctx* ctx, dpc_dgraph* g);
+// Marks a run launched without metrics whose header is NOT copied back:
+// flush_check will copy it.
+inline void defer_check(dpc_dgraph* g) {
+  g->check_pending = true;
+  g->hdr_copied = false;
+}
 // Frees the partitioned-SSSP step state of a graph (sssp.cu).
 void sssp_state_free(void* state);
 // Maps the device-side fault bits of a run header to a status + message.

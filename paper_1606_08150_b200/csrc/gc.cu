@@ -1113,8 +1113,10 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   clear_error();
   if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
   if (g->ncols != g->n) return fail(DPC_E_INVALID, "coloring needs a square graph (not a row slice)");
+  dpc_status st = flush_check(ctx, g);
+  if (st != DPC_OK) return st;
   Cfg c;
-  dpc_status st = resolve_cfg(ctx, DPC_APP_COLOR, cfg, &c);
+  st = resolve_cfg(ctx, DPC_APP_COLOR, cfg, &c);
   if (st != DPC_OK) return st;
   if (c.parent_threads != 256 || c.child_threads != 256)
     return fail(DPC_E_INVALID, "GC kernels are built for parent_threads = child_threads = 256");

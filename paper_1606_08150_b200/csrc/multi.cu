@@ -135,7 +135,6 @@ dpc_status dpc_multi_sssp(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, int64
   dpc_status st = dpc_msssp_begin(ctx, local, me * R, R, n_global, P, source, cfg);
   if (st != DPC_OK) return st;
   std::vector<uint32_t> sc(static_cast<size_t>(P));
-  uint2* recv = static_cast<uint2*>(dpc_msssp_recv_buffer(local));
   for (int64_t it = 0; it <= n_global; it++) {
     st = dpc_msssp_relax(ctx, local, sc.data());
     if (st != DPC_OK) return st;
@@ -144,6 +143,15 @@ dpc_status dpc_multi_sssp(dpc_ctx* ctx, dpc_comm* comm, dpc_dgraph* local, int64
                            comm->nccl, s));
     DPC_CUDA(cudaMemcpyAsync(comm->h_counts, comm->d_counts, sizeof(unsigned) * P * P, cudaMemcpyDeviceToHost, s));
     DPC_CUDA(cudaStreamSynchronize(s));
+    // the receive area must hold what every peer queued for this rank
+    // (bounded by the peers' edge counts, not this rank's)
+    uint64_t incoming = 0;
+    for (int q = 0; q < P; q++)
+      if (q != me) incoming += comm->h_counts[q * P + me];
+    void* rbuf = nullptr;
+    st = dpc_msssp_recv_reserve(ctx, local, incoming, &rbuf);
+    if (st != DPC_OK) return st;
+    uint2* recv = static_cast<uint2*>(rbuf);
     uint64_t total = 0;
     DPC_NCCL(ncclGroupStart());
     for (int q = 0; q < P; q++) {

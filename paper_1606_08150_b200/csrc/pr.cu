@@ -154,7 +154,8 @@ dpc_status dpc_pr_device(dpc_ctx* ctx, dpc_prgraph* h, int32_t iters, double dam
     pr::update_kernel<<<gb, 256, 0, s>>>(pt->x, pt->y, n, damping, h->dmass, h->dflag, it);
     DPC_CUDA(cudaGetLastError());
   }
-  if (met) met->host_launches += 1 + 2 * static_cast<int64_t>(iters);
+  // the SpMV calls counted their own launch; here: init + one update per iteration
+  if (met) met->host_launches += 1 + static_cast<int64_t>(iters);
   return DPC_OK;
 }
 
@@ -167,6 +168,7 @@ dpc_status dpc_run_pagerank(dpc_ctx* ctx, const dpc_csr* G, int32_t iters, doubl
   if (st != DPC_OK) return st;
   if (met) std::memset(met, 0, sizeof(*met));
   st = dpc_pr_device(ctx, h, iters, damping, cfg, met);
+  if (st == DPC_OK) st = flush_check(ctx, h->pt);  // asynchronous SpMV runs: their fault check
   if (st == DPC_OK && G->n > 0) st = dpc_copy_d2h(ctx, rank, h->pt->x, sizeof(float) * static_cast<size_t>(G->n));
   dpc_pr_free(h);
   return st;

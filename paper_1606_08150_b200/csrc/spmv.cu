@@ -37,6 +37,15 @@ using dev::kFull;
 using dev::Pool;
 using dev::RunHeader;
 
+// Timing probes that skip or fake part of the work (wrong results by design:
+// no drain, no y store, synthetic columns, confined gathers, parent-only
+// phases) exist only in a probe build (-DDPC_TIMING_PROBES=1); the product
+// library compiles them out, so no dpc_launch_cfg.flags value reaches them.
+#ifndef DPC_TIMING_PROBES
+#define DPC_TIMING_PROBES 0
+#endif
+constexpr bool kProbes = DPC_TIMING_PROBES != 0;
+
 // Resident 256-thread blocks per SM requested from ptxas for the drain
 // kernels (latency-bound gathers want warps in flight: 8 -> 64 warps/SM).
 #ifndef DPC_SPMV_MIN_BLOCKS
@@ -73,6 +82,12 @@ __device__ __forceinline__ float peer_x(const Args& a, unsigned idx) {
   const unsigned o = a.rshift != ~0u ? idx >> a.rshift : idx / a.rows;
   const unsigned l = a.rshift != ~0u ? idx & (a.rows - 1u) : idx - o * a.rows;
   return __ldg(a.xpeer[o] + l);
+}
+
+__device__ __forceinline__ float ld_weak_f(const float* p) {
+  float r;
+  asm volatile("ld.global.ca.f32 %0, [%1];" : "=f"(r) : "l"(p) : "memory");
+  return r;
 }
 
 __device__ __forceinline__ int4 ldg_stream(const int4* p) {
@@ -727,7 +742,7 @@ template <int G>
 __device__ __forceinline__ void grp_load(const Args& a, unsigned k, Grp<G>& g) {
 #pragma unroll
   for (int i = 0; i < G / 4; i++) {
-    if (a.xflags & 32u) {  // probe: no col/val traffic (synthetic columns)
+    if (kProbes && (a.xflags & 32u)) {  // probe: no col/val traffic (synthetic columns)
       const int cs = static_cast<int>(((k + 4 * i) * 2654435761u) & 0xfffffu);
       g.c[i] = make_int4(cs, cs ^ 1, cs ^ 2, cs ^ 3);
       g.w[i] = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -752,8 +767,8 @@ __device__ __forceinline__ float grp_dot(const Args& a, const Grp<G>& g, unsigne
     for (int e = 0; e < 4; e++) {
       const bool on = (m >> (4 * i + e)) & 1u;
       int idx = on ? cp[e] : 0;
-      if (a.xflags & 64u) idx &= 1023;      // probe: gathers confined to 4 KB of x
-      if (a.xflags & 128u) idx &= 0xffff;   // probe: gathers confined to 256 KB of x
+      if (kProbes && (a.xflags & 64u)) idx &= 1023;      // probe: gathers confined to 4 KB of x
+      if (kProbes && (a.xflags & 128u)) idx &= 0xffff;   // probe: gathers confined to 256 KB of x
       const float wt = on ? wp[e] : 0.f;
       float xv;
       if (SLOG > 0) {  // hot-column cache, misses to x (or the owner's x slice)
@@ -763,7 +778,12 @@ __device__ __forceinline__ float grp_dot(const Args& a, const Grp<G>& g, unsigne
                                                : __ldg(a.x + idx);
       } else if (a.xpeer && !a.xpull) {
         xv = peer_x(a, static_cast<unsigned>(idx));
-      } else if (a.xflags & 16u) {
+      } else if (a.xpull) {
+        // x was written by this kernel (the pull before the barrier): .nc
+        // loads are only defined for data read-only for the whole kernel, so
+        // a plain (weak, L1-cached) load, ordered by the barrier's acquire
+        xv = ld_weak_f(a.x + idx);
+      } else if (kProbes && (a.xflags & 16u)) {
         xv = 1.f;
       } else if (a.xflags & 256u) {
         xv = __ldcg(a.x + idx);  // probe: x gathers through L2 only
@@ -795,7 +815,7 @@ __device__ __forceinline__ void stream_insert(const Args& a, const Stream& st, u
     atomicOr(&a.hdr->overflow, 1u);
     return;
   }
-  if (!(a.xflags & 4u)) {
+  if (!kProbes || !(a.xflags & 4u)) {
     a.pool.items[slot] = Item{row, b};
     st.seg[slot] = make_uint2(static_cast<unsigned>(at & kNnzMask), e);
   }
@@ -1204,7 +1224,7 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
       const unsigned ball = __ballot_sync(kFull, cons);
       float sl = 0.f;
       if (INLINE) sl = warp_light_rows(a, b, in && !cons ? e - b : 0u);
-      if (in && !(a.xflags & 8u)) a.y[r] = cons ? 0.f : sl;
+      if (in && (!kProbes || !(a.xflags & 8u))) a.y[r] = cons ? 0.f : sl;
       if (cons) {
         const unsigned len = stream_len<G>(b, e);
         const unsigned long long at = base + s_w[k * NW + wib] +
@@ -1218,10 +1238,9 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
   if (a.xpull) {
     // fused multi-GPU pull: every owner's x slice into the local x with
     // coalesced 16-byte peer reads (NVLink), overlapping the insert phase's
-    // tail; the barrier below orders it before the drain's gathers.  Nothing
-    // reads the local x before that barrier in fused mode (threshold 0: no
-    // inline rows; the hot-column fill reads the owners), so no SM holds a
-    // stale line of it when the drain's read-only (__ldg) gathers start.
+    // tail; the barrier below orders it before the drain's gathers, which
+    // read the pulled x with plain weak loads (the barrier's acquire makes
+    // them see it), not through the read-only (.nc) path.
     const unsigned nx = a.ncols, stride = GB * NT;
     if ((a.rows & 3u) == 0) {
       for (unsigned i = blockIdx.x * NT + threadIdx.x; 4 * i < nx; i += stride) {
@@ -1243,7 +1262,7 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
     }
   }
   if (a.coop) cg::this_grid().sync();
-  else dev::soft_grid_barrier(&a.hdr->ticket);
+  else dev::soft_grid_barrier(&a.hdr->ticket, &a.hdr->overflow);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->t[1] = dev::global_ns();
   if (SLOG > 0) {
     for (unsigned i = threadIdx.x; i < (1u << SLOG); i += NT)
@@ -1257,17 +1276,18 @@ __global__ void __launch_bounds__(NT, MINB) grid_stream(Args a, Stream st) {
   const unsigned long long per = ((static_cast<unsigned long long>(total) + nw - 1) / nw + kWin - 1) /
                                  kWin * kWin;
   const unsigned long long s0 = static_cast<unsigned long long>(gw) * per;
-  if (ni > 0 && s0 < total && !(a.xflags & 1u) && PIPE == 2)
+  const bool drain_on = !kProbes || !(a.xflags & 1u);
+  if (ni > 0 && s0 < total && drain_on && PIPE == 2)
     stream_drain_cp<G, V, KB, SLOG>(a, st, ni, static_cast<unsigned>(s0),
                                     static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
                                     s_items + wib * KB, s_cache,
                                     reinterpret_cast<int4*>(s_dyn + NW * KB + (SLOG ? (1u << SLOG) / 2 : 0)) +
                                         wib * (2 * V * 32 * (G / 4) * 2));
-  else if (ni > 0 && s0 < total && !(a.xflags & 1u) && PIPE == 1)
+  else if (ni > 0 && s0 < total && drain_on && PIPE == 1)
     stream_drain_pipe<G, V, KB, SLOG>(a, st, ni, static_cast<unsigned>(s0),
                                       static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
                                       s_items + wib * KB, s_cache);
-  else if (ni > 0 && s0 < total && !(a.xflags & 1u))
+  else if (ni > 0 && s0 < total && drain_on)
     stream_drain<G, V, KB, SLOG>(a, st, ni, static_cast<unsigned>(s0),
                               static_cast<unsigned>(min(static_cast<unsigned long long>(total), s0 + per)),
                               s_items + wib * KB, s_cache);
@@ -1352,8 +1372,10 @@ using PersistentFn = void (*)(Args);
 // [LM][DM][MB == 8]
 static PersistentFn persistent_fn(unsigned flags) {
   const bool serial = flags & (1u << 8), warp_drain = flags & (1u << 9), low_occ = flags & (1u << 10);
+#if DPC_TIMING_PROBES
   if (flags & (1u << 16)) return grid_persistent<3, 1, 8>;
   if (flags & (1u << 17)) return grid_persistent<4, 1, 8>;
+#endif
   if (flags & (1u << 14)) return low_occ ? grid_persistent<1, 3, 4> : grid_persistent<1, 3, 8>;
   if (flags & (1u << 15)) return low_occ ? grid_persistent<1, 4, 4> : grid_persistent<1, 4, 8>;
   if (flags & (1u << 11)) return low_occ ? grid_persistent<2, 2, 4> : grid_persistent<2, 2, 8>;
@@ -1547,8 +1569,11 @@ dpc_status dpc::spmv_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d
     // malloc that does not fit raises the overflow fault
   }
   // the stream kernel zeroes its header counters on exit (its last block),
-  // so back-to-back stream runs need no per-run memset
+  // so back-to-back stream runs need no per-run memset; their fault bits
+  // are sticky until a check reads them (flush_check)
   if (!(use_stream && g->hdr_clean && !met)) {
+    st = flush_check(ctx, g);  // the memset below would erase a pending fault
+    if (st != DPC_OK) return st;
     st = begin_run(ctx, g->hdr);
     if (st != DPC_OK) return st;
   }
@@ -1606,5 +1631,6 @@ dpc_status dpc::spmv_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d
     met->iterations += 1;
     return finish_metrics(ctx, g->hdr, g->hdr_host, met);
   }
+  defer_check(g);  // fault bits stay in the header until the next check
   return DPC_OK;
 }

@@ -861,13 +861,6 @@ static dpc_status sssp_iterate(dpc_ctx* ctx, const Cfg& c, sssp::Args& a, unsign
 // A run without metrics returns as soon as its work is enqueued (like the
 // SpMV path): its header is copied back asynchronously and checked for
 // faults at the next call on this graph (or dpc_dgraph_check).
-static dpc_status flush_check(dpc_ctx* ctx, dpc_dgraph* g) {
-  if (!g->check_pending) return DPC_OK;
-  g->check_pending = false;
-  DPC_CUDA(cudaStreamSynchronize(ctx->stream));
-  return check_header(g->hdr_host);
-}
-
 extern "C" dpc_status dpc_dgraph_check(dpc_ctx* ctx, dpc_dgraph* g) {
   clear_error();
   if (!ctx || !g) return fail(DPC_E_INVALID, "NULL argument");
@@ -888,6 +881,7 @@ static dpc_status sssp_finish(dpc_ctx* ctx, dpc_dgraph* g, int64_t host_launches
   }
   DPC_CUDA(cudaMemcpyAsync(g->hdr_host, g->hdr, sizeof(dev::RunHeader), cudaMemcpyDeviceToHost, s));
   g->check_pending = true;
+  g->hdr_copied = true;
   return DPC_OK;
 }
 
@@ -1054,6 +1048,10 @@ extern "C" dpc_status dpc_msssp_begin(dpc_ctx* ctx, dpc_dgraph* g, int64_t r0, i
       r0 % rows_per_rank != 0)
     return fail(DPC_E_INVALID, "bad partition: need r0 = rank * rows_per_rank, ncols = n_global");
   if (source < 0 || source >= n_global) return fail(DPC_E_INVALID, "source out of range");
+  {
+    const dpc_status pst = flush_check(ctx, g);
+    if (pst != DPC_OK) return pst;
+  }
   if (!g->ms_state) g->ms_state = new (std::nothrow) MsState();
   MsState* m = ms_state(g);
   if (!m) return fail(DPC_E_OOM, "state allocation failed");
@@ -1077,6 +1075,7 @@ extern "C" dpc_status dpc_msssp_begin(dpc_ctx* ctx, dpc_dgraph* g, int64_t r0, i
     DPC_CUDA(cudaMalloc(&g->ms_cnt, sizeof(unsigned) * 2 * 64));
     g->ms_n = static_cast<size_t>(n_global);
     g->ms_cap = need_send;
+    g->ms_rcap = need_send;
   }
   if (world > 64) return fail(DPC_E_INVALID, "world > 64");
   m->world = world;
@@ -1151,6 +1150,27 @@ extern "C" const void* dpc_msssp_send_buffer(dpc_dgraph* g, int32_t owner) {
 }
 
 extern "C" void* dpc_msssp_recv_buffer(dpc_dgraph* g) { return g ? g->ms_recv : nullptr; }
+
+extern "C" uint64_t dpc_msssp_recv_capacity(dpc_dgraph* g) { return g ? g->ms_rcap : 0; }
+
+// A rank receives at most what its peers queued for it, which is bounded by
+// the PEERS' local edge counts, not by its own: the receive area grows to
+// the count the caller learned from the exchange of send counts.
+extern "C" dpc_status dpc_msssp_recv_reserve(dpc_ctx* ctx, dpc_dgraph* g, uint64_t pairs, void** out) {
+  clear_error();
+  if (!ctx || !g || !out) return fail(DPC_E_INVALID, "NULL argument");
+  if (!ms_state(g)) return fail(DPC_E_INVALID, "dpc_msssp_begin was not called");
+  if (pairs > g->ms_rcap) {
+    DPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (g->ms_recv) cudaFree(g->ms_recv);
+    g->ms_recv = nullptr;
+    g->ms_rcap = 0;
+    DPC_CUDA(cudaMalloc(&g->ms_recv, sizeof(uint2) * static_cast<size_t>(pairs)));
+    g->ms_rcap = static_cast<size_t>(pairs);
+  }
+  *out = g->ms_recv;
+  return DPC_OK;
+}
 
 extern "C" const uint32_t* dpc_msssp_send_counts(dpc_dgraph* g) {
   MsState* m = g ? ms_state(g) : nullptr;
