@@ -721,24 +721,28 @@ def run_reference(args):
     except (FileNotFoundError, OSError) as e:
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
         return
-    import paper_1606_08150_b200 as dpc
-    g = dpc.gen_rmat(SCALE, EDGEFACTOR, seed=SEED, weights=False, values=True)
+    # the input is built by the oracle's own R-MAT restatement (oracle.c
+    # orc_gen_rmat, test-pinned equal to dpc_gen_rmat): this leg loads no
+    # product code, only oracle/liboracle.so and oracle/_ref/libref_sim.so
+    from tests._oracle import Oracle
+    g_rowptr, g_col, _, g_val = Oracle().gen_rmat(SCALE, EDGEFACTOR, seed=SEED, weights=False, values=True)
+    n_rows = len(g_rowptr) - 1
     rng = np.random.default_rng(SEED)
-    x = (rng.integers(1, 1 << 24, g.n) / float(1 << 24)).astype(np.float32)
+    x = (rng.integers(1, 1 << 24, n_rows) / float(1 << 24)).astype(np.float32)
     src = ref.kdl("spmv.kdl")
     # bounded, representative sample: a seeded uniform random 1/k of the rows
     # (keeps the degree distribution; R-MAT ids are not exchangeable, so a
     # strided or contiguous window would be biased), k = args.ref_stride
-    sel = np.sort(np.random.default_rng(SEED).choice(g.n, g.n // args.ref_stride, replace=False))
+    sel = np.sort(np.random.default_rng(SEED).choice(n_rows, n_rows // args.ref_stride, replace=False))
     rows = len(sel)
-    deg = (g.rowptr[sel + 1] - g.rowptr[sel]).astype(np.int64)
+    deg = (g_rowptr[sel + 1] - g_rowptr[sel]).astype(np.int64)
     rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
     nnz = int(rp[-1])
-    idx = np.concatenate([np.arange(g.rowptr[r], g.rowptr[r + 1]) for r in sel])
-    col = g.col[idx]
-    val = g.val[idx].astype(np.float64)
+    idx = np.concatenate([np.arange(g_rowptr[r], g_rowptr[r + 1]) for r in sel])
+    col = g_col[idx]
+    val = g_val[idx].astype(np.float64)
     # columns index the full x; the sample keeps the full vector
-    scal = {"n": rows, "m": nnz, "nx": g.n, "thr": 32}
+    scal = {"n": rows, "m": nnz, "nx": n_rows, "thr": 32}
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -763,8 +767,11 @@ def run_reference(args):
         "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "BASELINE config 2 (row sample): SpMV CSR R-MAT scale-20",
-                   "rows": rows, "nnz": nnz},
+        "config": {"workload": f"BASELINE config 2, row sample: a seeded random 1/{args.ref_stride} of the rows of "
+                               "the SpMV CSR R-MAT scale-20 matrix (GTEPS is per nonzero, so the rate is "
+                               "comparable; the sample is not the whole matrix)",
+                   "rows": rows, "nnz": nnz, "same_config": False,
+                   "input": "oracle/oracle.c orc_gen_rmat (no product library loaded)"},
         "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

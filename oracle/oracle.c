@@ -2,6 +2,7 @@
  * reference's sequential oracles for the hot-path apps. */
 #include "oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 #include <pthread.h>
@@ -390,4 +391,94 @@ int orc_pagerank(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t i
   }
   free(nxt);
   return 0;
+}
+
+/* ---------------- R-MAT generator --------------------- */
+/* Independent restatement of the synthetic R-MAT graph the product generates
+ * ("R-MAT (a,b,c,d); duplicates and self loops kept"), drawn from
+ * the same counter hash so both sides produce the same graph: arc e descends
+ * `scale` quadrant levels, each consuming 16 bits of
+ * mix64(mix64(seed ^ STREAM_RMAT) ^ (e*8 + level/4)); a level picks the
+ * source bit (u >= a+b) and the destination bit (a <= u < a+b or u >= a+b+c)
+ * with the probabilities quantised to 1/65536.  Optional vertex permutation
+ * (Fisher-Yates from the top, j = draw(PERM, i) mod (i+1)).  Rows list their
+ * arcs in (dst, arc id) order; weights = wmin + draw(WEIGHT, e) mod range,
+ * values = ((draw(VALUE, e) >> 40) + 1) / 2^24.  Directed only.  Used by the
+ * reference arm of bench.py so that leg builds its input without libdpc.so,
+ * and by tests/test_oracle.py to check the product generator. */
+#define ORC_STREAM_RMAT 0x1000000000000000ull
+#define ORC_STREAM_WEIGHT 0x2000000000000000ull
+#define ORC_STREAM_VALUE 0x3000000000000000ull
+#define ORC_STREAM_PERM 0x4000000000000000ull
+
+static inline uint64_t orc_draw(uint64_t seed, uint64_t stream, uint64_t ctr) {
+  return orc_mix64(orc_mix64(seed ^ stream) ^ ctr);
+}
+
+static int key_cmp(const void* a, const void* b) {
+  uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+int orc_gen_rmat(int scale, int edgefactor, double a, double b, double c, int32_t wmin, int32_t wmax,
+                 uint64_t seed, int permute, int64_t* rowptr, int32_t* col, int32_t* w, float* val) {
+  const int64_t n = (int64_t)1 << scale, m = n * edgefactor;
+  const uint32_t ta = (uint32_t)llround(a * 65536.0), tb = (uint32_t)llround((a + b) * 65536.0),
+                 tc = (uint32_t)llround((a + b + c) * 65536.0);
+  uint32_t* perm = NULL;
+  uint32_t* src = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(m ? m : 1));
+  uint64_t* key = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(m ? m : 1));
+  if (!src || !key) goto oom;
+  if (permute) {
+    perm = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n);
+    if (!perm) goto oom;
+    for (int64_t i = 0; i < n; i++) perm[i] = (uint32_t)i;
+    for (int64_t i = n - 1; i > 0; i--) {
+      uint64_t j = orc_draw(seed, ORC_STREAM_PERM, (uint64_t)i) % (uint64_t)(i + 1);
+      uint32_t t = perm[i];
+      perm[i] = perm[j], perm[j] = t;
+    }
+  }
+  for (int64_t i = 0; i <= n; i++) rowptr[i] = 0;
+  for (int64_t e = 0; e < m; e++) {
+    uint32_t s = 0, d = 0;
+    uint64_t h = 0;
+    for (int lv = 0; lv < scale; lv++) {
+      if ((lv & 3) == 0) h = orc_draw(seed, ORC_STREAM_RMAT, (uint64_t)e * 8 + (uint64_t)(lv / 4));
+      uint32_t u = (uint32_t)(h >> (16 * (lv & 3))) & 0xffffu;
+      s = (s << 1) | (u >= tb);
+      d = (d << 1) | ((u >= ta && u < tb) || u >= tc);
+    }
+    if (perm) s = perm[s], d = perm[d];
+    src[e] = s;
+    key[e] = ((uint64_t)d << 32) | (uint64_t)e;
+    rowptr[s + 1]++;
+  }
+  for (int64_t i = 0; i < n; i++) rowptr[i + 1] += rowptr[i];
+  {
+    /* counting sort by source, then each row by (dst, arc id) */
+    int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    uint64_t* sorted = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(m ? m : 1));
+    if (!cur || !sorted) {
+      free(cur), free(sorted);
+      goto oom;
+    }
+    memcpy(cur, rowptr, sizeof(int64_t) * (size_t)n);
+    for (int64_t e = 0; e < m; e++) sorted[cur[src[e]]++] = key[e];
+    for (int64_t i = 0; i < n; i++)
+      qsort(sorted + rowptr[i], (size_t)(rowptr[i + 1] - rowptr[i]), sizeof(uint64_t), key_cmp);
+    const uint64_t wr = (uint64_t)((int64_t)wmax - wmin + 1);
+    for (int64_t p = 0; p < m; p++) {
+      uint64_t e = sorted[p] & 0xffffffffull;
+      col[p] = (int32_t)(sorted[p] >> 32);
+      if (w) w[p] = wmin + (int32_t)(orc_draw(seed, ORC_STREAM_WEIGHT, e) % wr);
+      if (val) val[p] = (float)((orc_draw(seed, ORC_STREAM_VALUE, e) >> 40) + 1) * (1.0f / 16777216.0f);
+    }
+    free(cur), free(sorted);
+  }
+  free(perm), free(src), free(key);
+  return 0;
+oom:
+  free(perm), free(src), free(key);
+  return -1;
 }

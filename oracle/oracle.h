@@ -50,4 +50,9 @@ int orc_bfs(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t source
 /* PageRank: iters power iterations, damping d, fp64. */
 int orc_pagerank(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t iters, double d,
                  double* rank);
+/* Directed R-MAT graph, the same graph as dpc_gen_rmat for the
+ * same arguments: rowptr[2^scale + 1], col/w/val[2^scale * edgefactor]
+ * caller-allocated (w / val may be NULL).  0 on success, -1 on alloc failure. */
+int orc_gen_rmat(int scale, int edgefactor, double a, double b, double c, int32_t wmin, int32_t wmax,
+                 uint64_t seed, int permute, int64_t* rowptr, int32_t* col, int32_t* w, float* val);
 #endif

@@ -43,6 +43,9 @@ class Oracle:
         L.orc_color_valid.restype, L.orc_color_valid.argtypes = C.c_int, [i64, P, P, P, i32]
         L.orc_tree_desc.restype, L.orc_tree_desc.argtypes = C.c_int, [i64, P, P]
         L.orc_tree_height.restype, L.orc_tree_height.argtypes = C.c_int, [i64, P, P]
+        L.orc_gen_rmat.restype = C.c_int
+        L.orc_gen_rmat.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, i32, i32, u64,
+                                   C.c_int, P, P, P, P]
 
     def mix64(self, z):
         return self.L.orc_mix64(z & (2**64 - 1))
@@ -112,6 +115,23 @@ class Oracle:
         out = np.empty(len(parent), np.int32)
         assert self.L.orc_tree_height(len(parent), _p(parent), _p(out)) == 0
         return out
+
+    def gen_rmat(self, scale, edgefactor=16, a=0.57, b=0.19, c=0.19, wmin=1, wmax=255, seed=1,
+                 weights=True, values=False, permute=False):
+        """Directed R-MAT graph, the oracle's own restatement (oracle.c
+        orc_gen_rmat): same graph as dpc_gen_rmat for the same arguments.
+        Returns (rowptr int64, col int32, w int32 | None, val float32 | None)."""
+        n = 1 << scale
+        m = n * edgefactor
+        rowptr = np.empty(n + 1, np.int64)
+        col = np.empty(m, np.int32)
+        w = np.empty(m, np.int32) if weights else None
+        val = np.empty(m, np.float32) if values else None
+        rc = self.L.orc_gen_rmat(scale, edgefactor, a, b, c, wmin, wmax, seed & (2**64 - 1), int(permute),
+                                 _p(rowptr), _p(col), _p(w), _p(val))
+        if rc != 0:
+            raise MemoryError("orc_gen_rmat: allocation failed")
+        return rowptr, col, w, val
 
 
 MODES = {"basic": 0, "flat": 0, "warp": 1, "block": 2, "grid": 3}

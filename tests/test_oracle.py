@@ -152,3 +152,20 @@ def test_pagerank_oracle_known_answers(orc):
     g = dpc.csr_from_arrays([0, 0, 1, 2, 3], [0, 0, 0])        # leaves -> hub 0 (dangling)
     r = orc.pagerank(g.rowptr, g.col, 50)
     assert r[0] > r[1] and np.isclose(r.sum(), 1.0) and np.allclose(r[1:], r[1])
+
+
+@pytest.mark.parametrize("scale,permute,weights,values", [(10, False, True, False), (12, True, True, True),
+                                                          (14, False, False, True)])
+def test_oracle_rmat_equals_product_generator(orc, scale, permute, weights, values):
+    """The oracle's own R-MAT restatement (oracle.c orc_gen_rmat) and the
+    product generator (dpc_gen_rmat, host.cpp) build the same graph: the
+    reference arm of bench.py builds its input with the former."""
+    import paper_1606_08150_b200 as dpc
+    g = dpc.gen_rmat(scale, 16, seed=3, weights=weights, values=values, permute=permute)
+    rp, col, w, val = orc.gen_rmat(scale, 16, seed=3, weights=weights, values=values, permute=permute)
+    assert np.array_equal(g.rowptr, rp)
+    assert np.array_equal(g.col, col)
+    if weights:
+        assert np.array_equal(g.w, w)
+    if values:
+        assert np.array_equal(g.val, val)
