@@ -190,6 +190,11 @@ typedef struct dpc_launch_cfg {
                                     owners' x slices into the local x with coalesced
                                     peer reads, before the device-wide barrier it
                                     already has, then gathers locally) */
+#define DPC_CFG_GRID_STREAM 64 /* SSSP / BFS persistent grid variant: frontier
+                                  stream form -- each level's frontier edges
+                                  cut into equal per-warp slices, bitmap
+                                  dedup (sssp_stream.cu) -- instead of the
+                                  light-list + chunk-item level form */
 #define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */
@@ -215,6 +220,7 @@ typedef struct dpc_metrics {
   double device_ms;             /* CUDA-event time of the run's kernels      */
   int32_t overflow;             /* nonzero: a buffer overflowed              */
   int32_t result_count;         /* colors used (GC), reached vertices (SSSP) */
+  int64_t vertices_processed;   /* SSSP / BFS: sum of the frontier sizes     */
 } dpc_metrics;
 
 /* ---- context ------------------------------------------------------------ */

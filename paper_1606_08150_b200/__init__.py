@@ -58,6 +58,7 @@ CFG_GRID_CDP = 1
 CFG_GRID_CHUNKED = 2
 CFG_GRID_ASYNC = 8
 CFG_X_PEER_GATHER = 32
+CFG_GRID_STREAM = 64
 
 
 class DpcError(RuntimeError):
@@ -97,7 +98,8 @@ class Metrics(C.Structure):
     _fields_ = [("child_launch_count", C.c_int64), ("buffer_items_inserted", C.c_int64),
                 ("pool_peak", C.c_int64), ("iterations", C.c_int64),
                 ("edges_processed", C.c_int64), ("host_launches", C.c_int64),
-                ("device_ms", C.c_double), ("overflow", C.c_int32), ("result_count", C.c_int32)]
+                ("device_ms", C.c_double), ("overflow", C.c_int32), ("result_count", C.c_int32),
+                ("vertices_processed", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -428,6 +430,8 @@ def launch_cfg(app: str, variant: str, **overrides) -> LaunchCfg:
             cfg.flags = (cfg.flags | CFG_GRID_CHUNKED) if v else (cfg.flags & ~CFG_GRID_CHUNKED)
         elif k == "grid_async":
             cfg.flags = (cfg.flags | CFG_GRID_ASYNC) if v else (cfg.flags & ~CFG_GRID_ASYNC)
+        elif k == "grid_stream":
+            cfg.flags = (cfg.flags | CFG_GRID_STREAM) if v else (cfg.flags & ~CFG_GRID_STREAM)
         else:
             setattr(cfg, k, int(v))
     return cfg

@@ -327,7 +327,7 @@ void dpc_dgraph_free(dpc_dgraph* g) {
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
                   g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val,
                   g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt, g->gc_q, g->gc_hstate, g->trace, g->gc_hcol, g->gc_hsplit,
-                  g->x2, g->y2};
+                  g->x2, g->y2, g->sst_items};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->ms_state) dpc::sssp_state_free(g->ms_state);

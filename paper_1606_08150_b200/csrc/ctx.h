@@ -82,6 +82,8 @@ struct dpc_dgraph {
   size_t ms_n = 0, ms_cap = 0;
   size_t ms_rcap = 0;  // pairs the receive area holds (grown by dpc_msssp_recv_reserve)
   void* ms_state = nullptr;
+  void* sst_items = nullptr;  // SSSP frontier stream form: 2 x (n + 1) items
+  size_t sst_cap = 0;
   int* xhot_col = nullptr;
   float* xhot_val = nullptr;
   int xhot_log = 0;
@@ -166,6 +168,9 @@ inline void defer_check(dpc_dgraph* g) {
 }
 // Frees the partitioned-SSSP step state of a graph (sssp.cu).
 void sssp_state_free(void* state);
+// SSSP / BFS grid variant, frontier stream form (sssp_stream.cu).
+dpc_status sssp_stream_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, bool unit, bool coop,
+                           int64_t* host_launches, int64_t* levels, dpc_metrics* met);
 // Maps the device-side fault bits of a run header to a status + message.
 dpc_status check_header(const dpc::dev::RunHeader* h);
 dpc_status finish_metrics(dpc_ctx* ctx, dpc::dev::RunHeader* hdr, dpc::dev::RunHeader* hdr_host,

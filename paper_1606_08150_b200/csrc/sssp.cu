@@ -909,6 +909,18 @@ static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dp
     a.classify = 1;
     a.coop = (c.flags & DPC_CFG_COOP_LAUNCH) ? 1u : 0u;
   }
+  if (c.variant == DPC_GRID && c.grid_persistent && (c.flags & DPC_CFG_GRID_STREAM)) {
+    int64_t host_launches = 0, levels = 0;
+    st = sssp_stream_run(ctx, g, source, unit, (c.flags & DPC_CFG_COOP_LAUNCH) != 0, &host_launches, &levels,
+                         met);
+    if (st != DPC_OK) return st;
+    if (met) {  // edges_processed was filled by the stream form's own counters
+      met->host_launches += host_launches;
+      met->iterations += levels;
+      return finish_metrics(ctx, g->hdr, g->hdr_host, met);
+    }
+    return sssp_finish(ctx, g, host_launches, levels, nullptr);
+  }
   const unsigned nb = std::max(1u, dev::ceil_div(a.n, 256u));
   sssp::init_kernel<<<nb, 256, 0, s>>>(a, static_cast<unsigned>(source));
   DPC_CUDA(cudaGetLastError());
