@@ -190,11 +190,14 @@ typedef struct dpc_launch_cfg {
                                     owners' x slices into the local x with coalesced
                                     peer reads, before the device-wide barrier it
                                     already has, then gathers locally) */
-#define DPC_CFG_GRID_STREAM 64 /* SSSP / BFS persistent grid variant: frontier
-                                  stream form -- each level's frontier edges
-                                  cut into equal per-warp slices, bitmap
-                                  dedup (sssp_stream.cu) -- instead of the
-                                  light-list + chunk-item level form */
+#define DPC_CFG_GRID_STREAM 64 /* SSSP / BFS persistent grid variant: force the
+                                  frontier stream form -- each level's frontier
+                                  edges cut into equal per-warp slices, bitmap
+                                  dedup (sssp_stream.cu); default when the graph
+                                  has >= 2^24 edges (measured faster there) */
+#define DPC_CFG_GRID_LEVEL 128 /* SSSP / BFS persistent grid variant: force the
+                                  light-list + chunk-item level form (default
+                                  below 2^24 edges) */
 #define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */

@@ -59,6 +59,7 @@ CFG_GRID_CHUNKED = 2
 CFG_GRID_ASYNC = 8
 CFG_X_PEER_GATHER = 32
 CFG_GRID_STREAM = 64
+CFG_GRID_LEVEL = 128
 
 
 class DpcError(RuntimeError):
@@ -432,6 +433,8 @@ def launch_cfg(app: str, variant: str, **overrides) -> LaunchCfg:
             cfg.flags = (cfg.flags | CFG_GRID_ASYNC) if v else (cfg.flags & ~CFG_GRID_ASYNC)
         elif k == "grid_stream":
             cfg.flags = (cfg.flags | CFG_GRID_STREAM) if v else (cfg.flags & ~CFG_GRID_STREAM)
+        elif k == "grid_level":
+            cfg.flags = (cfg.flags | CFG_GRID_LEVEL) if v else (cfg.flags & ~CFG_GRID_LEVEL)
         else:
             setattr(cfg, k, int(v))
     return cfg

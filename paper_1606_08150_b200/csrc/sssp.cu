@@ -909,7 +909,13 @@ static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dp
     a.classify = 1;
     a.coop = (c.flags & DPC_CFG_COOP_LAUNCH) ? 1u : 0u;
   }
-  if (c.variant == DPC_GRID && c.grid_persistent && (c.flags & DPC_CFG_GRID_STREAM)) {
+  // frontier stream form: forced by DPC_CFG_GRID_STREAM, default from 2^24
+  // edges (tools/probes/sssp_forms.py: equal at scale 20, 1.6x at scale 22,
+  // 4.4x at scale 24 where dist and the level form's stamps outgrow L2)
+  const bool stream_form = c.variant == DPC_GRID && c.grid_persistent &&
+                           !(c.flags & (DPC_CFG_GRID_ASYNC | DPC_CFG_GRID_CHUNKED | DPC_CFG_GRID_LEVEL)) &&
+                           ((c.flags & DPC_CFG_GRID_STREAM) || g->m >= (int64_t{1} << 24));
+  if (stream_form) {
     int64_t host_launches = 0, levels = 0;
     st = sssp_stream_run(ctx, g, source, unit, (c.flags & DPC_CFG_COOP_LAUNCH) != 0, &host_launches, &levels,
                          met);

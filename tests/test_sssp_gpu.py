@@ -121,3 +121,74 @@ def test_async_runs_without_metrics(ctx, orc):
     dt.run("tree_desc", "grid", metrics=False)
     assert np.array_equal(dt.result(), orc.tree_desc(t.parent))
     dt.close()
+
+
+# ---- the frontier stream form of the grid variant (sssp_stream.cu) -------
+STREAM = dict(grid_stream=True)
+
+
+@pytest.mark.parametrize("scale,permute", [(6, False), (10, True), (12, False), (14, True)])
+def test_sssp_stream_form_rmat(ctx, orc, scale, permute):
+    g = dpc.gen_rmat(scale, 16, seed=scale + 7, permute=permute)
+    s = _source(g)
+    for coop in (False, True):
+        cfg = dpc.launch_cfg("sssp", "grid", **STREAM)
+        if coop:
+            cfg.flags |= 4  # DPC_CFG_COOP_LAUNCH
+        d, met = dpc.run_sssp(g, s, cfg=cfg, ctx=ctx)
+        assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, s))
+        assert met.child_launch_count == 0 and met.vertices_processed >= 1
+
+
+def test_sssp_stream_form_edge_cases(ctx, orc):
+    cfg = dpc.launch_cfg("sssp", "grid", **STREAM)
+    g = dpc.csr_from_arrays([0, 0], [], w=[])
+    d, _ = dpc.run_sssp(g, 0, cfg=cfg, ctx=ctx)
+    assert d.tolist() == [0]
+    g = dpc.csr_from_arrays([0, 3, 4, 4, 5], [0, 1, 1, 2, 3], w=[5, 0, 7, 1, 2])
+    d, _ = dpc.run_sssp(g, 0, cfg=cfg, ctx=ctx)
+    assert d.tolist() == [0, 0, 1, 2**32 - 1]
+    # a hub whose stream spans every warp, then a chain (one vertex per level)
+    n = 50_001
+    rowptr = np.concatenate([[0], np.full(n, n - 1)]).astype(np.int64)
+    col = np.arange(1, n, dtype=np.int32)
+    w = (np.arange(1, n) % 13 + 1).astype(np.int32)
+    g = dpc.csr_from_arrays(rowptr, col, w=w)
+    d, _ = dpc.run_sssp(g, 0, cfg=cfg, ctx=ctx)
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, 0))
+    chain = 3000
+    g = dpc.csr_from_arrays(np.arange(chain + 1).clip(0, chain - 1).astype(np.int64),
+                            np.arange(1, chain, dtype=np.int32), w=np.full(chain - 1, 3, np.int32))
+    d, met = dpc.run_sssp(g, 0, cfg=cfg, ctx=ctx)
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, 0))
+    assert met.iterations >= chain - 1
+
+
+@pytest.mark.parametrize("wmax", [0, 1, 20])
+def test_sssp_stream_form_powerlaw(ctx, orc, wmax):
+    g = dpc.gen_graph(6000, powerlaw=(1.5, 5000), seed=11, wmin=0, wmax=wmax)
+    d, _ = dpc.run_sssp(g, 0, cfg=dpc.launch_cfg("sssp", "grid", **STREAM), ctx=ctx)
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, 0))
+
+
+def test_bfs_stream_form(ctx, orc):
+    g = dpc.gen_rmat(13, 16, seed=4, weights=False)
+    s = _source(g)
+    d, _ = dpc.run_bfs(g, s, cfg=dpc.launch_cfg("sssp", "grid", **STREAM), ctx=ctx)
+    assert np.array_equal(d, orc.bfs(g.rowptr, g.col, s))
+
+
+def test_sssp_scale22_default_grid_is_stream_form(ctx, orc):
+    """At >= 2^24 edges the grid default is the stream form: scale 22, bit-exact,
+    with the level form forced beside it."""
+    import os
+    g = dpc.gen_rmat(22, 16, seed=1)
+    s = _source(g)
+    ref, _ = orc.sssp_mt(g.rowptr, g.col, g.w, s, os.cpu_count() or 1)
+    dg = dpc.DeviceGraph(ctx, g)
+    met = dg.sssp(s, "grid")
+    assert np.array_equal(dg.get_dist(), ref)
+    assert met.vertices_processed > 0  # only the stream form counts frontier visits
+    dg.sssp(s, "grid", cfg=dpc.launch_cfg("sssp", "grid", grid_level=True))
+    assert np.array_equal(dg.get_dist(), ref)
+    dg.close()

@@ -23,7 +23,7 @@ for arg in sys.argv[1:] or ["12", "16", "20", "22", "24:p"]:
     mr = int(deg[ref != np.uint32(0xFFFFFFFF)].sum())
     dg = dpc.DeviceGraph(ctx, g)
     res = {"scale": arg}
-    forms = {"level": dpc.launch_cfg("sssp", "grid"), "stream": dpc.launch_cfg("sssp", "grid", grid_stream=True)}
+    forms = {"level": dpc.launch_cfg("sssp", "grid", grid_level=True), "stream": dpc.launch_cfg("sssp", "grid", grid_stream=True)}
     for name, cfg in forms.items():
         met = dg.sssp(s, "grid", cfg=cfg, metrics=True)
         ok = bool(np.array_equal(dg.get_dist(), ref))
