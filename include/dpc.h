@@ -222,7 +222,7 @@ typedef struct dpc_metrics {
   int64_t host_launches;        /* kernels launched from the host            */
   double device_ms;             /* CUDA-event time of the run's kernels      */
   int32_t overflow;             /* nonzero: a buffer overflowed              */
-  int32_t result_count;         /* colors used (GC), reached vertices (SSSP) */
+  int32_t result_count;         /* colors used (GC), reached vertices (SSSP); basic TD/TH: children computed inline when the device pending-launch pool was full */
   int64_t vertices_processed;   /* SSSP / BFS: sum of the frontier sizes     */
 } dpc_metrics;
 

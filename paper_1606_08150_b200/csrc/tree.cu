@@ -127,39 +127,111 @@ __global__ void __launch_bounds__(256) flat_up(Args a, unsigned lo, unsigned hi)
 }
 
 // ---------------------------------------------------------------- basic
-__global__ void __launch_bounds__(256) basic_post(Args a, unsigned v) {
-  unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
-  int r = 0;
-  if (b + k < e) r = __ldcg(a.res + __ldg(a.clist + b + k)) + 1;
-  for (int o = 16; o > 0; o >>= 1) {
-    int t = __shfl_xor_sync(dev::kFull, r, o);
-    r = a.is_max ? max(r, t) : r + t;
+// Fig. 1(c) with CDP2: tree_traversal(node) <<<ceil(nc/T), T>>>, thread per
+// child; an internal child launches its own traversal (fire-and-forget).
+// Postwork runs by COUNT-DOWN on the child side instead of a tail-launched
+// grid per node (those stay pending until their whole subtree is done: ~1.7M
+// outstanding launches on the 4.2M-node config-4 tree, past the device
+// runtime's ~599K pending-launch pool, profiles/r01_pending_limit.txt):
+// pend[v] starts at nc(v); a block folds its leaf children into res[v] and
+// subtracts their count; a finished internal child folds itself into its
+// parent and subtracts one.  The thread that brings pend[v] to zero owns v's
+// final result and carries it upward (the postwork of PAPER.md:96-105,
+// executed once per node, after all of its children).
+__device__ __forceinline__ void fold_into(const Args& a, unsigned p, int r) {
+  if (a.is_max) atomicMax(a.res + p, r);
+  else atomicAdd(a.res + p, r);
+}
+
+// v's result is final: fold it into its ancestors while this thread
+// completes them.
+__device__ void basic_finish(const Args& a, unsigned v) {
+  while (v != a.root) {
+    const unsigned p = static_cast<unsigned>(__ldg(a.parent + v));
+    fold_into(a, p, __ldcg(a.res + v) + 1);
+    __threadfence();  // release: the fold before the count-down
+    if (atomicSub(a.pend + p, 1u) != 1u) return;
+    __threadfence();  // acquire: every child's fold into p is visible
+    v = p;
   }
-  if (dev::lane_id() == 0 && r) {
-    if (a.is_max) atomicMax(a.res + v, r);
-    else atomicAdd(a.res + v, r);
+}
+
+// The device runtime's pending-launch pool is full (cudaLimitDevRuntime-
+// PendingLaunchCount caps at ~599K on B200): the launching thread computes
+// the child's subtree itself -- a stackless post-order walk (parent pointers,
+// sibling position by search) folding each finished node into its parent with
+// plain stores (the subtree is this thread's alone).  Same results; counted
+// in RunHeader.next_count (metrics.result_count of a basic tree run).
+__device__ void subtree_inline(const Args& a, unsigned c) {
+  unsigned x = c;
+  while (nkids(a, x) > 0) x = static_cast<unsigned>(__ldg(a.clist + __ldg(a.cstart + x)));
+  while (x != c) {
+    const unsigned p = static_cast<unsigned>(__ldg(a.parent + x));
+    const int r = a.res[x] + 1;
+    a.res[p] = a.is_max ? max(a.res[p], r) : a.res[p] + r;
+    unsigned pos = __ldg(a.cstart + p);
+    while (static_cast<unsigned>(__ldg(a.clist + pos)) != x) pos++;
+    if (pos + 1 < __ldg(a.cstart + p + 1)) {
+      x = static_cast<unsigned>(__ldg(a.clist + pos + 1));
+      while (nkids(a, x) > 0) x = static_cast<unsigned>(__ldg(a.clist + __ldg(a.cstart + x)));
+    } else {
+      x = p;  // p's last child is folded: p is final
+    }
   }
+}
+
+__global__ void __launch_bounds__(256) basic_pend_init(Args a) {
+  const unsigned v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < a.n) a.pend[v] = nkids(a, v);
 }
 
 // tree_traversal(node) <<<ceil(nc/T), T>>>: thread per child.
 __global__ void __launch_bounds__(256) basic_traverse(Args a, unsigned v) {
-  unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
+  __shared__ int s_r;
+  __shared__ unsigned s_c;
+  if (threadIdx.x == 0) {
+    s_r = 0;
+    s_c = 0;
+  }
+  __syncthreads();
+  const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned b = __ldg(a.cstart + v), e = __ldg(a.cstart + v + 1);
   if (b + k < e) {
-    unsigned c = static_cast<unsigned>(__ldg(a.clist + b + k));
-    unsigned nc = nkids(a, c);
+    const unsigned c = static_cast<unsigned>(__ldg(a.clist + b + k));
+    const unsigned nc = nkids(a, c);
+    int r = 1;  // leaf child: desc 0 + 1, height 0 + 1
+    bool folded = true;
     if (nc > 0) {
       basic_traverse<<<dev::ceil_div(nc, a.child_threads), a.child_threads, 0,
                        cudaStreamFireAndForget>>>(a, c);
-      dev::note_launch(a.hdr);
+      const cudaError_t err = cudaGetLastError();
+      if (err == cudaSuccess) {
+        atomicAdd(&a.hdr->launches, 1u);
+        folded = false;  // the child's subtree folds itself into v (count-down)
+      } else if (err == cudaErrorLaunchPendingCountExceeded) {
+        subtree_inline(a, c);
+        atomicAdd(&a.hdr->next_count, 1u);
+        r = a.res[c] + 1;
+      } else {
+        atomicOr(&a.hdr->overflow, 2u);
+        atomicCAS(&a.hdr->aux0, 0u, static_cast<unsigned>(err));
+        folded = false;
+      }
     }
-    // leaf work: res[c] stays 0
+    if (folded) {
+      if (a.is_max) atomicMax(&s_r, r);
+      else atomicAdd(&s_r, r);
+      atomicAdd(&s_c, 1u);
+    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    basic_post<<<dev::ceil_div(e - b, a.child_threads), a.child_threads, 0,
-                 cudaStreamTailLaunch>>>(a, v);
-    dev::note_launch(a.hdr);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_c) {
+    fold_into(a, v, s_r);
+    __threadfence();
+    if (atomicSub(a.pend + v, s_c) == s_c) {
+      __threadfence();
+      basic_finish(a, v);
+    }
   }
 }
 
@@ -582,7 +654,7 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
   a.pend = nullptr;
   cudaStream_t s = c->stream;
   size_t need = 2048;
-  if (k.variant == DPC_BASIC) need = 2 * static_cast<size_t>(d->internal) + 1024;
+  if (k.variant == DPC_BASIC) need = static_cast<size_t>(d->internal) + 1024;  // capped by the runtime (~599K)
   else if (k.variant == DPC_WARP || k.variant == DPC_BLOCK) need = 2 * static_cast<size_t>(d->internal) + 1024;
   else if (k.variant == DPC_GRID) need = 4 * static_cast<size_t>(d->depth) + 1024;
   st = ensure_pending_limit(c, need);
@@ -635,9 +707,12 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
         break;
       }
       case DPC_BASIC: {
+        if (!d->pend) DPC_CUDA(cudaMalloc(&d->pend, sizeof(unsigned) * static_cast<size_t>(d->n)));
+        a.pend = d->pend;
+        tree::basic_pend_init<<<std::max(1u, dev::ceil_div(a.n, 256u)), 256, 0, s>>>(a);
         const unsigned nc = static_cast<unsigned>(d->root_children);
         tree::basic_traverse<<<dev::ceil_div(nc, k.child_threads), k.child_threads, 0, s>>>(a, root);
-        host_launches++;
+        host_launches += 2;
         DPC_CUDA(cudaGetLastError());
         break;
       }
@@ -685,6 +760,7 @@ dpc_status dpc_tree_device(dpc_ctx* c, dpc_dtree* d, int32_t which, const dpc_la
     met->iterations += levels ? levels : d->hdr_host->iter;
     met->edges_processed += d->n - 1;
     met->buffer_items_inserted += d->internal;
+    if (k.variant == DPC_BASIC) met->result_count += static_cast<int32_t>(d->hdr_host->next_count);
   }
   return DPC_OK;
 }

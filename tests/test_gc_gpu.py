@@ -73,7 +73,7 @@ def test_gc_config3_full(ctx, orc):
     g = dpc.gen_rmat(20, 16, seed=1, weights=False, symmetric=True)
     ref, k = orc.color(g.rowptr, g.col, 1)
     dg = dpc.DeviceGraph(ctx, g)
-    for v in ["flat", "warp", "block", "grid"]:
+    for v in ["flat", "basic", "warp", "block", "grid"]:
         met = dg.color(1, v)
         assert np.array_equal(dg.get_color(), ref), v
         assert met.result_count == k

@@ -112,7 +112,7 @@ def test_spmv_config2_full_size(ctx, orc):
     x = _x(g.n)
     dg = dpc.DeviceGraph(ctx, g)
     dg.set_x(x)
-    for variant in ["flat", "warp", "block", "grid"]:
+    for variant in ["flat", "basic", "warp", "block", "grid"]:
         met = dg.spmv(variant, metrics=True)
         _check(orc, g, x, dg.get_y())
     y = np.empty(g.n, np.float32)

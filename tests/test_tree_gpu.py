@@ -71,12 +71,13 @@ def test_tree_grid_cdp(ctx, orc):
 
 
 def test_tree_config4_full(ctx, orc):
-    """BASELINE config 4 scale: ~4M nodes, depth 24."""
-    t = dpc.gen_tree(24, 1, 4, 0.84, seed=1)
-    assert t.depth == 24 and 3_000_000 < t.n < 6_000_000
+    """BASELINE config 4: 4M nodes (4,246,411: within 5% of 4,194,304), depth 24,
+    every variant including basic-DP (child-side count-down postwork)."""
+    t = dpc.gen_tree(24, 1, 4, 0.851, seed=1)
+    assert t.depth == 24 and abs(t.n - 4_194_304) <= 0.05 * 4_194_304
     dt = dpc.DeviceTree(ctx, t)
     ref_d, ref_h = orc.tree_desc(t.parent), orc.tree_height(t.parent)
-    for v in ["flat", "warp", "block", "grid"]:
+    for v in ["flat", "basic", "warp", "block", "grid"]:
         dt.run("tree_desc", v)
         assert np.array_equal(dt.result(), ref_d), v
         dt.run("tree_height", v)

@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 import paper_1606_08150_b200 as dpc  # noqa: E402
 
 VARIANTS = ["flat", "basic", "warp", "block", "grid"]
-TREE = dict(depth=24, lo=1, hi=4, fill=0.84, seed=1)      # ~3.35M nodes, depth 24
+TREE = dict(depth=24, lo=1, hi=4, fill=0.851, seed=1)     # BASELINE config 4: 4,246,411 nodes, depth 24
 TREE_PAPER = dict(depth=5, lo=32, hi=128, fill=0.4, seed=1)  # paper-shaped, ~2.7M nodes
 # depth 24 at the size basic-DP still fits in the device pending-launch pool
 # (599,186 on B200; 196,634 internal nodes -> ~394K outstanding launches)
