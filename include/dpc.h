@@ -198,6 +198,13 @@ typedef struct dpc_launch_cfg {
 #define DPC_CFG_GRID_LEVEL 128 /* SSSP / BFS persistent grid variant: force the
                                   light-list + chunk-item level form (default
                                   below 2^24 edges) */
+#define DPC_CFG_SPMV_STREAM 256 /* SpMV grid variant: the per-call stream kernel
+                                   (insert phase + item-table drain, round 1)
+                                   instead of the default drain with the cached
+                                   per-matrix window plan (row-start bits per
+                                   256 nonzeros, built once per uploaded matrix,
+                                   spmv_plan.cu); the fused multi-GPU forms
+                                   always run the stream kernel */
 #define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */

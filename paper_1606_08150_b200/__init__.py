@@ -35,7 +35,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libdpc.so")
+# DPC_LIB_PATH: load another build of the library (timing-probe builds, tools/probes)
+_LIB_PATH = os.environ.get("DPC_LIB_PATH") or os.path.join(_HERE, "libdpc.so")
 
 
 def lib_path() -> str:
@@ -60,6 +61,7 @@ CFG_GRID_ASYNC = 8
 CFG_X_PEER_GATHER = 32
 CFG_GRID_STREAM = 64
 CFG_GRID_LEVEL = 128
+CFG_SPMV_STREAM = 256
 
 
 class DpcError(RuntimeError):
@@ -433,6 +435,8 @@ def launch_cfg(app: str, variant: str, **overrides) -> LaunchCfg:
             cfg.flags = (cfg.flags | CFG_GRID_ASYNC) if v else (cfg.flags & ~CFG_GRID_ASYNC)
         elif k == "grid_stream":
             cfg.flags = (cfg.flags | CFG_GRID_STREAM) if v else (cfg.flags & ~CFG_GRID_STREAM)
+        elif k == "spmv_stream":
+            cfg.flags = (cfg.flags | CFG_SPMV_STREAM) if v else (cfg.flags & ~CFG_SPMV_STREAM)
         elif k == "grid_level":
             cfg.flags = (cfg.flags | CFG_GRID_LEVEL) if v else (cfg.flags & ~CFG_GRID_LEVEL)
         else:

@@ -74,6 +74,11 @@ dpc_status resolve_cfg(dpc_ctx* ctx, int app, const dpc_launch_cfg* in, Cfg* out
 dpc_status ensure_pending_limit(dpc_ctx* ctx, size_t need) {
   size_t want = std::max<size_t>(2048, need);
   if (want == ctx->pending_limit) return DPC_OK;
+  size_t cur = 0;  // another context of this process may have changed it
+  if (cudaDeviceGetLimit(&cur, cudaLimitDevRuntimePendingLaunchCount) == cudaSuccess && cur == want) {
+    ctx->pending_limit = want;
+    return DPC_OK;
+  }
   DPC_CUDA(cudaStreamSynchronize(ctx->stream));
   DPC_CUDA(cudaDeviceSetLimit(cudaLimitDevRuntimePendingLaunchCount, want));
   ctx->pending_limit = want;
@@ -213,15 +218,26 @@ dpc_status dpc_ctx_create(int32_t device, dpc_ctx** out) {
     c->flush_bytes = std::max<size_t>(2 * static_cast<size_t>(p.l2CacheSize), 256u << 20);
     e = cudaMalloc(&c->flush_buf, c->flush_bytes);
   }
-  if (e == cudaSuccess) e = cudaDeviceSetLimit(cudaLimitDevRuntimePendingLaunchCount, 2048);
-  // device heap for the allocator-study variants (DPC_CFG_ALLOC_MALLOC): must
-  // be sized before any kernel calls malloc
-  if (e == cudaSuccess) e = cudaDeviceSetLimit(cudaLimitMallocHeapSize, size_t{512} << 20);
+  // the device limits are per process: a second context keeps what an
+  // earlier one raised (never lowers them)
+  size_t pending = 0, heap = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetLimit(&pending, cudaLimitDevRuntimePendingLaunchCount);
+  if (e == cudaSuccess && pending < 2048) {
+    e = cudaDeviceSetLimit(cudaLimitDevRuntimePendingLaunchCount, 2048);
+    pending = 2048;
+  }
+  // device heap for the allocator-study variants (DPC_CFG_ALLOC_MALLOC): it
+  // can only be sized before the first kernel that calls malloc
+  if (e == cudaSuccess) e = cudaDeviceGetLimit(&heap, cudaLimitMallocHeapSize);
+  if (e == cudaSuccess && heap < (size_t{512} << 20)) {
+    if (cudaDeviceSetLimit(cudaLimitMallocHeapSize, size_t{512} << 20) != cudaSuccess)
+      cudaGetLastError();  // heap already in use: keep its size (malloc overflow is reported per run)
+  }
   if (e != cudaSuccess) {
     dpc_ctx_destroy(c);
     return cuda_fail(e, "dpc_ctx_create");
   }
-  c->pending_limit = 2048;
+  c->pending_limit = pending;
   *out = c;
   return DPC_OK;
 }
@@ -327,7 +343,8 @@ void dpc_dgraph_free(dpc_dgraph* g) {
                   g->dist,   g->color,    g->front[0], g->front[1], g->stamp, g->hdr,
                   g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val,
                   g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt, g->gc_q, g->gc_hstate, g->trace, g->gc_hcol, g->gc_hsplit,
-                  g->x2, g->y2, g->sst_items};
+                  g->x2, g->y2, g->sst_items, g->plan_mask, g->plan_sin, g->plan_segrow, g->plan_bar,
+                  g->plan8, g->plan8_segrow};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->ms_state) dpc::sssp_state_free(g->ms_state);

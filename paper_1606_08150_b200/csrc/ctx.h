@@ -82,6 +82,16 @@ struct dpc_dgraph {
   size_t ms_n = 0, ms_cap = 0;
   size_t ms_rcap = 0;  // pairs the receive area holds (grown by dpc_msssp_recv_reserve)
   void* ms_state = nullptr;
+  // SpMV grid plan (spmv_plan.cu): per 128-nonzero window row-start bits and
+  // open segment, the row of each non-empty row, a self-resetting barrier
+  unsigned* plan_mask = nullptr;
+  unsigned* plan_sin = nullptr;
+  unsigned* plan_segrow = nullptr;
+  unsigned* plan_bar = nullptr;
+  unsigned plan_nwin = 0;
+  unsigned* plan8 = nullptr;  // G = 8 window plan (64 B per 256 nonzeros)
+  unsigned* plan8_segrow = nullptr;
+  unsigned plan8_nwin = 0;
   void* sst_items = nullptr;  // SSSP frontier stream form: 2 x (n + 1) items
   size_t sst_cap = 0;
   int* xhot_col = nullptr;
@@ -168,6 +178,9 @@ inline void defer_check(dpc_dgraph* g) {
 }
 // Frees the partitioned-SSSP step state of a graph (sssp.cu).
 void sssp_state_free(void* state);
+// SpMV grid variant with the cached per-matrix window plan (spmv_plan.cu).
+dpc_status spmv_plan_build(dpc_ctx* ctx, dpc_dgraph* g);
+dpc_status spmv_plan_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, int flags);
 // SSSP / BFS grid variant, frontier stream form (sssp_stream.cu).
 dpc_status sssp_stream_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, bool unit, bool coop,
                            int64_t* host_launches, int64_t* levels, dpc_metrics* met);

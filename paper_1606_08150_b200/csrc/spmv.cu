@@ -1540,6 +1540,30 @@ dpc_status dpc::spmv_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d
   a.rshift = ~0u;
   if (rows && (rows & (rows - 1)) == 0) a.rshift = static_cast<unsigned>(__builtin_ctzll(rows));
   a.coop = 1;
+  // grid variant with the cached per-matrix window plan (spmv_plan.cu)
+  if (c.variant == DPC_GRID && c.grid_persistent && !xpeer &&
+      !(c.flags & (DPC_CFG_SPMV_STREAM | DPC_CFG_GRID_CHUNKED | DPC_CFG_COOP_LAUNCH))) {
+    if (!g->hdr_clean || met) {
+      st = flush_check(ctx, g);
+      if (st != DPC_OK) return st;
+      st = begin_run(ctx, g->hdr);
+      if (st != DPC_OK) return st;
+    }
+    if (g->m > 0 || g->n > 0) {
+      st = spmv_plan_run(ctx, g, d_x, d_y, c.flags);
+      if (st != DPC_OK) return st;
+      DPC_CUDA(cudaGetLastError());
+    }
+    g->hdr_clean = true;  // the plan kernel writes only fault bits into the header
+    if (met) {
+      met->host_launches += 1;
+      met->edges_processed += g->m;
+      met->iterations += 1;
+      return finish_metrics(ctx, g->hdr, g->hdr_host, met);
+    }
+    defer_check(g);
+    return DPC_OK;
+  }
   // stream-balanced grid drain (grid_stream)
   const bool use_stream = c.variant == DPC_GRID && c.grid_persistent && !(c.flags & DPC_CFG_GRID_CHUNKED);
   if (xpeer && !(use_stream && c.threshold == 0))

@@ -139,7 +139,7 @@ def test_spmv_grid_stream_forms(ctx, orc, shape, threshold):
     and on an R-MAT matrix."""
     for g in (_ragged(), dpc.gen_rmat(13, 16, seed=4, weights=False, values=True)):
         x = _x(g.n)
-        cfg = dpc.launch_cfg("spmv", "grid", threshold=threshold)
+        cfg = dpc.launch_cfg("spmv", "grid", threshold=threshold, spmv_stream=True)
         cfg.flags |= shape << 20
         y, met = dpc.run_spmv(g, x, "grid", cfg=cfg, ctx=ctx)
         _check(orc, g, x, y)
@@ -180,4 +180,78 @@ def test_spmv_host_batch_pipelined(ctx, orc, count):
     for x, y in zip(xs, ys):
         y64 = orc.spmv_f64(g.rowptr, g.col, g.val, x)
         assert np.all(np.abs(y - y64) <= 1e-5 * np.abs(y64) + 1e-30)
+    dg.close()
+
+
+# ---- the default grid form: drain with the cached per-matrix window plan
+PLAN_FORMS = {"w256": 0, "w128_reg": 1 << 9, "w128_tma": 1 << 12}
+
+
+def _plan_cases():
+    yield _ragged()
+    yield _ragged(seed=5, hub=3 * 256 * 32 + 17)        # a hub spanning several chunks
+    yield dpc.gen_rmat(13, 16, seed=4, weights=False, values=True)
+    yield dpc.gen_rmat(12, 8, seed=6, weights=False, values=True, permute=True)
+    # rows of exactly 256 / 128 / 512 nonzeros on window boundaries, then empty rows
+    lens = np.array([256, 128, 128, 512, 0, 0, 256, 1, 255, 0, 7, 0], np.int64)
+    rowptr = np.concatenate([[0], np.cumsum(lens)])
+    rng = np.random.default_rng(2)
+    col = rng.integers(0, len(lens), rowptr[-1]).astype(np.int32)
+    val = (rng.integers(1, 1 << 24, rowptr[-1]) / float(1 << 24)).astype(np.float32)
+    yield dpc.csr_from_arrays(rowptr, col, val=val)
+    # all rows empty except the last; a single nonzero; no nonzeros
+    yield dpc.csr_from_arrays(np.concatenate([np.zeros(1000, np.int64), [3]]), [5, 6, 7], val=[0.5, 0.25, 1.0])
+    yield dpc.csr_from_arrays([0, 1], [0], val=[2.0])
+    yield dpc.csr_from_arrays([0, 0, 0, 0], [], val=[])
+
+
+@pytest.mark.parametrize("form", list(PLAN_FORMS))
+def test_spmv_grid_plan_forms(ctx, orc, form):
+    """Cached-plan drain (default grid form) and its W = 128 variants on ragged
+    rows, window-boundary rows, chunk-spanning hubs, empty rows, R-MAT
+    (plain and permuted); repeated calls reuse the plan and the self-resetting
+    barrier; results independent of the previous y contents."""
+    for g in _plan_cases():
+        x = _x(g.ncols if g.ncols else g.n)
+        cfg = dpc.launch_cfg("spmv", "grid")
+        cfg.flags |= PLAN_FORMS[form]
+        dg = dpc.DeviceGraph(ctx, g)
+        dg.set_x(x)
+        for rep in range(3):
+            if g.n:
+                ctx.h2d(dg.y_ptr, np.full(g.n, 123.0, np.float32))  # stale y must not leak
+            met = dg.spmv("grid", cfg=cfg, metrics=rep == 0)
+            if met is not None:
+                assert met.child_launch_count == 0
+            if g.n:
+                _check(orc, g, x, dg.get_y())
+        dg.close()
+
+
+def test_spmv_grid_plan_unaligned_y_and_row_slice(ctx, orc):
+    """dpc_spmv_device with a y pointer that is not 16-byte aligned, and the
+    plan on a row slice of a larger matrix (global column ids, as the
+    partitioned path uploads it)."""
+    import ctypes as C
+    g = _ragged(seed=9)
+    x = _x(g.n)
+    dg = dpc.DeviceGraph(ctx, g)
+    dg.set_x(x)
+    buf = ctx.alloc(4 * (g.n + 1))
+    dpc._check(dpc._lib.dpc_spmv_device(ctx.handle, dg._h, C.c_void_p(dg.x_ptr), C.c_void_p(buf + 4),
+                                        C.byref(dpc.launch_cfg("spmv", "grid")), None))
+    ctx.synchronize()
+    dg.check()
+    _check(orc, g, x, ctx.d2h(buf + 4, g.n))
+    ctx.free(buf)
+    dg.close()
+    full = dpc.gen_rmat(12, 16, seed=3, weights=False, values=True, permute=True)
+    part = dpc.gen_rmat_rows(12, 1024, 2048, 16, seed=3, weights=False, values=True, permute=True)
+    xf = _x(full.n)
+    dg = dpc.DeviceGraph(ctx, part)
+    dg.set_x(xf)
+    dg.spmv("grid")
+    y64 = orc.spmv_f64(full.rowptr, full.col, full.val, xf)[1024:2048]
+    y = dg.get_y().astype(np.float64)
+    assert np.all(np.abs(y - y64) <= RTOL * np.abs(y64))
     dg.close()
