@@ -18,6 +18,7 @@ struct dpc_ctx {
   int device = 0;
   int sms = 148;
   int max_threads_per_sm = 2048;
+  int smem_per_sm = 233472;  // shared memory per SM (bytes)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[64] = {};
   size_t pending_limit = 0;  // current cudaLimitDevRuntimePendingLaunchCount
@@ -92,6 +93,13 @@ struct dpc_dgraph {
   unsigned* plan8 = nullptr;  // G = 8 window plan (64 B per 256 nonzeros)
   unsigned* plan8_segrow = nullptr;
   unsigned plan8_nwin = 0;
+  // hot-column x cache of the plan form: col re-encoded (hot columns as
+  // slot | 0x80000000), the column of each slot, per-call x at the slots
+  int* plan8h_col = nullptr;
+  int* plan8h_hot = nullptr;
+  float* plan8h_xh = nullptr;
+  unsigned plan8h_nhot4 = 0;
+  unsigned plan8h_cap = 0;  // slot capacity the plan was built for (0: none)
   void* sst_items = nullptr;  // SSSP frontier stream form: 2 x (n + 1) items
   size_t sst_cap = 0;
   int* xhot_col = nullptr;

@@ -28,11 +28,17 @@
 //   bit 12   W = 128, col / val / plan staged in a per-warp shared-memory
 //            ring by bulk copies (cp.async.bulk + mbarrier): the smem ring
 //            shrinks L1, whose hits the x gathers need (measured slower)
-// What bounds the default form: L1TEX at 82 % of peak, serving the 16.8M
-// scattered x gathers (one 128-byte line per lane per gather instruction).
+//   default form also caches the most used columns' x in shared memory
+//   (slot-encoded col, per-call hot_gather + bulk-copy fill) and splits the
+//   device-wide barrier (arrive after y = 0, wait before the first y write).
+// What bounds it: the latency of the remaining (cold) x gathers and of the
+// HBM stream on 32 warps per SM (profiles/r02_spmv_hot_lab.md).
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -181,10 +187,6 @@ __device__ __forceinline__ void win_drain(const Args& a, const Win& d, const flo
   }
 }
 
-// L2 prefetch of a contiguous range with one bulk-copy instruction (TMA unit).
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
-}
 
 template <int V, int NT, unsigned C>
 __global__ void __launch_bounds__(NT, 1024 / NT) plan_drain(Args a) {
@@ -365,35 +367,129 @@ __global__ void __launch_bounds__(NT, 1024 / NT) plan_drain_tma(Args a) {
   }
 }
 
-// ---- G = 8 form: 256-nonzero windows, 8 per lane (two int4 / float4 loads),
-// so the per-window work (plan entry, lane scan, carry) is paid once per 256
-// nonzeros.  Plan entry per window (64 B): row-start bits 0..255 (8 words),
-// s_in, and the 8 per-word prefix counts of the start bits (bytes).
+// ---- G = 8 form (default): 256-nonzero windows, 8 per lane (two int4 /
+// float4 loads each of col and val), so the per-window work (plan entry,
+// lane scan, carry) is paid once per 256 nonzeros.  Plan entry per window
+// (64 B): row-start bits 0..255 (8 words), s_in, and the 8 per-word prefix
+// counts of the start bits (bytes).
+//
+// Hot-column x cache: R-MAT / power-law matrices reuse few columns heavily
+// (config 2: the 32K most used columns take 71 % of the nonzeros).  A
+// per-matrix analysis (spmv_plan8_hot_build) picks them and re-encodes col
+// with those columns replaced by slot | 0x80000000; per call a small kernel
+// gathers x at the slots (hot_gather), and every block bulk-copies the slot
+// table into shared memory (cp.async.bulk, one mbarrier).  A hot gather is
+// then a 4-byte shared-memory access instead of a 128-byte L1TEX line per
+// lane (the bound of the plain form: L1TEX 82 %, profiles/r02_spmv_hot_lab.md).
 constexpr unsigned W8 = 256;
 
 struct Args8 {
-  const int* __restrict__ col;
+  const int* __restrict__ col;  // hot columns re-encoded (HOT)
   const float* __restrict__ val;
   const float* __restrict__ x;
   float* y;
   const unsigned* __restrict__ plan;  // [16 * nwin]
   const unsigned* __restrict__ seg_row;
   unsigned n, m, nwin;
-  unsigned* bar;
+  unsigned* bar;  // [2]: split-phase barrier count / generation (self-resetting)
   dev::RunHeader* hdr;
+  const float* xh;  // HOT: [nhot4] x at the hot columns (this call's, from hot_gather)
+  unsigned nhot4;   // slots, a multiple of 4
+  unsigned probe;   // timing-probe builds only (wrong results): 1 prologue only, 2 no x gathers,
+                    // 3 no segmentation / y stores, 4 = 2 + 3, 5 return at entry
 };
 
-__device__ __forceinline__ void row_put8(const Args8& a, unsigned seg, float s, bool atomic) {
-  const unsigned r = __ldg(a.seg_row + seg);
-  if (atomic) atomicAdd(a.y + r, s);
-  else a.y[r] = s;
+// x gather through the hot-column cache: slot-encoded columns read shared memory.
+template <bool HOT>
+__device__ __forceinline__ float xget(const float* __restrict__ x, const float* sx, int c) {
+  if (HOT && c < 0) return sx[c & 0x7fffffff];
+  return __ldg(x + c);
 }
 
-template <int NT, unsigned C>
+struct WinPlan {
+  unsigned word, sin, pre;  // this lane's start-bit word, the open segment, the word's prefix count
+};
+struct WinData {
+  int cc[8];
+  float vv[8];
+};
+__device__ __forceinline__ WinPlan load_plan(const Args8& a, unsigned w, unsigned j) {
+  const unsigned* pe = a.plan + 16 * w;
+  WinPlan P;
+  P.word = __ldg(pe + j);
+  P.sin = __ldg(pe + 8);
+  P.pre = (__ldg(pe + 9 + (j >> 2)) >> (8 * (j & 3))) & 0xffu;
+  return P;
+}
+__device__ __forceinline__ WinData load_data(const Args8& a, unsigned w, unsigned lane) {
+  WinData D;
+  const unsigned q = w * W8 + 8 * lane;
+  if (q + 8 <= a.m) {
+    const int4 c0 = ld_stream(reinterpret_cast<const int4*>(a.col + q));
+    const int4 c1 = ld_stream(reinterpret_cast<const int4*>(a.col + q + 4));
+    const float4 v0 = ld_stream(reinterpret_cast<const float4*>(a.val + q));
+    const float4 v1 = ld_stream(reinterpret_cast<const float4*>(a.val + q + 4));
+    D.cc[0] = c0.x, D.cc[1] = c0.y, D.cc[2] = c0.z, D.cc[3] = c0.w;
+    D.cc[4] = c1.x, D.cc[5] = c1.y, D.cc[6] = c1.z, D.cc[7] = c1.w;
+    D.vv[0] = v0.x, D.vv[1] = v0.y, D.vv[2] = v0.z, D.vv[3] = v0.w;
+    D.vv[4] = v1.x, D.vv[5] = v1.y, D.vv[6] = v1.z, D.vv[7] = v1.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const bool in = q + e < a.m;
+      D.cc[e] = in ? __ldg(a.col + q + e) : 0;
+      D.vv[e] = in ? __ldg(a.val + q + e) : 0.f;
+    }
+  }
+  return D;
+}
+
+// x at the hot columns, once per call.  The drain is launched as its
+// programmatic dependent and waits for it (griddepcontrol.wait) only before
+// the shared-memory fill.
+__global__ void hot_gather(const float* __restrict__ x, const int* __restrict__ hot, float* xh, unsigned n4) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x)
+    xh[i] = __ldg(x + __ldg(hot + i));
+}
+
+// Chunks of kChunk windows are dealt round-robin to the warps (warp rank
+// block-interleaved), so at any moment the grid streams one contiguous
+// region of col / val (HBM page locality; per-warp contiguous ranges measured
+// 17 % slower).  The device-wide barrier that orders y = 0 before the
+// atomics of cut rows is split-phase: a block arrives once its zeros are
+// written, and each warp waits just before its first y write, after its first
+// window's loads and gathers.
+constexpr unsigned kChunk = 2;
+
+template <int NT, bool HOT>
 __global__ void __launch_bounds__(NT, 1024 / NT) plan8_drain(Args8 a) {
+  extern __shared__ __align__(128) float sx[];  // HOT: x at the hot columns
+  __shared__ unsigned long long s_bar;
+  __shared__ unsigned s_gen0;
   const unsigned stride = gridDim.x * NT;
   const unsigned gtid = blockIdx.x * NT + threadIdx.x;
   const unsigned lane = dev::lane_id();
+  const unsigned nw = stride >> 5;
+  const unsigned gw = dev::warp_in_block() * gridDim.x + blockIdx.x;
+  const unsigned nchunks = (a.nwin + kChunk - 1) / kChunk;
+  const unsigned j = lane >> 2, sh = (lane & 3u) * 8u;
+  if (DPC_TIMING_PROBES && a.probe == 5) return;
+  // the warp's first window's loads go out first: their HBM latency overlaps
+  // the y = 0 pass, the barrier arrival and the hot-column fill
+  WinPlan P{};
+  WinData D{};
+  if (gw < nchunks) {
+    P = load_plan(a, gw * kChunk, j);
+    D = load_data(a, gw * kChunk, lane);
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(s_gen0) : "l"(a.bar + 1) : "memory");
+    if (HOT) {
+      mbar_init(&s_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   if ((reinterpret_cast<uintptr_t>(a.y) & 15u) == 0) {
     float4* y4 = reinterpret_cast<float4*>(a.y);
     for (unsigned i = gtid; i < a.n / 4; i += stride) y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -401,57 +497,97 @@ __global__ void __launch_bounds__(NT, 1024 / NT) plan8_drain(Args8 a) {
   } else {
     for (unsigned i = gtid; i < a.n; i += stride) a.y[i] = 0.f;
   }
-  dev::soft_grid_sync(a.bar, a.bar + 1, &a.hdr->overflow);
-  const unsigned nw = stride >> 5;
-  const unsigned gw = dev::warp_in_block() * gridDim.x + blockIdx.x;
-  const unsigned nchunks = (a.nwin + C - 1) / C;
-  const unsigned j = lane >> 2, sh = (lane & 3u) * 8u;
-  for (unsigned ch = gw; ch < nchunks; ch += nw) {
-    const unsigned w0 = ch * C, w1 = min(a.nwin, w0 + C);
-    float carry = 0.f;
-    bool partial = true;
-    bool skip = (__ldg(a.plan + 16 * w0) & 1u) != 0u;  // the chunk starts on a row start
-    unsigned seg_end = kNone;
-    for (unsigned w = w0; w < w1; w++) {
-      const unsigned* pe = a.plan + 16 * w;
-      const unsigned word = __ldg(pe + j);
-      const unsigned sin = __ldg(pe + 8);
-      const unsigned pre = (__ldg(pe + 9 + (j >> 2)) >> (8 * (j & 3))) & 0xffu;
-      const unsigned q = w * W8 + 8 * lane;
-      int cc[8];
-      float vv[8];
-      if (q + 8 <= a.m) {
-        const int4 c0 = ld_stream(reinterpret_cast<const int4*>(a.col + q));
-        const int4 c1 = ld_stream(reinterpret_cast<const int4*>(a.col + q + 4));
-        const float4 v0 = ld_stream(reinterpret_cast<const float4*>(a.val + q));
-        const float4 v1 = ld_stream(reinterpret_cast<const float4*>(a.val + q + 4));
-        cc[0] = c0.x, cc[1] = c0.y, cc[2] = c0.z, cc[3] = c0.w, cc[4] = c1.x, cc[5] = c1.y, cc[6] = c1.z, cc[7] = c1.w;
-        vv[0] = v0.x, vv[1] = v0.y, vv[2] = v0.z, vv[3] = v0.w, vv[4] = v1.x, vv[5] = v1.y, vv[6] = v1.z, vv[7] = v1.w;
-      } else {
+  __syncthreads();
+  if (threadIdx.x == 0) {  // barrier arrival (the last block opens the next generation)
+    __threadfence();
+    if (atomicAdd(a.bar, 1u) == gridDim.x - 1) {
+      *reinterpret_cast<volatile unsigned*>(a.bar) = 0;
+      __threadfence();
+      atomicAdd(a.bar + 1, 1u);
+    }
+    if (HOT) {  // the slot table: one bulk copy per 32 KB (TMA unit)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const unsigned bytes = a.nhot4 * 4u;
+      mbar_expect_tx(&s_bar, bytes);
+      for (unsigned off = 0; off < bytes; off += 32768u)
+        bulk_g2s(reinterpret_cast<unsigned char*>(sx) + off, reinterpret_cast<const unsigned char*>(a.xh) + off,
+                 min(32768u, bytes - off), &s_bar);
+    }
+  }
+  if (HOT) mbar_wait(&s_bar, 0);
+  if (DPC_TIMING_PROBES && a.probe == 1) return;
+  const bool no_gather = DPC_TIMING_PROBES && (a.probe == 2 || a.probe == 4);
+  const bool no_scan = DPC_TIMING_PROBES && (a.probe == 3 || a.probe == 4);
+  float probe_acc = 0.f;
+  bool wait_bar = true;  // this warp has not yet seen the barrier complete
+  unsigned ch = gw;
+  if (ch >= nchunks) return;
+  unsigned w = ch * kChunk;
+  bool first = true;
+  float carry = 0.f;
+  bool partial = true, skip = false;
+  for (;;) {
+    const unsigned w1 = min(a.nwin, ch * kChunk + kChunk);
+    if (!first) {
+      P = load_plan(a, w, j);
+      D = load_data(a, w, lane);
+    }
+    first = false;
+    const unsigned word = P.word, sin = P.sin, pre = P.pre;
+    // this lane's row starts, and the rows of the first two segments it
+    // closes, loaded while the gathers are in flight
+    const unsigned my8 = (word >> sh) & 0xffu;
+    const unsigned before = pre + __popc(word & ((1u << sh) - 1u));
+    const unsigned kl = __popc(my8);
+    const unsigned seg0 = sin + before;
+    const unsigned r0 = (kl && seg0 != kNone) ? __ldg(a.seg_row + seg0) : 0u;
+    const unsigned r1 = kl > 1 ? __ldg(a.seg_row + (seg0 + 1u)) : 0u;
+    if (w == ch * kChunk) {  // chunk start: the open segment is the previous chunk's alone when it starts a row
+      carry = 0.f;
+      partial = true;
+      skip = (__shfl_sync(kFull, word, 0) & 1u) != 0u;
+    }
+    float p[8];
 #pragma unroll
-        for (int e = 0; e < 8; e++) {
-          const bool in = q + e < a.m;
-          cc[e] = in ? __ldg(a.col + q + e) : 0;
-          vv[e] = in ? __ldg(a.val + q + e) : 0.f;
+    for (int e = 0; e < 8; e++)
+      p[e] = no_gather ? D.vv[e] + __int_as_float(D.cc[e]) : D.vv[e] * xget<HOT>(a.x, sx, D.cc[e]);
+    if (no_scan) {
+#pragma unroll
+      for (int e = 0; e < 8; e++) probe_acc += p[e] + __uint_as_float(word + sin + pre + r0 + r1);
+    } else {
+      if (wait_bar) {  // the device-wide barrier: every block's y = 0 is written
+        if (lane == 0) {
+          const unsigned long long t0 = dev::global_ns();
+          for (;;) {
+            unsigned gnow;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gnow) : "l"(a.bar + 1) : "memory");
+            if (gnow != s_gen0) break;
+            if (dev::global_ns() - t0 > 2000000000ull) {  // watchdog: a block never arrived
+              atomicOr(&a.hdr->overflow, 4u);
+              break;
+            }
+            __nanosleep(32);
+          }
         }
+        __syncwarp();
+        wait_bar = false;
       }
-      float p[8];
-#pragma unroll
-      for (int e = 0; e < 8; e++) p[e] = vv[e] * __ldg(a.x + cc[e]);
-      const unsigned my8 = (word >> sh) & 0xffu;
-      const unsigned before = pre + __popc(word & ((1u << sh) - 1u));
       float head = 0.f, run = 0.f;
       unsigned k = 0;
 #pragma unroll
       for (int e = 0; e < 8; e++) {
         const bool st = (my8 >> e) & 1u;
-        if (st && k) row_put8(a, sin + before + k, run, false);  // segment whole inside this lane
+        if (st && k) a.y[k == 1 ? r1 : __ldg(a.seg_row + (seg0 + k))] = run;  // segment whole inside this lane
         if (st && !k) head = run;
         run = st ? p[e] : run + p[e];
         k += st;
       }
       if (!k) head = run;
       const float tail = k ? run : 0.f;
+      // lanes' recurrence carry_l = (k_l == 0) ? carry_{l-1} + head_l : tail_l:
+      // a segmented inclusive scan whose segments start at the lanes holding a
+      // row start (known to every lane from one ballot)
       const unsigned starts = __ballot_sync(kFull, k != 0);
       const unsigned upto = starts & (lane == 31 ? kFull : (2u << lane) - 1u);
       const unsigned sfirst = upto ? 31u - __clz(upto) : 0u;
@@ -466,21 +602,30 @@ __global__ void __launch_bounds__(NT, 1024 / NT) plan8_drain(Args8 a) {
         const bool none_before = (starts & ((1u << lane) - 1u)) == 0u;
         if (lane == 0) ex = 0.f;
         if (none_before) ex += carry;
-        const unsigned seg = sin + before;
-        if (none_before) {
-          if (!skip && seg != kNone) row_put8(a, seg, ex + head, partial);
+        if (none_before) {  // closes the segment that entered the window
+          if (!skip && seg0 != kNone) {
+            if (partial) atomicAdd(a.y + r0, ex + head);
+            else a.y[r0] = ex + head;
+          }
         } else {
-          row_put8(a, seg, ex + head, false);
+          a.y[r0] = ex + head;
         }
       }
       const float v31 = __shfl_sync(kFull, v, 31);
       carry = starts ? v31 : carry + v31;
       if (starts) partial = false, skip = false;
-      // segment open at this window's end
-      seg_end = sin + __shfl_sync(kFull, before + k, 31);
+      if (w + 1 == w1) {  // chunk end: the segment still open continues into the next chunk
+        const unsigned seg_end = sin + __shfl_sync(kFull, before + k, 31);
+        if (lane == 0 && !skip && seg_end != kNone && carry != 0.f)
+          atomicAdd(a.y + __ldg(a.seg_row + seg_end), carry);
+      }
     }
-    if (lane == 0 && !skip && seg_end != kNone && carry != 0.f) row_put8(a, seg_end, carry, true);
+    unsigned nxt = w + 1;
+    if (nxt >= w1) ch += nw, nxt = ch * kChunk;
+    if (ch >= nchunks) break;
+    w = nxt;
   }
+  if (no_scan && probe_acc == 1.2345f) a.y[0] = probe_acc;  // keeps the probe's loads alive
 }
 
 }  // namespace spmvp
@@ -526,7 +671,6 @@ dpc_status spmv_plan_build(dpc_ctx* ctx, dpc_dgraph* g) {
   return DPC_OK;
 }
 
-// y = A x with the cached plan: one persistent launch (all blocks co-resident).
 // G = 8 window plan: 64 B per 256 nonzeros (+ the shared seg_row).
 dpc_status spmv_plan8_build(dpc_ctx* ctx, dpc_dgraph* g) {
   if (g->plan8) return DPC_OK;
@@ -569,7 +713,125 @@ dpc_status spmv_plan8_build(dpc_ctx* ctx, dpc_dgraph* g) {
   return DPC_OK;
 }
 
-static dpc_status spmv_plan8_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y) {
+namespace spmvp {
+__global__ void col_degree(const int* __restrict__ col, unsigned m, unsigned* cnt) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    atomicAdd(cnt + __ldg(col + i), 1u);
+}
+__global__ void col_encode(const int* __restrict__ col, unsigned m, const int* __restrict__ slot_of, int* colh) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int c = __ldg(col + i), sl = __ldg(slot_of + c);
+    colh[i] = sl >= 0 ? static_cast<int>(static_cast<unsigned>(sl) | 0x80000000u) : c;
+  }
+}
+}  // namespace spmvp
+
+// Hot-column plan (once per matrix and slot capacity): the `cap` most used
+// columns (at least kHotMin uses; ties: the smaller column), slots in column
+// order, and a copy of col with those columns replaced by their slot.
+static dpc_status spmv_plan8_hot_build(dpc_ctx* ctx, dpc_dgraph* g, unsigned cap) {
+  constexpr unsigned kHotMin = 2;
+  if (g->plan8h_cap == cap) return DPC_OK;
+  cudaStream_t s = ctx->stream;
+  DPC_CUDA(cudaStreamSynchronize(s));
+  for (void* b : {static_cast<void*>(g->plan8h_col), static_cast<void*>(g->plan8h_hot), static_cast<void*>(g->plan8h_xh)})
+    if (b) cudaFree(b);
+  g->plan8h_col = g->plan8h_hot = nullptr;
+  g->plan8h_xh = nullptr;
+  g->plan8h_cap = 0;
+  const size_t nc = static_cast<size_t>(std::max<int64_t>(g->ncols, 1));
+  if (g->ncols >= (int64_t{1} << 31)) return fail(DPC_E_INVALID, "SpMV hot plan: too many columns");
+  const unsigned m = static_cast<unsigned>(g->m);
+  std::vector<unsigned> cnt(nc, 0u);
+  unsigned* d_cnt = nullptr;
+  int* d_slot = nullptr;
+  DPC_CUDA(cudaMalloc(&d_cnt, sizeof(unsigned) * nc));
+  cudaError_t e = cudaMemsetAsync(d_cnt, 0, sizeof(unsigned) * nc, s);
+  const unsigned grid = 4u * static_cast<unsigned>(ctx->sms);
+  if (e == cudaSuccess && m) spmvp::col_degree<<<grid, 256, 0, s>>>(g->col, m, d_cnt);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(unsigned) * nc, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d_cnt);
+  if (e != cudaSuccess) return cuda_fail(e, "SpMV hot plan (degrees)");
+  std::vector<unsigned> cand;
+  for (size_t c = 0; c < nc; c++)
+    if (cnt[c] >= kHotMin) cand.push_back(static_cast<unsigned>(c));
+  auto hotter = [&](unsigned a, unsigned b) { return cnt[a] != cnt[b] ? cnt[a] > cnt[b] : a < b; };
+  if (cand.size() > cap) {
+    std::nth_element(cand.begin(), cand.begin() + cap, cand.end(), hotter);
+    cand.resize(cap);
+  }
+  std::sort(cand.begin(), cand.end());
+  const unsigned nhot4 = static_cast<unsigned>((cand.size() + 3) & ~size_t{3});
+  std::vector<int> hot(std::max(nhot4, 4u), 0), slot_of(nc, -1);
+  for (size_t i = 0; i < cand.size(); i++) hot[i] = static_cast<int>(cand[i]), slot_of[cand[i]] = static_cast<int>(i);
+  DPC_CUDA(cudaMalloc(&g->plan8h_col, sizeof(int) * (static_cast<size_t>(m) + 16)));
+  DPC_CUDA(cudaMalloc(&g->plan8h_hot, sizeof(int) * hot.size()));
+  DPC_CUDA(cudaMalloc(&g->plan8h_xh, sizeof(float) * hot.size()));
+  DPC_CUDA(cudaMalloc(&d_slot, sizeof(int) * nc));
+  e = cudaMemcpyAsync(g->plan8h_hot, hot.data(), sizeof(int) * hot.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_slot, slot_of.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->plan8h_col + m, 0, sizeof(int) * 16, s);  // the CSR arrays' padding
+  if (e == cudaSuccess && m) spmvp::col_encode<<<grid, 256, 0, s>>>(g->col, m, d_slot, g->plan8h_col);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d_slot);
+  if (e != cudaSuccess) return cuda_fail(e, "SpMV hot plan (encode)");
+  g->plan8h_nhot4 = nhot4;
+  g->plan8h_cap = cap;
+  return DPC_OK;
+}
+
+// Hot-column slot capacity: DPC_SPMV_HOT_CAP (slots; 0 disables; labs) or the
+// measured default, 32K slots = 128 KB of shared memory per block
+// (profiles/r02_spmv_hot_lab.md: 16K 61 us, 32K 54 us, 40K 56 us, 53K 85 us
+// on config 2 -- past ~160 KB the L1 left for the streaming loads in flight
+// is too small).
+static unsigned spmv_hot_cap() {
+  const char* e = getenv("DPC_SPMV_HOT_CAP");
+  return e ? static_cast<unsigned>(atoi(e)) : 32768u;
+}
+
+template <int NT, bool HOT>
+static dpc_status plan8_launch(dpc_ctx* ctx, const spmvp::Args8& a0, size_t smem) {
+  const void* fn = reinterpret_cast<const void*>(spmvp::plan8_drain<NT, HOT>);
+  static std::mutex mu;
+  static std::map<std::pair<int, size_t>, int> cache;  // (device, smem) -> blocks per SM
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({ctx->device, smem});
+    if (it != cache.end()) {
+      per_sm = it->second;
+    } else {
+      if (smem > 48 * 1024)
+        DPC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      DPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem));
+      cache[{ctx->device, smem}] = per_sm;
+    }
+  }
+  if (per_sm < 1) return fail(DPC_E_CUDA, "SpMV plan kernel does not fit on an SM");
+  spmvp::Args8 a = a0;
+  void* args[] = {&a};
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(static_cast<unsigned>(per_sm * ctx->sms));  // all blocks co-resident (the barrier)
+  lc.blockDim = dim3(NT);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = HOT ? 1 : 0;  // the hot-column gather kernel precedes it
+  DPC_CUDA(cudaLaunchKernelExC(&lc, fn, args));
+  return DPC_OK;
+}
+
+// y = A x with the G = 8 plan: one hot_gather launch + one persistent drain
+// launch (all blocks co-resident); nohot (shape bit 13) drops the x cache.
+static dpc_status spmv_plan8_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, bool nohot,
+                                 unsigned probe) {
   dpc_status st = spmv_plan8_build(ctx, g);
   if (st != DPC_OK) return st;
   spmvp::Args8 a{};
@@ -584,23 +846,30 @@ static dpc_status spmv_plan8_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, 
   a.nwin = g->plan8_nwin;
   a.bar = g->plan_bar;
   a.hdr = g->hdr;
-  constexpr int NT = 512;
-  constexpr unsigned C = 2;
-  const void* fn = reinterpret_cast<const void*>(spmvp::plan8_drain<NT, C>);
-  static int per_sm_cached[64] = {};
-  int& per_sm = per_sm_cached[ctx->device & 63];
-  if (!per_sm) DPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, 0));
-  if (per_sm < 1) return fail(DPC_E_CUDA, "SpMV plan kernel does not fit on an SM");
-  void* args[] = {&a};
-  DPC_CUDA(cudaLaunchKernel(fn, dim3(per_sm * ctx->sms), dim3(NT), args, 0, ctx->stream));
-  return DPC_OK;
+  a.probe = probe;
+  const unsigned cap = nohot ? 0u : spmv_hot_cap();
+  if (cap == 0 || g->m == 0) return plan8_launch<512, false>(ctx, a, 0);
+  st = spmv_plan8_hot_build(ctx, g, cap);
+  if (st != DPC_OK) return st;
+  a.col = g->plan8h_col;
+  a.xh = g->plan8h_xh;
+  a.nhot4 = g->plan8h_nhot4;
+  spmvp::hot_gather<<<static_cast<unsigned>(ctx->sms), 256, 0, ctx->stream>>>(d_x, g->plan8h_hot, g->plan8h_xh,
+                                                                            a.nhot4);
+  DPC_CUDA(cudaGetLastError());
+  const size_t smem = sizeof(float) * std::max(a.nhot4, 4u);
+  // two 512-thread blocks per SM while both copies fit, else one of 1024
+  if (2 * (smem + 1024) <= static_cast<size_t>(ctx->smem_per_sm)) return plan8_launch<512, true>(ctx, a, smem);
+  return plan8_launch<1024, true>(ctx, a, smem);
 }
 
 // flags: DPC_CFG_* shape bits: default = the G = 8 window form; bit 9 = the
 // G = 4 form with register-staged loads, bit 12 = the G = 4 form with the
 // TMA ring (both measured slower on BASELINE config 2).
 dpc_status spmv_plan_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, int flags) {
-  if (!(flags & ((1 << 9) | (1 << 12)))) return spmv_plan8_run(ctx, g, d_x, d_y);
+  if (!(flags & ((1 << 9) | (1 << 12))))
+    return spmv_plan8_run(ctx, g, d_x, d_y, (flags & (1 << 13)) != 0,
+                          DPC_TIMING_PROBES ? static_cast<unsigned>((flags >> 16) & 7) : 0u);
   dpc_status st = spmv_plan_build(ctx, g);
   if (st != DPC_OK) return st;
   spmvp::Args a{};
