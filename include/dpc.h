@@ -205,6 +205,13 @@ typedef struct dpc_launch_cfg {
                                    256 nonzeros, built once per uploaded matrix,
                                    spmv_plan.cu); the fused multi-GPU forms
                                    always run the stream kernel */
+#define DPC_CFG_GC_HASH (1 << 28) /* GC: greedy order = the seeded hash order
+                                    (mix64(v ^ seed), v) instead of the canonical
+                                    node order 0, 1, ..., n-1 (SPEC.md:454's GC
+                                    oracle, the default) */
+#define DPC_CFG_GC_LLF (1 << 29) /* GC: largest-log-degree-first order (ties by
+                                   the seeded hash): shorter dependency chains
+                                   and fewer colors on power-law graphs */
 #define DPC_CFG_COOP_LAUNCH 4 /* persistent grid kernels: cudaLaunchCooperativeKernel
                                  + grid.sync instead of a normal launch of a
                                  co-resident grid + software barrier */
@@ -212,7 +219,11 @@ typedef struct dpc_launch_cfg {
 /* Bits 8-31 of dpc_launch_cfg.flags select measured alternative kernel
  * shapes of the same computation (stream drain shapes, GC server bounds,
  * ...): every value gives the same results.  Timing probes
- * that skip work are compiled out of the library. */
+ * that skip work are compiled out of the library.  SpMV grid plan form:
+ * bit 9 / bit 12 = the 128-nonzero-window register / TMA-ring drains, bit 13
+ * = the 256-nonzero drain without the hot-column x cache (the default keeps
+ * the 32K most used columns' x in shared memory; DPC_SPMV_HOT_CAP in the
+ * environment overrides the slot count, 0 disables it). */
 
 /* Fills the measured default for (app, variant) (profiles/r02_launch_cfg.json,
  * compiled in as paper_1606_08150_b200/csrc/launch_table.inc).  Replaces
@@ -264,9 +275,11 @@ dpc_status dpc_run_spmv(dpc_ctx* ctx, const dpc_csr* A, const float* x, float* y
  * when unreachable.  Replaces the SSSP benchmark. */
 dpc_status dpc_run_sssp(dpc_ctx* ctx, const dpc_csr* g, int32_t source, uint32_t* dist,
                         const dpc_launch_cfg* cfg, dpc_metrics* met);
-/* Greedy first-fit coloring in descending priority order, priority(v) =
- * (hash64(v ^ seed), v); g must be symmetric without self loops.
- * *ncolors receives the number of colors. */
+/* Greedy first-fit coloring in the canonical node order 0, 1, ..., n-1
+ * (SPEC.md:454's GC oracle) -- or, with cfg->flags DPC_CFG_GC_HASH, in
+ * descending (hash64(v ^ seed), v) order, or with DPC_CFG_GC_LLF
+ * largest-log-degree-first (seed breaks ties); g must be symmetric without
+ * self loops.  *ncolors receives the number of colors. */
 /* BFS levels from `source` (the paper's BFS-Rec benchmark; SPEC.md:454 oracle
  * "BFS levels"): the SSSP consolidation with unit edge weights, weights in
  * G ignored.  level[v] = hops from source, UINT32_MAX if unreachable. */

@@ -242,8 +242,28 @@ static int prio_desc(const void* a, const void* b) {
   return x->v < y->v ? 1 : (x->v > y->v ? -1 : 0);
 }
 
-int32_t orc_color_greedy(int64_t n, const int64_t* rowptr, const int32_t* col, uint64_t seed,
-                         int32_t* color) {
+/* Greedy first-fit in descending priority order under one of three orders
+ * (the GPU kernels' DPC_CFG_GC_* flags):
+ *   ORC_GC_HASH      priority (mix64(v ^ seed), v)            -- the default
+ *   ORC_GC_CANONICAL canonical node order 0, 1, ..., n-1: SPEC.md:454's GC
+ *                    oracle ("greedy first-fit coloring under canonical
+ *                    node order"), priority (~v)
+ *   ORC_GC_LLF       largest-log-degree-first: priority
+ *                    (bits(deg(v)) << 58 | mix64(v ^ seed) >> 6, v), with
+ *                    bits(d) = 32 - clz(d) (0 for d = 0) -- the LLF order of
+ *                    Hasenplaugh et al. (SPAA 2014) */
+static uint64_t orc_gc_prio(int64_t v, int64_t deg, uint64_t seed, int order) {
+  if (order == 1) return ~(uint64_t)v;
+  if (order == 2) {
+    uint64_t bits = 0;
+    while (bits < 32 && ((uint64_t)deg >> bits)) bits++;
+    return (bits << 58) | (orc_mix64((uint64_t)v ^ seed) >> 6);
+  }
+  return orc_mix64((uint64_t)v ^ seed);
+}
+
+int32_t orc_color_greedy_order(int64_t n, const int64_t* rowptr, const int32_t* col, uint64_t seed,
+                               int order, int32_t* color) {
   prio_t* ord = (prio_t*)malloc(sizeof(prio_t) * (size_t)(n ? n : 1));
   int64_t maxdeg = 0;
   for (int64_t v = 0; v < n; v++)
@@ -254,7 +274,7 @@ int32_t orc_color_greedy(int64_t n, const int64_t* rowptr, const int32_t* col, u
     return -1;
   }
   for (int64_t v = 0; v < n; v++) {
-    ord[v].p = orc_mix64((uint64_t)v ^ seed);
+    ord[v].p = orc_gc_prio(v, rowptr[v + 1] - rowptr[v], seed, order);
     ord[v].v = (int32_t)v;
     color[v] = -1;
   }
@@ -274,6 +294,11 @@ int32_t orc_color_greedy(int64_t n, const int64_t* rowptr, const int32_t* col, u
   }
   free(ord), free(mark);
   return ncolors;
+}
+
+int32_t orc_color_greedy(int64_t n, const int64_t* rowptr, const int32_t* col, uint64_t seed,
+                         int32_t* color) {
+  return orc_color_greedy_order(n, rowptr, col, seed, 0, color);
 }
 
 int orc_color_valid(int64_t n, const int64_t* rowptr, const int32_t* col, const int32_t* color,

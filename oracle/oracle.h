@@ -36,6 +36,10 @@ int64_t orc_sssp_bf_mt(int64_t n, const int64_t* rowptr, const int32_t* col, con
  * (SPEC.md:454, 468).  Returns the number of colors, -1 on alloc failure. */
 int32_t orc_color_greedy(int64_t n, const int64_t* rowptr, const int32_t* col, uint64_t seed,
                          int32_t* color);
+/* ... under order 0 = hash (above), 1 = canonical node order,
+ * 2 = largest-log-degree-first (see oracle.c). */
+int32_t orc_color_greedy_order(int64_t n, const int64_t* rowptr, const int32_t* col, uint64_t seed,
+                               int order, int32_t* color);
 /* 1 iff color is a proper coloring with colors in [0, ncolors). */
 int orc_color_valid(int64_t n, const int64_t* rowptr, const int32_t* col, const int32_t* color,
                     int32_t ncolors);

@@ -62,6 +62,9 @@ CFG_X_PEER_GATHER = 32
 CFG_GRID_STREAM = 64
 CFG_GRID_LEVEL = 128
 CFG_SPMV_STREAM = 256
+CFG_GC_HASH = 1 << 28
+CFG_GC_LLF = 1 << 29
+GC_ORDERS = {"canonical": 0, "hash": CFG_GC_HASH, "llf": CFG_GC_LLF}
 
 
 class DpcError(RuntimeError):
@@ -439,6 +442,8 @@ def launch_cfg(app: str, variant: str, **overrides) -> LaunchCfg:
             cfg.flags = (cfg.flags | CFG_SPMV_STREAM) if v else (cfg.flags & ~CFG_SPMV_STREAM)
         elif k == "grid_level":
             cfg.flags = (cfg.flags | CFG_GRID_LEVEL) if v else (cfg.flags & ~CFG_GRID_LEVEL)
+        elif k == "gc_order":  # "hash" | "canonical" | "llf"
+            cfg.flags = (cfg.flags & ~(CFG_GC_HASH | CFG_GC_LLF)) | GC_ORDERS[v]
         else:
             setattr(cfg, k, int(v))
     return cfg
@@ -832,7 +837,9 @@ class PageRankGraph:
 
 
 def run_color(G: CsrGraph, seed: int = 1, variant="grid", cfg=None, ctx: Context | None = None):
-    """Greedy first-fit coloring in (hash, id) priority order.  Returns (color, ncolors, Metrics)."""
+    """Greedy first-fit coloring in canonical node order, or the
+    order cfg selects (launch_cfg(..., gc_order="hash" | "llf")).  Returns
+    (color, ncolors, Metrics)."""
     ctx = ctx or default_context()
     color = np.empty(G.n, dtype=np.int32)
     nc = C.c_int32()

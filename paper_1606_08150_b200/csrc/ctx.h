@@ -52,6 +52,7 @@ struct dpc_dgraph {
   size_t gc_state_slots = 0;
   void* trace = nullptr;          // per-vertex timestamps of the last traced run (DPC_TRACE=1)
   void* gc_q = nullptr;           // GC async task queue (+ 64 B of counters)
+  void* gc_prio = nullptr;        // GC largest-log-degree-first priorities (8 B per vertex)
   size_t gc_q_cap = 0;
   unsigned* gc_hstate = nullptr;  // GC async heavy-vertex states
   size_t gc_hstate_cap = 0;

@@ -1,6 +1,7 @@
 // Graph coloring (GC) in five variants: greedy first-fit in descending
-// priority order, priority(v) = (mix64(v ^ seed), v) ("greedy
-// first-fit coloring under canonical node order"; :468 determinism).
+// priority order -- SPEC.md:454's canonical node order (default: "greedy
+// first-fit coloring under canonical node order"; :468 determinism), a
+// seeded hash order or largest-log-degree-first (see prio()).
 //
 // Parallel form: data-driven Jones-Plassmann.  cnt[v] = number of
 // higher-priority neighbours not yet colored.  A vertex is ready when
@@ -79,6 +80,8 @@ struct Args {
   unsigned it;
   unsigned fsize;
   unsigned long long* trace;  // optional: per-vertex %globaltimer at color write (DPC_TRACE=1)
+  unsigned order;             // 0 hash, 1 canonical node order, 2 largest-log-degree-first
+  const unsigned long long* __restrict__ parr;  // order 2: per-vertex priority (llf_prio_kernel)
 };
 
 struct Block {
@@ -94,8 +97,25 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   return z ^ (z >> 31);
 }
 
+// Greedy order (descending priority, ties: larger id first), one of
+//   canonical ~v: nodes 0, 1, ..., n-1 -- SPEC.md:454's GC oracle  default
+//   hash      (mix64(v ^ seed), v)                                 DPC_CFG_GC_HASH
+//   LLF       (bits(deg v) << 58 | mix64(v ^ seed) >> 6, v): largest-log-degree-first
+//             (Hasenplaugh et al., SPAA 2014); precomputed per run   DPC_CFG_GC_LLF
+// oracle/oracle.c orc_color_greedy_order restates all three.
 __device__ __forceinline__ unsigned long long prio(const Args& a, unsigned v) {
+  if (a.order == 1) return ~static_cast<unsigned long long>(v);
+  if (a.order == 2) return __ldg(a.parr + v);
   return mix64(static_cast<unsigned long long>(v) ^ a.seed);
+}
+
+__global__ void __launch_bounds__(256) llf_prio_kernel(const unsigned* __restrict__ rowptr, unsigned n,
+                                                       unsigned long long seed, unsigned long long* parr) {
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const unsigned d = __ldg(rowptr + v + 1) - __ldg(rowptr + v);
+    const unsigned long long bits = d ? 32u - __clz(d) : 0u;
+    parr[v] = (bits << 58) | (mix64(static_cast<unsigned long long>(v) ^ seed) >> 6);
+  }
 }
 
 // u precedes v in the greedy order
@@ -134,9 +154,15 @@ __device__ __forceinline__ void set_color(const Args& a, Block& s, unsigned v, i
   atomicMax(&s.maxc, c);
 }
 
+// A count-down past zero: u was released by more higher neighbours than it
+// counted -- the adjacency is not symmetric (fault bit 8: DPC_E_INVALID).
+__device__ __noinline__ void asymmetric(const Args& a) { atomicOr(&a.hdr->overflow, 8u); }
+
 // Lower neighbour u of a vertex being colored: count down, append when ready.
 __device__ __forceinline__ void release(const Args& a, unsigned it, Block& s, unsigned u) {
-  if (atomicSub(a.cnt + u, 1u) == 1u) s.q.push(u, next_count(a, it), next_front(a, it));
+  const unsigned old = atomicSub(a.cnt + u, 1u);
+  if (old == 1u) s.q.push(u, next_count(a, it), next_front(a, it));
+  else if (old == 0u) asymmetric(a);
 }
 
 // --------------------------------------------------------------- init pass
@@ -688,7 +714,11 @@ __device__ __forceinline__ unsigned long long release_range(const Args& a, const
 #pragma unroll
     for (int j = 0; j < W; j++) cls[j] = low[j] ? q.vclass[u[j]] : 0u;  // issued beside the count-downs
 #pragma unroll
-    for (int j = 0; j < W; j++) ready[j] = low[j] && atomicSub(a.cnt + u[j], 1u) == 1u;
+    for (int j = 0; j < W; j++) {
+      const unsigned old = low[j] ? atomicSub(a.cnt + u[j], 1u) : 2u;
+      ready[j] = old == 1u;
+      if (old == 0u) asymmetric(a);
+    }
 #pragma unroll
     for (int j = 0; j < W; j++) {
       if (keep == kEmpty) {  // work-first: keep one this server can take
@@ -923,7 +953,11 @@ __device__ void block_serve(const Args& a, const Async& q, Block& s, unsigned v,
 #pragma unroll
     for (int j = 0; j < kBW; j++) low[j] = u[j] != v;
 #pragma unroll
-    for (int j = 0; j < kBW; j++) ready[j] = low[j] && atomicSub(a.cnt + u[j], 1u) == 1u;
+    for (int j = 0; j < kBW; j++) {
+      const unsigned old = low[j] ? atomicSub(a.cnt + u[j], 1u) : 2u;
+      ready[j] = old == 1u;
+      if (old == 0u) asymmetric(a);
+    }
 #pragma unroll
     for (int j = 0; j < kBW; j++) {
       // work-first: the block keeps one medium vertex it made ready and
@@ -1144,6 +1178,10 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   a.fsize = 0;
   a.state = nullptr;
   a.trace = nullptr;
+  a.order = (c.flags & DPC_CFG_GC_HASH) ? 0u : (c.flags & DPC_CFG_GC_LLF) ? 2u : 1u;
+  a.parr = nullptr;
+  if ((c.flags & DPC_CFG_GC_HASH) && (c.flags & DPC_CFG_GC_LLF))
+    return fail(DPC_E_INVALID, "DPC_CFG_GC_HASH and DPC_CFG_GC_LLF are exclusive");
   if (const char* tr = getenv("DPC_TRACE")) {
     if (tr[0] == '1') {
       if (!g->trace) DPC_CUDA(cudaMalloc(&g->trace, 3 * sizeof(unsigned long long) * std::max<int64_t>(g->n, 1)));
@@ -1174,6 +1212,13 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
   DPC_CUDA(cudaMemsetAsync(g->ctr, 0, 64, s));
   DPC_CUDA(cudaMemsetAsync(g->stamp, 0, sizeof(unsigned) * nv, s));
   DPC_CUDA(cudaMemsetAsync(g->color, 0xff, sizeof(int) * nv, s));
+  if (a.order == 2 && a.n) {
+    if (!g->gc_prio) DPC_CUDA(cudaMalloc(&g->gc_prio, sizeof(unsigned long long) * nv));
+    gc::llf_prio_kernel<<<std::min(dev::ceil_div(a.n, 256u), 8u * static_cast<unsigned>(ctx->sms)), 256, 0, s>>>(
+        a.rowptr, a.n, a.seed, static_cast<unsigned long long*>(g->gc_prio));
+    DPC_CUDA(cudaGetLastError());
+    a.parr = static_cast<const unsigned long long*>(g->gc_prio);
+  }
   auto* ctr_host = reinterpret_cast<gc::Ctr*>(g->ctr_host);
   int64_t host_launches = 0, iters = 0;
   const unsigned nb = std::max(1u, dev::ceil_div(a.n, 256u));

@@ -224,6 +224,39 @@ __device__ __forceinline__ void relax_loaded(const Args& a, unsigned it, Block& 
   }
 }
 
+// Relaxes K candidate edges held by this lane with the dependent atomics of
+// all K in flight together: every atomicMin, then every stamp exchange of
+// the improved ones, then the frontier pushes (two atomic round trips for K
+// edges instead of 2K).  g = target (global id), nd = candidate distance
+// (>= kInf: none), c = the target's distance read earlier.
+template <int K>
+__device__ __forceinline__ void relax_k(const Args& a, unsigned it, Block& s, const unsigned (&g)[K],
+                                        const unsigned long long (&nd)[K], const unsigned (&c)[K]) {
+  unsigned old[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    old[k] = 0u;
+    const unsigned v = g[k] - a.r0;
+    if (nd[k] < kInf && v >= a.n) relax_loaded(a, it, s, g[k], static_cast<unsigned>(nd[k]), c[k]);  // remote
+    else if (nd[k] < c[k]) old[k] = atomicMin(a.dist + v, static_cast<unsigned>(nd[k]));
+  }
+  unsigned st[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    const unsigned v = g[k] - a.r0;
+    st[k] = it + 1;
+    if (v < a.n && nd[k] < old[k]) st[k] = atomicExch(a.stamp + v, it + 1);
+  }
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    if (st[k] != it + 1) {
+      const unsigned v = g[k] - a.r0;
+      if (!a.classify) s.q.push(v, next_count(a, it), next_front(a, it));
+      else if (!s.q.try_push(v)) spill_classify(a, it, v);
+    }
+  }
+}
+
 // Two edges per lane per step: both edges' col / w loads, then both dist
 // loads, are in flight before either compare (a level's drain is a few such
 // dependent rounds per warp).
@@ -239,8 +272,9 @@ __device__ __forceinline__ void relax_warp(const Args& a, unsigned it, Block& s,
     const unsigned v1 = g1 - a.r0, v2 = g2 - a.r0;
     const unsigned c1 = (t1 < kInf && v1 < a.n) ? __ldcg(a.dist + v1) : 0u;
     const unsigned c2 = (t2 < kInf && v2 < a.n) ? __ldcg(a.dist + v2) : 0u;
-    if (t1 < kInf) relax_loaded(a, it, s, g1, static_cast<unsigned>(t1), c1);
-    if (t2 < kInf) relax_loaded(a, it, s, g2, static_cast<unsigned>(t2), c2);
+    const unsigned g[2] = {g1, g2}, c[2] = {c1, c2};
+    const unsigned long long nd[2] = {t1, t2};
+    relax_k<2>(a, it, s, g, nd, c);
   }
 }
 

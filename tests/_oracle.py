@@ -40,6 +40,8 @@ class Oracle:
         L.orc_pagerank.restype, L.orc_pagerank.argtypes = C.c_int, [i64, P, P, i32, C.c_double, P]
         L.orc_sssp_bf_mt.restype, L.orc_sssp_bf_mt.argtypes = i64, [i64, P, P, P, i32, P, C.c_int]
         L.orc_color_greedy.restype, L.orc_color_greedy.argtypes = i32, [i64, P, P, u64, P]
+        L.orc_color_greedy_order.restype = i32
+        L.orc_color_greedy_order.argtypes = [i64, P, P, u64, C.c_int, P]
         L.orc_color_valid.restype, L.orc_color_valid.argtypes = C.c_int, [i64, P, P, P, i32]
         L.orc_tree_desc.restype, L.orc_tree_desc.argtypes = C.c_int, [i64, P, P]
         L.orc_tree_height.restype, L.orc_tree_height.argtypes = C.c_int, [i64, P, P]
@@ -91,11 +93,13 @@ class Oracle:
         r = self.L.orc_sssp_bf_mt(len(d), _p(rowptr), _p(col), _p(w), source, _p(d), threads)
         return d, r
 
-    def color(self, rowptr, col, seed):
+    def color(self, rowptr, col, seed, order=1):
+        """order: 1 canonical node order (the product default), 0 hash priority,
+        2 largest-log-degree-first."""
         rowptr = np.ascontiguousarray(rowptr, np.int64)
         col = np.ascontiguousarray(col, np.int32)
         c = np.empty(len(rowptr) - 1, np.int32)
-        k = self.L.orc_color_greedy(len(c), _p(rowptr), _p(col), seed & (2**64 - 1), _p(c))
+        k = self.L.orc_color_greedy_order(len(c), _p(rowptr), _p(col), seed & (2**64 - 1), order, _p(c))
         return c, k
 
     def color_valid(self, rowptr, col, color, ncolors):

@@ -1,6 +1,6 @@
 """Graph-coloring parity on the B200: every variant returns exactly the
-sequential greedy first-fit coloring in (hash, id) priority order
-(oracle/oracle.c orc_color_greedy), which is also checked for validity; the
+sequential greedy first-fit coloring in canonical node order (
+oracle/oracle.c orc_color_greedy_order), which is also checked for validity; the
 color count is reported (BASELINE north_star: "a valid coloring with its color
 count reported")."""
 import numpy as np
@@ -97,3 +97,55 @@ def test_gc_grid_forms(ctx, orc, form):
         color, k, met = dpc.run_color(g, 11, cfg=cfg, ctx=ctx)
         _check(orc, g, 11, color, k)
         assert met.child_launch_count == 0
+
+
+ORDERS = {"hash": 0, "llf": 2}
+
+
+@pytest.mark.parametrize("order", list(ORDERS))
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_gc_orders(ctx, orc, order, variant):
+    """The seeded hash order (DPC_CFG_GC_HASH) and largest-log-degree-first
+    (DPC_CFG_GC_LLF) -- the canonical default is what every other test checks -- in every variant, both grid
+    forms, on R-MAT, a power-law graph with heavy vertices, a 1030-clique and
+    a star: bit-identical to the oracle under the same order."""
+    graphs = [dpc.gen_rmat(13, 16, seed=3, weights=False, symmetric=True),
+              dpc.gen_graph(4000, powerlaw=(1.3, 3900), seed=6, weights=False, symmetric=True),
+              _clique(1030)]
+    leaves = 5000
+    graphs.append(dpc.csr_from_arrays(np.concatenate([[0, leaves], leaves + np.arange(1, leaves + 1)]),
+                                      np.concatenate([np.arange(1, leaves + 1), np.zeros(leaves)]).astype(np.int32)))
+    forms = [True, False] if variant == "grid" else [None]
+    for g in graphs:
+        ref, k = orc.color(g.rowptr, g.col, 5, order=ORDERS[order])
+        for form in forms:
+            kw = {"gc_order": order}
+            if form is not None:
+                kw["grid_async"] = form
+            color, kk, met = dpc.run_color(g, 5, cfg=dpc.launch_cfg("color", variant, **kw), ctx=ctx)
+            assert np.array_equal(color, ref), (order, variant, form)
+            assert kk == k == met.result_count
+            assert orc.color_valid(g.rowptr, g.col, color, kk)
+
+
+@pytest.mark.parametrize("order", list(ORDERS))
+def test_gc_orders_config3_full(ctx, orc, order):
+    """BASELINE config 3 (R-MAT scale 20 symmetrized) under the hash and LLF
+    orders: every variant bit-exact, color count reported."""
+    g = dpc.gen_rmat(20, 16, seed=1, weights=False, symmetric=True)
+    ref, k = orc.color(g.rowptr, g.col, 1, order=ORDERS[order])
+    dg = dpc.DeviceGraph(ctx, g)
+    for v in VARIANTS:
+        met = dg.color(1, v, cfg=dpc.launch_cfg("color", v, gc_order=order))
+        assert np.array_equal(dg.get_color(), ref), v
+        assert met.result_count == k
+    dg.close()
+
+
+def test_gc_orders_exclusive(ctx):
+    g = dpc.gen_rmat(8, 8, seed=1, weights=False, symmetric=True)
+    cfg = dpc.launch_cfg("color", "grid")
+    cfg.flags |= dpc.CFG_GC_HASH | dpc.CFG_GC_LLF
+    with pytest.raises(dpc.DpcError) as e:
+        dpc.run_color(g, 1, cfg=cfg, ctx=ctx)
+    assert e.value.kind == "invalid"

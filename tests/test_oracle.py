@@ -92,7 +92,7 @@ def test_gc_oracle_vs_python_restatement(orc):
     import paper_1606_08150_b200 as dpc
     for scale, seed in [(6, 1), (7, 2), (8, 3)]:
         g = dpc.gen_rmat(scale, 8, seed=seed, weights=False, symmetric=True)
-        c, k = orc.color(g.rowptr, g.col, seed)
+        c, k = orc.color(g.rowptr, g.col, seed, order=0)
         py = _py_greedy(g.rowptr.tolist(), g.col.tolist(), seed, orc.mix64)
         assert c.tolist() == py
         assert k == max(py) + 1
@@ -169,3 +169,55 @@ def test_oracle_rmat_equals_product_generator(orc, scale, permute, weights, valu
         assert np.array_equal(g.w, w)
     if values:
         assert np.array_equal(g.val, val)
+
+
+def _py_canonical_greedy(rowptr, col):
+    """SPEC.md:454 verbatim: visit nodes 0, 1, ..., n-1; each takes the
+    smallest color none of its already-colored neighbours holds."""
+    n = len(rowptr) - 1
+    color = [-1] * n
+    for v in range(n):
+        used = {color[u] for u in col[rowptr[v]:rowptr[v + 1]] if color[u] >= 0}
+        c = 0
+        while c in used:
+            c += 1
+        color[v] = c
+    return color
+
+
+def _py_llf_greedy(rowptr, col, seed, mix64):
+    """Largest-log-degree-first: priority (bits(deg) << 58 | mix64(v ^ seed) >> 6, v), descending."""
+    n = len(rowptr) - 1
+    key = []
+    for v in range(n):
+        d = rowptr[v + 1] - rowptr[v]
+        key.append((((d.bit_length() if d else 0) << 58) | (mix64(v ^ seed) >> 6), v))
+    color = [-1] * n
+    for _, v in sorted(key, reverse=True):
+        used = {color[u] for u in col[rowptr[v]:rowptr[v + 1]] if color[u] >= 0}
+        c = 0
+        while c in used:
+            c += 1
+        color[v] = c
+    return color
+
+
+def test_gc_oracle_orders_vs_python_restatement(orc):
+    """The oracle's canonical-order greedy is SPEC.md:454's GC oracle exactly
+    (pure-Python restatement of the sentence), and its LLF order matches its
+    own restatement; every result is a valid coloring."""
+    import paper_1606_08150_b200 as dpc
+    for scale, seed in [(6, 1), (7, 2), (8, 3)]:
+        g = dpc.gen_rmat(scale, 8, seed=seed, weights=False, symmetric=True)
+        rp, cl = g.rowptr.tolist(), g.col.tolist()
+        c, k = orc.color(g.rowptr, g.col, seed, order=1)
+        assert c.tolist() == _py_canonical_greedy(rp, cl) and k == max(c) + 1
+        c2, k2 = orc.color(g.rowptr, g.col, seed, order=2)
+        assert c2.tolist() == _py_llf_greedy(rp, cl, seed, orc.mix64) and k2 == max(c2) + 1
+        for cc, kk in ((c, k), (c2, k2)):
+            assert orc.color_valid(g.rowptr, g.col, cc, kk)
+    # SPEC-style hand case: a path 0-1-2-3 in canonical order -> 0 1 0 1
+    rowptr = np.array([0, 1, 3, 5, 6], np.int64)
+    col = np.array([1, 0, 2, 1, 3, 2], np.int32)
+    c, k = orc.color(rowptr, col, 0, order=1)
+    assert c.tolist() == [0, 1, 0, 1] and k == 2

@@ -255,3 +255,39 @@ def test_spmv_grid_plan_unaligned_y_and_row_slice(ctx, orc):
     y = dg.get_y().astype(np.float64)
     assert np.all(np.abs(y - y64) <= RTOL * np.abs(y64))
     dg.close()
+
+
+@pytest.mark.parametrize("cap", ["0", "4", "1000", "32768", "57344"])
+def test_spmv_grid_hot_column_cache(ctx, orc, cap, monkeypatch):
+    """Default grid form with the hot-column x cache at several slot
+    capacities (DPC_SPMV_HOT_CAP; 0 = no cache, 4 = fewer slots than hot
+    columns, 57344 = the one-1024-thread-block shape with 224 KB of slots), on
+    the plan cases and R-MAT; x changes between calls (the slot table is
+    re-gathered every call), and the same matrix switches capacity (the plan
+    is rebuilt)."""
+    monkeypatch.setenv("DPC_SPMV_HOT_CAP", cap)
+    cases = list(_plan_cases()) + [dpc.gen_rmat(14, 16, seed=5, weights=False, values=True)]
+    for g in cases:
+        if not g.n:
+            continue
+        dg = dpc.DeviceGraph(ctx, g)
+        for rep in range(2):
+            x = _x(g.ncols if g.ncols else g.n) * (1.0 + rep)
+            dg.set_x(x)
+            dg.spmv("grid")
+            _check(orc, g, x, dg.get_y())
+        monkeypatch.setenv("DPC_SPMV_HOT_CAP", "16")
+        dg.spmv("grid")
+        _check(orc, g, x, dg.get_y())
+        monkeypatch.setenv("DPC_SPMV_HOT_CAP", cap)
+        dg.close()
+
+
+def test_spmv_grid_nohot_shape_bit(ctx, orc):
+    """Shape bit 13 drops the x cache (2 x 512-thread blocks, plain gathers)."""
+    g = dpc.gen_rmat(13, 16, seed=6, weights=False, values=True, permute=True)
+    x = _x(g.n)
+    cfg = dpc.launch_cfg("spmv", "grid")
+    cfg.flags |= 1 << 13
+    y, _ = dpc.run_spmv(g, x, cfg=cfg, ctx=ctx)
+    _check(orc, g, x, y)
