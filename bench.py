@@ -575,7 +575,7 @@ def run_multi(args, dist, rank, world, local):
         sys.exit(1)
 
 
-def _ncu_traffic(profile="r01_spmv_grid_stream.txt"):
+def _ncu_traffic(profile="r02_spmv_plan8_hot_ncu.txt"):
     """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel
     from the committed `ncu --set full` summary (profiles/), in bytes per
     launch -- the ncu capture cannot run inside the timed bench."""
@@ -811,8 +811,9 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "BASELINE config 2: SpMV CSR, synthetic R-MAT scale-20 matrix "
                                "(1,048,576 rows, 16,777,216 nnz, fp32 values/x in (0,1], seed 1)",
-                   "variant": "grid-consolidated: one persistent kernel (one 1024-thread block per SM, all co-resident), insert phase + "
-                              "device-wide barrier + stream-balanced drain (threshold 0, measured)",
+                   "variant": "grid-consolidated with the cached per-matrix window plan: a hot-column gather launch + one "
+                              "persistent drain launch (one 1024-thread block per SM, all co-resident; split-phase "
+                              "device-wide barrier; x at the 32K most used columns in shared memory)",
                    "n": n, "nnz": nnz, "l2": "flushed (512 MB memset) before every timed step",
                    "parallelism": f"replicas{world}" if world > 1 else "single GPU",
                    "generate_s": round(gen_s, 2)},
@@ -836,10 +837,10 @@ def run_ours(args):
                                   "api": "dpc_spmv_host (C ABI), one synchronous call per step, L2 flushed"}},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(),
-                     "traffic_source": "profiles/r01_spmv_grid_stream.txt (ncu --set full, dram bytes read+write per launch)",
-                     "algorithmic_bytes": alg, "kernel": "spmv::grid_stream (whole step)",
+                     "traffic_source": "profiles/r02_spmv_plan8_hot_ncu.txt (ncu --set full, dram bytes read+write per launch)",
+                     "algorithmic_bytes": alg, "kernel": "spmvp::plan8_drain<1024, HOT> (whole step incl. spmvp::hot_gather)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"},
-        "gpu_launches": args.steps * (1 + int(met.child_launch_count)),
+        "gpu_launches": args.steps * (int(met.host_launches) + int(met.child_launch_count)),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

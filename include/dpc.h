@@ -152,6 +152,15 @@ void dpc_tree_free(dpc_tree* t);
  * form (magic "DPCCSR01"). */
 dpc_status dpc_load_csr(const char* path, dpc_csr** out);
 dpc_status dpc_save_csr(const dpc_csr* g, const char* path);
+/* DIMACS ingest (the paper's datasets; SPEC.md:475 names a
+ * converter as the extension): the 9th challenge shortest-path format
+ * ("c" comments, "p sp n m", "a u v w" arcs, 1-based; weights kept) or the
+ * 10th challenge / METIS graph format (CiteSeer, Kron_log16: header
+ * "n m [fmt [ncon]]", then one line of 1-based neighbours per vertex, "%"
+ * comments; fmt 1 / 11 edge weights kept, vertex sizes / weights skipped;
+ * m counts undirected edges, so the CSR holds 2m arcs).  The format is taken
+ * from the first non-comment line.  Arcs keep file order within a row. */
+dpc_status dpc_load_dimacs(const char* path, dpc_csr** out);
 /* Tree text format SPEC.md:473: line 1 nodeCount, line 2 parent per node. */
 dpc_status dpc_load_tree(const char* path, dpc_tree** out);
 dpc_status dpc_save_tree(const dpc_tree* t, const char* path);

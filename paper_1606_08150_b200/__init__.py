@@ -131,6 +131,7 @@ _SIGS = {
     "dpc_tree_create": (C.c_int, [_i64, _P, C.POINTER(_TreeP)]),
     "dpc_tree_free": (None, [_TreeP]),
     "dpc_load_csr": (C.c_int, [C.c_char_p, C.POINTER(_CsrP)]),
+    "dpc_load_dimacs": (C.c_int, [C.c_char_p, C.POINTER(_CsrP)]),
     "dpc_save_csr": (C.c_int, [_CsrP, C.c_char_p]),
     "dpc_load_tree": (C.c_int, [C.c_char_p, C.POINTER(_TreeP)]),
     "dpc_save_tree": (C.c_int, [_TreeP, C.c_char_p]),
@@ -374,6 +375,14 @@ def tree_from_parent(parent) -> Tree:
 def load_csr(path: str) -> CsrGraph:
     h = _CsrP()
     _check(_lib.dpc_load_csr(os.fsencode(path), C.byref(h)))
+    return CsrGraph(h)
+
+
+def load_dimacs(path: str) -> CsrGraph:
+    """DIMACS 9th-challenge .gr (weighted arcs) or 10th-challenge / METIS
+    graph file (dpc_load_dimacs)."""
+    h = _CsrP()
+    _check(_lib.dpc_load_dimacs(os.fsencode(path), C.byref(h)))
     return CsrGraph(h)
 
 

@@ -189,7 +189,8 @@ inline void defer_check(dpc_dgraph* g) {
 void sssp_state_free(void* state);
 // SpMV grid variant with the cached per-matrix window plan (spmv_plan.cu).
 dpc_status spmv_plan_build(dpc_ctx* ctx, dpc_dgraph* g);
-dpc_status spmv_plan_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, int flags);
+// *launches += the host-side kernel launches of the call (1, or 2 with the hot-column gather).
+dpc_status spmv_plan_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, int flags, int* launches);
 // SSSP / BFS grid variant, frontier stream form (sssp_stream.cu).
 dpc_status sssp_stream_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, bool unit, bool coop,
                            int64_t* host_launches, int64_t* levels, dpc_metrics* met);

@@ -636,6 +636,104 @@ dpc_status dpc_load_csr(const char* path, dpc_csr** out) {
   DPC_TRY_END
 }
 
+dpc_status dpc_load_dimacs(const char* path, dpc_csr** out) {
+  DPC_TRY_BEGIN
+  if (!path || !out) return fail(DPC_E_INVALID, "NULL argument");
+  std::string p(path);
+  TextReader r;
+  if (!r.load(path)) return fail(DPC_E_IO, "cannot read " + p);
+  size_t b, e;
+  auto skip = [&](char c) { return b < e && r.buf[b] == c; };
+  // first non-comment line decides the format
+  bool found = false;
+  while (r.line(&b, &e)) {
+    while (b < e && (r.buf[b] == ' ' || r.buf[b] == '\t' || r.buf[b] == '\r')) b++;
+    if (b == e || skip('c') || skip('%')) continue;
+    found = true;
+    break;
+  }
+  if (!found) return fail(DPC_E_IO, "empty DIMACS file");
+  std::vector<int64_t> cnt;  // per-row arc counts, then offsets
+  std::vector<int32_t> src, dst, wt;
+  int64_t n = 0;
+  bool weighted = false;
+  if (skip('p')) {  // 9th challenge: p sp n m / a u v w
+    long long nn = -1, mm = -1;
+    char kind[16] = {0};
+    std::string head = r.buf.substr(b, e - b);
+    if (std::sscanf(head.c_str(), "p %15s %lld %lld", kind, &nn, &mm) != 3 || nn < 0 || mm < 0)
+      return fail(DPC_E_IO, "malformed DIMACS problem line");
+    n = nn;
+    weighted = true;
+    src.reserve(static_cast<size_t>(mm));
+    std::vector<int64_t> t;
+    while (r.line(&b, &e)) {
+      while (b < e && (r.buf[b] == ' ' || r.buf[b] == '\t' || r.buf[b] == '\r')) b++;
+      if (b == e || skip('c')) continue;
+      if (!skip('a')) return fail(DPC_E_IO, "DIMACS arc line expected ('a u v w')");
+      t.clear();
+      if (r.ints(b + 1, e, t) != 3) return fail(DPC_E_IO, "DIMACS arc line must hold u v w");
+      if (t[0] < 1 || t[0] > n || t[1] < 1 || t[1] > n) return fail(DPC_E_IO, "DIMACS arc endpoint out of range");
+      if (t[2] < 0 || t[2] > INT32_MAX) return fail(DPC_E_IO, "DIMACS arc weight out of range");
+      src.push_back(static_cast<int32_t>(t[0] - 1));
+      dst.push_back(static_cast<int32_t>(t[1] - 1));
+      wt.push_back(static_cast<int32_t>(t[2]));
+    }
+    if (static_cast<long long>(src.size()) != mm) return fail(DPC_E_IO, "DIMACS arc count differs from the problem line");
+  } else {  // 10th challenge / METIS: n m [fmt [ncon]], then n adjacency lines
+    std::vector<int64_t> h;
+    if (r.ints(b, e, h) < 2 || h[0] < 0 || h[1] < 0) return fail(DPC_E_IO, "malformed METIS header line");
+    n = h[0];
+    const int64_t fmt = h.size() > 2 ? h[2] : 0, ncon = h.size() > 3 ? h[3] : 1;
+    const bool vsize = (fmt / 100) % 10 == 1, vwgt = (fmt / 10) % 10 == 1;
+    weighted = fmt % 10 == 1;
+    if (fmt != 0 && fmt != 1 && fmt != 10 && fmt != 11 && fmt != 100 && fmt != 101 && fmt != 110 && fmt != 111)
+      return fail(DPC_E_IO, "unknown METIS fmt field");
+    const int64_t skipv = (vsize ? 1 : 0) + (vwgt ? ncon : 0);
+    src.reserve(static_cast<size_t>(2 * h[1]));
+    std::vector<int64_t> t;
+    int64_t v = 0;
+    while (v < n && r.line(&b, &e)) {
+      size_t bb = b;
+      while (bb < e && (r.buf[bb] == ' ' || r.buf[bb] == '\t' || r.buf[bb] == '\r')) bb++;
+      if (bb < e && r.buf[bb] == '%') continue;
+      t.clear();
+      if (r.ints(b, e, t) < 0) return fail(DPC_E_IO, "non-integer token in METIS adjacency line");
+      if (static_cast<int64_t>(t.size()) < skipv) return fail(DPC_E_IO, "METIS line shorter than its vertex fields");
+      const int64_t per = weighted ? 2 : 1;
+      if ((static_cast<int64_t>(t.size()) - skipv) % per) return fail(DPC_E_IO, "METIS neighbour / weight pairs incomplete");
+      for (size_t k = static_cast<size_t>(skipv); k < t.size(); k += per) {
+        if (t[k] < 1 || t[k] > n) return fail(DPC_E_IO, "METIS neighbour out of range");
+        src.push_back(static_cast<int32_t>(v));
+        dst.push_back(static_cast<int32_t>(t[k] - 1));
+        if (weighted) {
+          if (t[k + 1] < 0 || t[k + 1] > INT32_MAX) return fail(DPC_E_IO, "METIS edge weight out of range");
+          wt.push_back(static_cast<int32_t>(t[k + 1]));
+        }
+      }
+      v++;
+    }
+    if (v != n) return fail(DPC_E_IO, "METIS file ends before its n adjacency lines");
+    if (static_cast<int64_t>(src.size()) != 2 * h[1]) return fail(DPC_E_IO, "METIS arc count differs from 2 m");
+  }
+  // counting sort by source, stable (file order within a row)
+  const int64_t m = static_cast<int64_t>(src.size());
+  std::vector<int64_t> rp(static_cast<size_t>(n + 1), 0);
+  for (int64_t k = 0; k < m; k++) rp[src[k] + 1]++;
+  for (int64_t i = 0; i < n; i++) rp[i + 1] += rp[i];
+  std::vector<int64_t> at(rp.begin(), rp.end() - 1);
+  std::vector<int32_t> c(static_cast<size_t>(m)), w(weighted ? static_cast<size_t>(m) : 0);
+  for (int64_t k = 0; k < m; k++) {
+    const int64_t q = at[src[k]]++;
+    c[q] = dst[k];
+    if (weighted) w[q] = wt[k];
+  }
+  dpc_status st = dpc_csr_create(n, m, rp.data(), c.data(), weighted ? w.data() : nullptr, nullptr, out);
+  if (st != DPC_OK) return fail(DPC_E_IO, std::string("invalid graph in file: ") + dpc_last_error());
+  return DPC_OK;
+  DPC_TRY_END
+}
+
 dpc_status dpc_save_csr(const dpc_csr* g, const char* path) {
   DPC_TRY_BEGIN
   if (!path) return fail(DPC_E_INVALID, "path is NULL");

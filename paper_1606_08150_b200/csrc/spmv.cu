@@ -1549,14 +1549,15 @@ dpc_status dpc::spmv_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d
       st = begin_run(ctx, g->hdr);
       if (st != DPC_OK) return st;
     }
+    int launches = 0;
     if (g->m > 0 || g->n > 0) {
-      st = spmv_plan_run(ctx, g, d_x, d_y, c.flags);
+      st = spmv_plan_run(ctx, g, d_x, d_y, c.flags, &launches);
       if (st != DPC_OK) return st;
       DPC_CUDA(cudaGetLastError());
     }
     g->hdr_clean = true;  // the plan kernel writes only fault bits into the header
     if (met) {
-      met->host_launches += 1;
+      met->host_launches += launches;
       met->edges_processed += g->m;
       met->iterations += 1;
       return finish_metrics(ctx, g->hdr, g->hdr_host, met);

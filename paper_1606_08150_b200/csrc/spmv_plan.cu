@@ -831,7 +831,7 @@ static dpc_status plan8_launch(dpc_ctx* ctx, const spmvp::Args8& a0, size_t smem
 // y = A x with the G = 8 plan: one hot_gather launch + one persistent drain
 // launch (all blocks co-resident); nohot (shape bit 13) drops the x cache.
 static dpc_status spmv_plan8_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, bool nohot,
-                                 unsigned probe) {
+                                 unsigned probe, int* launches) {
   dpc_status st = spmv_plan8_build(ctx, g);
   if (st != DPC_OK) return st;
   spmvp::Args8 a{};
@@ -857,6 +857,7 @@ static dpc_status spmv_plan8_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, 
   spmvp::hot_gather<<<static_cast<unsigned>(ctx->sms), 256, 0, ctx->stream>>>(d_x, g->plan8h_hot, g->plan8h_xh,
                                                                             a.nhot4);
   DPC_CUDA(cudaGetLastError());
+  *launches += 1;
   const size_t smem = sizeof(float) * std::max(a.nhot4, 4u);
   // two 512-thread blocks per SM while both copies fit, else one of 1024
   if (2 * (smem + 1024) <= static_cast<size_t>(ctx->smem_per_sm)) return plan8_launch<512, true>(ctx, a, smem);
@@ -866,10 +867,11 @@ static dpc_status spmv_plan8_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, 
 // flags: DPC_CFG_* shape bits: default = the G = 8 window form; bit 9 = the
 // G = 4 form with register-staged loads, bit 12 = the G = 4 form with the
 // TMA ring (both measured slower on BASELINE config 2).
-dpc_status spmv_plan_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, int flags) {
+dpc_status spmv_plan_run(dpc_ctx* ctx, dpc_dgraph* g, const float* d_x, float* d_y, int flags, int* launches) {
+  *launches += 1;
   if (!(flags & ((1 << 9) | (1 << 12))))
     return spmv_plan8_run(ctx, g, d_x, d_y, (flags & (1 << 13)) != 0,
-                          DPC_TIMING_PROBES ? static_cast<unsigned>((flags >> 16) & 7) : 0u);
+                          DPC_TIMING_PROBES ? static_cast<unsigned>((flags >> 16) & 7) : 0u, launches);
   dpc_status st = spmv_plan_build(ctx, g);
   if (st != DPC_OK) return st;
   spmvp::Args a{};

@@ -221,3 +221,83 @@ def test_benchmark_registry():
         assert dpc.benchmark(name).name.lower() == name.lower()
     with pytest.raises(dpc.DpcError):
         dpc.benchmark("PR")
+
+
+def _write_gr(path, n, arcs, comment=True):
+    lines = (["c generated by test_host"] if comment else []) + [f"p sp {n} {len(arcs)}"]
+    lines += [f"a {u + 1} {v + 1} {w}" for u, v, w in arcs]
+    path.write_text("\n".join(lines) + "\n")
+
+
+def _write_metis(path, adj, weights=None):
+    n = len(adj)
+    m2 = sum(len(a) for a in adj)
+    fmt = " 1" if weights is not None else ""
+    lines = ["% METIS graph", f"{n} {m2 // 2}{fmt}"]
+    for v, a in enumerate(adj):
+        if weights is None:
+            lines.append(" ".join(str(u + 1) for u in a))
+        else:
+            lines.append(" ".join(f"{u + 1} {w}" for u, w in zip(a, weights[v])))
+    path.write_text("\n".join(lines) + "\n")
+
+
+def test_dimacs_gr_matches_generated_graph(tmp_path):
+    """A generated weighted R-MAT graph written as a DIMACS 9th-challenge .gr
+    file (arcs shuffled) loads back to the same CSR (rows regrouped, file
+    order kept within a row) with its weights."""
+    g = dpc.gen_rmat(9, 8, seed=4)
+    src = np.repeat(np.arange(g.n), g.degrees())
+    arcs = list(zip(src.tolist(), g.col.tolist(), g.w.tolist()))
+    p = tmp_path / "g.gr"
+    _write_gr(p, g.n, arcs)
+    h = dpc.load_dimacs(str(p))
+    assert np.array_equal(h.rowptr, g.rowptr) and np.array_equal(h.col, g.col) and np.array_equal(h.w, g.w)
+    rng = np.random.default_rng(1)
+    perm = rng.permutation(len(arcs))
+    _write_gr(p, g.n, [arcs[i] for i in perm], comment=False)
+    h = dpc.load_dimacs(str(p))
+    assert np.array_equal(h.rowptr, g.rowptr)
+    for v in range(g.n):  # same multiset of (col, w) per row
+        a = sorted(zip(g.col[g.rowptr[v]:g.rowptr[v + 1]].tolist(), g.w[g.rowptr[v]:g.rowptr[v + 1]].tolist()))
+        b = sorted(zip(h.col[h.rowptr[v]:h.rowptr[v + 1]].tolist(), h.w[h.rowptr[v]:h.rowptr[v + 1]].tolist()))
+        assert a == b
+
+
+def test_dimacs_metis_graph(tmp_path):
+    """DIMACS 10th-challenge / METIS adjacency (the paper's CiteSeer /
+    Kron_log16 format): undirected, 1-based, m = undirected edges; fmt 1 edge
+    weights; vertex-weight fields skipped; '%' comments."""
+    g = dpc.gen_rmat(8, 8, seed=2, weights=False, symmetric=True)
+    adj = [g.col[g.rowptr[v]:g.rowptr[v + 1]].tolist() for v in range(g.n)]
+    p = tmp_path / "g.graph"
+    _write_metis(p, adj)
+    h = dpc.load_dimacs(str(p))
+    assert np.array_equal(h.rowptr, g.rowptr) and np.array_equal(h.col, g.col)
+    wts = [[(v * 7 + u) % 13 + 1 for u in a] for v, a in enumerate(adj)]
+    _write_metis(p, adj, wts)
+    h = dpc.load_dimacs(str(p))
+    assert np.array_equal(h.col, g.col) and h.w.tolist() == [w for ws in wts for w in ws]
+    # fmt 10 (one vertex weight per line, skipped), isolated vertex, comment line
+    p.write_text("% tri + isolated\n4 3 10\n5 2 3\n% inner comment\n6 1 3\n7 1 2\n8\n")
+    h = dpc.load_dimacs(str(p))
+    assert h.rowptr.tolist() == [0, 2, 4, 6, 6] and h.col.tolist() == [1, 2, 0, 2, 0, 1]
+
+
+@pytest.mark.parametrize("text", ["p sp 2 1\na 1 3 5\n",          # endpoint out of range
+                                  "p sp 2 2\na 1 2 5\n",          # fewer arcs than declared
+                                  "p sp 2 1\nx 1 2 5\n",          # not an arc line
+                                  "3 2\n2\n1 3\n",                # METIS: missing line
+                                  "2 1\n2\n1\n",                  # ok shape but ... (valid: see below)
+                                  "2 1 1\n2\n1 4\n",              # fmt 1: neighbour without weight
+                                  "2 1 7\n2\n1\n"])               # unknown fmt
+def test_dimacs_errors(tmp_path, text):
+    p = tmp_path / "bad.gr"
+    p.write_text(text)
+    if text == "2 1\n2\n1\n":  # the one well-formed case
+        h = dpc.load_dimacs(str(p))
+        assert h.col.tolist() == [1, 0]
+        return
+    with pytest.raises(dpc.DpcError) as e:
+        dpc.load_dimacs(str(p))
+    assert e.value.kind == "io"

@@ -192,3 +192,19 @@ def test_sssp_scale22_default_grid_is_stream_form(ctx, orc):
     dg.sssp(s, "grid", cfg=dpc.launch_cfg("sssp", "grid", grid_level=True))
     assert np.array_equal(dg.get_dist(), ref)
     dg.close()
+
+
+def test_sssp_on_dimacs_ingested_graph(ctx, orc, tmp_path):
+    """A DIMACS 9th-challenge .gr file (the paper's dataset format) through
+    dpc_load_dimacs, then every SSSP variant on the GPU: bit-exact."""
+    g = dpc.gen_rmat(12, 16, seed=21)
+    src = np.repeat(np.arange(g.n), g.degrees())
+    p = tmp_path / "g.gr"
+    lines = [f"p sp {g.n} {g.m}"] + [f"a {u + 1} {v + 1} {w}" for u, v, w in zip(src, g.col, g.w)]
+    p.write_text("\n".join(lines) + "\n")
+    h = dpc.load_dimacs(str(p))
+    s = int(np.argmax(h.degrees()))
+    ref = orc.sssp(h.rowptr, h.col, h.w, s)
+    for v in ["flat", "basic", "warp", "block", "grid"]:
+        d, _ = dpc.run_sssp(h, s, v, ctx=ctx)
+        assert np.array_equal(d, ref), v
