@@ -295,7 +295,7 @@ def run_config5(args, dist, rank, world, device):
     if world == 1:
         dg.set_x(x_full)
         steps_of["single_gpu_grid"] = (lambda: dg.spmv("grid"), dg.get_y, dg.x_ptr, dg.y_ptr)
-        launches["single_gpu_grid"] = 1
+        launches["single_gpu_grid"] = 2  # hot-column gather + drain
     else:
         dx = ipc.alloc(4 * R)
         ctx.h2d(dx, x_full[r0:r0 + R])
@@ -304,7 +304,7 @@ def run_config5(args, dist, rank, world, device):
             dist.broadcast_object_list(uid, src=0)
             comm = dpc.Comm(ctx, rank, world, uid[0])
             steps_of["nccl_allgather"] = (lambda: comm.spmv(dg, dx, dg.y_ptr), dg.get_y, dx, dg.y_ptr)
-            launches["nccl_allgather"] = 2
+            launches["nccl_allgather"] = 3  # all-gather + hot-column gather + drain
         flags = ipc.alloc(16 * world)
         ctx.h2d(flags, np.zeros(2 * world, np.uint64))
         ctx.synchronize()
