@@ -594,6 +594,12 @@ __device__ __forceinline__ void flush_classify(const Args& a, unsigned it, Block
   __syncthreads();
 }
 
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // a.pool.cap = capacity of ONE half of the pool (the host allocates two).
 __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_iters) {
   __shared__ Block s;
@@ -602,8 +608,10 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
   block_begin(s);
   unsigned it = 0;
   for (; it < max_iters; it++) {
-    const unsigned fs = *reinterpret_cast<volatile unsigned*>(&a.ctr->fsize[it % 3]);
-    const unsigned pc = min(*reinterpret_cast<volatile unsigned*>(&a.ctr->pool[it % 3]), a.pool.cap);
+    // level sizes (written before the barrier; relaxed gpu-scope loads, the
+    // barrier orders them -- volatile would be system-scope)
+    const unsigned fs = ld_relaxed_gpu(&a.ctr->fsize[it % 3]);
+    const unsigned pc = min(ld_relaxed_gpu(&a.ctr->pool[it % 3]), a.pool.cap);
     if (fs == 0 && pc == 0) break;
     if (gtid == 0) {  // the counters level it+1 produces into were last read at level it-1
       atomicAdd(&a.hdr->aux1, pc);
