@@ -413,6 +413,9 @@ void dpc_host_free(void* p);
  * context stream (synchronous). */
 dpc_status dpc_copy_h2d(dpc_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
 dpc_status dpc_copy_d2h(dpc_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+/* Fills device memory with a byte value on the context stream (asynchronous;
+ * ordered before the stream's later work). */
+dpc_status dpc_dev_memset(dpc_ctx* ctx, void* dst_dev, int32_t value, size_t bytes);
 
 /* Diagnostics: with DPC_TRACE=1 in the environment, the coloring kernels
  * record per vertex %globaltimer (ns) at its color write [0, n), at its

@@ -193,6 +193,7 @@ _SIGS = {
     "dpc_host_alloc": (_P, [C.c_size_t]),
     "dpc_host_free": (None, [_P]),
     "dpc_copy_h2d": (C.c_int, [_P, _P, _P, C.c_size_t]),
+    "dpc_dev_memset": (C.c_int, [_P, _P, C.c_int32, C.c_size_t]),
     "dpc_copy_d2h": (C.c_int, [_P, _P, _P, C.c_size_t]),
     "dpc_comm_unique_id": (C.c_int, [_P]),
     "dpc_comm_init": (C.c_int, [_P, _i32, _i32, _P, C.POINTER(_P)]),
@@ -500,6 +501,10 @@ class Context:
 
     def free(self, p: int):
         _lib.dpc_dev_free(self._h, p)
+
+    def memset(self, dst: int, value: int, nbytes: int):
+        """Byte fill of device memory on the context stream (asynchronous)."""
+        _check(_lib.dpc_dev_memset(self._h, dst, value, nbytes))
 
     def h2d(self, dst: int, a: np.ndarray):
         a = np.ascontiguousarray(a)

@@ -325,6 +325,12 @@ dpc_status dpc_copy_h2d(dpc_ctx* c, void* dst, const void* src, size_t bytes) {
   return DPC_OK;
 }
 
+dpc_status dpc_dev_memset(dpc_ctx* c, void* dst, int32_t value, size_t bytes) {
+  if (!c) return fail(DPC_E_INVALID, "ctx is NULL");
+  DPC_CUDA(cudaMemsetAsync(dst, value, bytes, c->stream));
+  return DPC_OK;
+}
+
 dpc_status dpc_copy_d2h(dpc_ctx* c, void* dst, const void* src, size_t bytes) {
   if (!c) return fail(DPC_E_INVALID, "ctx is NULL");
   DPC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));

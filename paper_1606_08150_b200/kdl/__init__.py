@@ -152,9 +152,24 @@ class Result:
         self.arrays, self.launches, self.runs, self.kc, self.ms = arrays, launches, runs, kc, ms
 
 
+_CTX = {}
+
+
+def _context(device):
+    """The library context (device + stream) the modules run on: device
+    memory, copies, events and the launch stream all come from libdpc.so
+    (no torch on this path).  Raises DpcError('cuda') without an sm_100 GPU
+    -- there is no CPU fallback."""
+    from .. import Context
+    if device not in _CTX:
+        _CTX[device] = Context(device)
+    return _CTX[device]
+
+
 class Module:
-    """A compiled program.  run() owns device memory through torch (plumbing);
-    every kernel that executes is generated code from this module's .so."""
+    """A compiled program.  run() owns device memory through the library
+    context (dpc_dev_alloc / dpc_copy_* / dpc_dev_memset); every kernel that
+    executes is generated code from this module's .so."""
 
     def __init__(self, prog, so, kc, mode, width=64):
         self.prog, self.so, self.kc_rows, self.mode, self.width = prog, so, kc, mode, width
@@ -164,9 +179,7 @@ class Module:
                                if s.kind == "buf_decl" and s.gran == "grid"] or [0])
 
     def _load(self, device, pending):
-        import torch
-        if not torch.cuda.is_available():
-            raise RuntimeError("kdl modules run on the CUDA device only (no CPU fallback)")
+        ctx = _context(device)
         if self.lib is None:
             L = C.CDLL(self.so)
             L.dk_error.restype = C.c_char_p
@@ -178,14 +191,13 @@ class Module:
                 raise RuntimeError("kdl runtime struct layout mismatch")
             self.lib = L
         if self._dev != device:
-            torch.cuda.set_device(device)
-            torch.cuda.synchronize()
+            ctx.synchronize()
             if self.lib.dk_init(device, pending) != 0:
                 raise RuntimeError("dk_init: " + self.lib.dk_error().decode())
             self._dev = device
         kc = (C.c_longlong * max(1, len(self.kc_rows)))()
         self.lib.dk_kc_values(kc)
-        return {f"{k}/KC_{x}/T{t}": int(kc[i]) for i, (k, x, t) in enumerate(self.kc_rows)}
+        return ctx, {f"{k}/KC_{x}/T{t}": int(kc[i]) for i, (k, x, t) in enumerate(self.kc_rows)}
 
     def run(self, scalars, arrays=None, *, until_stable=None, max_runs=10000, device=0,
             pool_bytes=1 << 30, inst_cap=1 << 20, pending=1 << 17, timed=False):
@@ -193,99 +205,113 @@ class Module:
         repeat it until that array stops changing (the host sweep loop the
         SSSP / TH formulations need).  Returns Result(arrays as numpy,
         device launches, entry runs, KC block counts, device ms)."""
-        import torch
-        kc = self._load(device, pending)
+        ctx, kc = self._load(device, pending)
         arrays = arrays or {}
-        dev = torch.device("cuda", device)
         for n in arrays:
             if self.prog.global_(n) is None:
                 raise KdlError("run.array", f"{n!r} is not a global array of the program")
         rt = _Rt()
-        keep = []
-        tens = {}
-        for i, g in enumerate(self.prog.globals):
-            ln = int(eval_host(g.length, scalars))
-            if ln < 0:
-                raise KdlError("run.array", f"array {g.name!r} has negative length {ln}")
-            w32 = self.width == 32
-            dt = (torch.float32 if w32 else torch.float64) if g.type == ast.FLOAT else \
-                (torch.int32 if w32 else torch.int64)
-            if g.name in arrays:
-                npt = (np.float32 if w32 else np.float64) if g.type == ast.FLOAT else (np.int32 if w32 else np.int64)
-                src = np.asarray(arrays[g.name])
-                if w32 and g.type != ast.FLOAT and src.size and (src.min() < -2**31 or src.max() >= 2**31):
-                    raise KdlError("run.array", f"array {g.name!r} does not fit the 32-bit width")
-                a = src.astype(npt)
-                if a.shape != (ln,):
-                    raise KdlError("run.array", f"array {g.name!r} must have {ln} elements, got {a.shape}")
-                t = torch.from_numpy(a.copy()).to(dev)
-            else:
-                t = torch.zeros(max(ln, 0), dtype=dt, device=dev)
-            tens[g.name] = t
-            rt.arr[i] = t.data_ptr() if ln > 0 else 0
-            rt.len[i] = ln
-        rt.narr = len(self.prog.globals)
-        ctr = torch.zeros(8, dtype=torch.int64, device=dev)
-        arena_words = max(1, pool_bytes // 8)
-        arena = torch.empty(arena_words, dtype=torch.int64, device=dev)
-        inst = torch.zeros(3 * inst_cap, dtype=torch.int64, device=dev)
-        region_words = max(1, self.grid_total // 8) if self.grid_total else 1
-        regions = [torch.empty(region_words, dtype=torch.int64, device=dev) for _ in range(2)]
-        keep += [ctr, arena, inst] + regions
-        rt.ctr, rt.arena, rt.arena_words = ctr.data_ptr(), arena.data_ptr(), arena_words
-        rt.inst, rt.inst_cap = inst.data_ptr(), inst_cap
-        rt.region[0], rt.region[1] = regions[0].data_ptr(), regions[1].data_ptr()
-        rt.region_words = region_words
-        if self.lib.dk_set_rt(C.byref(rt)) != 0:
-            raise RuntimeError("dk_set_rt: " + self.lib.dk_error().decode())
+        bufs = []  # every device allocation of this run (freed at the end)
 
-        e = self.prog.entry
-        ek = self.prog.kernel(e.kernel)
-        g = int(eval_host(e.grid, scalars))
-        b = int(eval_host(e.block, scalars))
-        if len(e.args) != len(ek.params):
-            raise KdlError("run.entry", f"entry passes {len(e.args)} arguments, kernel takes {len(ek.params)}")
-        args = (C.c_longlong * max(1, len(e.args)))()
-        for j, (a, p) in enumerate(zip(e.args, ek.params)):
-            if p.is_array:
-                args[j] = [x.name for x in self.prog.globals].index(a.name)
-            elif p.type == ast.FLOAT:
-                args[j] = int(np.array([float(eval_host(a, scalars))], np.float64).view(np.int64)[0])
-            else:
-                v = eval_host(a, scalars)
-                if isinstance(v, float):
-                    raise KdlError("run.entry", f"float argument for int parameter {p.name!r}")
-                args[j] = int(v)
-        stream = torch.cuda.current_stream(dev)
-        launches, runs, ms = 0, 0, 0.0
-        watch = tens.get(until_stable) if until_stable else None
-        if until_stable and watch is None:
-            raise KdlError("run.array", f"until_stable names unknown array {until_stable!r}")
-        while True:
-            ctr.zero_()
-            ctr[3] = 1
-            inst[:3].zero_()
-            before = watch.clone() if watch is not None else None
-            if timed:
-                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                t0.record(stream)
-            rc = self.lib.dk_launch_entry(g, b, args, inst.data_ptr(), C.c_void_p(stream.cuda_stream))
-            if rc != 0:
-                raise RuntimeError("entry launch: " + self.lib.dk_error().decode())
-            if timed:
-                t1.record(stream)
-            stream.synchronize()
-            if timed:
-                ms += t0.elapsed_time(t1)
-            c = ctr.cpu().tolist()
-            runs += 1
-            launches += c[1]
-            if c[0]:
-                raise KdlFault(c[0])
-            if watch is None or torch.equal(before, watch) or runs >= max_runs:
-                break
-        out = {n: t.cpu().numpy() for n, t in tens.items()}
-        del keep
+        def alloc(nbytes):
+            p = ctx.alloc(max(int(nbytes), 8))
+            bufs.append(p)
+            return p
+
+        try:
+            devarr = {}  # name -> (device pointer, length, numpy dtype)
+            for i, g in enumerate(self.prog.globals):
+                ln = int(eval_host(g.length, scalars))
+                if ln < 0:
+                    raise KdlError("run.array", f"array {g.name!r} has negative length {ln}")
+                w32 = self.width == 32
+                npt = (np.float32 if w32 else np.float64) if g.type == ast.FLOAT else (np.int32 if w32 else np.int64)
+                ptr = 0
+                if ln > 0:
+                    ptr = alloc(ln * np.dtype(npt).itemsize)
+                    if g.name in arrays:
+                        src = np.asarray(arrays[g.name])
+                        if w32 and g.type != ast.FLOAT and src.size and (src.min() < -2**31 or src.max() >= 2**31):
+                            raise KdlError("run.array", f"array {g.name!r} does not fit the 32-bit width")
+                        a = src.astype(npt)
+                        if a.shape != (ln,):
+                            raise KdlError("run.array", f"array {g.name!r} must have {ln} elements, got {a.shape}")
+                        ctx.h2d(ptr, a)
+                    else:
+                        ctx.memset(ptr, 0, ln * np.dtype(npt).itemsize)
+                elif g.name in arrays and np.asarray(arrays[g.name]).size:
+                    raise KdlError("run.array", f"array {g.name!r} must have 0 elements")
+                devarr[g.name] = (ptr, ln, npt)
+                rt.arr[i] = ptr
+                rt.len[i] = ln
+            rt.narr = len(self.prog.globals)
+            ctr = alloc(8 * 8)
+            arena_words = max(1, pool_bytes // 8)
+            arena = alloc(8 * arena_words)
+            inst = alloc(8 * 3 * inst_cap)
+            ctx.memset(inst, 0, 8 * 3 * inst_cap)
+            region_words = max(1, self.grid_total // 8) if self.grid_total else 1
+            regions = [alloc(8 * region_words) for _ in range(2)]
+            rt.ctr, rt.arena, rt.arena_words = ctr, arena, arena_words
+            rt.inst, rt.inst_cap = inst, inst_cap
+            rt.region[0], rt.region[1] = regions[0], regions[1]
+            rt.region_words = region_words
+            if self.lib.dk_set_rt(C.byref(rt)) != 0:
+                raise RuntimeError("dk_set_rt: " + self.lib.dk_error().decode())
+
+            e = self.prog.entry
+            ek = self.prog.kernel(e.kernel)
+            gdim = int(eval_host(e.grid, scalars))
+            bdim = int(eval_host(e.block, scalars))
+            if len(e.args) != len(ek.params):
+                raise KdlError("run.entry", f"entry passes {len(e.args)} arguments, kernel takes {len(ek.params)}")
+            args = (C.c_longlong * max(1, len(e.args)))()
+            for j, (a, p) in enumerate(zip(e.args, ek.params)):
+                if p.is_array:
+                    args[j] = [x.name for x in self.prog.globals].index(a.name)
+                elif p.type == ast.FLOAT:
+                    args[j] = int(np.array([float(eval_host(a, scalars))], np.float64).view(np.int64)[0])
+                else:
+                    v = eval_host(a, scalars)
+                    if isinstance(v, float):
+                        raise KdlError("run.entry", f"float argument for int parameter {p.name!r}")
+                    args[j] = int(v)
+            stream = C.c_void_p(ctx.stream)
+            launches, runs, ms = 0, 0, 0.0
+            if until_stable and until_stable not in devarr:
+                raise KdlError("run.array", f"until_stable names unknown array {until_stable!r}")
+
+            def fetch(name):
+                ptr, ln, npt = devarr[name]
+                return ctx.d2h(ptr, ln, npt) if ln > 0 else np.zeros(0, npt)
+
+            ctr_init = np.array([0, 0, 0, 1, 0, 0, 0, 0], np.int64)
+            while True:
+                ctx.h2d(ctr, ctr_init)
+                ctx.memset(inst, 0, 8 * 3)
+                before = fetch(until_stable) if until_stable else None
+                if timed:
+                    ctx.record(60)
+                rc = self.lib.dk_launch_entry(gdim, bdim, args, C.c_void_p(inst), stream)
+                if rc != 0:
+                    raise RuntimeError("entry launch: " + self.lib.dk_error().decode())
+                if timed:
+                    ctx.record(61)
+                ctx.synchronize()
+                if timed:
+                    ms += ctx.elapsed_ms(60, 61)
+                c = ctx.d2h(ctr, 8, np.int64).tolist()
+                runs += 1
+                launches += c[1]
+                if c[0]:
+                    raise KdlFault(c[0])
+                if not until_stable or np.array_equal(before, fetch(until_stable)) or runs >= max_runs:
+                    break
+            out = {n: fetch(n) for n in devarr}
+        finally:
+            ctx.synchronize()
+            for p in bufs:
+                ctx.free(p)
         return Result(out, launches, runs, kc, ms)
 
 
