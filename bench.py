@@ -660,12 +660,14 @@ def sssp_section(ctx, args):
         alg = sssp_bytes(gr["relaxed_edges"], fv)
         peak = _peak_hbm()
         out["roofline"] = {"bound": "hbm", "achieved": round(alg / (gr["ms"] * 1e-3) / 1e9, 1), "peak": peak,
-                           "unit": "GB/s", "frac": round(alg / (gr["ms"] * 1e-3) / 1e9 / peak, 4), "traffic": None,
+                           "unit": "GB/s", "frac": round(alg / (gr["ms"] * 1e-3) / 1e9 / peak, 4),
+                           "traffic": _ncu_traffic("r02_sssp22_stream_ncu.txt"),
                            "algorithmic_bytes": alg,
                            "bytes_rule": "12 B x relaxed edges (metrics.edges_processed) + 12 B x frontier "
                                          "vertices (metrics.vertices_processed), SURVEY.md 8(d)",
                            "kernel": "ssst::stream_persistent (frontier stream form; whole run, one launch)",
-                           "traffic_source": "profiles/r02_sssp24_forms.txt (scale 24)"}
+                           "traffic_source": "profiles/r02_sssp22_stream_ncu.txt (ncu --set full, the same graph, "
+                                             "dram bytes read+write of the run's launch)"}
         if "ms" in variants.get("flat", {}):
             out["grid_vs_flat"] = round(variants["flat"]["ms"] / gr["ms"], 2)
     if not args.no_cpu_baseline:
