@@ -400,9 +400,13 @@ struct Args8 {
 };
 
 // x gather through the hot-column cache: slot-encoded columns read shared memory.
+// With the cache the remaining (cold) gathers are read L2-only (ld.global.cg):
+// measured 52.5 vs 54.3 us on config 2 (L1-allocating) and 55.8 us
+// (L1::no_allocate); without it, L1 is the only cache x has.
 template <bool HOT>
 __device__ __forceinline__ float xget(const float* __restrict__ x, const float* sx, int c) {
   if (HOT && c < 0) return sx[c & 0x7fffffff];
+  if (HOT) return __ldcg(x + c);
   return __ldg(x + c);
 }
 
