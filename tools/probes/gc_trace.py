@@ -8,12 +8,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import paper_1606_08150_b200 as dpc  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+order_name = sys.argv[2] if len(sys.argv) > 2 else "canonical"  # the library default since round 2
 ctx = dpc.Context(0)
 g = dpc.gen_rmat(scale, 16, seed=1, weights=False, symmetric=True)
 dg = dpc.DeviceGraph(ctx, g)
-dg.color(1, "grid")
+cfg = dpc.launch_cfg("color", "grid", gc_order=order_name)
+dg.color(1, "grid", cfg=cfg)
 ctx.flush_l2()
-dg.color(1, "grid", metrics=False)
+dg.color(1, "grid", cfg=cfg, metrics=False)
 n = g.n
 allt = dg.trace(3 * n).astype(np.int64)
 ts, tq, td = allt[:n].copy(), allt[n:2 * n].copy(), allt[2 * n:].copy()
@@ -34,9 +36,12 @@ def mix64(z):
 
 with np.errstate(over="ignore"):
     pr = mix64(np.arange(n, dtype=np.uint64) ^ np.uint64(1))
-order = np.lexsort((np.arange(n), pr))[::-1]
-rank = np.empty(n, np.int64)
-rank[order] = np.arange(n)
+if order_name == "canonical":
+    rank = np.arange(n, dtype=np.int64)  # node 0 first
+else:
+    order = np.lexsort((np.arange(n), pr))[::-1]
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
 # level + the predecessor that colored last (critical predecessor)
 src = np.repeat(np.arange(n), deg)
 col = g.col.astype(np.int64)
