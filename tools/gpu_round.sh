@@ -25,7 +25,7 @@ for s in $STAGES; do
         --no-cpu-baseline --no-kdl --apps > gpurun_out/ncu_launch_bench.log 2>&1
       echo "ncu-launches rc=$?" ;;
     full)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:grid_stream \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:plan8_drain \
         -s 2 -c 1 -f -o gpurun_out/prof_spmv_grid python tools/prof_spmv.py grid --reps 3 \
         > gpurun_out/ncu_full.log 2>&1
       echo "ncu-full rc=$?"; tail -3 gpurun_out/ncu_full.log ;;
