@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -194,34 +195,49 @@ __device__ __forceinline__ void warp_flush(const Args& a, Warp& wp, unsigned lvl
   __syncwarp();
 }
 
-// Relaxes the masked elements of one group (col c, weights wv) from du; a
-// vertex whose distance drops joins F_{lvl+1} once (bitmap dedup) through
-// the warp's queue.  All lanes call.
-template <bool UNIT>
-__device__ __forceinline__ void relax_grp(const Args& a, Warp& wp, unsigned* nbits, unsigned lvl, unsigned du,
-                                          const int4& c, const int4& wv, unsigned m) {
-  const int cc[4] = {c.x, c.y, c.z, c.w};
-  const int ww[4] = {wv.x, wv.y, wv.z, wv.w};
-  unsigned nd[4], cur[4];
+// Relaxes the masked elements of V groups (cols c[v], weights wv[v], from
+// source distances du[v]); a vertex whose distance drops joins F_{lvl+1}
+// once (bitmap dedup) through the warp's queue.  The 4V elements' distance
+// loads, then their atomicMins, then the improved ones' bitmap marks go out
+// together: three round trips per call, not up to 2 per element.  All lanes
+// call.
+template <bool UNIT, int V>
+__device__ __forceinline__ void relax_grps(const Args& a, Warp& wp, unsigned* nbits, unsigned lvl,
+                                           const unsigned (&du)[V], const int4 (&c)[V], const int4 (&wv)[V],
+                                           const unsigned (&m)[V]) {
+  unsigned cc[4 * V], nd[4 * V], old[4 * V];
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const unsigned long long t = static_cast<unsigned long long>(du) + (UNIT ? 1u : static_cast<unsigned>(ww[i]));
-    nd[i] = ((m >> i) & 1u) && t < kInf ? static_cast<unsigned>(t) : kInf;
-    cur[i] = nd[i] != kInf ? ld_dist(a.dist + cc[i]) : 0u;
+  for (int v = 0; v < V; v++) {
+    const int cv[4] = {c[v].x, c[v].y, c[v].z, c[v].w};
+    const int wvv[4] = {wv[v].x, wv[v].y, wv[v].z, wv[v].w};
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const unsigned long long t = static_cast<unsigned long long>(du[v]) + (UNIT ? 1u : static_cast<unsigned>(wvv[i]));
+      cc[4 * v + i] = static_cast<unsigned>(cv[i]);
+      nd[4 * v + i] = ((m[v] >> i) & 1u) && t < kInf ? static_cast<unsigned>(t) : kInf;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4 * V; k++) old[k] = nd[k] != kInf ? ld_dist(a.dist + cc[k]) : 0u;
+#pragma unroll
+  for (int k = 0; k < 4 * V; k++) old[k] = nd[k] < old[k] ? atomic_min_dist(a.dist + cc[k], nd[k]) : 0u;
+  unsigned ins = 0;
+#pragma unroll
+  for (int k = 0; k < 4 * V; k++) {
+    if (nd[k] < old[k]) {
+      const unsigned bit = 1u << (cc[k] & 31u);
+      if (!(atomicOr(nbits + (cc[k] >> 5), bit) & bit)) ins |= 1u << k;
+    }
   }
   const unsigned lane = dev::lane_id();
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    bool in = false;
-    if (nd[i] < cur[i] && nd[i] < atomic_min_dist(a.dist + cc[i], nd[i])) {
-      const unsigned v = static_cast<unsigned>(cc[i]), bit = 1u << (v & 31u);
-      in = !(atomicOr(nbits + (v >> 5), bit) & bit);
-    }
+  for (int k = 0; k < 4 * V; k++) {
+    const bool in = (ins >> k) & 1u;
     const unsigned ball = __ballot_sync(kFull, in);
-    if (in) wp.q[wp.qn + __popc(ball & ((1u << lane) - 1u))] = static_cast<unsigned>(cc[i]);
+    if (in) wp.q[wp.qn + __popc(ball & ((1u << lane) - 1u))] = cc[k];
     wp.qn += __popc(ball);
+    if (k % 4 == 3 && wp.qn > QW - 128) warp_flush(a, wp, lvl);
   }
-  if (wp.qn > QW - 128) warp_flush(a, wp, lvl);
 }
 
 // Per-warp window onto the level's item list: KB items + their sources'
@@ -287,9 +303,10 @@ __device__ __forceinline__ void drain(const Args& a, Warp& wp, const uint4* item
           c[v] = ld_stream4(a.col + kb + W * v);
           wv[v] = UNIT ? make_int4(1, 1, 1, 1) : ld_stream4(a.w + kb + W * v);
         }
+        unsigned dus[V], ms[V];
 #pragma unroll
-        for (int v = 0; v < V; v++)
-          relax_grp<UNIT>(a, wp, nbits, lvl, du, c[v], wv[v], grp_mask(kb + W * v, it.y, it.z));
+        for (int v = 0; v < V; v++) dus[v] = du, ms[v] = grp_mask(kb + W * v, it.y, it.z);
+        relax_grps<UNIT, V>(a, wp, nbits, lvl, dus, c, wv, ms);
         if (iend == p0 + W * V) ja++;
         continue;
       }
@@ -322,8 +339,7 @@ __device__ __forceinline__ void drain(const Args& a, Warp& wp, const uint4* item
       c[v] = mm[v] ? ld_stream4(a.col + kk[v]) : make_int4(0, 0, 0, 0);
       wv[v] = UNIT || !mm[v] ? make_int4(1, 1, 1, 1) : ld_stream4(a.w + kk[v]);
     }
-#pragma unroll
-    for (int v = 0; v < V; v++) relax_grp<UNIT>(a, wp, nbits, lvl, dd[v], c[v], wv[v], mm[v]);
+    relax_grps<UNIT, V>(a, wp, nbits, lvl, dd, c, wv, mm);
   }
 }
 
@@ -426,13 +442,14 @@ dpc_status sssp_stream_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, bool uni
   constexpr int NT = 512, V = 2;
   const void* fn = unit ? reinterpret_cast<const void*>(ssst::stream_persistent<true, NT, V>)
                         : reinterpret_cast<const void*>(ssst::stream_persistent<false, NT, V>);
+  const int nt = NT;
   int per_sm = 0;
-  DPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, 0));
+  DPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, 0));
   if (per_sm < 1) return fail(DPC_E_CUDA, "frontier stream kernel does not fit on an SM");
   const int blocks = per_sm * ctx->sms;
   void* args[] = {&a};
-  if (coop) DPC_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(NT), args, 0, s));
-  else DPC_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(NT), args, 0, s));
+  if (coop) DPC_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(nt), args, 0, s));
+  else DPC_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(nt), args, 0, s));
   *host_launches += 2;
   if (met) {
     ssst::Ctr c{};
