@@ -96,7 +96,7 @@ __device__ __forceinline__ unsigned warp_reserve(unsigned* counter, unsigned wan
 // multiple of 32, <= 1024).  Returns this thread's offset inside the block and
 // the block total in *btotal.  All threads call.
 __device__ __forceinline__ unsigned block_excl_scan(unsigned want, unsigned* btotal) {
-  __shared__ unsigned s_warp[32];
+  __shared__ unsigned s_warp[33];  // 32 warp offsets + the block total (a 1024-thread block has 32 warps)
   unsigned incl = warp_incl_scan(want);
   const unsigned w = warp_in_block(), nw = blockDim.x >> 5;
   if (lane_id() == 31) s_warp[w] = incl;
@@ -105,11 +105,11 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned want, unsigned* bto
     unsigned x = lane_id() < nw ? s_warp[lane_id()] : 0;
     unsigned xi = warp_incl_scan(x);
     if (lane_id() < nw) s_warp[lane_id()] = xi - x;  // exclusive warp offsets
-    if (lane_id() == 31) s_warp[31] = xi;             // nw <= 32: lane 31 holds the total
+    if (lane_id() == 31) s_warp[32] = xi;             // lane 31 holds the total
   }
   __syncthreads();
   unsigned off = s_warp[w] + incl - want;
-  *btotal = s_warp[31];
+  *btotal = s_warp[32];
   __syncthreads();  // s_warp is reused by the next call
   return off;
 }
