@@ -63,3 +63,29 @@ def test_tree_block_sizes(ctx, orc, variant, threads):
     r = _run_or_refuse(lambda: dpc.run_tree_height(t, variant, cfg=cfg_h, ctx=ctx))
     if r is not None:
         assert np.array_equal(r[0], orc.tree_height(t.parent))
+
+
+@pytest.mark.parametrize("kc", [(0, 0), (1, 0), (32, 0), (0, 1), (0, 7), (0, 1000)])
+@pytest.mark.parametrize("variant", ["warp", "block", "grid"])
+def test_child_geometry(ctx, orc, variant, kc):
+    """KC_X divisor (0 = "1-1") and explicit child block counts, down to a
+    single child block, for SpMV / SSSP / GC / TD: exact."""
+    kc_x, blocks = kc
+    over = {"kc_x": kc_x}
+    if blocks:
+        over["child_blocks"] = blocks
+    g = dpc.gen_rmat(12, 16, seed=9, weights=True, values=True)
+    x = _x(g.n)
+    y64 = orc.spmv_f64(g.rowptr, g.col, g.val, x)
+    y, _ = dpc.run_spmv(g, x, variant, cfg=dpc.launch_cfg("spmv", variant, threshold=8, **over), ctx=ctx)
+    assert np.all(np.abs(y.astype(np.float64) - y64) <= 1e-5 * np.abs(y64) + 1e-30)
+    s = int(np.argmax(g.degrees()))
+    d, _ = dpc.run_sssp(g, s, variant, cfg=dpc.launch_cfg("sssp", variant, threshold=8, **over), ctx=ctx)
+    assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, s))
+    gs = dpc.gen_rmat(12, 16, seed=9, weights=False, symmetric=True)
+    c, k, _ = dpc.run_color(gs, 1, variant, cfg=dpc.launch_cfg("color", variant, **over), ctx=ctx)
+    ref, kr = orc.color(gs.rowptr, gs.col, 1)
+    assert np.array_equal(c, ref) and k == kr
+    t = dpc.gen_tree(9, 1, 5, 0.8, 4)
+    r, _ = dpc.run_tree_desc(t, variant, cfg=dpc.launch_cfg("tree_desc", variant, **over), ctx=ctx)
+    assert np.array_equal(r, orc.tree_desc(t.parent))
