@@ -940,13 +940,23 @@ __device__ void block_serve(const Args& a, const Async& q, Block& s, unsigned v,
     set_color_async(a, q, s, v, c);
   }
   __syncthreads();
-  for (unsigned k0 = m; k0 < e; k0 += kBW * blockDim.x) {
+  // Only the first kBW * blockDim.x lower edges are released by this block:
+  // the rest go out as phase-B release chunks to the warp servers, so the
+  // block moves on to the medium vertex it keeps (work-first) without
+  // waiting for the whole lower part.
+  const unsigned rend = min(e, m + kBW * blockDim.x);
+  if (e > rend) {
+    const unsigned nchb = (e - m + kAsyncChunk - 1) / kAsyncChunk;
+    for (unsigned c0 = (rend - m) / kAsyncChunk; c0 < nchb; c0 += blockDim.x)
+      enqueue(a, q, c0 + tid < nchb, task(v, c0 + tid, 1, 1));
+  }
+  for (unsigned k0 = m; k0 < rend; k0 += kBW * blockDim.x) {
     bool low[kBW], ready[kBW];
     if (k0 != m) {
 #pragma unroll
       for (int j = 0; j < kBW; j++) {
         const unsigned k = k0 + j * blockDim.x + tid;
-        u[j] = k < e ? static_cast<unsigned>(__ldg(q.hcol + k)) : v;
+        u[j] = k < rend ? static_cast<unsigned>(__ldg(q.hcol + k)) : v;
         cls[j] = u[j] != v ? q.vclass[u[j]] : 0u;
       }
     }
