@@ -131,6 +131,33 @@ __device__ __forceinline__ unsigned block_reserve(unsigned* counter, unsigned wa
   return at;
 }
 
+// Two block-aggregated reservations at once (one scan pass, both global
+// atomics issued back to back by one thread): *at_a / *at_b receive this
+// thread's first slots on counters ca / cb.  All threads call; ends with a
+// barrier.
+__device__ __forceinline__ void block_reserve2(unsigned* ca, unsigned wa, unsigned* cb, unsigned wb,
+                                               unsigned* at_a, unsigned* at_b) {
+  __shared__ unsigned s_a[32], s_b[32], s_base[2];
+  const unsigned ia = warp_incl_scan(wa), ib = warp_incl_scan(wb);
+  const unsigned w = warp_in_block(), nw = blockDim.x >> 5;
+  if (lane_id() == 31) s_a[w] = ia, s_b[w] = ib;
+  __syncthreads();
+  if (w == 0) {
+    const unsigned x = lane_id() < nw ? s_a[lane_id()] : 0, y = lane_id() < nw ? s_b[lane_id()] : 0;
+    const unsigned xi = warp_incl_scan(x), yi = warp_incl_scan(y);
+    if (lane_id() < nw) s_a[lane_id()] = xi - x, s_b[lane_id()] = yi - y;
+    if (lane_id() == 31) {
+      const unsigned ba = xi ? atomicAdd(ca, xi) : 0u;
+      const unsigned bb = yi ? atomicAdd(cb, yi) : 0u;
+      s_base[0] = ba, s_base[1] = bb;
+    }
+  }
+  __syncthreads();
+  *at_a = s_base[0] + s_a[w] + ia - wa;
+  *at_b = s_base[1] + s_b[w] + ib - wb;
+  __syncthreads();  // the shared slots are reused by the next call
+}
+
 // Block-local append queue in shared memory: pushes are shared-memory
 // atomics; flush() publishes the block's items with ONE global atomic.  A
 // push that finds the queue full spills straight to global memory.

@@ -576,11 +576,9 @@ __device__ __forceinline__ void flush_classify(const Args& a, unsigned it, Block
       else light = 1;
     }
     dev::block_add_u64(&s.work, want ? e - b : 0u);  // heavy edges are relaxed next level (all lanes)
-    unsigned lbase, ltot;
-    const unsigned lat = dev::block_reserve(&a.ctr->fsize[nxt], light, &lbase, &ltot);
+    unsigned lat, cat;
+    dev::block_reserve2(&a.ctr->fsize[nxt], light, &a.ctr->pool[nxt], want, &lat, &cat);
     if (light) next_front(a, it)[lat] = v;
-    unsigned cbase, ctot;
-    const unsigned cat = dev::block_reserve(&a.ctr->pool[nxt], want, &cbase, &ctot);
     if (want) {
       const dev::Pool p{a.pool.items + half * a.pool.cap, a.pool.cap};
       dev::write_chunks(p, a.hdr, cat, v, b, e, a.chunk);
