@@ -664,6 +664,7 @@ dpc_status dpc_load_dimacs(const char* path, dpc_csr** out) {
     if (std::sscanf(head.c_str(), "p %15s %lld %lld", kind, &nn, &mm) != 3 || nn < 0 || mm < 0)
       return fail(DPC_E_IO, "malformed DIMACS problem line");
     n = nn;
+    if (n > INT32_MAX) return fail(DPC_E_IO, "DIMACS graph has more than 2^31 - 1 vertices");
     weighted = true;
     src.reserve(static_cast<size_t>(mm));
     std::vector<int64_t> t;
@@ -684,6 +685,7 @@ dpc_status dpc_load_dimacs(const char* path, dpc_csr** out) {
     std::vector<int64_t> h;
     if (r.ints(b, e, h) < 2 || h[0] < 0 || h[1] < 0) return fail(DPC_E_IO, "malformed METIS header line");
     n = h[0];
+    if (n > INT32_MAX) return fail(DPC_E_IO, "METIS graph has more than 2^31 - 1 vertices");
     const int64_t fmt = h.size() > 2 ? h[2] : 0, ncon = h.size() > 3 ? h[3] : 1;
     const bool vsize = (fmt / 100) % 10 == 1, vwgt = (fmt / 10) % 10 == 1;
     weighted = fmt % 10 == 1;
@@ -716,6 +718,7 @@ dpc_status dpc_load_dimacs(const char* path, dpc_csr** out) {
     if (v != n) return fail(DPC_E_IO, "METIS file ends before its n adjacency lines");
     if (static_cast<int64_t>(src.size()) != 2 * h[1]) return fail(DPC_E_IO, "METIS arc count differs from 2 m");
   }
+  if (n > INT32_MAX) return fail(DPC_E_IO, "DIMACS graph has more than 2^31 - 1 vertices");
   // counting sort by source, stable (file order within a row)
   const int64_t m = static_cast<int64_t>(src.size());
   std::vector<int64_t> rp(static_cast<size_t>(n + 1), 0);
