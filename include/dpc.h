@@ -138,6 +138,11 @@ dpc_status dpc_gen_tree(int32_t depth, int32_t min_children, int32_t max_childre
  * invariants.  w / val may be NULL. */
 dpc_status dpc_csr_create(int64_t n, int64_t m, const int64_t* rowptr, const int32_t* col,
                           const int32_t* w, const float* val, dpc_csr** out);
+/* The same for a row slice of a larger matrix (ncols > 0: column ids index
+ * the whole matrix's columns, as the partitioned multi-GPU paths need for a
+ * rank's row block of the caller's own graph). */
+dpc_status dpc_csr_create_rows(int64_t n, int64_t ncols, int64_t m, const int64_t* rowptr, const int32_t* col,
+                               const int32_t* w, const float* val, dpc_csr** out);
 dpc_status dpc_csr_validate(const dpc_csr* g);
 void dpc_csr_free(dpc_csr* g);
 

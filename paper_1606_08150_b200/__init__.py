@@ -126,6 +126,7 @@ _SIGS = {
     "dpc_gen_graph_powerlaw": (C.c_int, [_i64, _f64, _i32, _i32, _i32, _u64, _u32, C.POINTER(_CsrP)]),
     "dpc_gen_tree": (C.c_int, [_i32, _i32, _i32, _f64, _u64, C.POINTER(_TreeP)]),
     "dpc_csr_create": (C.c_int, [_i64, _i64, _P, _P, _P, _P, C.POINTER(_CsrP)]),
+    "dpc_csr_create_rows": (C.c_int, [_i64, _i64, _i64, _P, _P, _P, _P, C.POINTER(_CsrP)]),
     "dpc_csr_validate": (C.c_int, [_CsrP]),
     "dpc_csr_free": (None, [_CsrP]),
     "dpc_tree_create": (C.c_int, [_i64, _P, C.POINTER(_TreeP)]),
@@ -363,6 +364,19 @@ def csr_from_arrays(rowptr, col, w=None, val=None) -> CsrGraph:
     h = _CsrP()
     _check(_lib.dpc_csr_create(len(rowptr) - 1, len(col), _ptr(rowptr), _ptr(col), _ptr(w),
                                _ptr(val), C.byref(h)))
+    return CsrGraph(h)
+
+
+def csr_rows_from_arrays(rowptr, col, ncols, w=None, val=None) -> CsrGraph:
+    """A row slice of a larger matrix: col holds global column ids < ncols
+    (dpc_csr_create_rows; the partitioned multi-GPU paths take such slices)."""
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    w = None if w is None else np.ascontiguousarray(w, dtype=np.int32)
+    val = None if val is None else np.ascontiguousarray(val, dtype=np.float32)
+    h = _CsrP()
+    _check(_lib.dpc_csr_create_rows(len(rowptr) - 1, ncols, len(col), _ptr(rowptr), _ptr(col), _ptr(w),
+                                    _ptr(val), C.byref(h)))
     return CsrGraph(h)
 
 

@@ -351,16 +351,16 @@ dpc_status dpc_csr_validate(const dpc_csr* g) {
   return DPC_OK;
 }
 
-dpc_status dpc_csr_create(int64_t n, int64_t m, const int64_t* rowptr, const int32_t* col,
-                          const int32_t* w, const float* val, dpc_csr** out) {
-  DPC_TRY_BEGIN
+static dpc_status make_csr(int64_t n, int64_t ncols, int64_t m, const int64_t* rowptr, const int32_t* col,
+                           const int32_t* w, const float* val, dpc_csr** out) {
   if (!out) return fail(DPC_E_INVALID, "out is NULL");
-  dpc_csr tmp{n, m, const_cast<int64_t*>(rowptr), const_cast<int32_t*>(col), nullptr, nullptr, 0};
+  dpc_csr tmp{n, m, const_cast<int64_t*>(rowptr), const_cast<int32_t*>(col), nullptr, nullptr, ncols};
   dpc_status st = dpc_csr_validate(&tmp);
   if (st != DPC_OK) return st;
   std::unique_ptr<dpc_csr, void (*)(dpc_csr*)> g(new_csr(), dpc_csr_free);
   g->n = n;
   g->m = m;
+  g->ncols = ncols;
   g->rowptr = xalloc<int64_t>(n + 1);
   std::memcpy(g->rowptr, rowptr, sizeof(int64_t) * (n + 1));
   g->col = xalloc<int32_t>(m);
@@ -375,6 +375,20 @@ dpc_status dpc_csr_create(int64_t n, int64_t m, const int64_t* rowptr, const int
   }
   *out = g.release();
   return DPC_OK;
+}
+
+dpc_status dpc_csr_create(int64_t n, int64_t m, const int64_t* rowptr, const int32_t* col,
+                          const int32_t* w, const float* val, dpc_csr** out) {
+  DPC_TRY_BEGIN
+  return make_csr(n, 0, m, rowptr, col, w, val, out);
+  DPC_TRY_END
+}
+
+dpc_status dpc_csr_create_rows(int64_t n, int64_t ncols, int64_t m, const int64_t* rowptr, const int32_t* col,
+                               const int32_t* w, const float* val, dpc_csr** out) {
+  DPC_TRY_BEGIN
+  if (ncols <= 0) return fail(DPC_E_INVALID, "a row slice needs ncols > 0");
+  return make_csr(n, ncols, m, rowptr, col, w, val, out);
   DPC_TRY_END
 }
 

@@ -89,3 +89,72 @@ def test_fuzz_trees(ctx, orc, seed):
         assert np.array_equal(r, orc.tree_desc(parent)), v
         h, _ = dpc.run_tree_height(t, v, ctx=ctx)
         assert np.array_equal(h, orc.tree_height(parent)), v
+
+
+@pytest.mark.parametrize("seed", SEEDS[:8])
+def test_fuzz_partitioned_sssp_spmv(ctx, orc, seed):
+    """The caller's own graph cut into `world` row blocks
+    (dpc_csr_create_rows, global column ids): partitioned SSSP with the host
+    transport, bit-exact; fused SpMV partitions pulling x from the owners,
+    within 1e-5."""
+    g, rng = _graph(seed)
+    n = g.n
+    world = int(rng.integers(2, 6))
+    R = -(-n // world)
+    s = int(rng.integers(0, n))
+    want = orc.sssp(g.rowptr, g.col, g.w, s)
+    blocks = []
+    for p in range(world):
+        r0, r1 = min(n, p * R), min(n, (p + 1) * R)
+        lo, hi = g.rowptr[r0], g.rowptr[r1]
+        blocks.append(dpc.csr_rows_from_arrays(g.rowptr[r0:r1 + 1] - lo, g.col[lo:hi], ncols=n,
+                                               w=g.w[lo:hi], val=g.val[lo:hi]))
+    dgs = [dpc.DeviceGraph(ctx, b) for b in blocks]
+    try:
+        ranks = [dpc.PartitionedSSSP(dg, p, world, n, s, "grid") for p, dg in enumerate(dgs)]
+        for _ in range(n + 1):
+            counts = [r.relax() for r in ranks]
+            inbox = [[] for _ in range(world)]
+            for p, r in enumerate(ranks):
+                for q in range(world):
+                    if q != p and counts[p][q]:
+                        inbox[q].append(r.outgoing(q, int(counts[p][q])))
+            nxt = [r.apply(np.concatenate(inbox[q]) if inbox[q] else np.zeros((0, 2), np.uint32))
+                   for q, r in enumerate(ranks)]
+            if sum(nxt) == 0:
+                break
+        for r in ranks:
+            r.end()
+        got = np.concatenate([dg.get_dist() for dg in dgs])[:n]
+        np.testing.assert_array_equal(got, want)
+        # fused SpMV over the same blocks: x slices in a pointer table
+        x = (rng.integers(1, 1 << 20, n) / float(1 << 20)).astype(np.float32)
+        y64 = orc.spmv_f64(g.rowptr, g.col, g.val, x)
+        bufs = []
+        xs = []
+        for p in range(world):
+            d = ctx.alloc(4 * R)
+            bufs.append(d)
+            sl = np.zeros(R, np.float32)
+            part = x[p * R:min(n, (p + 1) * R)]
+            sl[:len(part)] = part
+            ctx.h2d(d, sl)
+            xs.append(d)
+        tab = ctx.alloc(8 * world)
+        bufs.append(tab)
+        ctx.h2d(tab, np.array(xs, np.uint64))
+        for p, dg in enumerate(dgs):
+            r0, r1 = min(n, p * R), min(n, (p + 1) * R)
+            if r1 == r0:
+                continue
+            yd = ctx.alloc(4 * (r1 - r0))
+            bufs.append(yd)
+            dg.spmv_fused(tab, world, R, yd, cfg=dpc.launch_cfg("spmv", "grid"))
+            y = ctx.d2h(yd, r1 - r0).astype(np.float64)
+            ref = y64[r0:r1]
+            assert np.all(np.abs(y - ref) <= 1e-5 * np.abs(ref) + 1e-30), p
+        for b in bufs:
+            ctx.free(b)
+    finally:
+        for dg in dgs:
+            dg.close()
