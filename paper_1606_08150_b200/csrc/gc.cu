@@ -903,6 +903,17 @@ __device__ void block_serve(const Args& a, const Async& q, Block& s, unsigned v,
   const unsigned tid = threadIdx.x;
   const unsigned b = __ldg(a.rowptr + v), e = __ldg(a.rowptr + v + 1);
   const unsigned m = b + __ldg(q.hsplit + v);
+  // the first release batch's neighbours and classes do not depend on the
+  // color: load them before the gather of the higher neighbours' colors,
+  // off the dependency chain
+  unsigned u[kBW], cls[kBW];
+#pragma unroll
+  for (int j = 0; j < kBW; j++) {
+    const unsigned k = m + j * blockDim.x + tid;
+    u[j] = k < e ? static_cast<unsigned>(__ldg(q.hcol + k)) : v;
+  }
+#pragma unroll
+  for (int j = 0; j < kBW; j++) cls[j] = u[j] != v ? q.vclass[u[j]] : 0u;
   if (tid < kVW) sbm[tid] = 0;
   if (tid == 0) *sflag = 0;
   __syncthreads();
@@ -924,16 +935,6 @@ __device__ void block_serve(const Args& a, const Async& q, Block& s, unsigned v,
   }
   if (over) atomicOr(sflag, 1u);
   __syncthreads();
-  // the first release batch's neighbours and classes do not depend on the
-  // color: load them before warp 0's mex / color store / fence, off the
-  // dependency chain
-  unsigned u[kBW], cls[kBW];
-#pragma unroll
-  for (int j = 0; j < kBW; j++) {
-    const unsigned k = m + j * blockDim.x + tid;
-    u[j] = k < e ? static_cast<unsigned>(__ldg(q.hcol + k)) : v;
-    cls[j] = u[j] != v ? q.vclass[u[j]] : 0u;
-  }
   if (tid < 32) {
     int c = bitmap_mex(sbm[tid]);
     if (c < 0) c = mex_windowed(a, q, v);
