@@ -83,3 +83,21 @@ def test_tree_config4_full(ctx, orc):
         dt.run("tree_height", v)
         assert np.array_equal(dt.result(), ref_h), v
     dt.close()
+
+
+@pytest.mark.parametrize("variant", ["flat", "basic", "warp", "block", "grid"])
+def test_tree_deeper_than_baseline(ctx, orc, variant):
+    """Depths far past BASELINE config 4's 24 (chains of 100 / 2000 nodes, a
+    300-deep comb with 50 leaves per spine node): exact in every variant
+    (basic-DP nests a device launch per level)."""
+    cases = [np.concatenate([[-1], np.arange(d - 1)]).astype(np.int32) for d in (100, 2000)]
+    par = [-1] + list(range(299))
+    for v in range(300):
+        par += [v] * 50
+    cases.append(np.array(par, np.int32))
+    for parent in cases:
+        t = dpc.tree_from_parent(parent)
+        r, _ = dpc.run_tree_desc(t, variant, ctx=ctx)
+        assert np.array_equal(r, orc.tree_desc(parent))
+        h, _ = dpc.run_tree_height(t, variant, ctx=ctx)
+        assert np.array_equal(h, orc.tree_height(parent))
