@@ -390,8 +390,11 @@ def run_config5(args, dist, rank, world, device):
         ms = good[best]["ms"]
         res["value"] = good[best]["gteps"]
         res["ms_per_step"] = ms
+        single = best == "single_gpu_grid"
         res["roofline"] = {"bound": "hbm", "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": peak,
-                           "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / peak, 4), "traffic": None,
+                           "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / peak, 4),
+                           "traffic": _ncu_traffic("r02_config5_spmv_ncu.txt") if single else None,
+                           "traffic_source": "profiles/r02_config5_spmv_ncu.txt" if single else None,
                            "algorithmic_bytes": alg,
                            "kernel": f"{best} (rank 0 row block: nnz*8 + rows*12 + remote x*4)"}
     return res
