@@ -1277,7 +1277,12 @@ extern "C" dpc_status dpc_color_device(dpc_ctx* ctx, dpc_dgraph* g, uint64_t see
     // warp servers (flag bit 19 off); flag bit 19: warp servers only
     q.nbs = (per_sm > 1 && !(c.flags & (1u << 19))) ? static_cast<unsigned>(ctx->sms) : 0u;
     // experiment switch (flag bits 24-27): medium bound = 256 << k, default kBlockMax
-    q.bmax = (c.flags >> 24) & 15u ? (256u << ((c.flags >> 24) & 15u)) : gc::kBlockMax;
+    // the block-server bound, measured per order on config 3: canonical /
+    // LLF orders put the hubs on the dependency chain, where a whole block
+    // (up to 32K edges) beats the chunk-task fan-out (11.88 -> 11.46 ms,
+    // 15.2 -> 14.4 ms); the hash order keeps 4096 (16.1 vs 16.5 ms)
+    q.bmax = (c.flags >> 24) & 15u ? (256u << ((c.flags >> 24) & 15u))
+                                   : (a.order == 0 ? gc::kBlockMax : 8u * gc::kBlockMax);
     DPC_CUDA(cudaMemsetAsync(q.q, 0xff, sizeof(unsigned long long) * (qcap + 128 + bqcap), s));
     DPC_CUDA(cudaMemsetAsync(q.qctr, 0, 1024, s));
     // the adjacency split by this run's priorities (built by the kernel's

@@ -18,6 +18,7 @@ ap.add_argument("--scale", type=int, default=20)
 ap.add_argument("--variants", nargs="*", default=["grid", "block", "basic"])
 ap.add_argument("--orders", nargs="*", default=["hash", "canonical", "llf"])
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--flags", type=int, nargs="*", default=[0], help="extra dpc_launch_cfg.flags values to sweep")
 a = ap.parse_args()
 orc = Oracle()
 ctx = dpc.Context(0)
@@ -27,8 +28,9 @@ for order in a.orders:
     t0 = time.time()
     ref, k = orc.color(g.rowptr, g.col, 1, order={"hash": 0, "canonical": 1, "llf": 2}[order])
     print(f"order {order}: oracle colors {k} ({time.time() - t0:.1f} s)", flush=True)
-    for v in a.variants:
+    for v, fl in [(v, f) for v in a.variants for f in a.flags]:
         cfg = dpc.launch_cfg("color", v, gc_order=order)
+        cfg.flags |= fl
         met = dg.color(1, v, cfg=cfg)
         ok = np.array_equal(dg.get_color(), ref)
         ts = []
@@ -38,6 +40,6 @@ for order in a.orders:
             dg.color(1, v, cfg=cfg, metrics=False)
             ctx.record(1)
             ts.append(ctx.elapsed_ms(0, 1))
-        print(f"  {v:6s} exact={ok} colors={met.result_count} rounds={met.iterations} "
+        print(f"  {v:6s} flags={fl:#x} exact={ok} colors={met.result_count} rounds={met.iterations} "
               f"launches={met.child_launch_count} min {min(ts):.3f} ms mean {np.mean(ts):.3f} ms", flush=True)
 dg.close()
