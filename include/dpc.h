@@ -368,6 +368,15 @@ dpc_status dpc_spmv_host(dpc_ctx* ctx, dpc_dgraph* dg, const float* x_host, floa
  * reference's per-call simulate() (sim.hpp:1746). */
 dpc_status dpc_spmv_host_batch(dpc_ctx* ctx, dpc_dgraph* dg, const float* const* x_host, float* const* y_host,
                                int64_t count, const dpc_launch_cfg* cfg, dpc_metrics* met);
+/* The same over `count` vectors stored back to back in host memory (x_host:
+ * count x ncols floats, y_host: count x n floats, pinned for overlap):
+ * the copies move `group` vectors at a time (0 = about 32 MB per copy) --
+ * PCIe copies of a few MB each run well below the link rate when both
+ * directions are busy (measured: 4 MB pairs 58 GB/s aggregate, 64 MB pairs
+ * 83 GB/s) -- double-buffered, group k+1 coming in and group k-1 going out
+ * while group k is multiplied.  Returns when every y is in host memory. */
+dpc_status dpc_spmv_host_batch_contig(dpc_ctx* ctx, dpc_dgraph* dg, const float* x_host, float* y_host,
+                                      int64_t count, int64_t group, const dpc_launch_cfg* cfg, dpc_metrics* met);
 
 /* ---- fused multi-GPU path over peer memory (BASELINE config 5) ----
  * CUDA IPC export / import of a device buffer; the caller moves the 64-byte

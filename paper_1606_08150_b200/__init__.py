@@ -162,6 +162,8 @@ _SIGS = {
     "dpc_spmv_device": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host": (C.c_int, [_P, _P, _P, _P, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
     "dpc_spmv_host_batch": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(LaunchCfg), C.POINTER(Metrics)]),
+    "dpc_spmv_host_batch_contig": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.POINTER(LaunchCfg),
+                                             C.POINTER(Metrics)]),
     "dpc_dtree_phase_ns": (C.c_int, [_P, _P]),
     "dpc_dgraph_check": (C.c_int, [_P, _P]),
     "dpc_dtree_check": (C.c_int, [_P, _P]),
@@ -624,6 +626,17 @@ class DeviceGraph:
         yp = (C.c_void_p * max(1, k))(*[y.ctypes.data for y in ys])
         _check(_lib.dpc_spmv_host_batch(self.ctx.handle, self._h, xp, yp, k, _cfg_arg("spmv", variant, cfg),
                                         None))
+
+    def spmv_host_batch_contig(self, xs: np.ndarray, ys: np.ndarray, group: int = 0, variant="grid", cfg=None):
+        """Pipelined end-to-end SpMV over the rows of xs (count x ncols,
+        float32, C-contiguous, pinned for overlap) into ys (count x n):
+        copies move `group` vectors at a time (0 = about 32 MB)."""
+        if xs.dtype != np.float32 or ys.dtype != np.float32 or not xs.flags.c_contiguous or not ys.flags.c_contiguous:
+            raise ValueError("xs / ys must be C-contiguous float32")
+        if xs.shape[0] != ys.shape[0]:
+            raise ValueError("xs and ys must hold the same number of vectors")
+        _check(_lib.dpc_spmv_host_batch_contig(self.ctx.handle, self._h, xs.ctypes.data, ys.ctypes.data, xs.shape[0],
+                                               group, _cfg_arg("spmv", variant, cfg), None))
 
     def spmv_fused(self, d_xpeer_table: int, world: int, rows_per_rank: int, d_y: int, variant="grid", cfg=None):
         """Fused multi-GPU SpMV of this row block: x gathered from the owners

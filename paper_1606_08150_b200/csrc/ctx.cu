@@ -351,7 +351,7 @@ void dpc_dgraph_free(dpc_dgraph* g) {
                   g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val,
                   g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt, g->gc_q, g->gc_hstate, g->trace, g->gc_hcol, g->gc_hsplit,
                   g->x2, g->y2, g->sst_items, g->plan_mask, g->plan_sin, g->plan_segrow, g->plan_bar,
-                  g->plan8, g->plan8_segrow, g->plan8h_col, g->plan8h_hot, g->plan8h_xh, g->gc_prio};
+                  g->plan8, g->plan8_segrow, g->plan8h_col, g->plan8h_hot, g->plan8h_xh, g->gc_prio, g->batch_buf};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->ms_state) dpc::sssp_state_free(g->ms_state);
@@ -500,6 +500,74 @@ dpc_status dpc_spmv_host_batch(dpc_ctx* c, dpc_dgraph* g, const float* const* xs
     DPC_CUDA(cudaEventRecord(e[6 + s], c->d2h));
   }
   // the context stream (and its timing events) is ordered after the last copy-out
+  DPC_CUDA(cudaEventRecord(e[8], c->d2h));
+  DPC_CUDA(cudaStreamWaitEvent(c->stream, e[8], 0));
+  DPC_CUDA(cudaStreamSynchronize(c->d2h));
+  return flush_check(c, g);  // a device-side fault of any vector voids the batch
+}
+
+dpc_status dpc_spmv_host_batch_contig(dpc_ctx* c, dpc_dgraph* g, const float* xs, float* ys, int64_t count,
+                                      int64_t group, const dpc_launch_cfg* cfg, dpc_metrics* met) {
+  clear_error();
+  if (!c || !g || (count > 0 && (!xs || !ys)) || count < 0 || group < 0) return fail(DPC_E_INVALID, "bad arguments");
+  if (count == 0) return DPC_OK;
+  DPC_CUDA(cudaSetDevice(c->device));
+  if (!c->h2d) {
+    DPC_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    DPC_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (auto& ev : c->pev) DPC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  const size_t nx = static_cast<size_t>(g->ncols), ny = static_cast<size_t>(g->n);
+  const size_t vbytes = sizeof(float) * (nx + ny);
+  // default: ~32 MB per copy (config 2, 128-vector batch: 2 / 4 / 8 / 16 / 32
+  // vectors per copy -> 0.114 / 0.102 / 0.102 / 0.104 / 0.117 ms per vector;
+  // tools/probes/lab_r02/e2e_contig.py)
+  int64_t G = group ? group : std::max<int64_t>(1, static_cast<int64_t>((size_t{32} << 20) / std::max<size_t>(vbytes / 2, 1)));
+  G = std::min<int64_t>(G, count);
+  // two slots of G vectors: x part then y part (16-byte aligned vectors when n, ncols are multiples of 4)
+  const size_t slot_x = sizeof(float) * nx * static_cast<size_t>(G), slot_y = sizeof(float) * ny * static_cast<size_t>(G);
+  if (g->batch_bytes < 2 * (slot_x + slot_y)) {
+    DPC_CUDA(cudaStreamSynchronize(c->stream));
+    if (g->batch_buf) cudaFree(g->batch_buf);
+    g->batch_buf = nullptr;
+    g->batch_bytes = 0;
+    DPC_CUDA(cudaMalloc(&g->batch_buf, 2 * (slot_x + slot_y)));
+    g->batch_bytes = 2 * (slot_x + slot_y);
+  }
+  auto* base = static_cast<unsigned char*>(g->batch_buf);
+  float* dx[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + slot_x)};
+  float* dy[2] = {reinterpret_cast<float*>(base + 2 * slot_x), reinterpret_cast<float*>(base + 2 * slot_x + slot_y)};
+  // pev: [0,1] x ready  [2,3] x free  [4,5] y ready  [6,7] y free  [8] start
+  cudaEvent_t* e = c->pev;
+  DPC_CUDA(cudaEventRecord(e[8], c->stream));
+  DPC_CUDA(cudaStreamWaitEvent(c->h2d, e[8], 0));
+  DPC_CUDA(cudaStreamWaitEvent(c->d2h, e[8], 0));
+  const int64_t ngroups = (count + G - 1) / G;
+  for (int64_t k = 0; k < ngroups; k++) {
+    const int s = static_cast<int>(k & 1);
+    const int64_t v0 = k * G, nv = std::min<int64_t>(G, count - v0);
+    if (k >= 2) DPC_CUDA(cudaStreamWaitEvent(c->h2d, e[2 + s], 0));
+    DPC_CUDA(cudaMemcpyAsync(dx[s], xs + static_cast<size_t>(v0) * nx, sizeof(float) * nx * static_cast<size_t>(nv),
+                             cudaMemcpyHostToDevice, c->h2d));
+    DPC_CUDA(cudaEventRecord(e[s], c->h2d));
+    DPC_CUDA(cudaStreamWaitEvent(c->stream, e[s], 0));
+    if (k >= 2) DPC_CUDA(cudaStreamWaitEvent(c->stream, e[6 + s], 0));
+    for (int64_t v = 0; v < nv; v++) {
+      dpc_status st = dpc_spmv_device(c, g, dx[s] + static_cast<size_t>(v) * nx, dy[s] + static_cast<size_t>(v) * ny,
+                                      cfg, (k + 1 == ngroups && v + 1 == nv) ? met : nullptr);
+      if (st != DPC_OK) {  // no copy may still touch the caller's host vectors
+        cudaStreamSynchronize(c->h2d);
+        cudaStreamSynchronize(c->d2h);
+        return st;
+      }
+    }
+    DPC_CUDA(cudaEventRecord(e[2 + s], c->stream));
+    DPC_CUDA(cudaEventRecord(e[4 + s], c->stream));
+    DPC_CUDA(cudaStreamWaitEvent(c->d2h, e[4 + s], 0));
+    DPC_CUDA(cudaMemcpyAsync(ys + static_cast<size_t>(v0) * ny, dy[s], sizeof(float) * ny * static_cast<size_t>(nv),
+                             cudaMemcpyDeviceToHost, c->d2h));
+    DPC_CUDA(cudaEventRecord(e[6 + s], c->d2h));
+  }
   DPC_CUDA(cudaEventRecord(e[8], c->d2h));
   DPC_CUDA(cudaStreamWaitEvent(c->stream, e[8], 0));
   DPC_CUDA(cudaStreamSynchronize(c->d2h));

@@ -65,6 +65,8 @@ struct dpc_dgraph {
   bool hdr_clean = false;  // the last run (SpMV stream) left the header zeroed itself
   bool check_pending = false;  // an asynchronous run awaits its fault check
   bool hdr_copied = false;     // ... and its header copy is already enqueued
+  void* batch_buf = nullptr;  // dpc_spmv_host_batch_contig: two slots of grouped x / y vectors
+  size_t batch_bytes = 0;
   float* x2 = nullptr;     // second x / y slot of the pipelined host-vector path
   float* y2 = nullptr;
   // consolidation pool

@@ -291,3 +291,29 @@ def test_spmv_grid_nohot_shape_bit(ctx, orc):
     cfg.flags |= 1 << 13
     y, _ = dpc.run_spmv(g, x, cfg=cfg, ctx=ctx)
     _check(orc, g, x, y)
+
+
+@pytest.mark.parametrize("count,group", [(1, 0), (5, 2), (33, 0), (7, 7), (9, 16)])
+def test_spmv_host_batch_contig(ctx, orc, count, group):
+    """dpc_spmv_host_batch_contig: vectors back to back in (pinned) host
+    memory, copied `group` at a time, double-buffered; every y exact vs the
+    fp64 oracle, ragged last group included."""
+    import ctypes as C
+    g = dpc.gen_rmat(12, 16, seed=11, weights=False, values=True)
+    n = g.n
+    xp = dpc._lib.dpc_host_alloc(4 * n * count)
+    yp = dpc._lib.dpc_host_alloc(4 * n * count)
+    try:
+        xs = np.frombuffer((C.c_float * (n * count)).from_address(xp), np.float32).reshape(count, n)
+        ys = np.frombuffer((C.c_float * (n * count)).from_address(yp), np.float32).reshape(count, n)
+        for i in range(count):
+            xs[i] = _x(n, seed=100 + i)
+        ys[:] = -1.0
+        dg = dpc.DeviceGraph(ctx, g)
+        dg.spmv_host_batch_contig(xs, ys, group=group)
+        for i in range(count):
+            _check(orc, g, xs[i], ys[i])
+        dg.close()
+    finally:
+        dpc._lib.dpc_host_free(xp)
+        dpc._lib.dpc_host_free(yp)
