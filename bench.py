@@ -373,6 +373,26 @@ def run_config5(args, dist, rank, world, device):
                                    "dpc_copy_d2h (C ABI), per rank")}
         dpc._lib.dpc_host_free(xh)
         dpc._lib.dpc_host_free(yh)
+        if world == 1:  # the serving form: consecutive vectors' copies overlap the SpMV in between
+            kv = 8
+            xp, yp = dpc._lib.dpc_host_alloc(4 * n * kv), dpc._lib.dpc_host_alloc(4 * A.n * kv)
+            xs = np.frombuffer((C.c_float * (n * kv)).from_address(xp), np.float32).reshape(kv, n)
+            ys = np.frombuffer((C.c_float * (A.n * kv)).from_address(yp), np.float32).reshape(kv, A.n)
+            xs[:] = x_full
+            dg.spmv_host_batch_contig(xs[:2], ys[:2])
+            ctx.record(2)
+            dg.spmv_host_batch_contig(xs, ys)
+            ctx.record(3)
+            bms = ctx.elapsed_ms(2, 3) / kv
+            bok = y_ok(ys[0]) and y_ok(ys[kv - 1])
+            dpc._lib.dpc_host_free(xp)
+            dpc._lib.dpc_host_free(yp)
+            e2e["forms_ms_per_vector"] = {"synchronous": e2e["ms_per_step"], "host_batch_contig": round(bms, 4)}
+            if bok and bms < e2e["ms_per_step"]:
+                e2e.update({"value": round(n * EDGEFACTOR / (bms * 1e-3) / 1e9, 3), "ms_per_step": round(bms, 4),
+                            "api": f"dpc_spmv_host_batch_contig (C ABI): {kv} host vectors of 64 MB, copy-in / "
+                                   "SpMV / copy-out of consecutive vectors overlapped (double-buffered)"})
+            e2e["parity_ok"] = e2e["parity_ok"] and bok
 
     sssp = _config5_sssp(args, dist, rank, world, ctx, dg, A, comm, ipc, shared, orc)
     if comm is not None:
