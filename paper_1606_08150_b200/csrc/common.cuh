@@ -136,8 +136,9 @@ __device__ __forceinline__ unsigned block_reserve(unsigned* counter, unsigned wa
 // thread's first slots on counters ca / cb.  All threads call; ends with a
 // barrier.
 __device__ __forceinline__ void block_reserve2(unsigned* ca, unsigned wa, unsigned* cb, unsigned wb,
-                                               unsigned* at_a, unsigned* at_b) {
-  __shared__ unsigned s_a[32], s_b[32], s_base[2];
+                                               unsigned* at_a, unsigned* at_b, unsigned* base_b = nullptr,
+                                               unsigned* tot_b = nullptr) {
+  __shared__ unsigned s_a[32], s_b[32], s_base[2], s_totb;
   const unsigned ia = warp_incl_scan(wa), ib = warp_incl_scan(wb);
   const unsigned w = warp_in_block(), nw = blockDim.x >> 5;
   if (lane_id() == 31) s_a[w] = ia, s_b[w] = ib;
@@ -149,12 +150,14 @@ __device__ __forceinline__ void block_reserve2(unsigned* ca, unsigned wa, unsign
     if (lane_id() == 31) {
       const unsigned ba = xi ? atomicAdd(ca, xi) : 0u;
       const unsigned bb = yi ? atomicAdd(cb, yi) : 0u;
-      s_base[0] = ba, s_base[1] = bb;
+      s_base[0] = ba, s_base[1] = bb, s_totb = yi;
     }
   }
   __syncthreads();
   *at_a = s_base[0] + s_a[w] + ia - wa;
   *at_b = s_base[1] + s_b[w] + ib - wb;
+  if (base_b) *base_b = s_base[1];
+  if (tot_b) *tot_b = s_totb;
   __syncthreads();  // the shared slots are reused by the next call
 }
 

@@ -106,9 +106,12 @@ __device__ __forceinline__ unsigned edge_w(const Args& a, unsigned k) {
 }
 
 // Per-block state every relaxing kernel carries in shared memory.
+constexpr unsigned kCoopW = 256;  // cooperative chunk writing in the flush (blocks up to this size)
+
 struct Block {
   Queue q;
   unsigned long long work;
+  unsigned coff[kCoopW], cv[kCoopW], cb[kCoopW];  // flush: per-thread chunk offsets, vertices, row starts
 };
 
 __device__ __forceinline__ unsigned* cur_front(const Args& a, unsigned it) {
@@ -576,11 +579,31 @@ __device__ __forceinline__ void flush_classify(const Args& a, unsigned it, Block
       else light = 1;
     }
     dev::block_add_u64(&s.work, want ? e - b : 0u);  // heavy edges are relaxed next level (all lanes)
-    unsigned lat, cat;
-    dev::block_reserve2(&a.ctr->fsize[nxt], light, &a.ctr->pool[nxt], want, &lat, &cat);
+    unsigned lat, cat, cbase, ctot;
+    dev::block_reserve2(&a.ctr->fsize[nxt], light, &a.ctr->pool[nxt], want, &lat, &cat, &cbase, &ctot);
     if (light) next_front(a, it)[lat] = v;
-    if (want) {
-      const dev::Pool p{a.pool.items + half * a.pool.cap, a.pool.cap};
+    const dev::Pool p{a.pool.items + half * a.pool.cap, a.pool.cap};
+    if (blockDim.x <= kCoopW) {
+      // the block's chunk items written cooperatively: slot t belongs to the
+      // last thread whose exclusive offset is <= t (a hub's hundreds of
+      // chunks no longer serialise on one thread)
+      s.coff[threadIdx.x] = cat - cbase;
+      s.cv[threadIdx.x] = v;
+      s.cb[threadIdx.x] = b;
+      __syncthreads();
+      for (unsigned t = threadIdx.x; t < ctot; t += blockDim.x) {
+        unsigned lo = 0, hi = blockDim.x;  // upper_bound(t) over s.coff[0, blockDim)
+        while (lo < hi) {
+          const unsigned mid = (lo + hi) >> 1;
+          if (s.coff[mid] <= t) lo = mid + 1;
+          else hi = mid;
+        }
+        const unsigned o = lo - 1, at = cbase + t;
+        if (at < p.cap) p.items[at] = Item{s.cv[o], s.cb[o] + (t - s.coff[o]) * a.chunk};
+        else atomicOr(&a.hdr->overflow, 1u);
+      }
+      __syncthreads();
+    } else if (want) {
       dev::write_chunks(p, a.hdr, cat, v, b, e, a.chunk);
     }
   }
