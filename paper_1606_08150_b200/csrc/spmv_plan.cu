@@ -23,16 +23,18 @@
 // barrier).
 //   default  W = 256 (8 nonzeros per lane): plan 64 B per window; the
 //            per-window work (plan entry, scan, carry) is paid once per 256
-//            nonzeros -- 17M warp instructions on config 2 (grid_stream: 36M)
+//            nonzeros -- 17M warp instructions on config 2 (grid_stream:
+//            36M).  It also keeps the 32K most used columns' x in shared
+//            memory (slot-encoded col, per-call hot_gather + bulk-copy
+//            fill; the remaining gathers read L2 only) and splits the
+//            device-wide barrier (arrive after y = 0, wait before the
+//            first y write).  Shape bit 13 drops the x cache.
 //   bit 9    W = 128, register-staged loads (24M instructions)
 //   bit 12   W = 128, col / val / plan staged in a per-warp shared-memory
 //            ring by bulk copies (cp.async.bulk + mbarrier): the smem ring
 //            shrinks L1, whose hits the x gathers need (measured slower)
-//   default form also caches the most used columns' x in shared memory
-//   (slot-encoded col, per-call hot_gather + bulk-copy fill) and splits the
-//   device-wide barrier (arrive after y = 0, wait before the first y write).
-// What bounds it: the latency of the remaining (cold) x gathers and of the
-// HBM stream on 32 warps per SM (profiles/r02_spmv_hot_lab.md).
+// What bounds the default: the latency of the remaining (cold) x gathers
+// and of the HBM stream on 32 warps per SM (profiles/r02_spmv_hot_lab.md).
 #include <cuda_runtime.h>
 
 #include <algorithm>
