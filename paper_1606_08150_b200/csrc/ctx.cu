@@ -5,7 +5,8 @@
 //  - KC_X (config.hpp:68-75) keeps its meaning — B = max(1, B_occ / X) — but
 //    B_occ comes from the B200 (148 SMs, 2048 threads/SM) and the defaults for
 //    (threshold, chunk, X) come from the measured sweep (tools/sweep.py ->
-//    configs/launch_cfg.json), not from the occupancy calculator.
+//    profiles/r02_launch_cfg.json -> launch_table.inc), not from the occupancy
+//    calculator.
 //  - per-buffer sizing (memplan.hpp:61-168, const = 4) is replaced by exact
 //    counts: the pool holds sum over rows with deg > threshold of
 //    ceil(deg / chunk) items, the most any parent pass can insert.
