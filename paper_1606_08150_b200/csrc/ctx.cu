@@ -4,7 +4,7 @@
 // Policy replaced here:
 //  - KC_X (config.hpp:68-75) keeps its meaning — B = max(1, B_occ / X) — but
 //    B_occ comes from the B200 (148 SMs, 2048 threads/SM) and the defaults for
-//    (threshold, chunk, X) come from the measured sweep (tools/sweep.py ->
+//    (threshold, chunk, X) come from the measured sweep (tools/sweep_launch.py ->
 //    profiles/r02_launch_cfg.json -> launch_table.inc), not from the occupancy
 //    calculator.
 //  - per-buffer sizing (memplan.hpp:61-168, const = 4) is replaced by exact
