@@ -352,7 +352,7 @@ void dpc_dgraph_free(dpc_dgraph* g) {
                   g->items, g->ctr, g->gc_state, g->soff, g->xhot_col, g->xhot_val,
                   g->ms_rdist, g->ms_send, g->ms_recv, g->ms_cnt, g->gc_q, g->gc_hstate, g->trace, g->gc_hcol, g->gc_hsplit,
                   g->x2, g->y2, g->sst_items, g->plan_mask, g->plan_sin, g->plan_segrow, g->plan_bar,
-                  g->plan8, g->plan8_segrow, g->plan8h_col, g->plan8h_hot, g->plan8h_xh, g->gc_prio, g->batch_buf};
+                  g->plan8, g->plan8_segrow, g->plan8h_col, g->plan8h_hot, g->plan8h_xh, g->gc_prio, g->batch_buf, g->sssp_fbe};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (g->ms_state) dpc::sssp_state_free(g->ms_state);

@@ -48,6 +48,7 @@ struct dpc_dgraph {
   // frontier / worklist buffers (SSSP, GC)
   unsigned* front[2] = {nullptr, nullptr};
   unsigned* stamp = nullptr;  // SSSP dedup stamp / GC pending counts
+  uint2* sssp_fbe = nullptr;  // SSSP level form: {row start, row end} beside each light-list entry (2 x n)
   unsigned* gc_state = nullptr;  // GC heavy-vertex bitmaps (36 words per pool slot)
   size_t gc_state_slots = 0;
   void* trace = nullptr;          // per-vertex timestamps of the last traced run (DPC_TRACE=1)

@@ -84,6 +84,9 @@ struct Args {
   unsigned classify;       // grid_persistent1: next-level vertices are classified at push time
   unsigned long long* ptrace;  // optional phase timeline (DPC_SSSP_PHASES=1): per level, max over blocks
   const struct Peer* peers;    // fused multi-GPU relaxation: every rank's buffers (nullptr = send buffers)
+  uint2* fbe0;                 // classify form: {row start, row end} of each light-list entry (front0 / front1)
+  uint2* fbe1;
+  unsigned m;                  // edges (bound of the drain's speculative col / w loads)
 };
 
 // One rank's SSSP buffers as seen from this process (own or IPC-mapped):
@@ -119,6 +122,12 @@ __device__ __forceinline__ unsigned* cur_front(const Args& a, unsigned it) {
 }
 __device__ __forceinline__ unsigned* next_front(const Args& a, unsigned it) {
   return (it & 1) ? a.front0 : a.front1;
+}
+__device__ __forceinline__ uint2* cur_fbe(const Args& a, unsigned it) {
+  return (it & 1) ? a.fbe1 : a.fbe0;
+}
+__device__ __forceinline__ uint2* next_fbe(const Args& a, unsigned it) {
+  return (it & 1) ? a.fbe0 : a.fbe1;
 }
 __device__ __forceinline__ unsigned* next_count(const Args& a, unsigned it) {
   return &a.ctr->fsize[(it + 1) % 3];
@@ -193,7 +202,9 @@ __device__ __noinline__ void spill_classify(const Args& a, unsigned it, unsigned
     const dev::Pool p{a.pool.items + ((it + 1) % 2) * a.pool.cap, a.pool.cap};
     dev::write_chunks(p, a.hdr, at, v, b, e, a.chunk);
   } else {
-    next_front(a, it)[atomicAdd(&a.ctr->fsize[nxt], 1u)] = v;
+    const unsigned at = atomicAdd(&a.ctr->fsize[nxt], 1u);
+    next_front(a, it)[at] = v;
+    next_fbe(a, it)[at] = make_uint2(b, e);
   }
 }
 
@@ -308,6 +319,7 @@ __global__ void __launch_bounds__(256) init_kernel(Args a, unsigned source) {
     a.ctr->iters = 0;
     if (mine && a.classify) {  // one-barrier form: a heavy source starts as chunk items
       const unsigned b = a.rowptr[ls], e = a.rowptr[ls + 1];
+      a.fbe0[0] = make_uint2(b, e);
       if (e - b > a.threshold) {
         a.ctr->pool[0] = dev::nchunks(e - b, a.chunk);
         a.ctr->fsize[0] = 0;
@@ -564,6 +576,82 @@ __global__ void __launch_bounds__(256) grid_persistent(Args a, unsigned max_iter
 // light list (warp-cooperative) and drains its share of the chunk items in
 // the same pass.  (Vertices spilled past the shared queue land in the list
 // and are relaxed warp-cooperatively whatever their degree.)
+// Level form (grid_persistent1) light pass: like warp_light_relax, two edges
+// per lane, with each list entry's row bounds read beside it (fbe) and the
+// col / w loads issued before the owner's distance is needed -- the entry's
+// distance load, the edge loads and the bounds are one round trip.
+__device__ __forceinline__ void light_relax1(const Args& a, unsigned it, Block& s, unsigned b, unsigned du,
+                                             unsigned dl) {
+  const unsigned lane = dev::lane_id();
+  const unsigned incl = dev::warp_incl_scan(dl);
+  const unsigned total = __shfl_sync(kFull, incl, 31);
+  const unsigned lo = incl - dl;
+  for (unsigned base = 0; base < total; base += 64) {  // warp-uniform
+    unsigned l[2], g[2], wk[2];
+    bool ok[2];
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      const unsigned jj = base + 32 * j + lane;
+      unsigned q = 0;
+#pragma unroll
+      for (unsigned st = 16; st > 0; st >>= 1) {
+        const unsigned c = q + st;
+        if (__shfl_sync(kFull, lo, c) <= jj) q = c;
+      }
+      l[j] = q;
+      ok[j] = jj < total;
+      const unsigned k = __shfl_sync(kFull, b, q) + (jj - __shfl_sync(kFull, lo, q));
+      g[j] = ok[j] ? static_cast<unsigned>(__ldg(a.col + k)) : a.r0;
+      wk[j] = ok[j] ? edge_w(a, k) : 0u;
+    }
+    unsigned long long nd[2];
+    unsigned c[2];
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      const unsigned dul = __shfl_sync(kFull, du, l[j]);
+      nd[j] = ok[j] ? static_cast<unsigned long long>(dul) + wk[j] : kInf;
+      const unsigned v = g[j] - a.r0;
+      c[j] = (nd[j] < kInf && v < a.n) ? __ldcg(a.dist + v) : 0u;
+    }
+    relax_k<2>(a, it, s, g, nd, c);
+  }
+}
+
+// Level form drain: item t (prefetched one item ahead) relaxes its first 64
+// edges with the col / w loads issued speculatively up to begin + chunk
+// (bounded by m) beside the row-end and distance loads of its vertex, one
+// round trip instead of two.
+__device__ __forceinline__ void drain_items1(const Args& a, unsigned it, Block& s, const Item* items,
+                                             unsigned count, unsigned gwarp, unsigned nwarps, Item t) {
+  const unsigned lane = dev::lane_id();
+  for (unsigned i = gwarp; i < count; i += nwarps) {
+    Item tn{0u, 0u};
+    if (i + nwarps < count) tn = items[i + nwarps];
+    const unsigned lim = min(t.begin + a.chunk, a.m);
+    const unsigned k1 = t.begin + lane, k2 = k1 + 32;
+    unsigned g[2], wk[2];
+    g[0] = k1 < lim ? static_cast<unsigned>(__ldg(a.col + k1)) : a.r0;
+    g[1] = k2 < lim ? static_cast<unsigned>(__ldg(a.col + k2)) : a.r0;
+    wk[0] = k1 < lim ? edge_w(a, k1) : 0u;
+    wk[1] = k2 < lim ? edge_w(a, k2) : 0u;
+    const unsigned e = min(t.begin + a.chunk, __ldg(a.rowptr + t.v + 1));
+    const unsigned du = __ldcg(a.dist + t.v);
+    unsigned long long nd[2];
+    unsigned c[2];
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      const bool ok = (j ? k2 : k1) < e;
+      if (!ok) g[j] = a.r0;
+      nd[j] = ok ? static_cast<unsigned long long>(du) + wk[j] : kInf;
+      const unsigned v = g[j] - a.r0;
+      c[j] = (nd[j] < kInf && v < a.n) ? __ldcg(a.dist + v) : 0u;
+    }
+    relax_k<2>(a, it, s, g, nd, c);
+    if (t.begin + 64 < e) relax_warp(a, it, s, du, t.begin + 64, e);  // chunks above 64 edges
+    t = tn;
+  }
+}
+
 __device__ __forceinline__ void flush_classify(const Args& a, unsigned it, Block& s, unsigned half) {
   __syncthreads();
   const unsigned n = min(s.q.n, kQueue);
@@ -581,7 +669,10 @@ __device__ __forceinline__ void flush_classify(const Args& a, unsigned it, Block
     dev::block_add_u64(&s.work, want ? e - b : 0u);  // heavy edges are relaxed next level (all lanes)
     unsigned lat, cat, cbase, ctot;
     dev::block_reserve2(&a.ctr->fsize[nxt], light, &a.ctr->pool[nxt], want, &lat, &cat, &cbase, &ctot);
-    if (light) next_front(a, it)[lat] = v;
+    if (light) {
+      next_front(a, it)[lat] = v;
+      next_fbe(a, it)[lat] = make_uint2(b, e);  // the next level's light pass needs no rowptr round trip
+    }
     const dev::Pool p{a.pool.items + half * a.pool.cap, a.pool.cap};
     if (blockDim.x <= kCoopW) {
       // the block's chunk items written cooperatively: slot t belongs to the
@@ -651,6 +742,15 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
       }
     };
     mark(0);
+    // the level's chunk items (inserted while the previous level flushed);
+    // warp rank block-interleaved: consecutive items land in different
+    // blocks, so a short item list (e.g. the source's chunks) spreads its
+    // pushes over every block's queue instead of a few.  The warp's first
+    // item is loaded now, under the light pass.
+    const Item* items = a.pool.items + (it % 2) * a.pool.cap;
+    const unsigned iw = dev::warp_in_block() * gridDim.x + blockIdx.x;
+    Item t0{0u, 0u};
+    if (iw < pc) t0 = items[iw];
     // the level's light list, warp-cooperatively (any degree), spread over
     // ALL warps: each takes a contiguous slice of ceil(fs / warps) vertices
     // (a level's relax rounds per warp, not the first fs / 256 blocks, set
@@ -663,22 +763,18 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
         const unsigned i = base + dev::lane_id();
         unsigned b = 0, du = 0, deg = 0;
         if (i < v1) {
-          const unsigned u = cur_front(a, it)[i];
-          b = __ldg(a.rowptr + u);
-          deg = __ldg(a.rowptr + u + 1) - b;
+          const unsigned u = __ldcg(cur_front(a, it) + i);
+          const uint2 be = __ldcg(cur_fbe(a, it) + i);
+          b = be.x;
+          deg = be.y - be.x;
           du = __ldcg(a.dist + u);
         }
         dev::block_add_u64(&s.work, deg);
-        warp_light_relax(a, it, s, b, du, deg);
+        light_relax1(a, it, s, b, du, deg);
       }
     }
-    // the level's chunk items (inserted while the previous level flushed)
     mark(1);
-    // warp rank block-interleaved: consecutive items land in different
-    // blocks, so a short item list (e.g. the source's chunks) spreads its
-    // pushes over every block's queue instead of a few
-    drain_items(a, it, s, a.pool.items + (it % 2) * a.pool.cap, pc,
-                dev::warp_in_block() * gridDim.x + blockIdx.x, stride >> 5);
+    drain_items1(a, it, s, items, pc, iw, stride >> 5, t0);
     mark(2);
     flush_classify(a, it, s, (it + 1) % 2);
     mark(3);
@@ -880,6 +976,7 @@ static dpc_status sssp_setup(dpc_ctx* ctx, dpc_dgraph* g, const dpc_launch_cfg* 
   a->ctr = reinterpret_cast<sssp::Ctr*>(g->ctr);
   a->hdr = g->hdr;
   a->n = static_cast<unsigned>(g->n);
+  a->m = static_cast<unsigned>(g->m);
   a->threshold = c->threshold;
   a->chunk = c->chunk;
   a->child_threads = c->child_threads;
@@ -970,6 +1067,9 @@ static dpc_status sssp_run(dpc_ctx* ctx, dpc_dgraph* g, int32_t source, const dp
     if (st != DPC_OK) return st;
     a.pool = dev::Pool{g->items, static_cast<unsigned>(half)};
     a.classify = 1;
+    if (!g->sssp_fbe) DPC_CUDA(cudaMalloc(&g->sssp_fbe, sizeof(uint2) * 2 * static_cast<size_t>(std::max<int64_t>(g->n, 1))));
+    a.fbe0 = g->sssp_fbe;
+    a.fbe1 = g->sssp_fbe + std::max<int64_t>(g->n, 1);
     a.coop = (c.flags & DPC_CFG_COOP_LAUNCH) ? 1u : 0u;
   }
   // frontier stream form: forced by DPC_CFG_GRID_STREAM, default from 2^24
