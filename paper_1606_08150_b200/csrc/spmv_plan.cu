@@ -664,15 +664,26 @@ dpc_status spmv_plan_build(dpc_ctx* ctx, dpc_dgraph* g) {
     plan[8 * i + 4] = s_in[i];
   }
   cudaStream_t s = ctx->stream;
-  DPC_CUDA(cudaMalloc(&g->plan_mask, sizeof(uint32_t) * plan.size()));
-  DPC_CUDA(cudaMalloc(&g->plan_segrow, sizeof(uint32_t) * nseg));
-  DPC_CUDA(cudaMalloc(&g->plan_bar, 2 * sizeof(unsigned)));
-  DPC_CUDA(cudaMemcpyAsync(g->plan_mask, plan.data(), sizeof(uint32_t) * plan.size(), cudaMemcpyHostToDevice, s));
-  if (!seg_row.empty())
-    DPC_CUDA(cudaMemcpyAsync(g->plan_segrow, seg_row.data(), sizeof(uint32_t) * seg_row.size(),
-                             cudaMemcpyHostToDevice, s));
-  DPC_CUDA(cudaMemsetAsync(g->plan_bar, 0, 2 * sizeof(unsigned), s));
-  DPC_CUDA(cudaStreamSynchronize(s));  // the host vectors go out of scope
+  uint32_t* d_plan = nullptr;
+  uint32_t* d_seg = nullptr;
+  cudaError_t e = cudaMalloc(&d_plan, sizeof(uint32_t) * plan.size());
+  if (e == cudaSuccess) e = cudaMalloc(&d_seg, sizeof(uint32_t) * nseg);
+  if (e == cudaSuccess && !g->plan_bar) {
+    e = cudaMalloc(&g->plan_bar, 2 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemsetAsync(g->plan_bar, 0, 2 * sizeof(unsigned), s);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_plan, plan.data(), sizeof(uint32_t) * plan.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && !seg_row.empty())
+    e = cudaMemcpyAsync(d_seg, seg_row.data(), sizeof(uint32_t) * seg_row.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host vectors go out of scope
+  if (e != cudaSuccess) {  // nothing half-built is published
+    cudaFree(d_plan);
+    cudaFree(d_seg);
+    return cuda_fail(e, "SpMV plan (upload)");
+  }
+  g->plan_mask = d_plan;
+  g->plan_segrow = d_seg;
   g->plan_nwin = static_cast<unsigned>(nwin);
   return DPC_OK;
 }
@@ -703,18 +714,29 @@ dpc_status spmv_plan8_build(dpc_ctx* ctx, dpc_dgraph* g) {
       acc += static_cast<uint32_t>(__builtin_popcount(plan[16 * i + jj]));
     }
   }
+  // built into locals and published only when complete: a failed build
+  // leaves no half-filled plan behind for the next call to trust
   cudaStream_t s = ctx->stream;
-  DPC_CUDA(cudaMalloc(&g->plan8, sizeof(uint32_t) * plan.size()));
-  DPC_CUDA(cudaMalloc(&g->plan8_segrow, sizeof(uint32_t) * std::max<size_t>(seg_row.size(), 1)));
-  if (!g->plan_bar) {
-    DPC_CUDA(cudaMalloc(&g->plan_bar, 2 * sizeof(unsigned)));
-    DPC_CUDA(cudaMemsetAsync(g->plan_bar, 0, 2 * sizeof(unsigned), s));
+  uint32_t* d_plan = nullptr;
+  uint32_t* d_seg = nullptr;
+  cudaError_t e = cudaMalloc(&d_plan, sizeof(uint32_t) * plan.size());
+  if (e == cudaSuccess) e = cudaMalloc(&d_seg, sizeof(uint32_t) * std::max<size_t>(seg_row.size(), 1));
+  if (e == cudaSuccess && !g->plan_bar) {
+    e = cudaMalloc(&g->plan_bar, 2 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemsetAsync(g->plan_bar, 0, 2 * sizeof(unsigned), s);
   }
-  DPC_CUDA(cudaMemcpyAsync(g->plan8, plan.data(), sizeof(uint32_t) * plan.size(), cudaMemcpyHostToDevice, s));
-  if (!seg_row.empty())
-    DPC_CUDA(cudaMemcpyAsync(g->plan8_segrow, seg_row.data(), sizeof(uint32_t) * seg_row.size(),
-                             cudaMemcpyHostToDevice, s));
-  DPC_CUDA(cudaStreamSynchronize(s));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_plan, plan.data(), sizeof(uint32_t) * plan.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && !seg_row.empty())
+    e = cudaMemcpyAsync(d_seg, seg_row.data(), sizeof(uint32_t) * seg_row.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host vectors go out of scope
+  if (e != cudaSuccess) {
+    cudaFree(d_plan);
+    cudaFree(d_seg);
+    return cuda_fail(e, "SpMV plan (upload)");
+  }
+  g->plan8 = d_plan;
+  g->plan8_segrow = d_seg;
   g->plan8_nwin = static_cast<unsigned>(nwin);
   return DPC_OK;
 }
