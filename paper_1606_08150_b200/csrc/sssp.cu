@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
     flush_classify(a, it, s, (it + 1) % 2);
     mark(3);
     if (a.coop) cg::this_grid().sync();
-    else dev::soft_grid_sync(&a.hdr->ticket, &a.hdr->iter, &a.hdr->overflow);
+    else dev::grid_sync64(&a.hdr->bar, &a.hdr->overflow);
     mark(4);
   }
   if (gtid == 0) a.ctr->iters = it;

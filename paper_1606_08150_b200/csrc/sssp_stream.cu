@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stream_persistent(Args a) {
       s_edges = 0;
     }
     if (a.coop) cooperative_groups::this_grid().sync();
-    else dev::soft_grid_sync(&a.hdr->ticket, &a.hdr->iter, &a.hdr->overflow);
+    else dev::grid_sync64(&a.hdr->bar, &a.hdr->overflow);
   }
   if (gtid == 0) a.ctr->levels = lvl;
 }
