@@ -762,11 +762,13 @@ def run_ours(args):
     # such a sequence reads 144.8 MB from DRAM, the same as a launch after a
     # flush (profiles/r02_spmv_b2b_ncu.txt).  The same K steps timed one by
     # one with a flush before each (round 1's form) are reported beside it.
-    for _ in range(args.warmup):
-        dg.spmv("grid")
-    ctx.synchronize()
-    _barrier(dist)
     with Clocks(local) as clk:
+        # warm-up after the clock sampler's start (it idles the GPU for
+        # 0.3 s): the timed steps must not pay the clock ramp from idle
+        for _ in range(args.warmup):
+            dg.spmv("grid")
+        ctx.synchronize()
+        _barrier(dist)
         ctx.flush_l2()
         ctx.record(0)
         for _ in range(args.steps):
