@@ -713,6 +713,31 @@ def sssp_section(ctx, args):
     return out
 
 
+def _summary(out):
+    """The line's key numbers in one small object (printed last)."""
+    def grid_ms(app):
+        try:
+            return out["apps"][app]["variants"]["grid"]["ms"]
+        except (KeyError, TypeError):
+            return None
+    apps = {}
+    for k, v in (out.get("apps") or {}).items():
+        if isinstance(v, dict) and "best_vs_basic" in v:
+            apps[k] = {"grid_ms": grid_ms(k), "vs_basic": v.get("best_vs_basic"), "vs_flat": v.get("best_vs_flat")}
+    roof = out.get("roofline") or {}
+    sssp = out.get("sssp") or {}
+    c5 = out.get("config5") or {}
+    return {"spmv_gteps": out.get("value"), "spmv_ms_per_step": out.get("ms_per_step"),
+            "spmv_ms_per_step_flushed_each": (out.get("config") or {}).get("ms_per_step_flushed_each"),
+            "roofline_frac": roof.get("frac"), "e2e_gteps": (out.get("e2e") or {}).get("value"),
+            "spmv_vs_basic": (out.get("speedup") or {}).get("grid_vs_basic"),
+            "spmv_vs_flat": (out.get("speedup") or {}).get("grid_vs_flat"),
+            "sssp_scale22_gteps": sssp.get("value"), "sssp_scale22_frac": (sssp.get("roofline") or {}).get("frac"),
+            "config5_1gpu_spmv_gteps": c5.get("value"), "config5_1gpu_sssp_gteps": (c5.get("sssp") or {}).get("value"),
+            "cpu_baseline_gteps": (out.get("cpu_baseline") or {}).get("value"), "apps": apps,
+            "parity_failed": out.get("parity_failed", [])}
+
+
 def run_ours(args):
     import paper_1606_08150_b200 as dpc
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
@@ -970,6 +995,7 @@ def run_ours(args):
         except Exception as e:  # noqa: BLE001 - the headline line must still print
             out["kdl"] = {"error": str(e)[:300]}
     if rank == 0:
+        out["summary"] = _summary(out)  # last key: what a truncated tail of the line still shows
         print(json.dumps(out), flush=True)
     dg.close()
     ctx.close()
