@@ -698,11 +698,7 @@ __device__ __forceinline__ void flush_classify(const Args& a, unsigned it, Block
       dev::write_chunks(p, a.hdr, cat, v, b, e, a.chunk);
     }
   }
-  if (threadIdx.x == 0) {
-    s.q.n = 0;
-    if (s.work) atomicAdd(&a.hdr->work, s.work);
-    s.work = 0;
-  }
+  if (threadIdx.x == 0) s.q.n = 0;  // (s.work is published once, at kernel end)
   __syncthreads();
 }
 
@@ -783,6 +779,9 @@ __global__ void __launch_bounds__(256) grid_persistent1(Args a, unsigned max_ite
     mark(4);
   }
   if (gtid == 0) a.ctr->iters = it;
+  // the block's edge count (a metric): one atomic per block per run, not per
+  // level -- per-level adds queued on the header line beside the barrier's
+  if (threadIdx.x == 0 && s.work) atomicAdd(&a.hdr->work, s.work);
 }
 
 // ---------------------------------------------------------------------------

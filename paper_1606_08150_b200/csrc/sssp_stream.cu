@@ -378,14 +378,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stream_persistent(Args a) {
     wp.edges = 0;
     if (dev::lane_id() == 0 && we) atomicAdd(&s_edges, static_cast<unsigned long long>(we));
     __syncthreads();
-    if (threadIdx.x == 0 && s_edges) {
-      atomicAdd(&a.ctr->relaxed, s_edges);
-      s_edges = 0;
-    }
     if (a.coop) cooperative_groups::this_grid().sync();
     else dev::grid_sync64(&a.hdr->bar, &a.hdr->overflow);
   }
   if (gtid == 0) a.ctr->levels = lvl;
+  // the block's edge count: one atomic per block per run, not per level (the
+  // counters' line also carries the levels' reservations)
+  __syncthreads();
+  if (threadIdx.x == 0 && s_edges) atomicAdd(&a.ctr->relaxed, s_edges);
 }
 
 // Seeds F_0 = {source}.
