@@ -317,3 +317,37 @@ def test_spmv_host_batch_contig(ctx, orc, count, group):
     finally:
         dpc._lib.dpc_host_free(xp)
         dpc._lib.dpc_host_free(yp)
+
+
+@pytest.mark.parametrize("scale", [12, 20])
+def test_spmv_back_to_back_chain(ctx, orc, scale):
+    """The bench's back-to-back form with data flowing between calls: three
+    independent products, then a power-iteration chain that reads the previous
+    call's y as its x, all enqueued without a host synchronisation (the
+    hot-column gather of call i+1 must see call i's y)."""
+    g = dpc.gen_rmat(scale, 16, seed=3, weights=False, values=True)
+    dg = dpc.DeviceGraph(ctx, g)
+    n = g.n
+    xs = [_x(n, seed=s) for s in (1, 2, 3)]
+    bx = [ctx.alloc(4 * n) for _ in range(3)]
+    by = [ctx.alloc(4 * n) for _ in range(6)]
+    for p, x in zip(bx, xs):
+        ctx.h2d(p, x)
+    ctx.synchronize()
+    cfg = dpc._cfg_arg("spmv", "grid", None)
+    for i in range(3):
+        dpc._check(dpc._lib.dpc_spmv_device(ctx.handle, dg._h, bx[i], by[i], cfg, None))
+    chain = [by[0]] + by[3:]
+    for i in range(3):  # y3 = A y0, y4 = A y3, y5 = A y4
+        dpc._check(dpc._lib.dpc_spmv_device(ctx.handle, dg._h, chain[i], chain[i + 1], cfg, None))
+    ctx.synchronize()
+    ys = [ctx.d2h(p, n) for p in by]
+    dg.check()
+    for i in range(3):
+        _check(orc, g, xs[i], ys[i])
+    _check(orc, g, ys[0], ys[3])
+    _check(orc, g, ys[3], ys[4])
+    _check(orc, g, ys[4], ys[5])
+    for p in bx + by:
+        ctx.free(p)
+    dg.close()
