@@ -208,3 +208,38 @@ def test_sssp_on_dimacs_ingested_graph(ctx, orc, tmp_path):
     for v in ["flat", "basic", "warp", "block", "grid"]:
         d, _ = dpc.run_sssp(h, s, v, ctx=ctx)
         assert np.array_equal(d, ref), v
+
+
+@pytest.mark.parametrize("unit", [False, True])
+def test_sssp_hub_spills_level_form(ctx, orc, unit):
+    """A hub with 2^20 out-edges: its chunk items push more vertices into
+    each block's shared queue than it holds (2048), so the level form's
+    spill path classifies them (and records their row bounds for the light
+    pass) -- then a second hub level and a tail of light vertices."""
+    L = 1 << 20
+    n = L + 64 + 2
+    hub, hub2 = 0, L + 1
+    rng = np.random.default_rng(5)
+    # hub -> leaves 1..L; every leaf -> hub2, every 64th leaf also -> one of
+    # the 64 tail vertices; hub2 -> the 64 tail vertices
+    deg = np.ones(n, np.int64)
+    deg[hub] = L
+    deg[1:L + 1] = 1 + (np.arange(1, L + 1) % 64 == 0)
+    deg[hub2] = 64
+    deg[L + 2:] = 0
+    rowptr = np.concatenate([[0], np.cumsum(deg)])
+    col = np.empty(rowptr[-1], np.int64)
+    col[:L] = np.arange(1, L + 1)
+    leaf_start = rowptr[1:L + 1]
+    col[leaf_start] = hub2
+    extra = np.nonzero(deg[1:L + 1] == 2)[0] + 1
+    col[rowptr[extra] + 1] = L + 2 + (extra // 64) % 64
+    col[rowptr[hub2]:rowptr[hub2] + 64] = L + 2 + np.arange(64)
+    w = rng.integers(1, 256, len(col)).astype(np.int32)
+    g = dpc.csr_from_arrays(rowptr, col.astype(np.int32), w=w)
+    if unit:
+        d, _ = dpc.run_bfs(g, hub, "grid", ctx=ctx)
+        assert np.array_equal(d, orc.bfs(g.rowptr, g.col, hub))
+    else:
+        d, _ = dpc.run_sssp(g, hub, "grid", ctx=ctx)
+        assert np.array_equal(d, orc.sssp(g.rowptr, g.col, g.w, hub))
