@@ -946,10 +946,10 @@ def run_ours(args):
                                   "ms_per_step": round(e2e_sync_max, 4),
                                   "api": "dpc_spmv_host (C ABI), one synchronous call per step, L2 flushed"}},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": _ncu_traffic("r02_spmv_b2b_ncu.txt"),
-                     "traffic_source": ("profiles/r02_spmv_b2b_ncu.txt (dram bytes read + write per launch of the "
-                                        "back-to-back sequence, ncu --cache-control none; the --set full capture "
-                                        "after a flush: profiles/r02_spmv_plan8_hot_ncu.txt)"),
+                     "frac": round(achieved / peak, 4), "traffic": _ncu_traffic(),
+                     "traffic_source": ("profiles/r02_spmv_plan8_hot_ncu.txt (ncu --set full, dram bytes read + "
+                                        "write per launch after a flush); in the headline's back-to-back sequence "
+                                        "each launch reads the same 144.8 MB (profiles/r02_spmv_b2b_ncu.txt)"),
                      "algorithmic_bytes": alg, "kernel": "spmvp::plan8_drain<1024, HOT> (whole step incl. spmvp::hot_gather)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"},
         "gpu_launches": args.steps * (int(met.host_launches) + int(met.child_launch_count)),
