@@ -611,8 +611,10 @@ constexpr int kBW = BW_CFG;           // edges per thread per block-server step
 // throughput) for the 18 ms config-3 run, mostly polling, yet longer sleeps
 // measured slower (100 ns: 18.2 ms, 400: 18.6, 1500: 19.6): the detection
 // delay on the dependency chain costs more than the issue slots.
+// Round 2, config 3 canonical / hash (min of 5, two passes): 64 ns 11.41 /
+// 16.17 ms, 16 ns 11.35 / 15.96, 4 ns 11.34 / 15.97, 0 ns 11.34 / 15.97.
 #ifndef POLL_NS
-#define POLL_NS 64
+#define POLL_NS 16
 #endif
 constexpr unsigned kPollNs = POLL_NS;
 
